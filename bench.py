@@ -1,0 +1,286 @@
+"""Benchmark: network evals/s of the NEAT evaluation step at BASELINE config 2.
+
+One step = transform (K1) + forward with the fused func-fit fitness (K2) of a
+10k-genome shard (N_max=64, C_max=256, fill 0.75, tanh/sum) over a
+1024-sample batch, plus the fitness all-gather across ranks (the real
+per-generation exchange).  Weak scaling: every rank owns a 10k shard, so the
+job evaluates 10k*N genomes per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Rank 0 prints one JSON line.  --impl reference times the reference's own CPU
+path (oracle/_ref = the unmodified reference headers, all host threads) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "network evals/sec (genomes x inputs) at pop 10k"
+UNIT = "evals/s"
+P_SHARD, N_MAX, C_MAX, FILL, BATCH, NI, NO = 10_000, 64, 256, 0.75, 1024, 4, 1
+WORKLOAD = "C2 func-regression: pop 10k per GPU, B=1024, N_max=64, C_max=256, fill 0.75, tanh/sum"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                    if r.returncode == 0 and r.stdout.strip():
+                        self.samples.append([x.strip() for x in r.stdout.strip().split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference(P_sample: int, seed: int = 0, target_s: float = 8.0):
+    """Reference batch_forward (transform + forward, network.hpp:122/294) on all host cores via oracle/_ref."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as ol
+    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
+    if ol.ref_available():
+        kind = "reference"
+    else:
+        kind = "port"
+    threads = os.cpu_count() or 1
+    prob = ol.Problem(N_MAX, C_MAX, list(range(NI)), list(range(NI, NI + NO)))
+    schema = ol.SchemaSpec()
+    X, Y = regression_dataset(BATCH, NI, NO, seed=seed)
+
+    def run(P):
+        nodes, conns = synthetic_population(P, N_MAX, C_MAX, FILL, NI, NO, seed=seed)
+        t0 = time.perf_counter()
+        if kind == "reference":
+            st, bad, msg, out = ol.ref_batch_forward(prob, schema, nodes, conns, X, nthreads=threads)
+            assert st == 0, msg
+        else:
+            for p in range(P):
+                net = ol.oracle_transform(prob, schema, nodes[p], conns[p])
+                out = ol.oracle_forward(prob, schema, nodes[p], net, X)
+        _ = -np.mean((Y[None] - out) ** 2, axis=(1, 2)) if out.ndim == 3 else None
+        return time.perf_counter() - t0
+
+    probe = max(threads * 4, 64)
+    dt = run(probe)
+    P = int(min(P_sample or 10**9, max(probe, probe * target_s / max(dt, 1e-6))))
+    P = min(P, P_SHARD)
+    dt = run(P)
+    return {"value": P * BATCH / dt, "unit": UNIT, "cores": threads if kind == "reference" else 1, "kind": kind,
+            "sample": f"{P} genomes x {BATCH} samples of the C2 workload, transform+forward+MSE, {dt:.2f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        vals = []
+        for _ in range(args.warmup):
+            pass
+        base = None
+        for _ in range(max(1, args.steps)):
+            base = cpu_reference(0, target_s=max(1.0, 20.0 / max(1, args.steps)))
+            vals.append(base["value"])
+        v = float(np.median(vals))
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": P_SHARD * BATCH / v * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": BATCH, "pop": P_SHARD},
+                "cpu_baseline": {**base, "value": v},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2504_08339_b200 as fnb
+    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    nodes_h, conns_h = synthetic_population(P_SHARD, N_MAX, C_MAX, FILL, NI, NO, seed=1000 + rank)
+    X_h, Y_h = regression_dataset(BATCH, NI, NO, seed=0)
+    eng = fnb.Engine(fnb.GenomeLimits(N_MAX, C_MAX), list(range(NI)), list(range(NI, NI + NO)),
+                     fnb.AttributeSchema(), device=local)
+    nodes = torch.from_numpy(nodes_h).to(dev)
+    conns = torch.from_numpy(conns_h).to(dev)
+    X = torch.from_numpy(X_h.astype(np.float32)).to(dev)
+    Y = torch.from_numpy(Y_h.astype(np.float32)).to(dev)
+    nets = eng.alloc_nets(P_SHARD)
+    fit = torch.empty(P_SHARD, dtype=torch.float64, device=dev)
+    fit_all = torch.empty(P_SHARD * world, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        eng.transform_d(nodes, conns, nets, stream)
+        if ev is not None:
+            ev[0].record(stream)
+        eng.forward_d(nets, P_SHARD, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(fit_all, fit)
+
+    # correctness gate once, outside timing
+    step()
+    eng.check_nets_d(nodes, conns, nets)
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = eng.launch_count
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        starts[i].record(stream)
+        step(kev[i])
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    launches = eng.launch_count - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    fwd_ms = [a.elapsed_time(b) for a, b in kev]
+    tot_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.barrier()
+    clocks = sampler.stop()
+    ms_per_step = tot_ms / args.steps
+    value = P_SHARD * world * BATCH / (ms_per_step / 1e3)
+
+    # ---- e2e through the public host API (pinned host buffers, H2D + D2H inside) ----
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    nodes_p, conns_p, X_p, Y_p = pin(nodes_h), pin(conns_h), pin(X_h), pin(Y_h)
+    eng.evaluate(nodes_p, conns_p, X_p, Y_p, fnb.FIT_NEG_MSE)
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        fit_h = eng.evaluate(nodes_p, conns_p, X_p, Y_p, fnb.FIT_NEG_MSE)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = nodes_h.nbytes + conns_h.nbytes + X_h.nbytes + Y_h.nbytes
+    d2h = fit_h.nbytes
+
+    # ---- roofline for the dominant kernel (K2 forward) ----
+    n_en = int(np.sum(conns_h[:, :, 2] == 1.0))
+    n_ops = int(np.sum(~np.isnan(nodes_h[:, :, 0]))) - P_SHARD * NI
+    flops = 2.0 * BATCH * (n_en + n_ops)          # FMA per enabled edge + resp*agg+bias per node
+    fwd_s = float(np.mean(fwd_ms)) / 1e3
+    pk = peaks()
+    sm_clock = (pk.get("sm_max_mhz") or 1965.0) * 1e6
+    fp32_peak = 148 * 128 * 2 * sm_clock / 1e12
+    achieved = flops / fwd_s / 1e12
+    smem_bytes = 4.0 * BATCH * (n_en + n_ops)     # one 4-byte LDS per edge-sample, one STS per node-sample
+    smem_peak = 148 * 128 * sm_clock / 1e12       # TB/s (128 B/clk/SM)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference(0)
+        except Exception as e:  # reported, never silently substituted
+            cpu = {"value": None, "error": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (forward), f64 (fitness)", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "pop_per_gpu": P_SHARD, "global_pop": P_SHARD * world,
+                       "global_batch": BATCH, "max_nodes": N_MAX, "max_conns": C_MAX, "fill": FILL,
+                       "parallelism": f"dp{world} (population shards)", "l2": "flushed between timed steps"},
+            "e2e": {"value": P_SHARD * world * BATCH / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "api": "fnb_evaluate (host buffers, pinned)"},
+            "gpu_launches": int(launches),
+            "kernels": {"transform_plus_forward_ms": ms_per_step, "forward_ms": fwd_s * 1e3,
+                        "transform_ms": ms_per_step - fwd_s * 1e3},
+            "roofline": {"kernel": "k_forward (K2)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
+                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                         "peak_source": "nominal FP32 FMA peak at MEASURED_PEAKS sm_max_mhz (no measured FP32 peak)",
+                         "smem": {"achieved_TBps": smem_bytes / fwd_s / 1e12, "peak_TBps": smem_peak,
+                                  "frac": smem_bytes / fwd_s / 1e12 / smem_peak}},
+            "clocks": clocks,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

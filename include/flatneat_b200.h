@@ -1,0 +1,142 @@
+/*
+ * flatneat_b200.h -- C ABI of the B200-native NEAT generation loop.
+ *
+ * Drop-in boundary for the reference's header-only C++ API
+ * (/root/reference/proj/include/flatneat/).  Plain pointers and sizes only,
+ * no exceptions, no torch types.  Genomes cross the boundary in the
+ * reference's own PopulationTensors layout (genome.hpp:315-338): P x N_max x 5
+ * node rows [key,bias,response,agg_id,act_id] and P x C_max x 4 connection
+ * rows [in,out,enabled,weight], FP64, NaN-padded.
+ *
+ * Status: every function returns 0 on success or 1 + Errc (errors.hpp:10-31);
+ * fnb_last_error() then returns the reference's what() string
+ * "<errc_name>: <detail>" and fnb_last_error_index() the lowest failing
+ * genome (the lowest-chunk rule of parallel.hpp:69-73,108-109).
+ *
+ * Two layers:
+ *   host layer   (fnb_transform, fnb_batch_forward, fnb_evaluate, ...)
+ *                synchronous, host buffers in and out -- mirrors the reference
+ *                free functions one for one;
+ *   device layer (fnb_*_d) asynchronous on a caller stream, device pointers
+ *                -- what the generation loop and multi-GPU driver compose.
+ * A context owns one device and is not thread-safe (one host thread per ctx).
+ */
+#ifndef FLATNEAT_B200_H
+#define FLATNEAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FNB_ABI_VERSION 1
+#define FNB_MAX_NODES_LIMIT 256   /* transform bitsets cover <= 256 rows */
+
+/* Errc (errors.hpp:10-31); status = 1 + code. */
+enum fnb_errc {
+  FNB_E_UNKNOWN_FUNCTION = 0, FNB_E_GENOME_FULL, FNB_E_DUPLICATE_KEY,
+  FNB_E_DUPLICATE_CONN, FNB_E_DANGLING_ENDPOINT, FNB_E_KEY_NOT_FOUND,
+  FNB_E_PROTECTED_NODE, FNB_E_ATTR_OUT_OF_RANGE, FNB_E_SHAPE_MISMATCH,
+  FNB_E_CORRUPT_ROW, FNB_E_CYCLE_DETECTED, FNB_E_NON_FINITE_INPUT,
+  FNB_E_NON_FINITE_STATE, FNB_E_EMPTY_AGGREGATION, FNB_E_EMPTY_DATASET,
+  FNB_E_PARSE_ERROR, FNB_E_VERSION_UNSUPPORTED, FNB_E_LIMITS_TOO_SMALL,
+  FNB_E_CONFIG_ERROR, FNB_E_EVAL_ERROR
+};
+
+/* Built-in node functions (functions.hpp:17-21, 32). */
+enum fnb_act { FNB_ACT_IDENTITY = 0, FNB_ACT_TANH, FNB_ACT_SIGMOID, FNB_ACT_RELU, FNB_ACT_SIN };
+enum fnb_agg { FNB_AGG_SUM = 0, FNB_AGG_PRODUCT, FNB_AGG_MAX, FNB_AGG_MEAN };
+
+/* Fitness epilogues fused into the forward. */
+enum fnb_fitness {
+  FNB_FIT_NONE = 0,          /* outputs only                                 */
+  FNB_FIT_NEG_MSE = 1,       /* func-fit: -(1/(B*O)) sum (y - o)^2           */
+  FNB_FIT_OFFSET_SSE = 2     /* xor:      offset - sum (y - o)^2             */
+};
+
+/* GenomeLimits + input/output keys (genome.hpp:87-92, 151-152). */
+typedef struct fnb_shape {
+  int max_nodes;
+  int max_conns;
+  int num_inputs;
+  int num_outputs;
+  const int* input_keys;
+  const int* output_keys;
+} fnb_shape;
+
+/* AttributeSchema (genome.hpp:42-85) with names resolved to built-in codes. */
+typedef struct fnb_schema {
+  int n_act; int act[8];
+  int n_agg; int agg[8];
+  int default_act, default_agg;
+} fnb_schema;
+
+/* AttrMutation / MutationConfig / DistanceConfig (ops.hpp:117-140). */
+typedef struct fnb_attr_mutation {
+  double init_mean, init_std, mutate_power, mutate_rate, replace_rate;
+} fnb_attr_mutation;
+
+typedef struct fnb_mutation_config {
+  double node_add, node_delete, conn_add, conn_delete;
+  fnb_attr_mutation bias, response, weight;
+  double activation_replace_rate, aggregation_replace_rate;
+} fnb_mutation_config;
+
+typedef struct fnb_distance_config {
+  double compatibility_disjoint, compatibility_homologous;
+} fnb_distance_config;
+
+typedef struct fnb_ctx fnb_ctx;
+
+/* ---- context --------------------------------------------------------- */
+int fnb_abi_version(void);
+int fnb_ctx_create(const fnb_shape* shape, const fnb_schema* schema, int device, fnb_ctx** out);
+void fnb_ctx_destroy(fnb_ctx* ctx);
+const char* fnb_last_error(const fnb_ctx* ctx);
+int fnb_last_error_index(const fnb_ctx* ctx);
+/* bytes of one transformed network in the device net buffer */
+size_t fnb_net_bytes(const fnb_ctx* ctx);
+/* number of kernel launches this context issued since creation */
+long long fnb_launch_count(const fnb_ctx* ctx);
+
+/* ---- host layer (synchronous) ------------------------------------------ */
+
+/* transform() over a population (network.hpp:122-220).  order_out: P*max_nodes
+ * int32 rows, -1 padded (network.hpp:32); either output may be NULL. */
+int fnb_transform(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
+                  int32_t* order_out, int32_t* order_count_out);
+
+/* transform() + batch_forward() (network.hpp:294-330): out[P][B][O].
+ * inputs[B][I] sample-major like the reference; computed in FP32. */
+int fnb_batch_forward(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
+                      const double* inputs, int batch, double* out);
+
+/* transform + forward + fused fitness epilogue -> fitness[P] (FP64). */
+int fnb_evaluate(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
+                 const double* inputs, const double* targets, int batch, int fitness_kind,
+                 double fitness_offset, double* fitness_out);
+
+/* ---- device layer (asynchronous on `stream`, device pointers) ------------ */
+
+/* K1: d_nets must hold P * fnb_net_bytes(ctx) bytes. */
+int fnb_transform_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, int P,
+                    void* d_nets, void* stream);
+/* Copy the int32 topological order (network.hpp:32) out of the net buffer. */
+int fnb_net_order_d(fnb_ctx* ctx, const void* d_nets, int P, int32_t* d_order,
+                    int32_t* d_order_count, void* stream);
+/* Lowest failing genome (or -1) and its status; synchronises `stream` and
+ * fills fnb_last_error() with the reference-format message. */
+int fnb_check_nets_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns,
+                     const void* d_nets, int P, void* stream);
+/* K2: forward of P nets over X[B][I] (FP32); Y[B][O] targets for the fitness
+ * epilogue; d_out (P*B*O doubles) and d_fitness (P doubles) may be NULL. */
+int fnb_forward_d(fnb_ctx* ctx, const void* d_nets, int P, const float* d_X, const float* d_Y,
+                  int batch, int fitness_kind, double fitness_offset, double* d_fitness,
+                  double* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLATNEAT_B200_H */

@@ -1,0 +1,80 @@
+"""ctypes binding of libflatneat_b200.so (include/flatneat_b200.h).
+
+There is no fallback: if the CUDA library is missing or cannot be loaded,
+importing the package fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libflatneat_b200.so")
+
+
+class fnb_shape(C.Structure):
+    _fields_ = [("max_nodes", C.c_int), ("max_conns", C.c_int), ("num_inputs", C.c_int),
+                ("num_outputs", C.c_int), ("input_keys", C.POINTER(C.c_int)),
+                ("output_keys", C.POINTER(C.c_int))]
+
+
+class fnb_schema(C.Structure):
+    _fields_ = [("n_act", C.c_int), ("act", C.c_int * 8), ("n_agg", C.c_int), ("agg", C.c_int * 8),
+                ("default_act", C.c_int), ("default_agg", C.c_int)]
+
+
+class fnb_attr_mutation(C.Structure):
+    _fields_ = [("init_mean", C.c_double), ("init_std", C.c_double), ("mutate_power", C.c_double),
+                ("mutate_rate", C.c_double), ("replace_rate", C.c_double)]
+
+
+class fnb_mutation_config(C.Structure):
+    _fields_ = [("node_add", C.c_double), ("node_delete", C.c_double), ("conn_add", C.c_double),
+                ("conn_delete", C.c_double), ("bias", fnb_attr_mutation), ("response", fnb_attr_mutation),
+                ("weight", fnb_attr_mutation), ("activation_replace_rate", C.c_double),
+                ("aggregation_replace_rate", C.c_double)]
+
+
+class fnb_distance_config(C.Structure):
+    _fields_ = [("compatibility_disjoint", C.c_double), ("compatibility_homologous", C.c_double)]
+
+
+VP = C.c_void_p
+DP = C.POINTER(C.c_double)
+IP = C.POINTER(C.c_int32)
+U32P = C.POINTER(C.c_uint32)
+
+# name -> (restype, argtypes); every symbol include/flatneat_b200.h declares
+SIGNATURES = {
+    "fnb_abi_version": (C.c_int, []),
+    "fnb_ctx_create": (C.c_int, [C.POINTER(fnb_shape), C.POINTER(fnb_schema), C.c_int, C.POINTER(VP)]),
+    "fnb_ctx_destroy": (None, [VP]),
+    "fnb_last_error": (C.c_char_p, [VP]),
+    "fnb_last_error_index": (C.c_int, [VP]),
+    "fnb_net_bytes": (C.c_size_t, [VP]),
+    "fnb_launch_count": (C.c_longlong, [VP]),
+    "fnb_transform": (C.c_int, [VP, DP, DP, C.c_int, IP, IP]),
+    "fnb_batch_forward": (C.c_int, [VP, DP, DP, C.c_int, DP, C.c_int, DP]),
+    "fnb_evaluate": (C.c_int, [VP, DP, DP, C.c_int, DP, DP, C.c_int, C.c_int, C.c_double, DP]),
+    "fnb_transform_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP]),
+    "fnb_net_order_d": (C.c_int, [VP, VP, C.c_int, VP, VP, VP]),
+    "fnb_check_nets_d": (C.c_int, [VP, VP, VP, VP, C.c_int, VP]),
+    "fnb_forward_d": (C.c_int, [VP, VP, C.c_int, VP, VP, C.c_int, C.c_int, C.c_double, VP, VP, VP]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(the CUDA library is required; there is no CPU fallback)")
+        lib_ = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(lib_, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib_
+    return _lib

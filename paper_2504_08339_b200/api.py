@@ -1,0 +1,302 @@
+"""Host-side mirror of the reference flatneat API over the CUDA C ABI.
+
+Names and meanings follow /root/reference/proj/include/flatneat/:
+AttributeSchema / GenomeLimits / PopulationTensors (genome.hpp), transform /
+batch_forward / BatchResult (network.hpp), MutationConfig / DistanceConfig /
+InnovationTable semantics (ops.hpp) and Error / Errc (errors.hpp).  Failures
+raise FlatneatError carrying the reference's Errc name, its what() string
+and the lowest failing genome index (parallel.hpp:69-73).
+
+Two call styles:
+  * host arrays (numpy) -- synchronous, mirrors the reference free functions;
+  * device tensors (torch.cuda) -- asynchronous on the current stream, used by
+    the generation loop and the benchmark.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+ERRC = ["unknown_function", "genome_full", "duplicate_key", "duplicate_conn", "dangling_endpoint",
+        "key_not_found", "protected_node", "attr_out_of_range", "shape_mismatch", "corrupt_row",
+        "cycle_detected", "non_finite_input", "non_finite_state", "empty_aggregation", "empty_dataset",
+        "parse_error", "version_unsupported", "limits_too_small", "config_error", "eval_error"]
+
+ACTIVATIONS = {"identity": 0, "tanh": 1, "sigmoid": 2, "relu": 3, "sin": 4}   # functions.hpp:23-30
+AGGREGATIONS = {"sum": 0, "product": 1, "max": 2, "mean": 3}                  # functions.hpp:34-40
+
+FIT_NONE, FIT_NEG_MSE, FIT_OFFSET_SSE = 0, 1, 2
+NODE_COLS, CONN_COLS = 5, 4
+
+
+class FlatneatError(RuntimeError):
+    """flatneat::Error (errors.hpp:59-69): code name, what() and genome index."""
+
+    def __init__(self, status: int, what: str, index: int = -1):
+        self.code = ERRC[status - 1] if 1 <= status <= len(ERRC) else "unknown"
+        self.status = status
+        self.index = index
+        super().__init__(what or self.code)
+
+
+@dataclass
+class AttributeSchema:
+    """genome.hpp:42-85; registry order is significant."""
+    activations: Sequence[str] = ("tanh",)
+    aggregations: Sequence[str] = ("sum",)
+    default_activation: int = 0
+    default_aggregation: int = 0
+
+    def to_c(self) -> N.fnb_schema:
+        s = N.fnb_schema()
+        s.n_act = len(self.activations)
+        s.n_agg = len(self.aggregations)
+        for i, a in enumerate(self.activations):
+            if a not in ACTIVATIONS:
+                raise FlatneatError(1, f"unknown_function: activation '{a}' is not built in")
+            s.act[i] = ACTIVATIONS[a]
+        for i, a in enumerate(self.aggregations):
+            if a not in AGGREGATIONS:
+                raise FlatneatError(1, f"unknown_function: aggregation '{a}' is not built in")
+            s.agg[i] = AGGREGATIONS[a]
+        s.default_act = self.default_activation
+        s.default_agg = self.default_aggregation
+        return s
+
+
+@dataclass
+class GenomeLimits:
+    """genome.hpp:87-92"""
+    max_nodes: int = 50
+    max_conns: int = 100
+
+
+@dataclass
+class PopulationTensors:
+    """genome.hpp:315-338: pop_nodes [P, N, 5], pop_conns [P, C, 4], FP64, NaN padded."""
+    pop_nodes: np.ndarray
+    pop_conns: np.ndarray
+    input_keys: Sequence[int]
+    output_keys: Sequence[int]
+
+    @property
+    def pop_size(self) -> int:
+        return int(self.pop_nodes.shape[0])
+
+    @property
+    def limits(self) -> GenomeLimits:
+        return GenomeLimits(int(self.pop_nodes.shape[1]), int(self.pop_conns.shape[1]))
+
+
+@dataclass
+class AttrMutation:
+    """ops.hpp:117-123"""
+    init_mean: float = 0.0
+    init_std: float = 1.0
+    mutate_power: float = 0.5
+    mutate_rate: float = 0.7
+    replace_rate: float = 0.1
+
+    def to_c(self):
+        return N.fnb_attr_mutation(self.init_mean, self.init_std, self.mutate_power, self.mutate_rate,
+                                   self.replace_rate)
+
+
+@dataclass
+class MutationConfig:
+    """ops.hpp:125-135 (Appendix-A defaults)."""
+    node_add: float = 0.2
+    node_delete: float = 0.0
+    conn_add: float = 0.4
+    conn_delete: float = 0.0
+    bias: AttrMutation = field(default_factory=lambda: AttrMutation(0.0, 1.0, 0.5, 0.7, 0.1))
+    response: AttrMutation = field(default_factory=lambda: AttrMutation(1.0, 0.0, 0.0, 0.0, 0.0))
+    weight: AttrMutation = field(default_factory=lambda: AttrMutation(0.0, 1.0, 0.5, 0.8, 0.1))
+    activation_replace_rate: float = 0.0
+    aggregation_replace_rate: float = 0.0
+
+    def to_c(self):
+        return N.fnb_mutation_config(self.node_add, self.node_delete, self.conn_add, self.conn_delete,
+                                     self.bias.to_c(), self.response.to_c(), self.weight.to_c(),
+                                     self.activation_replace_rate, self.aggregation_replace_rate)
+
+
+@dataclass
+class DistanceConfig:
+    """ops.hpp:137-140"""
+    compatibility_disjoint: float = 1.0
+    compatibility_homologous: float = 0.5
+
+    def to_c(self):
+        return N.fnb_distance_config(self.compatibility_disjoint, self.compatibility_homologous)
+
+
+@dataclass
+class BatchResult:
+    """network.hpp:281-292: values[P][B][O]."""
+    values: np.ndarray
+
+    @property
+    def pop_size(self):
+        return self.values.shape[0]
+
+    @property
+    def batch(self):
+        return self.values.shape[1]
+
+    @property
+    def outputs(self):
+        return self.values.shape[2]
+
+    def at(self, p, b, o):
+        return float(self.values[p, b, o])
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(N.DP)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _stream_handle(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+class Engine:
+    """One CUDA context (fnb_ctx) for a fixed genome shape and schema."""
+
+    def __init__(self, limits: GenomeLimits, input_keys: Sequence[int], output_keys: Sequence[int],
+                 schema: AttributeSchema = AttributeSchema(), device: int = 0):
+        self.limits = limits
+        self.input_keys = list(input_keys)
+        self.output_keys = list(output_keys)
+        self.schema = schema
+        self.device = device
+        self._ik = (C.c_int * max(1, len(self.input_keys)))(*self.input_keys)
+        self._ok = (C.c_int * max(1, len(self.output_keys)))(*self.output_keys)
+        shape = N.fnb_shape(limits.max_nodes, limits.max_conns, len(self.input_keys), len(self.output_keys),
+                            self._ik, self._ok)
+        self._lib = N.lib()
+        h = C.c_void_p()
+        st = self._lib.fnb_ctx_create(C.byref(shape), C.byref(schema.to_c()), device, C.byref(h))
+        if st:
+            raise FlatneatError(st, f"{ERRC[st - 1]}: fnb_ctx_create failed")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.fnb_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- helpers -----------------------------------------------------------
+    @property
+    def num_inputs(self):
+        return len(self.input_keys)
+
+    @property
+    def num_outputs(self):
+        return len(self.output_keys)
+
+    @property
+    def net_bytes(self) -> int:
+        return int(self._lib.fnb_net_bytes(self._h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.fnb_launch_count(self._h))
+
+    def _raise(self, st: int):
+        if st:
+            what = self._lib.fnb_last_error(self._h).decode()
+            raise FlatneatError(st, what, int(self._lib.fnb_last_error_index(self._h)))
+
+    def _check_pop(self, pop_nodes, pop_conns):
+        n, c = _f64(pop_nodes), _f64(pop_conns)
+        P = n.shape[0]
+        if n.shape != (P, self.limits.max_nodes, NODE_COLS) or c.shape != (P, self.limits.max_conns, CONN_COLS):
+            raise FlatneatError(9, "shape_mismatch: population tensors do not match the engine limits")
+        return n, c, P
+
+    # -- host layer (network.hpp) -----------------------------------------------
+    def transform(self, pop_nodes, pop_conns):
+        """transform() of every genome (network.hpp:122-220) -> (order[P,N] int32 with -1 tail, order_count[P])."""
+        n, c, P = self._check_pop(pop_nodes, pop_conns)
+        order = np.empty((P, self.limits.max_nodes), dtype=np.int32)
+        cnt = np.empty(P, dtype=np.int32)
+        self._raise(self._lib.fnb_transform(self._h, _dp(n), _dp(c), P, order.ctypes.data_as(N.IP),
+                                            cnt.ctypes.data_as(N.IP)))
+        return order, cnt
+
+    def batch_forward(self, pop_nodes, pop_conns, inputs, batch: Optional[int] = None) -> BatchResult:
+        """transform() + batch_forward() (network.hpp:294-330); FP32 on the device."""
+        n, c, P = self._check_pop(pop_nodes, pop_conns)
+        x = _f64(inputs).reshape(-1)
+        B = batch if batch is not None else x.size // max(1, self.num_inputs)
+        if x.size != B * self.num_inputs:
+            raise FlatneatError(9, "shape_mismatch: input matrix is not batch x num_inputs")
+        out = np.empty((P, B, self.num_outputs), dtype=np.float64)
+        self._raise(self._lib.fnb_batch_forward(self._h, _dp(n), _dp(c), P, _dp(x), B, _dp(out)))
+        return BatchResult(out)
+
+    def evaluate(self, pop_nodes, pop_conns, inputs, targets, kind: int = FIT_NEG_MSE,
+                 offset: float = 0.0) -> np.ndarray:
+        """transform + forward + fused fitness -> fitness[P] (FP64)."""
+        n, c, P = self._check_pop(pop_nodes, pop_conns)
+        x = _f64(inputs).reshape(-1)
+        y = _f64(targets).reshape(-1)
+        B = x.size // max(1, self.num_inputs)
+        if x.size != B * self.num_inputs or y.size != B * self.num_outputs:
+            raise FlatneatError(9, "shape_mismatch: inputs/targets are not batch x I / batch x O")
+        fit = np.empty(P, dtype=np.float64)
+        self._raise(self._lib.fnb_evaluate(self._h, _dp(n), _dp(c), P, _dp(x), _dp(y), B, kind, offset, _dp(fit)))
+        return fit
+
+    # -- device layer (torch tensors, current stream) -----------------------------
+    def alloc_nets(self, P: int):
+        import torch
+        return torch.empty(P * self.net_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def transform_d(self, nodes, conns, nets=None, stream=None):
+        P = nodes.shape[0]
+        if nets is None:
+            nets = self.alloc_nets(P)
+        self._raise(self._lib.fnb_transform_d(self._h, nodes.data_ptr(), conns.data_ptr(), P, nets.data_ptr(),
+                                              _stream_handle(stream)))
+        return nets
+
+    def check_nets_d(self, nodes, conns, nets, stream=None):
+        self._raise(self._lib.fnb_check_nets_d(self._h, nodes.data_ptr(), conns.data_ptr(), nets.data_ptr(),
+                                               nodes.shape[0], _stream_handle(stream)))
+
+    def net_order_d(self, nets, P, stream=None):
+        import torch
+        order = torch.empty((P, self.limits.max_nodes), dtype=torch.int32, device=nets.device)
+        cnt = torch.empty(P, dtype=torch.int32, device=nets.device)
+        self._raise(self._lib.fnb_net_order_d(self._h, nets.data_ptr(), P, order.data_ptr(), cnt.data_ptr(),
+                                              _stream_handle(stream)))
+        return order, cnt
+
+    def forward_d(self, nets, P: int, X, Y=None, kind: int = FIT_NONE, offset: float = 0.0, fitness=None,
+                  out=None, stream=None):
+        B = X.shape[0]
+        self._raise(self._lib.fnb_forward_d(self._h, nets.data_ptr(), P, X.data_ptr(),
+                                            Y.data_ptr() if Y is not None else None, B, kind, offset,
+                                            fitness.data_ptr() if fitness is not None else None,
+                                            out.data_ptr() if out is not None else None, _stream_handle(stream)))
+        return fitness if fitness is not None else out

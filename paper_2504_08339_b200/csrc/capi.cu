@@ -1,0 +1,350 @@
+// capi.cu -- extern "C" boundary (include/flatneat_b200.h): contexts, the
+// synchronous host layer mirroring the reference free functions, and the
+// asynchronous device layer.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fnb_common.cuh"
+
+namespace fnb {
+// host launchers (transform.cu / forward.cu)
+cudaError_t launch_transform(const double* n, const double* c, int P, uint8_t* nets, const NetLayout& L,
+                             const DevShape& sh, cudaStream_t st);
+cudaError_t launch_describe_cycle(const double* n, const double* c, const uint8_t* net, const NetLayout& L,
+                                  int* path, cudaStream_t st);
+cudaError_t launch_first_error(const uint8_t* nets, size_t stride, int P, int* out, cudaStream_t st);
+cudaError_t launch_net_order(const uint8_t* nets, const NetLayout& L, int P, int32_t* order, int32_t* count,
+                             cudaStream_t st);
+int launch_forward(const void* nets, NetLayout L, int P, const float* X, const float* Y, int B,
+                   int fit_kind, double offset, double* fitness, double* out, double* partial_buf,
+                   size_t partial_cap, cudaStream_t st, long long* launches);
+size_t forward_partial_needed(NetLayout L, int P, int B);
+cudaError_t launch_to_float(const double* src, float* dst, size_t n, int* bad, cudaStream_t st);
+}  // namespace fnb
+
+using namespace fnb;
+
+namespace {
+
+const char* errc_name(int c) {  // errors.hpp:33-57
+  static const char* names[] = {
+      "unknown_function", "genome_full", "duplicate_key", "duplicate_conn",
+      "dangling_endpoint", "key_not_found", "protected_node", "attr_out_of_range",
+      "shape_mismatch", "corrupt_row", "cycle_detected", "non_finite_input",
+      "non_finite_state", "empty_aggregation", "empty_dataset", "parse_error",
+      "version_unsupported", "limits_too_small", "config_error", "eval_error"};
+  return (c >= 0 && c < 20) ? names[c] : "unknown";
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct fnb_ctx {
+  int device = 0;
+  DevShape sh{};
+  NetLayout L{0, 0, 0, 0};
+  std::string err;
+  int err_index = -1;
+  long long launches = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc;
+};
+
+static int fnb_cuda_fail_ctx(fnb_ctx* ctx, cudaError_t e, const char* what) {
+  if (ctx) {
+    ctx->err = std::string("eval_error: CUDA ") + cudaGetErrorString(e) + " at " + what;
+    ctx->err_index = -1;
+  }
+  return 1 + FNB_E_EVAL_ERROR;
+}
+
+#define CK(expr)                                                 \
+  do {                                                           \
+    cudaError_t e_ = (expr);                                     \
+    if (e_ != cudaSuccess) return fnb_cuda_fail_ctx(ctx, e_, #expr); \
+  } while (0)
+
+static int set_err(fnb_ctx* ctx, int code, const std::string& detail, int index) {
+  ctx->err = std::string(errc_name(code)) + ": " + detail;
+  ctx->err_index = index;
+  return 1 + code;
+}
+
+extern "C" {
+
+int fnb_abi_version(void) { return FNB_ABI_VERSION; }
+
+int fnb_ctx_create(const fnb_shape* shape, const fnb_schema* schema, int device, fnb_ctx** out) {
+  if (!shape || !schema || !out) return 1 + FNB_E_CONFIG_ERROR;
+  *out = nullptr;
+  if (shape->max_nodes < 1 || shape->max_nodes > FNB_MAX_NODES_LIMIT || shape->max_conns < 1 ||
+      shape->max_conns > 65535 || shape->num_inputs < 0 || shape->num_inputs > 32 ||
+      shape->num_outputs < 0 || shape->num_outputs > 32)
+    return 1 + FNB_E_LIMITS_TOO_SMALL;
+  if (schema->n_act < 1 || schema->n_act > 8 || schema->n_agg < 1 || schema->n_agg > 8)
+    return 1 + FNB_E_CONFIG_ERROR;
+  for (int i = 0; i < schema->n_act; ++i)
+    if (schema->act[i] < FNB_ACT_IDENTITY || schema->act[i] > FNB_ACT_SIN) return 1 + FNB_E_UNKNOWN_FUNCTION;
+  for (int i = 0; i < schema->n_agg; ++i)
+    if (schema->agg[i] < FNB_AGG_SUM || schema->agg[i] > FNB_AGG_MEAN) return 1 + FNB_E_UNKNOWN_FUNCTION;
+  auto* ctx = new fnb_ctx();
+  ctx->device = device;
+  DevShape& sh = ctx->sh;
+  sh.N = shape->max_nodes;
+  sh.C = shape->max_conns;
+  sh.I = shape->num_inputs;
+  sh.O = shape->num_outputs;
+  sh.n_act = schema->n_act;
+  sh.n_agg = schema->n_agg;
+  for (int i = 0; i < 8; ++i) {
+    sh.act[i] = uint8_t(i < schema->n_act ? schema->act[i] : 0);
+    sh.agg[i] = uint8_t(i < schema->n_agg ? schema->agg[i] : 0);
+  }
+  sh.default_act = schema->default_act;
+  sh.default_agg = schema->default_agg;
+  for (int i = 0; i < sh.I; ++i) sh.input_keys[i] = shape->input_keys[i];
+  for (int i = 0; i < sh.O; ++i) sh.output_keys[i] = shape->output_keys[i];
+  ctx->L = NetLayout(sh.N, sh.C, sh.I, sh.O);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return 1 + FNB_E_EVAL_ERROR;
+  }
+  *out = ctx;
+  return 0;
+}
+
+void fnb_ctx_destroy(fnb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (DevBuf* b : {&ctx->nodes, &ctx->conns, &ctx->nets, &ctx->X, &ctx->Y, &ctx->fit, &ctx->out,
+                    &ctx->partial, &ctx->misc})
+    b->release();
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* fnb_last_error(const fnb_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+int fnb_last_error_index(const fnb_ctx* ctx) { return ctx ? ctx->err_index : -1; }
+size_t fnb_net_bytes(const fnb_ctx* ctx) { return ctx ? ctx->L.bytes : 0; }
+long long fnb_launch_count(const fnb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- device layer ------------------------------------------------------
+
+int fnb_transform_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, int P, void* d_nets,
+                    void* stream) {
+  if (P <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_transform(d_nodes, d_conns, P, static_cast<uint8_t*>(d_nets), ctx->L, ctx->sh,
+                      static_cast<cudaStream_t>(stream)));
+  ctx->launches++;
+  return 0;
+}
+
+int fnb_net_order_d(fnb_ctx* ctx, const void* d_nets, int P, int32_t* d_order, int32_t* d_count,
+                    void* stream) {
+  if (P <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_net_order(static_cast<const uint8_t*>(d_nets), ctx->L, P, d_order, d_count,
+                      static_cast<cudaStream_t>(stream)));
+  ctx->launches++;
+  return 0;
+}
+
+int fnb_check_nets_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, const void* d_nets,
+                     int P, void* stream) {
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (P <= 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  const int N = ctx->L.N;
+  CK(ctx->misc.ensure(sizeof(int) * size_t(N + 8)));
+  int* d_first = static_cast<int*>(ctx->misc.p);
+  const int big = 0x7fffffff;
+  CK(cudaMemcpyAsync(d_first, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  CK(launch_first_error(static_cast<const uint8_t*>(d_nets), ctx->L.bytes, P, d_first, st));
+  ctx->launches++;
+  int first = big;
+  CK(cudaMemcpyAsync(&first, d_first, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (first == big) return 0;
+  NetHeader h;
+  const uint8_t* net = static_cast<const uint8_t*>(d_nets) + size_t(first) * ctx->L.bytes;
+  CK(cudaMemcpy(&h, net, sizeof(h), cudaMemcpyDeviceToHost));
+  const int code = h.status - 1;
+  char buf[64];
+  switch (h.err_kind) {
+    case kErrActId: std::snprintf(buf, sizeof buf, "activation id %d out of range", h.err_a); break;
+    case kErrAggId: std::snprintf(buf, sizeof buf, "aggregation id %d out of range", h.err_a); break;
+    case kErrInputKey: std::snprintf(buf, sizeof buf, "input key %d", h.err_a); break;
+    case kErrOutputKey: std::snprintf(buf, sizeof buf, "output key %d", h.err_a); break;
+    case kErrConn: std::snprintf(buf, sizeof buf, "conn (%d, %d)", h.err_a, h.err_b); break;
+    case kErrCycle: {
+      int* d_path = d_first + 1;
+      CK(launch_describe_cycle(d_nodes + size_t(first) * N * kNodeCols,
+                               d_conns + size_t(first) * ctx->L.C * kConnCols, net, ctx->L, d_path, st));
+      ctx->launches++;
+      std::vector<int> path(size_t(N) + 2);
+      CK(cudaMemcpyAsync(path.data(), d_path, sizeof(int) * (size_t(N) + 2), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::string s = "cycle ";
+      if (path[0] < 0) {
+        s += "unlocatable cycle";
+      } else {
+        for (int i = 0; i < path[0]; ++i) {
+          if (i) s += "->";
+          s += std::to_string(path[1 + i]);
+        }
+      }
+      return set_err(ctx, code, s, first);
+    }
+    default: std::snprintf(buf, sizeof buf, "status %d", h.status);
+  }
+  return set_err(ctx, code, buf, first);
+}
+
+int fnb_forward_d(fnb_ctx* ctx, const void* d_nets, int P, const float* d_X, const float* d_Y, int batch,
+                  int fitness_kind, double fitness_offset, double* d_fitness, double* d_out, void* stream) {
+  if (P <= 0 || batch <= 0) return 0;
+  if (fitness_kind != FNB_FIT_NONE && (!d_Y || !d_fitness)) return set_err(ctx, FNB_E_CONFIG_ERROR, "fitness needs targets and output", -1);
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->partial.ensure(forward_partial_needed(ctx->L, P, batch)));
+  return launch_forward(d_nets, ctx->L, P, d_X, d_Y, batch, fitness_kind, fitness_offset, d_fitness, d_out,
+                        static_cast<double*>(ctx->partial.p), ctx->partial.cap,
+                        static_cast<cudaStream_t>(stream), &ctx->launches)
+             ? fnb_cuda_fail_ctx(ctx, cudaGetLastError(), "forward launch")
+             : 0;
+}
+
+// ---- host layer ----------------------------------------------------------
+
+static int upload_pop(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P) {
+  const size_t nb = sizeof(double) * size_t(P) * ctx->L.N * kNodeCols;
+  const size_t cb = sizeof(double) * size_t(P) * ctx->L.C * kConnCols;
+  CK(ctx->nodes.ensure(nb));
+  CK(ctx->conns.ensure(cb));
+  CK(ctx->nets.ensure(ctx->L.bytes * size_t(P)));
+  CK(cudaMemcpyAsync(ctx->nodes.p, pop_nodes, nb, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->conns.p, pop_conns, cb, cudaMemcpyHostToDevice, ctx->stream));
+  return 0;
+}
+
+static int transform_and_check(fnb_ctx* ctx, int P) {
+  int st = fnb_transform_d(ctx, static_cast<double*>(ctx->nodes.p), static_cast<double*>(ctx->conns.p), P,
+                           ctx->nets.p, ctx->stream);
+  if (st) return st;
+  return fnb_check_nets_d(ctx, static_cast<double*>(ctx->nodes.p), static_cast<double*>(ctx->conns.p),
+                          ctx->nets.p, P, ctx->stream);
+}
+
+int fnb_transform(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P, int32_t* order_out,
+                  int32_t* order_count_out) {
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (P <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  int st = upload_pop(ctx, pop_nodes, pop_conns, P);
+  if (!st) st = transform_and_check(ctx, P);
+  if (st) return st;
+  if (order_out || order_count_out) {
+    const size_t ob = sizeof(int32_t) * size_t(P) * ctx->L.N, cb = sizeof(int32_t) * size_t(P);
+    CK(ctx->out.ensure(ob + cb));
+    int32_t* d_order = static_cast<int32_t*>(ctx->out.p);
+    int32_t* d_cnt = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ctx->out.p) + ob);
+    st = fnb_net_order_d(ctx, ctx->nets.p, P, d_order, d_cnt, ctx->stream);
+    if (st) return st;
+    if (order_out) CK(cudaMemcpyAsync(order_out, d_order, ob, cudaMemcpyDeviceToHost, ctx->stream));
+    if (order_count_out) CK(cudaMemcpyAsync(order_count_out, d_cnt, cb, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return 0;
+}
+
+static int upload_floats(fnb_ctx* ctx, DevBuf& dst, const double* src, size_t n, bool check_finite) {
+  // doubles go up as-is and are narrowed on the device (no host-side pass)
+  CK(dst.ensure(n * sizeof(float) + n * sizeof(double) + 16));
+  double* d_tmp = reinterpret_cast<double*>(static_cast<uint8_t*>(dst.p) + ((n * sizeof(float) + 15) & ~size_t(15)));
+  CK(cudaMemcpyAsync(d_tmp, src, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(ctx->misc.ensure(sizeof(int) * size_t(ctx->L.N + 8)));
+  int* d_bad = static_cast<int*>(ctx->misc.p);
+  CK(cudaMemsetAsync(d_bad, 0, sizeof(int), ctx->stream));
+  CK(launch_to_float(d_tmp, static_cast<float*>(dst.p), n, d_bad, ctx->stream));
+  ctx->launches++;
+  if (check_finite) {
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (bad) return set_err(ctx, FNB_E_NON_FINITE_INPUT, "input not finite", 0);  // network.hpp:245-246
+  }
+  return 0;
+}
+
+static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
+                         const double* inputs, const double* targets, int batch, int kind, double offset,
+                         double* fitness_out, double* out) {
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (P <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  int st = upload_pop(ctx, pop_nodes, pop_conns, P);
+  if (!st) st = transform_and_check(ctx, P);
+  if (!st) st = upload_floats(ctx, ctx->X, inputs, size_t(batch) * ctx->L.I, true);
+  if (!st && kind != FNB_FIT_NONE) st = upload_floats(ctx, ctx->Y, targets, size_t(batch) * ctx->L.O, false);
+  if (st) return st;
+  double* d_out = nullptr;
+  double* d_fit = nullptr;
+  if (out) {
+    CK(ctx->out.ensure(sizeof(double) * size_t(P) * batch * ctx->L.O));
+    d_out = static_cast<double*>(ctx->out.p);
+  }
+  if (kind != FNB_FIT_NONE) {
+    CK(ctx->fit.ensure(sizeof(double) * size_t(P)));
+    d_fit = static_cast<double*>(ctx->fit.p);
+  }
+  st = fnb_forward_d(ctx, ctx->nets.p, P, static_cast<float*>(ctx->X.p),
+                     kind != FNB_FIT_NONE ? static_cast<float*>(ctx->Y.p) : nullptr, batch, kind, offset, d_fit,
+                     d_out, ctx->stream);
+  if (st) return st;
+  if (out)
+    CK(cudaMemcpyAsync(out, d_out, sizeof(double) * size_t(P) * batch * ctx->L.O, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  if (fitness_out) CK(cudaMemcpyAsync(fitness_out, d_fit, sizeof(double) * size_t(P), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int fnb_batch_forward(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
+                      const double* inputs, int batch, double* out) {
+  return evaluate_impl(ctx, pop_nodes, pop_conns, P, inputs, nullptr, batch, FNB_FIT_NONE, 0.0, nullptr, out);
+}
+
+int fnb_evaluate(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P, const double* inputs,
+                 const double* targets, int batch, int fitness_kind, double fitness_offset, double* fitness_out) {
+  if (fitness_kind == FNB_FIT_NONE) return set_err(ctx, FNB_E_CONFIG_ERROR, "fitness kind required", -1);
+  return evaluate_impl(ctx, pop_nodes, pop_conns, P, inputs, targets, batch, fitness_kind, fitness_offset,
+                       fitness_out, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// fnb_common.cuh -- device-side layout shared by the sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "flatneat_b200.h"
+
+namespace fnb {
+
+// Row layout of the reference tensors (genome.hpp:19-38).
+constexpr int kNodeCols = 5, kConnCols = 4;
+constexpr int kKey = 0, kBias = 1, kResp = 2, kAgg = 3, kAct = 4;
+constexpr int kIn = 0, kOut = 1, kEn = 2, kW = 3;
+
+// Error detail kinds written by K1 next to the status (for the reference
+// what() strings of network.hpp:147-178, 216-218).
+enum ErrKind : int32_t {
+  kErrNone = 0,
+  kErrActId = 1,       // "activation id %d out of range"
+  kErrAggId = 2,       // "aggregation id %d out of range"
+  kErrInputKey = 3,    // "input key %d"
+  kErrOutputKey = 4,   // "output key %d"
+  kErrConn = 5,        // "conn (%d, %d)"
+  kErrCycle = 6,       // "cycle <path>" (path rebuilt by the describe kernel)
+};
+
+// ---- transformed network (one fixed-stride block per genome in HBM) ------
+// Compact replacement of TransformedNetwork (network.hpp:29-67): the dense
+// max_nodes^2 `expanded` tensor is never materialised; each node op carries
+// its incoming edges in ascending source row, the accumulation order of
+// network.hpp:184-190.
+struct NetHeader {          // 32 B
+  int32_t status;           // 0 or 1 + Errc
+  int32_t err_kind;
+  int32_t err_a, err_b;
+  int16_t order_count;
+  int16_t n_ops;            // non-input rows in order
+  int16_t n_edges;
+  int16_t pad0;
+  int32_t pad1, pad2;
+};
+static_assert(sizeof(NetHeader) == 32, "header");
+
+struct Op {                 // 16 B, one per non-input node in topological order
+  float bias;
+  float resp;
+  uint16_t dst;             // node row
+  uint16_t e_begin;
+  uint16_t e_end;
+  uint8_t act;              // built-in code (fnb_act)
+  uint8_t agg;              // built-in code (fnb_agg)
+};
+static_assert(sizeof(Op) == 16, "op");
+
+struct Edge {               // 8 B
+  float w;
+  uint16_t src;             // source node row
+  uint16_t conn_row;        // connection row the weight came from
+};
+static_assert(sizeof(Edge) == 8, "edge");
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct NetLayout {
+  int N, C, I, O;
+  size_t ops_off, edges_off, order_off, in_off, out_off, bytes;
+  __host__ __device__ NetLayout() : NetLayout(0, 0, 0, 0) {}
+  __host__ __device__ NetLayout(int n, int c, int i, int o) : N(n), C(c), I(i), O(o) {
+    ops_off = sizeof(NetHeader);
+    edges_off = align16(ops_off + size_t(N) * sizeof(Op));
+    order_off = align16(edges_off + size_t(C) * sizeof(Edge));
+    in_off = align16(order_off + size_t(N) * sizeof(uint16_t));
+    out_off = in_off + size_t(I) * sizeof(uint16_t);
+    bytes = align16(out_off + size_t(O) * sizeof(uint16_t));
+  }
+};
+
+// Schema + shape constants passed by value to kernels.
+struct DevShape {
+  int N, C, I, O;
+  int n_act, n_agg;
+  uint8_t act[8];
+  uint8_t agg[8];
+  int default_act, default_agg;
+  int input_keys[32];
+  int output_keys[32];
+};
+
+}  // namespace fnb
+
+#define FNB_CUDA_OK(expr)                                   \
+  do {                                                      \
+    cudaError_t fnb_e_ = (expr);                            \
+    if (fnb_e_ != cudaSuccess) return fnb_cuda_fail(fnb_e_, #expr); \
+  } while (0)

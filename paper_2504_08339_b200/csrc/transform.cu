@@ -1,0 +1,450 @@
+// transform.cu -- K1: per-genome transform (network.hpp:122-220) on sm_100a.
+//
+// One warp per genome.  The reference builds a dense max_nodes^2 `expanded`
+// tensor, runs Kahn's algorithm with a sorted ready list and keeps per-row
+// incoming lists; here the enabled graph lives in a per-warp shared-memory
+// predecessor bitset (max_nodes bits per row), the min-(key,row) pop of
+// network.hpp:192-214 is a warp __reduce_min over node ranks, and the output
+// is the compact op/edge program of fnb_common.cuh.  Semantics kept bit for
+// bit: error precedence (act id, agg id per row; inputs; outputs; conn rows;
+// cycle), duplicate keys resolving to the lowest row (lower_bound over
+// (key,row), network.hpp:57-63), in-degree counting per enabled ROW while
+// Kahn decrements per distinct cell (so duplicate enabled pairs and NaN
+// weights block their target exactly like the reference), the
+// initial-ready `key >= 0` filter (network.hpp:195), and incoming edges in
+// ascending source row (network.hpp:184-190).
+#include "fnb_common.cuh"
+
+namespace fnb {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+struct TfSmem {
+  long long* kr;        // [N] (key << 8 | row) or INT64_MAX for empty rows
+  int* sorted_key;      // [N]
+  int* R;               // [N] enabled rows per destination
+  uint32_t* pred;       // [N * W]
+  uint16_t* row_of_rank;// [N]
+  uint16_t* rank;       // [N]
+  uint16_t* order;      // [N]
+  uint16_t* ebeg;       // [N] edge begin of the op writing row r
+  uint8_t* flags;       // [N] bit0 non-empty, bit1 input
+  int16_t* csrc;        // [C]
+  int16_t* cdst;        // [C] destination row of an enabled finite edge, else -1
+};
+
+__host__ __device__ inline size_t tf_smem_bytes(int N, int C, int W) {
+  size_t b = 0;
+  b += align16(size_t(N) * 8);           // kr
+  b += align16(size_t(N) * 4);           // sorted_key
+  b += align16(size_t(N) * 4);           // R
+  b += align16(size_t(N) * W * 4);       // pred
+  b += align16(size_t(N) * 2) * 4;       // row_of_rank, rank, order, ebeg
+  b += align16(size_t(N));               // flags
+  b += align16(size_t(C) * 2) * 2;       // csrc, cdst
+  return b;
+}
+
+__device__ inline TfSmem tf_carve(uint8_t* p, int N, int C, int W) {
+  TfSmem s;
+  s.kr = reinterpret_cast<long long*>(p); p += align16(size_t(N) * 8);
+  s.sorted_key = reinterpret_cast<int*>(p); p += align16(size_t(N) * 4);
+  s.R = reinterpret_cast<int*>(p); p += align16(size_t(N) * 4);
+  s.pred = reinterpret_cast<uint32_t*>(p); p += align16(size_t(N) * W * 4);
+  s.row_of_rank = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
+  s.rank = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
+  s.order = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
+  s.ebeg = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
+  s.flags = p; p += align16(size_t(N));
+  s.csrc = reinterpret_cast<int16_t*>(p); p += align16(size_t(C) * 2);
+  s.cdst = reinterpret_cast<int16_t*>(p);
+  return s;
+}
+
+// lower_bound over the sorted keys; row of the first (key,row) or -1
+// (TransformedNetwork::row_of_key, network.hpp:57-63).
+__device__ inline int tf_lookup(const TfSmem& s, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (s.sorted_key[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return (lo < n && s.sorted_key[lo] == key) ? int(s.row_of_rank[lo]) : -1;
+}
+
+__device__ inline void tf_fail(uint8_t* net, int status, int kind, int a, int b,
+                               int order_count) {
+  NetHeader* h = reinterpret_cast<NetHeader*>(net);
+  h->status = status;
+  h->err_kind = kind;
+  h->err_a = a;
+  h->err_b = b;
+  h->order_count = int16_t(order_count);
+  h->n_ops = 0;
+  h->n_edges = 0;
+}
+
+template <int W>
+__global__ void __launch_bounds__(128)
+k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, int P,
+            uint8_t* __restrict__ nets, NetLayout L, DevShape sh, size_t smem_per_warp) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (g >= P) return;
+  const int N = sh.N, C = sh.C;
+  TfSmem s = tf_carve(smem_raw + size_t(warp) * smem_per_warp, N, C, W);
+  const double* nrow = nodes + size_t(g) * N * kNodeCols;
+  const double* crow = conns + size_t(g) * C * kConnCols;
+  uint8_t* net = nets + size_t(g) * L.bytes;
+
+  // ---- 1. node rows: keys, activation/aggregation ids (network.hpp:139-152)
+  int populated = 0;
+  for (int r0 = 0; r0 < N; r0 += 32) {
+    const int r = r0 + lane;
+    int bad = kErrNone, badid = 0;
+    bool ne = false;
+    if (r < N) {
+      const double k = nrow[r * kNodeCols + kKey];
+      ne = !isnan(k);
+      long long kr = 0x7fffffffffffffffll;
+      if (ne) {
+        const int key = int(k);
+        kr = (static_cast<long long>(key) << 8) | r;
+        const int act = int(nrow[r * kNodeCols + kAct]);
+        const int agg = int(nrow[r * kNodeCols + kAgg]);
+        if (act < 0 || act >= sh.n_act) { bad = kErrActId; badid = act; }
+        else if (agg < 0 || agg >= sh.n_agg) { bad = kErrAggId; badid = agg; }
+      }
+      s.kr[r] = kr;
+      s.flags[r] = ne ? 1 : 0;
+      s.R[r] = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) s.pred[r * W + w] = 0u;
+    }
+    const unsigned m = __ballot_sync(kFull, bad != kErrNone);
+    if (m) {
+      const int l = __ffs(m) - 1;
+      const int kind = __shfl_sync(kFull, bad, l);
+      const int id = __shfl_sync(kFull, badid, l);
+      if (lane == 0) tf_fail(net, 1 + FNB_E_UNKNOWN_FUNCTION, kind, id, 0, 0);
+      return;
+    }
+    populated += __popc(__ballot_sync(kFull, ne));
+  }
+  __syncwarp();
+
+  // ---- 2. ranks of (key,row): the Kahn priority and the key_to_row sort
+  for (int r = lane; r < N; r += 32) {
+    const long long mine = s.kr[r];
+    if (mine == 0x7fffffffffffffffll) continue;
+    int rk = 0;
+    for (int q = 0; q < N; ++q) rk += (s.kr[q] < mine) ? 1 : 0;
+    s.rank[r] = uint16_t(rk);
+    s.row_of_rank[rk] = uint16_t(r);
+    s.sorted_key[rk] = int(mine >> 8);
+  }
+  __syncwarp();
+
+  // ---- 3. inputs then outputs (network.hpp:155-165)
+  uint16_t* in_rows = reinterpret_cast<uint16_t*>(net + L.in_off);
+  uint16_t* out_rows = reinterpret_cast<uint16_t*>(net + L.out_off);
+  for (int pass = 0; pass < 2; ++pass) {
+    const int n = pass == 0 ? sh.I : sh.O;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      int row = 0, key = 0;
+      if (i < n) {
+        key = pass == 0 ? sh.input_keys[i] : sh.output_keys[i];
+        row = tf_lookup(s, populated, key);
+      }
+      const unsigned m = __ballot_sync(kFull, i < n && row < 0);
+      if (m) {
+        const int l = __ffs(m) - 1;
+        const int k = __shfl_sync(kFull, key, l);
+        if (lane == 0)
+          tf_fail(net, 1 + FNB_E_DANGLING_ENDPOINT, pass == 0 ? kErrInputKey : kErrOutputKey, k, 0, 0);
+        return;
+      }
+      if (i < n) {
+        if (pass == 0) { in_rows[i] = uint16_t(row); s.flags[row] |= 2; }
+        else out_rows[i] = uint16_t(row);
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- 4. connection rows: dangling check, in-degree, predecessor bits
+  //         (network.hpp:167-183)
+  for (int r0 = 0; r0 < C; r0 += 32) {
+    const int r = r0 + lane;
+    double cin = __longlong_as_double(0x7ff8000000000000ll), cout = 0, en = 0, w = 0;
+    if (r < C) {
+      const double2 a = *reinterpret_cast<const double2*>(crow + r * kConnCols);
+      const double2 b = *reinterpret_cast<const double2*>(crow + r * kConnCols + 2);
+      cin = a.x; cout = a.y; en = b.x; w = b.y;
+    }
+    const bool ne = !isnan(cin);
+    int src = -1, dst = -1;
+    if (ne) {
+      src = tf_lookup(s, populated, int(cin));
+      dst = tf_lookup(s, populated, int(cout));
+    }
+    const bool bad = ne && (src < 0 || dst < 0);
+    const unsigned m = __ballot_sync(kFull, bad);
+    if (m) {
+      const int l = __ffs(m) - 1;
+      const int a = __shfl_sync(kFull, ne ? int(cin) : 0, l);
+      const int b = __shfl_sync(kFull, ne ? int(cout) : 0, l);
+      if (lane == 0) tf_fail(net, 1 + FNB_E_DANGLING_ENDPOINT, kErrConn, a, b, 0);
+      return;
+    }
+    if (r < C) {
+      const bool edge = ne && en == 1.0;
+      int16_t d = -1;
+      if (edge) {
+        atomicAdd(&s.R[dst], 1);
+        if (!isnan(w)) {
+          atomicOr(&s.pred[dst * W + (src >> 5)], 1u << (src & 31));
+          d = int16_t(dst);
+        }
+      }
+      s.csrc[r] = int16_t(src);
+      s.cdst[r] = d;
+    }
+  }
+  __syncwarp();
+
+  // ---- 5. Kahn with min-(key,row) pop (network.hpp:192-214)
+  constexpr int NJ = W;  // rows per lane (N <= 32*W)
+  int cnt[NJ];
+  unsigned rk[NJ];
+  unsigned live = 0;     // bit j: eligible and not yet emitted
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int r = lane + 32 * j;
+    cnt[j] = 0;
+    rk[j] = 0xffffffffu;
+    if (r < N && (s.flags[r] & 1)) {
+      int pc = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) pc += __popc(s.pred[r * W + w]);
+      const int R = s.R[r];
+      const int key = int(s.kr[r] >> 8);
+      if (R == pc && (key >= 0 || R > 0)) live |= 1u << j;
+      cnt[j] = pc;
+      rk[j] = s.rank[r];
+    }
+  }
+  int count = 0;
+  for (;;) {
+    unsigned best = 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      if (((live >> j) & 1u) && cnt[j] == 0) best = min(best, rk[j]);
+    best = __reduce_min_sync(kFull, best);
+    if (best == 0xffffffffu) break;
+    const int u = s.row_of_rank[best];
+    if (lane == 0) s.order[count] = uint16_t(u);
+    ++count;
+    const int uw = u >> 5;
+    const uint32_t ub = 1u << (u & 31);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      if (!((live >> j) & 1u)) continue;
+      if (rk[j] == best) { live &= ~(1u << j); continue; }
+      const int r = lane + 32 * j;
+      if (s.pred[r * W + uw] & ub) --cnt[j];
+    }
+  }
+  __syncwarp();
+  uint16_t* gorder = reinterpret_cast<uint16_t*>(net + L.order_off);
+  for (int p = lane; p < count; p += 32) gorder[p] = s.order[p];
+  if (count != populated) {  // network.hpp:216-218; path rebuilt by k_describe
+    if (lane == 0) tf_fail(net, 1 + FNB_E_CYCLE_DETECTED, kErrCycle, 0, 0, count);
+    return;
+  }
+
+  // ---- 6. ops in topological order, skipping input rows (network.hpp:252-254)
+  Op* gops = reinterpret_cast<Op*>(net + L.ops_off);
+  int op_base = 0, edge_base = 0;
+  for (int p0 = 0; p0 < count; p0 += 32) {
+    const int p = p0 + lane;
+    int row = 0, ne = 0;
+    bool is_op = false;
+    if (p < count) {
+      row = s.order[p];
+      is_op = !(s.flags[row] & 2);
+      if (is_op) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) ne += __popc(s.pred[row * W + w]);
+      }
+    }
+    const unsigned m = __ballot_sync(kFull, is_op);
+    const int op = op_base + __popc(m & ((1u << lane) - 1u));
+    // inclusive scan of edge counts within the chunk
+    int incl = ne;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const int eb = edge_base + incl - ne;
+    if (is_op) {
+      Op o;
+      o.bias = float(nrow[row * kNodeCols + kBias]);
+      o.resp = float(nrow[row * kNodeCols + kResp]);
+      o.dst = uint16_t(row);
+      o.e_begin = uint16_t(eb);
+      o.e_end = uint16_t(eb + ne);
+      o.act = sh.act[int(nrow[row * kNodeCols + kAct])];
+      o.agg = sh.agg[int(nrow[row * kNodeCols + kAgg])];
+      gops[op] = o;
+      s.ebeg[row] = uint16_t(eb);
+    }
+    op_base += __popc(m);
+    edge_base += __shfl_sync(kFull, incl, 31);
+  }
+  __syncwarp();
+
+  // ---- 7. edges: slot = op edge begin + rank of src among dst's predecessors
+  Edge* gedges = reinterpret_cast<Edge*>(net + L.edges_off);
+  for (int r = lane; r < C; r += 32) {
+    const int dst = s.cdst[r];
+    if (dst < 0 || (s.flags[dst] & 2)) continue;
+    const int src = s.csrc[r];
+    int below = 0;
+    const int sw = src >> 5;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t bits = s.pred[dst * W + w];
+      if (w < sw) below += __popc(bits);
+      else if (w == sw) below += __popc(bits & ((1u << (src & 31)) - 1u));
+    }
+    Edge e;
+    e.w = float(crow[r * kConnCols + kW]);
+    e.src = uint16_t(src);
+    e.conn_row = uint16_t(r);
+    gedges[s.ebeg[dst] + below] = e;
+  }
+  if (lane == 0) {
+    NetHeader* h = reinterpret_cast<NetHeader*>(net);
+    h->status = 0;
+    h->err_kind = kErrNone;
+    h->err_a = 0;
+    h->err_b = 0;
+    h->order_count = int16_t(count);
+    h->n_ops = int16_t(op_base);
+    h->n_edges = int16_t(edge_base);
+  }
+}
+
+// describe_cycle (network.hpp:73-115) for one failing genome, one thread.
+// Emitted rows = the partial order K1 stored.  Writes the key path
+// (path[0] = length) for the host to format "k1->k2->...->k1".
+__global__ void k_describe_cycle(const double* __restrict__ nodes, const double* __restrict__ conns,
+                                 const uint8_t* __restrict__ net, NetLayout L, int* path_out) {
+  if (threadIdx.x != 0) return;
+  const int N = L.N, C = L.C;
+  const NetHeader* h = reinterpret_cast<const NetHeader*>(net);
+  const uint16_t* order = reinterpret_cast<const uint16_t*>(net + L.order_off);
+  uint32_t emitted[FNB_MAX_NODES_LIMIT / 32] = {0};
+  for (int i = 0; i < h->order_count; ++i) emitted[order[i] >> 5] |= 1u << (order[i] & 31);
+  auto empty = [&](int r) { return isnan(nodes[r * kNodeCols]); };
+  auto key_of = [&](int r) { return int(nodes[r * kNodeCols]); };
+  auto is_em = [&](int r) { return (emitted[r >> 5] >> (r & 31)) & 1u; };
+  int start = -1;
+  for (int r = 0; r < N; ++r)
+    if (!empty(r) && !is_em(r) && (start < 0 || key_of(r) < key_of(start))) start = r;
+  if (start < 0) { path_out[0] = -1; return; }
+  int16_t pos[FNB_MAX_NODES_LIMIT];
+  for (int r = 0; r < N; ++r) pos[r] = -1;
+  int len = 0;
+  int at = start;
+  for (;;) {
+    if (pos[at] >= 0) {
+      int n = 0;
+      for (int i = pos[at]; i < len; ++i) path_out[1 + n++] = path_out[1 + i];
+      path_out[1 + n++] = key_of(at);
+      path_out[0] = n;
+      return;
+    }
+    pos[at] = int16_t(len);
+    path_out[1 + len++] = key_of(at);
+    int next = -1;
+    for (int r = 0; r < C; ++r) {
+      const double* row = conns + size_t(r) * kConnCols;
+      if (isnan(row[kIn]) || row[kEn] != 1.0 || int(row[kIn]) != key_of(at)) continue;
+      for (int rr = 0; rr < N; ++rr) {
+        if (empty(rr) || is_em(rr)) continue;
+        if (key_of(rr) == int(row[kOut]) && (next < 0 || key_of(rr) < key_of(next))) next = rr;
+      }
+    }
+    if (next < 0) { path_out[0] = -1; return; }
+    at = next;
+  }
+}
+
+// Lowest failing genome: atomicMin over statuses in the net headers.
+__global__ void k_first_error(const uint8_t* __restrict__ nets, size_t stride, int P, int* out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P) return;
+  if (reinterpret_cast<const NetHeader*>(nets + size_t(g) * stride)->status != 0) atomicMin(out, g);
+}
+
+// int32 order (-1 padded) for parity checks and the host API (network.hpp:32).
+__global__ void k_net_order(const uint8_t* __restrict__ nets, NetLayout L, int P,
+                            int32_t* __restrict__ order, int32_t* __restrict__ count) {
+  const int g = blockIdx.x;
+  if (g >= P) return;
+  const uint8_t* net = nets + size_t(g) * L.bytes;
+  const NetHeader* h = reinterpret_cast<const NetHeader*>(net);
+  const uint16_t* o = reinterpret_cast<const uint16_t*>(net + L.order_off);
+  const int n = h->status == 0 ? h->order_count : 0;
+  for (int i = threadIdx.x; i < L.N; i += blockDim.x)
+    if (order) order[size_t(g) * L.N + i] = i < n ? int32_t(o[i]) : -1;
+  if (threadIdx.x == 0 && count) count[g] = n;
+}
+
+// ---- host launchers --------------------------------------------------------
+
+template <int W>
+static cudaError_t launch_transform_w(const double* n, const double* c, int P, uint8_t* nets,
+                                      const NetLayout& L, const DevShape& sh, cudaStream_t st) {
+  const size_t per_warp = tf_smem_bytes(sh.N, sh.C, W);
+  const int warps = 4;
+  const size_t smem = per_warp * warps;
+  cudaError_t e = cudaFuncSetAttribute(k_transform<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const int blocks = (P + warps - 1) / warps;
+  k_transform<W><<<blocks, 32 * warps, smem, st>>>(n, c, P, nets, L, sh, per_warp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transform(const double* n, const double* c, int P, uint8_t* nets, const NetLayout& L,
+                             const DevShape& sh, cudaStream_t st) {
+  const int W = (sh.N + 31) / 32;
+  if (W <= 1) return launch_transform_w<1>(n, c, P, nets, L, sh, st);
+  if (W <= 2) return launch_transform_w<2>(n, c, P, nets, L, sh, st);
+  if (W <= 4) return launch_transform_w<4>(n, c, P, nets, L, sh, st);
+  return launch_transform_w<8>(n, c, P, nets, L, sh, st);
+}
+
+cudaError_t launch_describe_cycle(const double* n, const double* c, const uint8_t* net, const NetLayout& L,
+                                  int* path, cudaStream_t st) {
+  k_describe_cycle<<<1, 32, 0, st>>>(n, c, net, L, path);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_first_error(const uint8_t* nets, size_t stride, int P, int* out, cudaStream_t st) {
+  k_first_error<<<(P + 255) / 256, 256, 0, st>>>(nets, stride, P, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_net_order(const uint8_t* nets, const NetLayout& L, int P, int32_t* order, int32_t* count,
+                             cudaStream_t st) {
+  k_net_order<<<P, 128, 0, st>>>(nets, L, P, order, count);
+  return cudaGetLastError();
+}
+
+}  // namespace fnb

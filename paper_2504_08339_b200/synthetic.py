@@ -1,0 +1,75 @@
+"""Seeded synthetic populations and datasets of the BASELINE shapes.
+
+Genomes are rank-ordered random DAGs with exact sizes: floor(fill*N_max)
+nodes (inputs keys 0..I-1, outputs I..I+O-1, hidden after), floor(fill*C_max)
+distinct rank-forward connections (15% disabled), weights and biases ~ N(0,1),
+response 1.0 -- the same construction as the reference's test generator
+(tests/support/generators.hpp:37-84) but with fixed counts so every genome
+fills the configured limits.  Data generation only; nothing here is on the
+timed path.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def synthetic_population(P: int, max_nodes: int, max_conns: int, fill: float = 0.75, num_inputs: int = 4,
+                         num_outputs: int = 1, disabled_prob: float = 0.15, n_act: int = 1, n_agg: int = 1,
+                         seed: int = 0, chunk: int = 4096):
+    rng = np.random.default_rng(seed)
+    n_nodes = max(num_inputs + num_outputs, int(fill * max_nodes))
+    n_conns = int(fill * max_conns)
+    I, O = num_inputs, num_outputs
+    H = n_nodes - I - O
+    # candidate (a, b) rank pairs with a < b and target not an input
+    a_idx, b_idx = np.triu_indices(n_nodes, k=1)
+    keep = b_idx >= I
+    a_idx, b_idx = a_idx[keep], b_idx[keep]
+    ncand = a_idx.size
+    if n_conns > ncand:
+        raise ValueError(f"{n_conns} connections exceed the {ncand} acyclic candidates")
+    nodes = np.full((P, max_nodes, 5), np.nan)
+    conns = np.full((P, max_conns, 4), np.nan)
+    keys = np.arange(n_nodes, dtype=np.float64)
+    for lo in range(0, P, chunk):
+        hi = min(P, lo + chunk)
+        n = hi - lo
+        # rank position -> key: inputs, shuffled hidden, outputs
+        hidden = I + O + np.argsort(rng.random((n, H)), axis=1)
+        by_rank = np.concatenate([np.broadcast_to(np.arange(I), (n, I)), hidden,
+                                  np.broadcast_to(np.arange(I, I + O), (n, O))], axis=1)
+        nd = nodes[lo:hi]
+        nd[:, :n_nodes, 0] = keys
+        nd[:, :n_nodes, 1] = rng.standard_normal((n, n_nodes))
+        nd[:, :n_nodes, 2] = 1.0
+        nd[:, :n_nodes, 3] = rng.integers(0, n_agg, (n, n_nodes)) if n_agg > 1 else 0
+        nd[:, :n_nodes, 4] = rng.integers(0, n_act, (n, n_nodes)) if n_act > 1 else 0
+        pick = np.argpartition(rng.random((n, ncand)), n_conns - 1, axis=1)[:, :n_conns]
+        pick.sort(axis=1)
+        src = np.take_along_axis(by_rank, a_idx[pick], axis=1)
+        dst = np.take_along_axis(by_rank, b_idx[pick], axis=1)
+        cn = conns[lo:hi]
+        cn[:, :n_conns, 0] = src
+        cn[:, :n_conns, 1] = dst
+        cn[:, :n_conns, 2] = (rng.random((n, n_conns)) >= disabled_prob).astype(np.float64)
+        cn[:, :n_conns, 3] = rng.standard_normal((n, n_conns))
+    return nodes, conns
+
+
+def regression_dataset(batch: int, num_inputs: int = 4, num_outputs: int = 1, seed: int = 0):
+    """X ~ U(-2, 2) sample-major [B, I]; y = a smooth fixed target [B, O]."""
+    rng = np.random.default_rng(seed)
+    X = rng.uniform(-2.0, 2.0, size=(batch, num_inputs))
+    w = np.linspace(0.5, -0.5, num_inputs)
+    base = np.sin(X @ w) + 0.25 * X[:, 0] * X[:, -1]
+    Y = np.stack([np.tanh(base + 0.1 * o) for o in range(num_outputs)], axis=1)
+    return X, Y
+
+
+def xor_dataset(bias_input: bool = False):
+    """XOR truth table; optional constant bias input."""
+    X = np.array([[0, 0], [0, 1], [1, 0], [1, 1]], dtype=np.float64)
+    if bias_input:
+        X = np.concatenate([X, np.ones((4, 1))], axis=1)
+    Y = np.array([[0], [1], [1], [0]], dtype=np.float64)
+    return X, Y

@@ -1,0 +1,168 @@
+"""GPU parity for K1 (transform) and K2 (forward + fitness) through the C ABI.
+
+Checker: the reference compiled from /root/reference (oracle/_ref) when
+present, else the C restatement (oracle/liboracle.so) -- both pinned to each
+other by tests/test_oracle_vs_ref.py.  Bars (north star): topological order,
+error codes and messages bit-exact; outputs within rtol 1e-5 + atol 1e-5 of
+the FP64 reference; fitness within rtol 1e-5.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as ol
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-5
+
+
+@pytest.fixture(scope="module")
+def fnb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_08339_b200 as m
+    return m
+
+
+def _engine(fnb, prob, schema):
+    return fnb.Engine(fnb.GenomeLimits(prob.max_nodes, prob.max_conns), prob.input_keys, prob.output_keys,
+                      fnb.AttributeSchema(list(schema.activations), list(schema.aggregations)))
+
+
+def _ref_transform(prob, schema, n, c):
+    return ol.ref_transform(prob, schema, n, c) if ol.ref_available() else ol.oracle_transform(prob, schema, n, c)
+
+
+def _ref_forward(prob, schema, n, c, X):
+    if ol.ref_available():
+        st, bad, msg, out = ol.ref_batch_forward(prob, schema, n, c, X)
+        assert st == 0, msg
+        return out
+    outs = []
+    for i in range(n.shape[0]):
+        net = ol.oracle_transform(prob, schema, n[i], c[i])
+        outs.append(ol.oracle_forward(prob, schema, n[i], net, X))
+    return np.stack(outs)
+
+
+def test_transform_order_matches_reference(fnb):
+    prob = ol.Problem(16, 60, [0, 1, 2], [3])
+    schema = ol.RICH
+    nodes, conns = ol.random_genomes(71, schema, 300, 16, 60)
+    eng = _engine(fnb, prob, schema)
+    order, cnt = eng.transform(nodes, conns)
+    for i in range(nodes.shape[0]):
+        r = _ref_transform(prob, schema, nodes[i], conns[i])
+        assert r["status"] == 0
+        assert cnt[i] == r["order_count"]
+        np.testing.assert_array_equal(order[i], r["order"])
+
+
+@pytest.mark.parametrize("kind", ["cycle", "selfloop", "dangling", "bad_act", "bad_agg", "missing_output",
+                                  "dup_pair"])
+def test_transform_errors_match_reference(fnb, kind):
+    from test_oracle_vs_ref import _corrupt
+    prob = ol.Problem(16, 60, [0, 1, 2], [3])
+    schema = ol.RICH
+    nodes, conns = ol.random_genomes(5150, schema, 40, 16, 60)
+    rng = np.random.default_rng(11)
+    eng = _engine(fnb, prob, schema)
+    for i in range(0, 40, 4):
+        n, c = _corrupt(nodes[i], conns[i], rng, kind)
+        r = _ref_transform(prob, schema, n, c)
+        # the failing genome sits after a valid one: lowest-index error wins
+        pn = np.stack([nodes[i + 1], n, nodes[i + 2]])
+        pc = np.stack([conns[i + 1], c, conns[i + 2]])
+        if r["status"] == 0:
+            eng.transform(pn, pc)
+            continue
+        with pytest.raises(fnb.FlatneatError) as ei:
+            eng.transform(pn, pc)
+        assert ei.value.status == r["status"]
+        assert ei.value.index == 1
+        assert str(ei.value) == r["msg"], (kind, str(ei.value), r["msg"])
+
+
+@pytest.mark.parametrize("seed,limits,schema_name", [
+    (1312, (16, 60), "rich"), (90210, (50, 100), "rich"), (7, (20, 80), "tanh")])
+def test_batch_forward_matches_reference(fnb, seed, limits, schema_name):
+    schema = ol.RICH if schema_name == "rich" else ol.SchemaSpec()
+    prob = ol.Problem(limits[0], limits[1], [0, 1, 2], [3])
+    nodes, conns = ol.random_genomes(seed, schema, 200, *limits)
+    rng = np.random.default_rng(seed)
+    for B in (1, 4, 37, 300):
+        X = rng.uniform(-2, 2, size=(B, 3))
+        want = _ref_forward(prob, schema, nodes, conns, X)
+        got = _engine(fnb, prob, schema).batch_forward(nodes, conns, X).values
+        np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+def test_forward_c2_shape_and_fitness(fnb):
+    """Config-2 shape (N_max=64, C_max=256, fill 0.75) on a 512-genome slice."""
+    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
+    nodes, conns = synthetic_population(512, 64, 256, fill=0.75, n_act=5, n_agg=4, seed=3)
+    schema = ol.RICH
+    prob = ol.Problem(64, 256, [0, 1, 2, 3], [4])
+    X, Y = regression_dataset(1024, seed=1)
+    eng = _engine(fnb, prob, schema)
+    got = eng.batch_forward(nodes, conns, X).values
+    want = _ref_forward(prob, schema, nodes, conns, X)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    fit = eng.evaluate(nodes, conns, X, Y, fnb.FIT_NEG_MSE)
+    want_fit = -np.mean((Y[None, :, :] - want) ** 2, axis=(1, 2))
+    np.testing.assert_allclose(fit, want_fit, rtol=RTOL, atol=0)
+    fit2 = eng.evaluate(nodes, conns, X, Y, fnb.FIT_OFFSET_SSE, 4.0)
+    np.testing.assert_allclose(fit2, 4.0 - np.sum((Y[None] - want) ** 2, axis=(1, 2)), rtol=RTOL)
+
+
+def test_padding_invariance_bit_exact(fnb):
+    """test_network.cpp:192-206: (50,100) vs (200,400) give identical outputs."""
+    schema = ol.RICH
+    small = ol.random_genomes(90210, schema, 60, 50, 100)
+    big_n = np.full((60, 200, 5), np.nan)
+    big_c = np.full((60, 400, 4), np.nan)
+    big_n[:, :50] = small[0]
+    big_c[:, :100] = small[1]
+    X = np.random.default_rng(0).uniform(-2, 2, size=(64, 3))
+    a = _engine(fnb, ol.Problem(50, 100, [0, 1, 2], [3]), schema).batch_forward(*small, X).values
+    b = _engine(fnb, ol.Problem(200, 400, [0, 1, 2], [3]), schema).batch_forward(big_n, big_c, X).values
+    assert np.array_equal(a, b)
+
+
+def test_batch_equals_single(fnb):
+    """test_network.cpp:131-159: batch result == per-genome forward, bit for bit."""
+    schema = ol.RICH
+    prob = ol.Problem(16, 60, [0, 1, 2], [3])
+    nodes, conns = ol.random_genomes(1312, schema, 64, 16, 60)
+    X = np.random.default_rng(1).uniform(-2, 2, size=(16, 3))
+    eng = _engine(fnb, prob, schema)
+    allv = eng.batch_forward(nodes, conns, X).values
+    for p in range(0, 64, 7):
+        one = eng.batch_forward(nodes[p:p + 1], conns[p:p + 1], X).values[0]
+        assert np.array_equal(one, allv[p])
+
+
+def test_non_finite_input_rejected(fnb):
+    schema = ol.RICH
+    prob = ol.Problem(16, 60, [0, 1, 2], [3])
+    nodes, conns = ol.random_genomes(3, schema, 4, 16, 60)
+    X = np.zeros((2, 3))
+    X[1, 2] = np.nan
+    with pytest.raises(fnb.FlatneatError) as ei:
+        _engine(fnb, prob, schema).batch_forward(nodes, conns, X)
+    assert ei.value.code == "non_finite_input" and str(ei.value) == "non_finite_input: input not finite"
+
+
+def test_known_answers(fnb):
+    """test_network.cpp:74-106: identity network, tanh(0.6), two-input sum."""
+    schema = ol.SchemaSpec(["tanh", "sigmoid", "identity", "relu", "sin"], ["sum", "product", "max", "mean"])
+    prob = ol.Problem(6, 8, [0], [1])
+    n = np.full((1, 6, 5), np.nan)
+    n[0, 0] = [0, 0.0, 1.0, 0, 2]
+    n[0, 1] = [1, 0.1, 1.0, 0, 0]
+    n[0, 2] = [2, 0.0, 1.0, 0, 0]
+    c = np.full((1, 8, 4), np.nan)
+    c[0, 0] = [0, 1, 1, 0.5]
+    out = _engine(fnb, prob, schema).batch_forward(n, c, np.array([[1.0]])).values
+    assert abs(out[0, 0, 0] - 0.5370495669980353) < 1e-6
