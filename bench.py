@@ -124,6 +124,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--spt", type=int, default=0, help="forward columns per thread (tuning; 0 = auto)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -155,6 +156,8 @@ def main():
     import paper_2504_08339_b200 as fnb
     from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
 
+    if args.spt:
+        fnb._native.lib().fnb_set_forward_spt(args.spt)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:

@@ -100,6 +100,10 @@ int fnb_last_error_index(const fnb_ctx* ctx);
 size_t fnb_net_bytes(const fnb_ctx* ctx);
 /* number of kernel launches this context issued since creation */
 long long fnb_launch_count(const fnb_ctx* ctx);
+/* tuning knob: sample columns per thread of the forward kernel (1, 2 or 4;
+ * 0 = automatic).  Process-wide; results do not depend on it beyond FP32
+ * summation order, which it does not change. */
+void fnb_set_forward_spt(int spt);
 
 /* ---- host layer (synchronous) ------------------------------------------ */
 

@@ -19,8 +19,9 @@ cudaError_t launch_net_order(const uint8_t* nets, const NetLayout& L, int P, int
                              cudaStream_t st);
 int launch_forward(const void* nets, NetLayout L, int P, const float* X, const float* Y, int B,
                    int fit_kind, double offset, double* fitness, double* out, double* partial_buf,
-                   size_t partial_cap, cudaStream_t st, long long* launches);
+                   size_t partial_cap, int uniform_agg, int uniform_act, cudaStream_t st, long long* launches);
 size_t forward_partial_needed(NetLayout L, int P, int B);
+void set_forward_spt(int spt);
 cudaError_t launch_to_float(const double* src, float* dst, size_t n, int* bad, cudaStream_t st);
 }  // namespace fnb
 
@@ -149,6 +150,7 @@ const char* fnb_last_error(const fnb_ctx* ctx) { return ctx ? ctx->err.c_str() :
 int fnb_last_error_index(const fnb_ctx* ctx) { return ctx ? ctx->err_index : -1; }
 size_t fnb_net_bytes(const fnb_ctx* ctx) { return ctx ? ctx->L.bytes : 0; }
 long long fnb_launch_count(const fnb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void fnb_set_forward_spt(int spt) { set_forward_spt(spt); }
 
 // ---- device layer ------------------------------------------------------
 
@@ -233,6 +235,7 @@ int fnb_forward_d(fnb_ctx* ctx, const void* d_nets, int P, const float* d_X, con
   CK(ctx->partial.ensure(forward_partial_needed(ctx->L, P, batch)));
   return launch_forward(d_nets, ctx->L, P, d_X, d_Y, batch, fitness_kind, fitness_offset, d_fitness, d_out,
                         static_cast<double*>(ctx->partial.p), ctx->partial.cap,
+                        ctx->sh.n_agg == 1 ? int(ctx->sh.agg[0]) : -1, ctx->sh.n_act == 1 ? int(ctx->sh.act[0]) : -1,
                         static_cast<cudaStream_t>(stream), &ctx->launches)
              ? fnb_cuda_fail_ctx(ctx, cudaGetLastError(), "forward launch")
              : 0;

@@ -35,8 +35,8 @@ struct NetHeader {          // 32 B
   int32_t err_a, err_b;
   int16_t order_count;
   int16_t n_ops;            // non-input rows in order
-  int16_t n_edges;
-  int16_t pad0;
+  int16_t n_edges;          // enabled edges feeding ops
+  int16_t n_rec;            // forward records
   int32_t pad1, pad2;
 };
 static_assert(sizeof(NetHeader) == 32, "header");
@@ -54,10 +54,31 @@ static_assert(sizeof(Op) == 16, "op");
 
 struct Edge {               // 8 B
   float w;
-  uint16_t src;             // source node row
-  uint16_t conn_row;        // connection row the weight came from
+  uint16_t src;             // source node row (max_nodes = the all-zero pad row)
+  uint16_t conn_row;        // connection row the weight came from (0xffff: pad)
 };
 static_assert(sizeof(Edge) == 8, "edge");
+
+// Forward program record: one node op split into chunks of four incoming
+// edges (ascending source row).  Pad slots have w = 0 and read the extra
+// all-zero value row, so the hot loop is branch-free.
+constexpr int kRecSlots = 4;
+constexpr uint8_t kRecFirst = 1, kRecLast = 2;
+struct RecHeader {          // 16 B
+  float bias;
+  float resp;
+  uint16_t dst;             // node row written by the op's last record
+  uint8_t cnt;              // real edges in this record (0..4)
+  uint8_t flags;            // kRecFirst | kRecLast
+  uint8_t act, agg;
+  uint16_t fanin;           // op's total fan-in (mean)
+};
+struct Rec {                // 48 B
+  RecHeader h;
+  Edge slot[kRecSlots];
+};
+static_assert(sizeof(RecHeader) == 16 && sizeof(Rec) == 48, "record");
+__host__ __device__ inline int max_records(int N, int C) { return N + (C + kRecSlots - 1) / kRecSlots; }
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -66,9 +87,9 @@ struct NetLayout {
   size_t ops_off, edges_off, order_off, in_off, out_off, bytes;
   __host__ __device__ NetLayout() : NetLayout(0, 0, 0, 0) {}
   __host__ __device__ NetLayout(int n, int c, int i, int o) : N(n), C(c), I(i), O(o) {
-    ops_off = sizeof(NetHeader);
-    edges_off = align16(ops_off + size_t(N) * sizeof(Op));
-    order_off = align16(edges_off + size_t(C) * sizeof(Edge));
+    ops_off = sizeof(NetHeader);  // forward records (Rec)
+    edges_off = ops_off;          // (edges live inside the records)
+    order_off = align16(ops_off + size_t(max_records(N, C)) * sizeof(Rec));
     in_off = align16(order_off + size_t(N) * sizeof(uint16_t));
     out_off = in_off + size_t(I) * sizeof(uint16_t);
     bytes = align16(out_off + size_t(O) * sizeof(uint16_t));

@@ -2,31 +2,89 @@
 // (forward_into / batch_forward, network.hpp:238-330; func-fit and XOR
 // fitness) on sm_100a CUDA cores.
 //
-// Mapping: a "group" of T threads evaluates one genome; T = min(256,
-// pow2 >= B) so small batches (XOR, B=4) pack many genomes per CTA while
-// B >= 256 gives one genome per CTA.  Each thread owns SPT sample columns.
-// The genome's op/edge program (K1 output) is staged once into shared
-// memory and read as warp-broadcasts; node values live in shared memory as
-// v[row][column] so the dynamic source indices of the irregular DAG hit
-// conflict-free LDS (consecutive threads = consecutive columns).  A thread
-// only ever touches its own columns, so the op loop needs no barriers.
-// Arithmetic is FP32 (north star: 1e-5 relative to the FP64 reference);
-// the squared-error fitness accumulates in FP64.
+// Mapping.  A "group" of T threads evaluates one genome over a tile of
+// TC = T*SPT sample columns; each thread owns SPT ADJACENT columns so one
+// 4/8/16-byte LDS fetches all of its values of a source node.  Node values
+// live in shared memory as v[row][TC] (+ one all-zero row); consecutive
+// threads touch consecutive 4*SPT-byte chunks, so the irregular per-edge
+// source rows never bank-conflict.
+//
+// Program.  K1 emits each node op as records of exactly four edge slots
+// (ascending source row; pad slots carry w = 0 and read the zero row).  The
+// records are staged once per CTA with source/destination rows rewritten
+// into byte offsets, and the hot loop walks them branch-free: three
+// broadcast LDS.128 for the record (prefetched one record ahead), four value
+// loads, the FMA chain, and a warp-uniform finalize (activation + store) on
+// an op's last record.  A thread only touches its own columns, so the loop
+// has no barriers.  Schemas with a single activation/aggregation (the paper
+// default {tanh},{sum}) get an instantiation without per-op dispatch.
+// Arithmetic is FP32 (north star: 1e-5 relative to the FP64 reference); the
+// squared-error fitness accumulates in FP64.
 #include <algorithm>
 
 #include "fnb_common.cuh"
 
 namespace fnb {
 
+// ---- activations (functions.hpp:17-21) in FP32 -----------------------------
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// tanh(x) = 1 - 2/(exp(2x)+1): absolute error ~2e-7 on the whole line,
+// saturating exactly to +-1 (inf/0 out of ex2).
+__device__ __forceinline__ float tanh_fast(float x) {
+  return fmaf(-2.0f, rcp_approx(ex2_approx(x * 2.8853900817779268f) + 1.0f), 1.0f);
+}
+__device__ __forceinline__ float sigmoid_fast(float x) {
+  return rcp_approx(1.0f + ex2_approx(x * -1.4426950408889634f));
+}
+
+template <int ACT>
 __device__ __forceinline__ float act_apply(int code, float x) {
-  switch (code) {  // functions.hpp:17-21
+  const int c = ACT >= 0 ? ACT : code;
+  switch (c) {
     case FNB_ACT_IDENTITY: return x;
-    case FNB_ACT_TANH: return tanhf(x);
-    case FNB_ACT_SIGMOID: return 1.0f / (1.0f + expf(-x));
+    case FNB_ACT_TANH: return tanh_fast(x);
+    case FNB_ACT_SIGMOID: return sigmoid_fast(x);
     case FNB_ACT_RELU: return x > 0.0f ? x : 0.0f;
     case FNB_ACT_SIN: return sinf(x);
   }
   return x;
+}
+
+// ---- staged record (48 B, three float4) ------------------------------------
+//   h  = {bias, resp, dst_off | fanin << 20, cnt | flags << 8 | act << 16 | agg << 24}
+//   s01 = {w0, off0, w1, off1},  s23 = {w2, off2, w3, off3}   (off = byte offset of the row)
+struct SRec {
+  float4 h, s01, s23;
+};
+static_assert(sizeof(SRec) == 48, "staged record");
+
+template <int SPT> struct VecT;
+template <> struct VecT<1> { using T = float; };
+template <> struct VecT<2> { using T = float2; };
+template <> struct VecT<4> { using T = float4; };
+
+template <int SPT>
+__device__ __forceinline__ void vload(const uint8_t* base, uint32_t off, float (&x)[SPT]) {
+  const auto v = *reinterpret_cast<const typename VecT<SPT>::T*>(base + off);
+  if constexpr (SPT == 1) { x[0] = v; }
+  else if constexpr (SPT == 2) { x[0] = v.x; x[1] = v.y; }
+  else { x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w; }
+}
+template <int SPT>
+__device__ __forceinline__ void vstore(uint8_t* base, uint32_t off, const float (&x)[SPT]) {
+  auto* p = reinterpret_cast<typename VecT<SPT>::T*>(base + off);
+  if constexpr (SPT == 1) { *p = x[0]; }
+  else if constexpr (SPT == 2) { *p = make_float2(x[0], x[1]); }
+  else { *p = make_float4(x[0], x[1], x[2], x[3]); }
 }
 
 struct FwdParams {
@@ -37,6 +95,7 @@ struct FwdParams {
   const float* Y;       // [B][O] or null
   int B;
   int T;                // threads per genome group (power of two)
+  int groups;           // genome groups per CTA (threads beyond groups*T idle)
   int fit_kind;
   double fit_offset;
   double* fitness;      // [P] or null
@@ -46,124 +105,163 @@ struct FwdParams {
 };
 
 __host__ __device__ inline size_t fwd_group_smem(int N, int C, int I, int O, int T, int spt) {
-  size_t b = align16(size_t(N) * sizeof(Op)) + align16(size_t(C) * sizeof(Edge));
-  b += align16(size_t(I + O) * sizeof(uint16_t));
-  b += align16(size_t(T) * sizeof(double));            // reduction scratch
-  b += size_t(N) * size_t(T) * spt * sizeof(float);    // node values
+  size_t b = align16(size_t(max_records(N, C) + 1) * sizeof(SRec));  // + zero sentinel
+  b += align16(size_t(I + O) * sizeof(uint32_t));
+  b += 8 * sizeof(double);                                  // reduction scratch (T/32 <= 8 warps)
+  b += size_t(N + 1) * size_t(T) * spt * sizeof(float);     // node values + zero row
   return align16(b);
 }
 
-template <int SPT>
+template <int SPT, int AGG, int ACT>
 __global__ void __launch_bounds__(256)
 k_forward(FwdParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int T = p.T;
-  const int groups = blockDim.x / T;
   const int grp = threadIdx.x / T;
   const int j = threadIdx.x % T;
-  const int g = blockIdx.x * groups + grp;
+  const int g = blockIdx.x * p.groups + grp;
   const NetLayout& L = p.L;
-  uint8_t* base = smem_raw + size_t(grp) * p.group_smem;
-  Op* s_ops = reinterpret_cast<Op*>(base);
-  Edge* s_edges = reinterpret_cast<Edge*>(base + align16(size_t(L.N) * sizeof(Op)));
-  uint16_t* s_io = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(s_edges) +
-                                               align16(size_t(L.C) * sizeof(Edge)));
+  uint8_t* base = smem_raw + size_t(grp < p.groups ? grp : 0) * p.group_smem;
+  SRec* s_rec = reinterpret_cast<SRec*>(base);
+  uint32_t* s_io = reinterpret_cast<uint32_t*>(base + align16(size_t(max_records(L.N, L.C) + 1) * sizeof(SRec)));
   double* s_red = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(s_io) +
-                                            align16(size_t(L.I + L.O) * sizeof(uint16_t)));
-  float* v = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s_red) + align16(size_t(T) * sizeof(double)));
-  const int TC = T * SPT;  // columns per group
+                                            align16(size_t(L.I + L.O) * sizeof(uint32_t)));
+  uint8_t* v = reinterpret_cast<uint8_t*>(s_red) + 8 * sizeof(double);
+  const int TC = T * SPT;                        // columns per tile
+  const uint32_t row_bytes = uint32_t(TC) * 4u;  // v row stride
+  const uint32_t my = uint32_t(j) * SPT * 4u;    // this thread's byte offset in a row
 
-  const bool live = g < p.P;
-  int n_ops = 0;
+  const bool live = grp < p.groups && g < p.P;
+  int n_rec = 0;
   if (live) {
     const uint8_t* net = p.nets + size_t(g) * L.bytes;
-    const NetHeader* h = reinterpret_cast<const NetHeader*>(net);
-    n_ops = h->n_ops;
-    const int n_edges = h->n_edges;
-    // stage the program: 16-byte vector copies
-    const int4* so = reinterpret_cast<const int4*>(net + L.ops_off);
-    int4* dop = reinterpret_cast<int4*>(s_ops);
-    for (int i = j; i < n_ops; i += T) dop[i] = so[i];
-    const int2* se = reinterpret_cast<const int2*>(net + L.edges_off);
-    int2* de = reinterpret_cast<int2*>(s_edges);
-    for (int i = j; i < n_edges; i += T) de[i] = se[i];
+    n_rec = reinterpret_cast<const NetHeader*>(net)->n_rec;
+    const Rec* gr = reinterpret_cast<const Rec*>(net + L.ops_off);
+    for (int i = j; i < n_rec; i += T) {
+      const Rec r = gr[i];
+      SRec s;
+      const uint32_t meta = uint32_t(r.h.cnt) | (uint32_t(r.h.flags) << 8) | (uint32_t(r.h.act) << 16) |
+                            (uint32_t(r.h.agg) << 24);
+      s.h = make_float4(r.h.bias, r.h.resp, __uint_as_float(uint32_t(r.h.dst) * row_bytes | (uint32_t(r.h.fanin) << 20)),
+                        __uint_as_float(meta));
+      s.s01 = make_float4(r.slot[0].w, __uint_as_float(uint32_t(r.slot[0].src) * row_bytes), r.slot[1].w,
+                          __uint_as_float(uint32_t(r.slot[1].src) * row_bytes));
+      s.s23 = make_float4(r.slot[2].w, __uint_as_float(uint32_t(r.slot[2].src) * row_bytes), r.slot[3].w,
+                          __uint_as_float(uint32_t(r.slot[3].src) * row_bytes));
+      s_rec[i] = s;
+    }
+    if (j == 0) s_rec[n_rec] = SRec{make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
     const uint16_t* sio = reinterpret_cast<const uint16_t*>(net + L.in_off);
-    for (int i = j; i < L.I + L.O; i += T) s_io[i] = sio[i];
+    for (int i = j; i < L.I + L.O; i += T) s_io[i] = uint32_t(sio[i]) * row_bytes;
+    float z[SPT];
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) z[k] = 0.0f;
+    vstore<SPT>(v, uint32_t(L.N) * row_bytes + my, z);  // the all-zero pad row
   }
   __syncthreads();
 
   const int I = L.I, O = L.O;
+  const uint8_t* vb = v + my;  // this thread's columns
   double err = 0.0;
-  // sample tiles assigned to this CTA's y-chunk; dead groups (g >= P) run
-  // zero tiles but stay resident for the warp-synchronous reduction below
+  // sample tiles of this CTA's y-chunk; dead groups (g >= P) run zero tiles
+  // but stay resident for the warp-synchronous reduction below
   const int tiles = (p.B + TC - 1) / TC;
   const int per = (tiles + gridDim.y - 1) / gridDim.y;
   const int t_lo = blockIdx.y * per;
   const int t_hi = live ? min(tiles, t_lo + per) : t_lo;
   for (int tile = t_lo; tile < t_hi; ++tile) {
-    int sidx[SPT];
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) sidx[k] = tile * TC + k * T + j;
+    const int s0 = tile * TC + j * SPT;  // first sample of this thread
     // seed input rows (network.hpp:249-250)
     for (int i = 0; i < I; ++i) {
-      float* vr = v + size_t(s_io[i]) * TC;
+      float x[SPT];
 #pragma unroll
-      for (int k = 0; k < SPT; ++k) vr[k * T + j] = sidx[k] < p.B ? p.X[size_t(sidx[k]) * I + i] : 0.0f;
+      for (int k = 0; k < SPT; ++k) x[k] = (s0 + k < p.B) ? __ldg(p.X + size_t(s0 + k) * I + i) : 0.0f;
+      vstore<SPT>(v, s_io[i] + my, x);
     }
-    // ops in topological order (network.hpp:252-264)
-    for (int oi = 0; oi < n_ops; ++oi) {
-      const Op op = s_ops[oi];
-      float acc[SPT];
-      if (op.agg == FNB_AGG_SUM || op.agg == FNB_AGG_MEAN) {
+    // ops in topological order (network.hpp:252-264), one record per step,
+    // the next record prefetched
+    float acc[SPT];
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) acc[k] = 0.0f;
-        for (int e = op.e_begin; e < op.e_end; ++e) {
-          const Edge ed = s_edges[e];
-          const float* vs = v + size_t(ed.src) * TC + j;
+    for (int k = 0; k < SPT; ++k) acc[k] = 0.0f;
+    // cur.s01/s23 (edge slots) are reloaded as soon as their value loads and
+    // FMAs are done and cur.h after the finalize, so the next record's fetch
+    // overlaps this record's activation without extra registers or moves.
+    SRec cur = s_rec[0];
+#pragma unroll 1
+    for (int r = 0; r < n_rec; ++r) {
+      const uint32_t meta = __float_as_uint(cur.h.w);
+      const bool first = (meta >> 8) & kRecFirst;
+      const bool last = (meta >> 8) & kRecLast;
+      const int agg = AGG >= 0 ? AGG : int(meta >> 24);
+      float x0[SPT], x1[SPT], x2[SPT], x3[SPT];
+      vload<SPT>(vb, __float_as_uint(cur.s01.y), x0);
+      vload<SPT>(vb, __float_as_uint(cur.s01.w), x1);
+      vload<SPT>(vb, __float_as_uint(cur.s23.y), x2);
+      vload<SPT>(vb, __float_as_uint(cur.s23.w), x3);
+      if (agg == FNB_AGG_SUM || agg == FNB_AGG_MEAN) {
+        // pad slots contribute 0 * 0: branch-free
 #pragma unroll
-          for (int k = 0; k < SPT; ++k) acc[k] = fmaf(ed.w, vs[k * T], acc[k]);
+        for (int k = 0; k < SPT; ++k) {
+          float a = first ? 0.0f : acc[k];
+          a = fmaf(cur.s01.x, x0[k], a);
+          a = fmaf(cur.s01.z, x1[k], a);
+          a = fmaf(cur.s23.x, x2[k], a);
+          a = fmaf(cur.s23.z, x3[k], a);
+          acc[k] = a;
         }
-        if (op.agg == FNB_AGG_MEAN && op.e_end > op.e_begin) {
-          const float n = float(op.e_end - op.e_begin);
+      } else {
+        const int cnt = int(meta & 0xff);
+        const float w[4] = {cur.s01.x, cur.s01.z, cur.s23.x, cur.s23.z};
 #pragma unroll
-          for (int k = 0; k < SPT; ++k) acc[k] = acc[k] / n;
-        }
-      } else if (op.agg == FNB_AGG_PRODUCT) {
+        for (int k = 0; k < SPT; ++k) {
+          const float xs[4] = {x0[k], x1[k], x2[k], x3[k]};
+          if (agg == FNB_AGG_PRODUCT) {
+            float a = first ? 1.0f : acc[k];
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) acc[k] = 1.0f;
-        for (int e = op.e_begin; e < op.e_end; ++e) {
-          const Edge ed = s_edges[e];
-          const float* vs = v + size_t(ed.src) * TC + j;
+            for (int q = 0; q < 4; ++q)
+              if (q < cnt) a *= w[q] * xs[q];
+            acc[k] = a;
+          } else {  // max; empty fan-in falls back to 0 (network.hpp:258-261)
+            float a = first ? 0.0f : acc[k];
 #pragma unroll
-          for (int k = 0; k < SPT; ++k) acc[k] *= ed.w * vs[k * T];
-        }
-      } else {  // max; empty fan-in falls back to 0 (network.hpp:258-261)
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) acc[k] = 0.0f;
-        for (int e = op.e_begin; e < op.e_end; ++e) {
-          const Edge ed = s_edges[e];
-          const float* vs = v + size_t(ed.src) * TC + j;
-#pragma unroll
-          for (int k = 0; k < SPT; ++k) {
-            const float x = ed.w * vs[k * T];
-            acc[k] = (e == op.e_begin || x > acc[k]) ? x : acc[k];
+            for (int q = 0; q < 4; ++q) {
+              const float t = w[q] * xs[q];
+              if (q < cnt) a = ((first && q == 0) || t > a) ? t : a;
+            }
+            acc[k] = a;
           }
         }
       }
-      float* vd = v + size_t(op.dst) * TC + j;
+      cur.s01 = s_rec[r + 1].s01;
+      cur.s23 = s_rec[r + 1].s23;
+      if (last) {
+        const uint32_t dw = __float_as_uint(cur.h.z);
+        if (agg == FNB_AGG_MEAN) {
+          const uint32_t fanin = dw >> 20;
+          if (fanin > 0) {
+            const float n = float(fanin);
 #pragma unroll
-      for (int k = 0; k < SPT; ++k) vd[k * T] = act_apply(op.act, fmaf(op.resp, acc[k], op.bias));
+            for (int k = 0; k < SPT; ++k) acc[k] = acc[k] / n;
+          }
+        }
+        float y[SPT];
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) y[k] = act_apply<ACT>(int((meta >> 16) & 0xff), fmaf(cur.h.y, acc[k], cur.h.x));
+        vstore<SPT>(v, (dw & 0xfffffu) + my, y);
+      }
+      cur.h = s_rec[r + 1].h;
     }
     // outputs + fitness epilogue
     for (int o = 0; o < O; ++o) {
-      const float* vr = v + size_t(s_io[I + o]) * TC + j;
+      float val[SPT];
+      vload<SPT>(vb, s_io[I + o], val);
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        if (sidx[k] >= p.B) continue;
-        const float val = vr[k * T];
-        if (p.out) p.out[(size_t(g) * p.B + sidx[k]) * O + o] = double(val);
+        const int s = s0 + k;
+        if (s >= p.B) continue;
+        if (p.out) p.out[(size_t(g) * p.B + s) * O + o] = double(val[k]);
         if (p.fit_kind != FNB_FIT_NONE) {
-          const double d = double(p.Y[size_t(sidx[k]) * O + o]) - double(val);
+          const double d = double(__ldg(p.Y + size_t(s) * O + o)) - double(val[k]);
           err += d * d;
         }
       }
@@ -174,10 +272,9 @@ k_forward(FwdParams p) {
   // sum of warp partials.
   const int width = T < 32 ? T : 32;
   for (int d = width >> 1; d > 0; d >>= 1) err += __shfl_down_sync(0xffffffffu, err, d, width);
-  if (T > 32) {
+  if (T > 32) {  // every thread of the CTA (dead groups included) reaches here
     if ((j & 31) == 0) s_red[j >> 5] = err;
-    // all threads of the group are live; sync only this group's warps
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(T));
+    __syncthreads();
     if (j == 0) {
       err = 0.0;
       for (int w = 0; w < T / 32; ++w) err += s_red[w];
@@ -187,9 +284,7 @@ k_forward(FwdParams p) {
     if (gridDim.y > 1) {
       p.partial[size_t(g) * gridDim.y + blockIdx.y] = err;
     } else {
-      const double sse = err;
-      p.fitness[g] = p.fit_kind == FNB_FIT_NEG_MSE ? -(sse / (double(p.B) * double(O)))
-                                                   : p.fit_offset - sse;
+      p.fitness[g] = p.fit_kind == FNB_FIT_NEG_MSE ? -(err / (double(p.B) * double(O))) : p.fit_offset - err;
     }
   }
 }
@@ -214,27 +309,40 @@ __global__ void k_to_float(const double* __restrict__ src, float* __restrict__ d
 // ---- host launchers --------------------------------------------------------
 
 struct FwdConfig {
-  int T, groups, chunks, grid_x;
+  int T, spt, block, groups, chunks, grid_x;
   size_t group_smem, cta_smem;
 };
 
+static int g_force_spt = 0;  // tuning override (fnb_set_forward_spt)
+
 static FwdConfig fwd_config(const NetLayout& L, int P, int B) {
   FwdConfig c{};
-  int T = 1;
-  while (T < B && T < 256) T <<= 1;
-  // keep a CTA's shared memory small enough for >= 2 resident CTAs per SM
-  while (T > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, T, 1) * (256 / T) > 100 * 1024) T >>= 1;
+  // columns per group: cover the batch, at most 256, shrinking until a
+  // group fits ~72 KB (3 resident CTAs per SM)
+  int cols = 1;
+  while (cols < B && cols < 256) cols <<= 1;
+  int spt = g_force_spt ? g_force_spt : (cols >= 128 ? 2 : 1);
+  while (cols > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, std::max(1, cols / spt), spt) > 72 * 1024) cols >>= 1;
+  spt = std::min(spt, cols);
+  const int T = std::max(1, cols / spt);
+  c.spt = spt;
   c.T = T;
-  c.groups = 256 / T;
-  c.group_smem = fwd_group_smem(L.N, L.C, L.I, L.O, T, 1);
-  c.cta_smem = c.group_smem * c.groups;
-  c.grid_x = (P + c.groups - 1) / c.groups;
-  const int tiles = (B + T - 1) / T;
+  c.group_smem = fwd_group_smem(L.N, L.C, L.I, L.O, T, spt);
+  // groups per CTA: up to 256 threads and ~96 KB of shared memory
+  int groups = std::max(1, 256 / T);
+  while (groups > 1 && c.group_smem * groups > 96 * 1024) groups >>= 1;
+  c.groups = groups;
+  c.block = std::max(32, groups * T);
+  c.cta_smem = c.group_smem * groups;
+  c.grid_x = (P + groups - 1) / groups;
+  const int tiles = (B + T * spt - 1) / (T * spt);
   const int target = 4 * 148;  // >= 4 CTAs per SM before splitting samples
   c.chunks = 1;
   if (c.grid_x < target) c.chunks = std::min(tiles, (target + c.grid_x - 1) / c.grid_x);
   return c;
 }
+
+void set_forward_spt(int spt) { g_force_spt = (spt == 1 || spt == 2 || spt == 4) ? spt : 0; }
 
 size_t forward_partial_needed(NetLayout L, int P, int B) {
   const FwdConfig c = fwd_config(L, P, B);
@@ -247,9 +355,37 @@ cudaError_t launch_to_float(const double* src, float* dst, size_t n, int* bad, c
   return cudaGetLastError();
 }
 
+template <int SPT, int AGG, int ACT>
+static cudaError_t launch_k(const FwdConfig& c, const FwdParams& p, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(k_forward<SPT, AGG, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(c.cta_smem));
+  if (e != cudaSuccess) return e;
+  // node values are the occupancy limiter: ask for the full 228 KB carveout
+  e = cudaFuncSetAttribute(k_forward<SPT, AGG, ACT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           int(cudaSharedmemCarveoutMaxShared));
+  if (e != cudaSuccess) return e;
+  k_forward<SPT, AGG, ACT><<<dim3(c.grid_x, c.chunks), c.block, c.cta_smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int SPT>
+static cudaError_t launch_spt(const FwdConfig& c, const FwdParams& p, int agg, int act, cudaStream_t st) {
+  if (agg == FNB_AGG_SUM) {
+    switch (act) {
+      case FNB_ACT_TANH: return launch_k<SPT, FNB_AGG_SUM, FNB_ACT_TANH>(c, p, st);
+      case FNB_ACT_SIGMOID: return launch_k<SPT, FNB_AGG_SUM, FNB_ACT_SIGMOID>(c, p, st);
+      case FNB_ACT_IDENTITY: return launch_k<SPT, FNB_AGG_SUM, FNB_ACT_IDENTITY>(c, p, st);
+      case FNB_ACT_RELU: return launch_k<SPT, FNB_AGG_SUM, FNB_ACT_RELU>(c, p, st);
+      default: break;
+    }
+  }
+  return launch_k<SPT, -1, -1>(c, p, st);
+}
+
+// uniform_agg / uniform_act: the single registry entry, or -1 for mixed schemas
 int launch_forward(const void* nets, NetLayout L, int P, const float* X, const float* Y, int B, int fit_kind,
                    double offset, double* fitness, double* out, double* partial_buf, size_t partial_cap,
-                   cudaStream_t st, long long* launches) {
+                   int uniform_agg, int uniform_act, cudaStream_t st, long long* launches) {
   const FwdConfig c = fwd_config(L, P, B);
   if (c.cta_smem > 227 * 1024) return 1;
   FwdParams p;
@@ -260,6 +396,7 @@ int launch_forward(const void* nets, NetLayout L, int P, const float* X, const f
   p.Y = Y;
   p.B = B;
   p.T = c.T;
+  p.groups = c.groups;
   p.fit_kind = fit_kind;
   p.fit_offset = offset;
   p.fitness = fitness;
@@ -267,11 +404,13 @@ int launch_forward(const void* nets, NetLayout L, int P, const float* X, const f
   p.partial = partial_buf;
   p.group_smem = c.group_smem;
   if (c.chunks > 1 && fit_kind != FNB_FIT_NONE && sizeof(double) * size_t(P) * c.chunks > partial_cap) return 1;
-  if (cudaFuncSetAttribute(k_forward<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c.cta_smem)) !=
-      cudaSuccess)
-    return 1;
-  k_forward<1><<<dim3(c.grid_x, c.chunks), 256, c.cta_smem, st>>>(p);
-  if (cudaGetLastError() != cudaSuccess) return 1;
+  cudaError_t e;
+  switch (c.spt) {
+    case 4: e = launch_spt<4>(c, p, uniform_agg, uniform_act, st); break;
+    case 2: e = launch_spt<2>(c, p, uniform_agg, uniform_act, st); break;
+    default: e = launch_spt<1>(c, p, uniform_agg, uniform_act, st); break;
+  }
+  if (e != cudaSuccess) return 1;
   ++*launches;
   if (c.chunks > 1 && fit_kind != FNB_FIT_NONE) {
     k_fitness_finalize<<<(P + 255) / 256, 256, 0, st>>>(partial_buf, c.chunks, P, B, L.O, fit_kind, offset,

@@ -82,6 +82,7 @@ __device__ inline void tf_fail(uint8_t* net, int status, int kind, int a, int b,
   h->order_count = int16_t(order_count);
   h->n_ops = 0;
   h->n_edges = 0;
+  h->n_rec = 0;
 }
 
 template <int W>
@@ -265,12 +266,13 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     return;
   }
 
-  // ---- 6. ops in topological order, skipping input rows (network.hpp:252-254)
-  Op* gops = reinterpret_cast<Op*>(net + L.ops_off);
-  int op_base = 0, edge_base = 0;
+  // ---- 6. forward records: ops in topological order, skipping input rows
+  //         (network.hpp:252-254); each op = max(1, ceil(fanin/4)) records
+  Rec* grec = reinterpret_cast<Rec*>(net + L.ops_off);
+  int op_base = 0, rec_base = 0, edge_total = 0;
   for (int p0 = 0; p0 < count; p0 += 32) {
     const int p = p0 + lane;
-    int row = 0, ne = 0;
+    int row = 0, ne = 0, nrec = 0;
     bool is_op = false;
     if (p < count) {
       row = s.order[p];
@@ -278,37 +280,46 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
       if (is_op) {
 #pragma unroll
         for (int w = 0; w < W; ++w) ne += __popc(s.pred[row * W + w]);
+        nrec = ne == 0 ? 1 : (ne + kRecSlots - 1) / kRecSlots;
       }
     }
     const unsigned m = __ballot_sync(kFull, is_op);
-    const int op = op_base + __popc(m & ((1u << lane) - 1u));
-    // inclusive scan of edge counts within the chunk
-    int incl = ne;
+    int incl = nrec, incl_e = ne;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int t = __shfl_up_sync(kFull, incl, d);
-      if (lane >= d) incl += t;
+      const int te = __shfl_up_sync(kFull, incl_e, d);
+      if (lane >= d) { incl += t; incl_e += te; }
     }
-    const int eb = edge_base + incl - ne;
+    const int rb = rec_base + incl - nrec;
     if (is_op) {
-      Op o;
-      o.bias = float(nrow[row * kNodeCols + kBias]);
-      o.resp = float(nrow[row * kNodeCols + kResp]);
-      o.dst = uint16_t(row);
-      o.e_begin = uint16_t(eb);
-      o.e_end = uint16_t(eb + ne);
-      o.act = sh.act[int(nrow[row * kNodeCols + kAct])];
-      o.agg = sh.agg[int(nrow[row * kNodeCols + kAgg])];
-      gops[op] = o;
-      s.ebeg[row] = uint16_t(eb);
+      RecHeader h;
+      h.bias = float(nrow[row * kNodeCols + kBias]);
+      h.resp = float(nrow[row * kNodeCols + kResp]);
+      h.dst = uint16_t(row);
+      h.act = sh.act[int(nrow[row * kNodeCols + kAct])];
+      h.agg = sh.agg[int(nrow[row * kNodeCols + kAgg])];
+      h.fanin = uint16_t(ne);
+      for (int k = 0; k < nrec; ++k) {
+        h.cnt = uint8_t(min(kRecSlots, ne - k * kRecSlots > 0 ? ne - k * kRecSlots : 0));
+        h.flags = uint8_t((k == 0 ? kRecFirst : 0) | (k == nrec - 1 ? kRecLast : 0));
+        grec[rb + k].h = h;
+      }
+      Edge z;  // pad slots of the last record: zero weight, all-zero row N
+      z.w = 0.0f;
+      z.src = uint16_t(N);
+      z.conn_row = 0xffff;
+      for (int q = ne; q < nrec * kRecSlots; ++q) grec[rb + q / kRecSlots].slot[q % kRecSlots] = z;
+      s.ebeg[row] = uint16_t(rb);
     }
     op_base += __popc(m);
-    edge_base += __shfl_sync(kFull, incl, 31);
+    rec_base += __shfl_sync(kFull, incl, 31);
+    edge_total += __shfl_sync(kFull, incl_e, 31);
   }
   __syncwarp();
 
-  // ---- 7. edges: slot = op edge begin + rank of src among dst's predecessors
-  Edge* gedges = reinterpret_cast<Edge*>(net + L.edges_off);
+  // ---- 7. edges: the i-th predecessor (ascending source row) of an op goes
+  //         to slot i%4 of its record i/4
   for (int r = lane; r < C; r += 32) {
     const int dst = s.cdst[r];
     if (dst < 0 || (s.flags[dst] & 2)) continue;
@@ -325,7 +336,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     e.w = float(crow[r * kConnCols + kW]);
     e.src = uint16_t(src);
     e.conn_row = uint16_t(r);
-    gedges[s.ebeg[dst] + below] = e;
+    grec[s.ebeg[dst] + below / kRecSlots].slot[below % kRecSlots] = e;
   }
   if (lane == 0) {
     NetHeader* h = reinterpret_cast<NetHeader*>(net);
@@ -335,7 +346,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     h->err_b = 0;
     h->order_count = int16_t(count);
     h->n_ops = int16_t(op_base);
-    h->n_edges = int16_t(edge_base);
+    h->n_edges = int16_t(edge_total);
+    h->n_rec = int16_t(rec_base);
   }
 }
 
