@@ -32,7 +32,7 @@ extern "C" {
 #endif
 
 #define FNB_ABI_VERSION 1
-#define FNB_MAX_NODES_LIMIT 256   /* transform bitsets cover <= 256 rows */
+#define FNB_MAX_NODES_LIMIT 255   /* node rows fit a byte; row 255 is the forward's zero row */
 
 /* Errc (errors.hpp:10-31); status = 1 + code. */
 enum fnb_errc {
@@ -122,7 +122,39 @@ int fnb_evaluate(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns,
                  const double* inputs, const double* targets, int batch, int fitness_kind,
                  double fitness_offset, double* fitness_out);
 
+/* distance() (ops.hpp:415-473) of every genome against S representatives:
+ * out[P][S] = distance(genome_p, rep_s), FP64, bit-exact. */
+int fnb_distance(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
+                 const double* rep_nodes, const double* rep_conns, int S,
+                 const fnb_distance_config* cfg, double* out);
+
+/* crossover() (ops.hpp:382-407) of n parent pairs; keys[n][4] are RngKey
+ * words (rng.hpp:44-72).  child_* receive n genomes. */
+int fnb_crossover(fnb_ctx* ctx, const double* fit_nodes, const double* fit_conns,
+                  const double* other_nodes, const double* other_conns, int n, const uint32_t* keys,
+                  double* child_nodes, double* child_conns);
+
+/* RngKey(seed) and RngKey::split (rng.hpp:48-66), host side. */
+void fnb_key_seed(uint64_t seed, uint32_t out[4]);
+void fnb_key_split(const uint32_t key[4], uint64_t index, uint32_t out[4]);
+
 /* ---- device layer (asynchronous on `stream`, device pointers) ------------ */
+
+/* K3: d_out[P][S]. */
+int fnb_distance_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, int P,
+                   const double* d_rep_nodes, const double* d_rep_conns, int S,
+                   const fnb_distance_config* cfg, double* d_out, void* stream);
+/* K5: child c = crossover(pop[fit[c]], pop[other[c]], keys[c]). */
+int fnb_crossover_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, const int32_t* d_fit,
+                    const int32_t* d_other, const uint32_t* d_keys, int n, double* d_child_nodes,
+                    double* d_child_conns, void* stream);
+/* Sequential RngStream draws per key (parity tooling): kind 0 next_u64,
+ * 1 uniform() bits, 2 below(n).  d_out[n_keys][n_draws]. */
+int fnb_stream_draws_d(fnb_ctx* ctx, const uint32_t* d_keys, int n_keys, int n_draws, int kind,
+                       uint64_t n, uint64_t* d_out, void* stream);
+/* d_out[i] = key.split(base + i), i < n (RngKey tree on the device). */
+int fnb_split_keys_d(fnb_ctx* ctx, const uint32_t key[4], uint64_t base, int n, uint32_t* d_out,
+                     void* stream);
 
 /* K1: d_nets must hold P * fnb_net_bytes(ctx) bytes. */
 int fnb_transform_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, int P,

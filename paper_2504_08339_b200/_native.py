@@ -61,6 +61,14 @@ SIGNATURES = {
     "fnb_net_order_d": (C.c_int, [VP, VP, C.c_int, VP, VP, VP]),
     "fnb_check_nets_d": (C.c_int, [VP, VP, VP, VP, C.c_int, VP]),
     "fnb_forward_d": (C.c_int, [VP, VP, C.c_int, VP, VP, C.c_int, C.c_int, C.c_double, VP, VP, VP]),
+    "fnb_distance": (C.c_int, [VP, DP, DP, C.c_int, DP, DP, C.c_int, C.POINTER(fnb_distance_config), DP]),
+    "fnb_crossover": (C.c_int, [VP, DP, DP, DP, DP, C.c_int, U32P, DP, DP]),
+    "fnb_key_seed": (None, [C.c_uint64, U32P]),
+    "fnb_key_split": (None, [U32P, C.c_uint64, U32P]),
+    "fnb_distance_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.c_int, C.POINTER(fnb_distance_config), VP, VP]),
+    "fnb_crossover_d": (C.c_int, [VP, VP, VP, VP, VP, VP, C.c_int, VP, VP, VP]),
+    "fnb_stream_draws_d": (C.c_int, [VP, VP, C.c_int, C.c_int, C.c_int, C.c_uint64, VP, VP]),
+    "fnb_split_keys_d": (C.c_int, [VP, U32P, C.c_uint64, C.c_int, VP, VP]),
 }
 
 _lib = None

@@ -300,3 +300,93 @@ class Engine:
                                             fitness.data_ptr() if fitness is not None else None,
                                             out.data_ptr() if out is not None else None, _stream_handle(stream)))
         return fitness if fitness is not None else out
+
+
+# ---------------------------------------------------------------------------
+# RngKey tree (rng.hpp:44-72) -- host helpers over the C ABI
+# ---------------------------------------------------------------------------
+
+def key_seed(seed: int) -> np.ndarray:
+    """RngKey(seed).words() (rng.hpp:48-56)."""
+    out = np.zeros(4, dtype=np.uint32)
+    N.lib().fnb_key_seed(C.c_uint64(seed), out.ctypes.data_as(N.U32P))
+    return out
+
+
+def key_split(key, index: int) -> np.ndarray:
+    """RngKey::split(index).words() (rng.hpp:58-66)."""
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    N.lib().fnb_key_split(k.ctypes.data_as(N.U32P), C.c_uint64(index), out.ctypes.data_as(N.U32P))
+    return out
+
+
+def _engine_distance(self, pop_nodes, pop_conns, rep_nodes, rep_conns, cfg: DistanceConfig = DistanceConfig()):
+    """distance(genome_p, rep_s) (ops.hpp:415-473) -> [P, S], FP64 bit-exact."""
+    n, c, P = self._check_pop(pop_nodes, pop_conns)
+    rn, rc, S = self._check_pop(rep_nodes, rep_conns)
+    out = np.empty((P, S), dtype=np.float64)
+    cc = cfg.to_c()
+    self._raise(self._lib.fnb_distance(self._h, _dp(n), _dp(c), P, _dp(rn), _dp(rc), S, C.byref(cc), _dp(out)))
+    return out
+
+
+def _engine_crossover(self, fit_nodes, fit_conns, other_nodes, other_conns, keys):
+    """crossover(fit, other, key) (ops.hpp:382-407) for n pairs; keys [n, 4] uint32."""
+    fn, fc, n = self._check_pop(fit_nodes, fit_conns)
+    on, oc, n2 = self._check_pop(other_nodes, other_conns)
+    if n2 != n:
+        raise FlatneatError(9, "shape_mismatch: parents have different counts")
+    k = np.ascontiguousarray(keys, dtype=np.uint32).reshape(n, 4)
+    cn = np.empty_like(fn)
+    cc = np.empty_like(fc)
+    self._raise(self._lib.fnb_crossover(self._h, _dp(fn), _dp(fc), _dp(on), _dp(oc), n, k.ctypes.data_as(N.U32P),
+                                        _dp(cn), _dp(cc)))
+    return cn, cc
+
+
+def _engine_distance_d(self, nodes, conns, rep_nodes, rep_conns, out=None, cfg: DistanceConfig = DistanceConfig(),
+                       stream=None):
+    import torch
+    P, S = nodes.shape[0], rep_nodes.shape[0]
+    if out is None:
+        out = torch.empty((P, S), dtype=torch.float64, device=nodes.device)
+    cc = cfg.to_c()
+    self._raise(self._lib.fnb_distance_d(self._h, nodes.data_ptr(), conns.data_ptr(), P, rep_nodes.data_ptr(),
+                                         rep_conns.data_ptr(), S, C.byref(cc), out.data_ptr(), _stream_handle(stream)))
+    return out
+
+
+def _engine_crossover_d(self, nodes, conns, fit_idx, other_idx, keys, child_nodes, child_conns, stream=None):
+    n = fit_idx.shape[0]
+    self._raise(self._lib.fnb_crossover_d(self._h, nodes.data_ptr(), conns.data_ptr(), fit_idx.data_ptr(),
+                                          other_idx.data_ptr(), keys.data_ptr(), n, child_nodes.data_ptr(),
+                                          child_conns.data_ptr(), _stream_handle(stream)))
+    return child_nodes, child_conns
+
+
+def _engine_stream_draws_d(self, keys, n_draws: int, kind: int = 0, n: int = 0, stream=None):
+    import torch
+    nk = keys.shape[0]
+    out = torch.empty((nk, n_draws), dtype=torch.int64, device=keys.device)
+    self._raise(self._lib.fnb_stream_draws_d(self._h, keys.data_ptr(), nk, n_draws, kind, C.c_uint64(n),
+                                             out.data_ptr(), _stream_handle(stream)))
+    return out
+
+
+def _engine_split_keys_d(self, key, base: int, n: int, out=None, stream=None):
+    import torch
+    if out is None:
+        out = torch.empty((n, 4), dtype=torch.int32, device=f"cuda:{self.device}")
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    self._raise(self._lib.fnb_split_keys_d(self._h, k.ctypes.data_as(N.U32P), C.c_uint64(base), n, out.data_ptr(),
+                                           _stream_handle(stream)))
+    return out
+
+
+Engine.distance = _engine_distance
+Engine.crossover = _engine_crossover
+Engine.distance_d = _engine_distance_d
+Engine.crossover_d = _engine_crossover_d
+Engine.stream_draws_d = _engine_stream_draws_d
+Engine.split_keys_d = _engine_split_keys_d

@@ -68,7 +68,7 @@ struct fnb_ctx {
   int err_index = -1;
   long long launches = 0;
   cudaStream_t stream = nullptr;
-  DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc;
+  DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc, scratch;
 };
 
 static int fnb_cuda_fail_ctx(fnb_ctx* ctx, cudaError_t e, const char* what) {
@@ -140,7 +140,7 @@ void fnb_ctx_destroy(fnb_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->nodes, &ctx->conns, &ctx->nets, &ctx->X, &ctx->Y, &ctx->fit, &ctx->out,
-                    &ctx->partial, &ctx->misc})
+                    &ctx->partial, &ctx->misc, &ctx->scratch})
     b->release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -348,6 +348,135 @@ int fnb_evaluate(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns,
   if (fitness_kind == FNB_FIT_NONE) return set_err(ctx, FNB_E_CONFIG_ERROR, "fitness kind required", -1);
   return evaluate_impl(ctx, pop_nodes, pop_conns, P, inputs, targets, batch, fitness_kind, fitness_offset,
                        fitness_out, nullptr);
+}
+
+}  // extern "C"
+
+// ---- distance / crossover / rng ---------------------------------------------
+namespace fnb {
+cudaError_t launch_distance(const double* nodes, const double* conns, int P, const double* rn, const double* rc,
+                            int S, int N, int C, double cd, double ch, double* out, void* scratch,
+                            size_t scratch_bytes, cudaStream_t st);
+size_t distance_scratch_bytes(int S, int N, int C);
+cudaError_t launch_crossover(const double* nodes, const double* conns, const int32_t* fit, const int32_t* oth,
+                             const uint32_t* keys, int n, int N, int C, double* cn, double* cc, cudaStream_t st);
+cudaError_t launch_stream_draws(const uint32_t* keys, int n_keys, int n_draws, int kind, uint64_t n, uint64_t* out,
+                                cudaStream_t st);
+cudaError_t launch_split_keys(const uint32_t parent[4], uint64_t base, int n, uint32_t* out, cudaStream_t st);
+}  // namespace fnb
+
+#include "philox.cuh"
+
+extern "C" {
+
+void fnb_key_seed(uint64_t seed, uint32_t out[4]) {
+  const Key4 k = key_from_seed(seed);
+  for (int i = 0; i < 4; ++i) out[i] = k.w[i];
+}
+
+void fnb_key_split(const uint32_t key[4], uint64_t index, uint32_t out[4]) {
+  const Key4 k = key_split(Key4{{key[0], key[1], key[2], key[3]}}, index);
+  for (int i = 0; i < 4; ++i) out[i] = k.w[i];
+}
+
+int fnb_distance_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, int P, const double* d_rep_nodes,
+                   const double* d_rep_conns, int S, const fnb_distance_config* cfg, double* d_out, void* stream) {
+  if (P <= 0 || S <= 0) return 0;
+  if (S > 32) return set_err(ctx, FNB_E_CONFIG_ERROR, "at most 32 representatives per distance call", -1);
+  CK(cudaSetDevice(ctx->device));
+  const size_t need = distance_scratch_bytes(S, ctx->L.N, ctx->L.C);
+  CK(ctx->scratch.ensure(need));
+  CK(launch_distance(d_nodes, d_conns, P, d_rep_nodes, d_rep_conns, S, ctx->L.N, ctx->L.C,
+                     cfg->compatibility_disjoint, cfg->compatibility_homologous, d_out, ctx->scratch.p,
+                     ctx->scratch.cap, static_cast<cudaStream_t>(stream)));
+  ctx->launches += 2;
+  return 0;
+}
+
+int fnb_crossover_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, const int32_t* d_fit,
+                    const int32_t* d_other, const uint32_t* d_keys, int n, double* d_child_nodes,
+                    double* d_child_conns, void* stream) {
+  if (n <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_crossover(d_nodes, d_conns, d_fit, d_other, d_keys, n, ctx->L.N, ctx->L.C, d_child_nodes,
+                      d_child_conns, static_cast<cudaStream_t>(stream)));
+  ctx->launches++;
+  return 0;
+}
+
+int fnb_stream_draws_d(fnb_ctx* ctx, const uint32_t* d_keys, int n_keys, int n_draws, int kind, uint64_t n,
+                       uint64_t* d_out, void* stream) {
+  if (kind == 2 && n == 0) return set_err(ctx, FNB_E_CONFIG_ERROR, "below(0)", -1);
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_stream_draws(d_keys, n_keys, n_draws, kind, n, d_out, static_cast<cudaStream_t>(stream)));
+  ctx->launches++;
+  return 0;
+}
+
+int fnb_split_keys_d(fnb_ctx* ctx, const uint32_t key[4], uint64_t base, int n, uint32_t* d_out, void* stream) {
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_split_keys(key, base, n, d_out, static_cast<cudaStream_t>(stream)));
+  ctx->launches++;
+  return 0;
+}
+
+int fnb_distance(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P, const double* rep_nodes,
+                 const double* rep_conns, int S, const fnb_distance_config* cfg, double* out) {
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (P <= 0 || S <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  const size_t nb = sizeof(double) * ctx->L.N * kNodeCols, cb = sizeof(double) * ctx->L.C * kConnCols;
+  // population and representatives go up in one buffer pair: [pop | reps]
+  CK(ctx->nodes.ensure(nb * size_t(P + S)));
+  CK(ctx->conns.ensure(cb * size_t(P + S)));
+  CK(ctx->out.ensure(sizeof(double) * size_t(P) * S));
+  double* dn = static_cast<double*>(ctx->nodes.p);
+  double* dc = static_cast<double*>(ctx->conns.p);
+  CK(cudaMemcpyAsync(dn, pop_nodes, nb * P, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dc, pop_conns, cb * P, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dn) + nb * P, rep_nodes, nb * S, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dc) + cb * P, rep_conns, cb * S, cudaMemcpyHostToDevice, ctx->stream));
+  const int st = fnb_distance_d(ctx, dn, dc, P, reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(dn) + nb * P),
+                                reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(dc) + cb * P), S, cfg,
+                                static_cast<double*>(ctx->out.p), ctx->stream);
+  if (st) return st;
+  CK(cudaMemcpyAsync(out, ctx->out.p, sizeof(double) * size_t(P) * S, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int fnb_crossover(fnb_ctx* ctx, const double* fit_nodes, const double* fit_conns, const double* other_nodes,
+                  const double* other_conns, int n, const uint32_t* keys, double* child_nodes, double* child_conns) {
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (n <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  const size_t nb = sizeof(double) * ctx->L.N * kNodeCols, cb = sizeof(double) * ctx->L.C * kConnCols;
+  // parents as one 2n population [fit | other]; children after them
+  CK(ctx->nodes.ensure(nb * size_t(3 * n)));
+  CK(ctx->conns.ensure(cb * size_t(3 * n)));
+  CK(ctx->misc.ensure(sizeof(int32_t) * 2 * size_t(n) + sizeof(uint32_t) * 4 * size_t(n) + 64));
+  uint8_t* dn = static_cast<uint8_t*>(ctx->nodes.p);
+  uint8_t* dc = static_cast<uint8_t*>(ctx->conns.p);
+  CK(cudaMemcpyAsync(dn, fit_nodes, nb * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dn + nb * n, other_nodes, nb * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dc, fit_conns, cb * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dc + cb * n, other_conns, cb * n, cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<int32_t> idx(2 * size_t(n));
+  for (int i = 0; i < n; ++i) { idx[size_t(i)] = i; idx[size_t(n + i)] = n + i; }
+  int32_t* d_idx = static_cast<int32_t*>(ctx->misc.p);
+  uint32_t* d_keys = reinterpret_cast<uint32_t*>(d_idx + 2 * n);
+  CK(cudaMemcpyAsync(d_idx, idx.data(), sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d_keys, keys, sizeof(uint32_t) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+  const int st = fnb_crossover_d(ctx, reinterpret_cast<double*>(dn), reinterpret_cast<double*>(dc), d_idx,
+                                 d_idx + n, d_keys, n, reinterpret_cast<double*>(dn + 2 * nb * n),
+                                 reinterpret_cast<double*>(dc + 2 * cb * n), ctx->stream);
+  if (st) return st;
+  CK(cudaMemcpyAsync(child_nodes, dn + 2 * nb * n, nb * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(child_conns, dc + 2 * cb * n, cb * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return 0;
 }
 
 }  // extern "C"

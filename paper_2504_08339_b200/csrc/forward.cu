@@ -59,13 +59,15 @@ __device__ __forceinline__ float act_apply(int code, float x) {
   return x;
 }
 
-// ---- staged record (48 B, three float4) ------------------------------------
-//   h  = {bias, resp, dst_off | fanin << 20, cnt | flags << 8 | act << 16 | agg << 24}
-//   s01 = {w0, off0, w1, off1},  s23 = {w2, off2, w3, off3}   (off = byte offset of the row)
+// ---- staged record (32 B, two float4) ---------------------------------------
+//   a = {bias, resp, meta, srcs}   meta = dst | cnt << 8 | first << 11 | last << 12
+//                                         | act << 13 | agg << 16 | fanin << 18
+//                                  srcs = four u8 source rows (row N = zero row)
+//   w = {w0, w1, w2, w3}
 struct SRec {
-  float4 h, s01, s23;
+  float4 a, w;
 };
-static_assert(sizeof(SRec) == 48, "staged record");
+static_assert(sizeof(SRec) == 32, "staged record");
 
 template <int SPT> struct VecT;
 template <> struct VecT<1> { using T = float; };
@@ -85,6 +87,35 @@ __device__ __forceinline__ void vstore(uint8_t* base, uint32_t off, const float 
   if constexpr (SPT == 1) { *p = x[0]; }
   else if constexpr (SPT == 2) { *p = make_float2(x[0], x[1]); }
   else { *p = make_float4(x[0], x[1], x[2], x[3]); }
+}
+
+// Value-row traffic of the hot loop goes through volatile PTX so loads and
+// stores stay in program order (a node's result is read by later records),
+// and so pad-slot loads can be predicated off: a warp-uniform false
+// predicate issues the instruction but moves no shared-memory wavefronts.
+template <int SPT>
+__device__ __forceinline__ void lds_pred(bool p, uint32_t addr, float (&x)[SPT]) {
+  if constexpr (SPT == 1) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %1, 0; @q ld.shared.f32 %0, [%2]; }"
+                 : "+f"(x[0]) : "r"(int(p)), "r"(addr));
+  } else if constexpr (SPT == 2) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.shared.v2.f32 {%0, %1}, [%3]; }"
+                 : "+f"(x[0]), "+f"(x[1]) : "r"(int(p)), "r"(addr));
+  } else {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %4, 0; @q ld.shared.v4.f32 {%0, %1, %2, %3}, [%5]; }"
+                 : "+f"(x[0]), "+f"(x[1]), "+f"(x[2]), "+f"(x[3]) : "r"(int(p)), "r"(addr));
+  }
+}
+template <int SPT>
+__device__ __forceinline__ void sts(uint32_t addr, const float (&x)[SPT]) {
+  if constexpr (SPT == 1) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(x[0]));
+  } else if constexpr (SPT == 2) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(x[0]), "f"(x[1]));
+  } else {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(x[0]), "f"(x[1]), "f"(x[2]),
+                 "f"(x[3]));
+  }
 }
 
 struct FwdParams {
@@ -127,9 +158,10 @@ k_forward(FwdParams p) {
   double* s_red = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(s_io) +
                                             align16(size_t(L.I + L.O) * sizeof(uint32_t)));
   uint8_t* v = reinterpret_cast<uint8_t*>(s_red) + 8 * sizeof(double);
-  const int TC = T * SPT;                        // columns per tile
-  const uint32_t row_bytes = uint32_t(TC) * 4u;  // v row stride
-  const uint32_t my = uint32_t(j) * SPT * 4u;    // this thread's byte offset in a row
+  const int TC = T * SPT;                                 // columns per tile
+  const uint32_t row_shift = uint32_t(__ffs(TC * 4) - 1);  // v row stride = TC*4 bytes (a power of two)
+  const uint32_t row_bytes = uint32_t(TC) * 4u;
+  const uint32_t vb = uint32_t(__cvta_generic_to_shared(v)) + uint32_t(j) * SPT * 4u;  // my columns
 
   const bool live = grp < p.groups && g < p.P;
   int n_rec = 0;
@@ -139,29 +171,24 @@ k_forward(FwdParams p) {
     const Rec* gr = reinterpret_cast<const Rec*>(net + L.ops_off);
     for (int i = j; i < n_rec; i += T) {
       const Rec r = gr[i];
-      SRec s;
-      const uint32_t meta = uint32_t(r.h.cnt) | (uint32_t(r.h.flags) << 8) | (uint32_t(r.h.act) << 16) |
-                            (uint32_t(r.h.agg) << 24);
-      s.h = make_float4(r.h.bias, r.h.resp, __uint_as_float(uint32_t(r.h.dst) * row_bytes | (uint32_t(r.h.fanin) << 20)),
-                        __uint_as_float(meta));
-      s.s01 = make_float4(r.slot[0].w, __uint_as_float(uint32_t(r.slot[0].src) * row_bytes), r.slot[1].w,
-                          __uint_as_float(uint32_t(r.slot[1].src) * row_bytes));
-      s.s23 = make_float4(r.slot[2].w, __uint_as_float(uint32_t(r.slot[2].src) * row_bytes), r.slot[3].w,
-                          __uint_as_float(uint32_t(r.slot[3].src) * row_bytes));
-      s_rec[i] = s;
+      const uint32_t meta = uint32_t(r.h.dst) | (uint32_t(r.h.cnt) << 8) | (uint32_t(r.h.flags) << 11) |
+                            (uint32_t(r.h.act) << 13) | (uint32_t(r.h.agg) << 16) | (uint32_t(r.h.fanin) << 18);
+      const uint32_t srcs = uint32_t(r.slot[0].src) | (uint32_t(r.slot[1].src) << 8) |
+                            (uint32_t(r.slot[2].src) << 16) | (uint32_t(r.slot[3].src) << 24);
+      s_rec[i] = SRec{make_float4(r.h.bias, r.h.resp, __uint_as_float(meta), __uint_as_float(srcs)),
+                      make_float4(r.slot[0].w, r.slot[1].w, r.slot[2].w, r.slot[3].w)};
     }
-    if (j == 0) s_rec[n_rec] = SRec{make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
+    if (j == 0) s_rec[n_rec] = SRec{make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0)};
     const uint16_t* sio = reinterpret_cast<const uint16_t*>(net + L.in_off);
-    for (int i = j; i < L.I + L.O; i += T) s_io[i] = uint32_t(sio[i]) * row_bytes;
+    for (int i = j; i < L.I + L.O; i += T) s_io[i] = uint32_t(sio[i]) << row_shift;
     float z[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) z[k] = 0.0f;
-    vstore<SPT>(v, uint32_t(L.N) * row_bytes + my, z);  // the all-zero pad row
+    sts<SPT>(vb + (uint32_t(L.N) << row_shift), z);  // the all-zero pad row
   }
   __syncthreads();
 
   const int I = L.I, O = L.O;
-  const uint8_t* vb = v + my;  // this thread's columns
   double err = 0.0;
   // sample tiles of this CTA's y-chunk; dead groups (g >= P) run zero tiles
   // but stay resident for the warp-synchronous reduction below
@@ -176,42 +203,45 @@ k_forward(FwdParams p) {
       float x[SPT];
 #pragma unroll
       for (int k = 0; k < SPT; ++k) x[k] = (s0 + k < p.B) ? __ldg(p.X + size_t(s0 + k) * I + i) : 0.0f;
-      vstore<SPT>(v, s_io[i] + my, x);
+      sts<SPT>(vb + s_io[i], x);
     }
-    // ops in topological order (network.hpp:252-264), one record per step,
-    // the next record prefetched
+    // ops in topological order (network.hpp:252-264), one record per step.
+    // cur.w is reloaded once this record's FMAs are done and cur.a after its
+    // finalize, so the next record's fetch overlaps this record's activation.
     float acc[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) acc[k] = 0.0f;
-    // cur.s01/s23 (edge slots) are reloaded as soon as their value loads and
-    // FMAs are done and cur.h after the finalize, so the next record's fetch
-    // overlaps this record's activation without extra registers or moves.
     SRec cur = s_rec[0];
 #pragma unroll 1
     for (int r = 0; r < n_rec; ++r) {
-      const uint32_t meta = __float_as_uint(cur.h.w);
-      const bool first = (meta >> 8) & kRecFirst;
-      const bool last = (meta >> 8) & kRecLast;
-      const int agg = AGG >= 0 ? AGG : int(meta >> 24);
+      const uint32_t meta = __float_as_uint(cur.a.z);
+      const uint32_t srcs = __float_as_uint(cur.a.w);
+      const int cnt = int((meta >> 8) & 7u);
+      const bool first = (meta >> 11) & 1u;
+      const bool last = (meta >> 12) & 1u;
+      const int agg = AGG >= 0 ? AGG : int((meta >> 16) & 3u);
       float x0[SPT], x1[SPT], x2[SPT], x3[SPT];
-      vload<SPT>(vb, __float_as_uint(cur.s01.y), x0);
-      vload<SPT>(vb, __float_as_uint(cur.s01.w), x1);
-      vload<SPT>(vb, __float_as_uint(cur.s23.y), x2);
-      vload<SPT>(vb, __float_as_uint(cur.s23.w), x3);
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) x0[k] = x1[k] = x2[k] = x3[k] = 0.0f;
+      // pad slots are predicated off (no shared-memory traffic), reading 0
+      // one PRMT (byte extract) + one IMAD (row address) per slot
+      lds_pred<SPT>(cnt > 0, vb + __byte_perm(srcs, 0u, 0x4440) * row_bytes, x0);
+      lds_pred<SPT>(cnt > 1, vb + __byte_perm(srcs, 0u, 0x4441) * row_bytes, x1);
+      lds_pred<SPT>(cnt > 2, vb + __byte_perm(srcs, 0u, 0x4442) * row_bytes, x2);
+      lds_pred<SPT>(cnt > 3, vb + __byte_perm(srcs, 0u, 0x4443) * row_bytes, x3);
       if (agg == FNB_AGG_SUM || agg == FNB_AGG_MEAN) {
-        // pad slots contribute 0 * 0: branch-free
+        // pad slots contribute 0 * 0: branch-free, ascending source row
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
           float a = first ? 0.0f : acc[k];
-          a = fmaf(cur.s01.x, x0[k], a);
-          a = fmaf(cur.s01.z, x1[k], a);
-          a = fmaf(cur.s23.x, x2[k], a);
-          a = fmaf(cur.s23.z, x3[k], a);
+          a = fmaf(cur.w.x, x0[k], a);
+          a = fmaf(cur.w.y, x1[k], a);
+          a = fmaf(cur.w.z, x2[k], a);
+          a = fmaf(cur.w.w, x3[k], a);
           acc[k] = a;
         }
       } else {
-        const int cnt = int(meta & 0xff);
-        const float w[4] = {cur.s01.x, cur.s01.z, cur.s23.x, cur.s23.z};
+        const float w[4] = {cur.w.x, cur.w.y, cur.w.z, cur.w.w};
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
           const float xs[4] = {x0[k], x1[k], x2[k], x3[k]};
@@ -232,12 +262,10 @@ k_forward(FwdParams p) {
           }
         }
       }
-      cur.s01 = s_rec[r + 1].s01;
-      cur.s23 = s_rec[r + 1].s23;
+      cur.w = s_rec[r + 1].w;
       if (last) {
-        const uint32_t dw = __float_as_uint(cur.h.z);
         if (agg == FNB_AGG_MEAN) {
-          const uint32_t fanin = dw >> 20;
+          const uint32_t fanin = meta >> 18;
           if (fanin > 0) {
             const float n = float(fanin);
 #pragma unroll
@@ -246,15 +274,16 @@ k_forward(FwdParams p) {
         }
         float y[SPT];
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) y[k] = act_apply<ACT>(int((meta >> 16) & 0xff), fmaf(cur.h.y, acc[k], cur.h.x));
-        vstore<SPT>(v, (dw & 0xfffffu) + my, y);
+        for (int k = 0; k < SPT; ++k)
+          y[k] = act_apply<ACT>(int((meta >> 13) & 7u), fmaf(cur.a.y, acc[k], cur.a.x));
+        sts<SPT>(vb + ((meta & 0xffu) << row_shift), y);
       }
-      cur.h = s_rec[r + 1].h;
+      cur.a = s_rec[r + 1].a;
     }
     // outputs + fitness epilogue
     for (int o = 0; o < O; ++o) {
       float val[SPT];
-      vload<SPT>(vb, s_io[I + o], val);
+      lds_pred<SPT>(true, vb + s_io[I + o], val);
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         const int s = s0 + k;

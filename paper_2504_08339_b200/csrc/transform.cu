@@ -360,7 +360,7 @@ __global__ void k_describe_cycle(const double* __restrict__ nodes, const double*
   const int N = L.N, C = L.C;
   const NetHeader* h = reinterpret_cast<const NetHeader*>(net);
   const uint16_t* order = reinterpret_cast<const uint16_t*>(net + L.order_off);
-  uint32_t emitted[FNB_MAX_NODES_LIMIT / 32] = {0};
+  uint32_t emitted[(FNB_MAX_NODES_LIMIT + 32) / 32] = {0};
   for (int i = 0; i < h->order_count; ++i) emitted[order[i] >> 5] |= 1u << (order[i] & 31);
   auto empty = [&](int r) { return isnan(nodes[r * kNodeCols]); };
   auto key_of = [&](int r) { return int(nodes[r * kNodeCols]); };
@@ -369,7 +369,7 @@ __global__ void k_describe_cycle(const double* __restrict__ nodes, const double*
   for (int r = 0; r < N; ++r)
     if (!empty(r) && !is_em(r) && (start < 0 || key_of(r) < key_of(start))) start = r;
   if (start < 0) { path_out[0] = -1; return; }
-  int16_t pos[FNB_MAX_NODES_LIMIT];
+  int16_t pos[FNB_MAX_NODES_LIMIT + 1];
   for (int r = 0; r < N; ++r) pos[r] = -1;
   int len = 0;
   int at = start;

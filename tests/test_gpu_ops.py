@@ -1,0 +1,119 @@
+"""GPU parity for the device RNG (philox.cuh), K3 distance and K5 crossover.
+
+All three are bit-exact against the reference (oracle/_ref when present,
+else the pinned C restatement)."""
+import numpy as np
+import pytest
+
+import oracle_lib as ol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fnb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_08339_b200 as m
+    return m
+
+
+def _engine(fnb, prob, schema):
+    return fnb.Engine(fnb.GenomeLimits(prob.max_nodes, prob.max_conns), prob.input_keys, prob.output_keys,
+                      fnb.AttributeSchema(list(schema.activations), list(schema.aggregations)))
+
+
+def test_host_key_tree_matches_reference(fnb):
+    from paper_2504_08339_b200.api import key_seed, key_split
+    for seed in (0, 1, 42, 2**40 + 3):
+        k = key_seed(seed)
+        assert np.array_equal(k, ol.key_words(ol.key_seed(seed)))
+        for i in (0, 5, 2**33 + 1):
+            assert np.array_equal(key_split(k, i), ol.key_words(ol.key_split(ol.key_seed(seed), i)))
+
+
+def test_device_streams_match_reference(fnb):
+    import torch
+    prob = ol.Problem(8, 8, [0], [1])
+    eng = _engine(fnb, prob, ol.SchemaSpec())
+    root = ol.key_seed(7)
+    keys = np.stack([ol.key_words(ol.key_split(root, i)) for i in range(64)])
+    dk = torch.from_numpy(keys.view(np.int32)).cuda()
+    # split_keys_d reproduces RngKey::split on the device
+    sk = eng.split_keys_d(ol.key_words(root), 0, 64).cpu().numpy().view(np.uint32)
+    assert np.array_equal(sk, keys)
+    u = eng.stream_draws_d(dk, 33, kind=0).cpu().numpy().view(np.uint64)
+    b = eng.stream_draws_d(dk, 33, kind=2, n=3 * 2**61).cpu().numpy().view(np.uint64)
+    f = eng.stream_draws_d(dk, 33, kind=1).cpu().numpy().view(np.float64)
+    for i in range(64):
+        s = ol.stream(ol.key_from_words(keys[i]))
+        assert [ol.oracle().fo_next_u64(ol.C.byref(s)) for _ in range(33)] == [int(x) for x in u[i]]
+        s = ol.stream(ol.key_from_words(keys[i]))
+        assert [ol.oracle().fo_below(ol.C.byref(s), 3 * 2**61) for _ in range(33)] == [int(x) for x in b[i]]
+        s = ol.stream(ol.key_from_words(keys[i]))
+        assert [ol.oracle().fo_uniform(ol.C.byref(s)) for _ in range(33)] == list(f[i])
+
+
+@pytest.mark.parametrize("seed,limits", [(31, (20, 80)), (2024, (64, 256))])
+def test_distance_bit_exact(fnb, seed, limits):
+    schema = ol.SchemaSpec(["tanh", "identity", "sigmoid"], ["sum", "product"])
+    prob = ol.Problem(limits[0], limits[1], [0, 1, 2], [3])
+    nodes, conns = ol.random_genomes(seed, schema, 120, *limits)
+    # representatives: genomes from the same pool plus mutated relatives
+    cfg = ol.mut_cfg(node_add=0.5, conn_add=0.5, node_delete=0.2, conn_delete=0.2)
+    keys = np.stack([ol.key_words(ol.key_split(ol.key_seed(seed), i)) for i in range(120)])
+    st, _, _, mn, mc = ol.mutate_population(prob, schema, nodes, conns, keys, cfg, 1000)
+    assert st == 0
+    reps_n = np.concatenate([nodes[:5], mn[5:10]])
+    reps_c = np.concatenate([conns[:5], mc[5:10]])
+    got = _engine(fnb, prob, schema).distance(mn, mc, reps_n, reps_c)
+    use_ref = ol.ref_available()
+    for p in range(mn.shape[0]):
+        for s in range(reps_n.shape[0]):
+            want = ol.distance(prob, mn[p], mc[p], reps_n[s], reps_c[s], use_ref=use_ref)
+            assert got[p, s] == want, (p, s, got[p, s], want)
+
+
+def test_distance_known_answer(fnb):
+    """test_ops.cpp:244-255: identical genomes -> 0, one extra node -> 1/5."""
+    schema = ol.SchemaSpec(["tanh", "identity"], ["sum"])
+    prob = ol.Problem(8, 8, [0], [1])
+    n = np.full((1, 8, 5), np.nan)
+    for k in range(4):
+        n[0, k] = [k, 0.0, 1.0, 0, 0]
+    c = np.full((1, 8, 4), np.nan)
+    n2 = n.copy()
+    n2[0, 4] = [9, 0.0, 1.0, 0, 0]
+    eng = _engine(fnb, prob, schema)
+    assert eng.distance(n, c, n, c)[0, 0] == 0.0
+    assert eng.distance(n, c, n2, c)[0, 0] == 1.0 / 5.0
+
+
+@pytest.mark.parametrize("seed,limits", [(88, (20, 80)), (5, (64, 256))])
+def test_crossover_bit_exact(fnb, seed, limits):
+    schema = ol.SchemaSpec(["tanh", "identity"], ["sum"])
+    prob = ol.Problem(limits[0], limits[1], [0, 1, 2], [3])
+    nodes, conns = ol.random_genomes(seed, schema, 80, *limits)
+    # related parents (shared markers) from a mutation step
+    keys = np.stack([ol.key_words(ol.key_split(ol.key_seed(seed + 1), i)) for i in range(80)])
+    st, _, _, mn, mc = ol.mutate_population(prob, schema, nodes, conns, keys, ol.mut_cfg(), 500)
+    assert st == 0
+    ck = np.stack([ol.key_words(ol.key_split(ol.key_seed(9), t)) for t in range(80)])
+    cn, cc = _engine(fnb, prob, schema).crossover(nodes, conns, mn, mc, ck)
+    use_ref = ol.ref_available()
+    for t in range(80):
+        wn, wc = ol.crossover(prob, nodes[t], conns[t], mn[t], mc[t], ol.key_from_words(ck[t]), use_ref=use_ref)
+        np.testing.assert_array_equal(cn[t], wn)
+        np.testing.assert_array_equal(cc[t], wc)
+
+
+def test_crossover_identical_parents(fnb):
+    """test_ops.cpp:198-204: identical parents give an identical child."""
+    schema = ol.SchemaSpec(["tanh", "identity"], ["sum"])
+    prob = ol.Problem(20, 80, [0, 1, 2], [3])
+    nodes, conns = ol.random_genomes(3, schema, 16, 20, 80)
+    ck = np.stack([ol.key_words(ol.key_split(ol.key_seed(1), t)) for t in range(16)])
+    cn, cc = _engine(fnb, prob, schema).crossover(nodes, conns, nodes, conns, ck)
+    np.testing.assert_array_equal(cn, nodes)
+    np.testing.assert_array_equal(cc, conns)
