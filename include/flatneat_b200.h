@@ -134,6 +134,14 @@ int fnb_crossover(fnb_ctx* ctx, const double* fit_nodes, const double* fit_conns
                   const double* other_nodes, const double* other_conns, int n, const uint32_t* keys,
                   double* child_nodes, double* child_conns);
 
+/* mutate() (ops.hpp:363-374) of P genomes in slot order with ONE
+ * InnovationTable starting at *next_key (the population pattern of
+ * ops.hpp:169-175), in place; keys[P][4] RngKey words.  On return *next_key
+ * is the table's next key.  On error genomes below the failing index are
+ * mutated and the rest untouched, as a sequential loop would leave them. */
+int fnb_mutate(fnb_ctx* ctx, double* pop_nodes, double* pop_conns, int P, const uint32_t* keys,
+               const fnb_mutation_config* cfg, int* next_key);
+
 /* RngKey(seed) and RngKey::split (rng.hpp:48-66), host side. */
 void fnb_key_seed(uint64_t seed, uint32_t out[4]);
 void fnb_key_split(const uint32_t key[4], uint64_t index, uint32_t out[4]);
@@ -148,6 +156,14 @@ int fnb_distance_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, i
 int fnb_crossover_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, const int32_t* d_fit,
                     const int32_t* d_other, const uint32_t* d_keys, int n, double* d_child_nodes,
                     double* d_child_conns, void* stream);
+/* K6+K7: mutate P genomes in place (child c uses keys[c]); d_active[c] = 0
+ * skips a child (elites; NULL = all).  d_next_key: 2 ints, [0] is the
+ * InnovationTable counter (advanced in place), [1] scratch.  d_status[P]
+ * receives 0 or 1 + Errc per child.  d_new_key[P] (may be NULL) receives the
+ * key handed to each splitting child. */
+int fnb_mutate_d(fnb_ctx* ctx, double* d_nodes, double* d_conns, int P, const uint32_t* d_keys,
+                 const uint8_t* d_active, const fnb_mutation_config* cfg, int* d_next_key, int* d_status,
+                 int* d_new_key, void* stream);
 /* Sequential RngStream draws per key (parity tooling): kind 0 next_u64,
  * 1 uniform() bits, 2 below(n).  d_out[n_keys][n_draws]. */
 int fnb_stream_draws_d(fnb_ctx* ctx, const uint32_t* d_keys, int n_keys, int n_draws, int kind,

@@ -67,6 +67,8 @@ SIGNATURES = {
     "fnb_key_split": (None, [U32P, C.c_uint64, U32P]),
     "fnb_distance_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.c_int, C.POINTER(fnb_distance_config), VP, VP]),
     "fnb_crossover_d": (C.c_int, [VP, VP, VP, VP, VP, VP, C.c_int, VP, VP, VP]),
+    "fnb_mutate": (C.c_int, [VP, DP, DP, C.c_int, U32P, C.POINTER(fnb_mutation_config), C.POINTER(C.c_int)]),
+    "fnb_mutate_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.POINTER(fnb_mutation_config), VP, VP, VP, VP]),
     "fnb_stream_draws_d": (C.c_int, [VP, VP, C.c_int, C.c_int, C.c_int, C.c_uint64, VP, VP]),
     "fnb_split_keys_d": (C.c_int, [VP, U32P, C.c_uint64, C.c_int, VP, VP]),
 }

@@ -390,3 +390,36 @@ Engine.distance_d = _engine_distance_d
 Engine.crossover_d = _engine_crossover_d
 Engine.stream_draws_d = _engine_stream_draws_d
 Engine.split_keys_d = _engine_split_keys_d
+
+
+def _engine_mutate(self, pop_nodes, pop_conns, keys, cfg: MutationConfig = MutationConfig(), next_key: int = 0):
+    """mutate() of every genome in slot order with one InnovationTable(next_key)
+    (ops.hpp:363-374, 169-175) -> (nodes, conns, next_key).  Raises
+    FlatneatError at the lowest failing genome (its .index)."""
+    n = np.array(pop_nodes, dtype=np.float64, copy=True, order="C")
+    c = np.array(pop_conns, dtype=np.float64, copy=True, order="C")
+    P = n.shape[0]
+    self._check_pop(n, c)
+    k = np.ascontiguousarray(keys, dtype=np.uint32).reshape(P, 4)
+    nk = C.c_int(next_key)
+    mc = cfg.to_c()
+    st = self._lib.fnb_mutate(self._h, _dp(n), _dp(c), P, k.ctypes.data_as(N.U32P), C.byref(mc), C.byref(nk))
+    if st:
+        err = FlatneatError(st, self._lib.fnb_last_error(self._h).decode(), int(self._lib.fnb_last_error_index(self._h)))
+        err.partial = (n, c, nk.value)
+        raise err
+    return n, c, nk.value
+
+
+def _engine_mutate_d(self, nodes, conns, keys, next_key, status, cfg: MutationConfig = MutationConfig(),
+                     active=None, new_key=None, stream=None):
+    P = nodes.shape[0]
+    mc = cfg.to_c()
+    self._raise(self._lib.fnb_mutate_d(self._h, nodes.data_ptr(), conns.data_ptr(), P, keys.data_ptr(),
+                                       active.data_ptr() if active is not None else None, C.byref(mc),
+                                       next_key.data_ptr(), status.data_ptr(),
+                                       new_key.data_ptr() if new_key is not None else None, _stream_handle(stream)))
+
+
+Engine.mutate = _engine_mutate
+Engine.mutate_d = _engine_mutate_d

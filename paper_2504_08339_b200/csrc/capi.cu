@@ -480,3 +480,79 @@ int fnb_crossover(fnb_ctx* ctx, const double* fit_nodes, const double* fit_conns
 }
 
 }  // extern "C"
+
+// ---- mutation -----------------------------------------------------------------
+namespace fnb {
+size_t mutate_scratch_bytes(int n);
+cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, int n, const uint8_t* active,
+                          const fnb_mutation_config* m, const DevShape& sh, int* d_next_key, int* d_status,
+                          void* scratch, size_t scratch_bytes, int* d_new_key_out, cudaStream_t st,
+                          long long* launches);
+}  // namespace fnb
+
+extern "C" {
+
+int fnb_mutate_d(fnb_ctx* ctx, double* d_nodes, double* d_conns, int P, const uint32_t* d_keys,
+                 const uint8_t* d_active, const fnb_mutation_config* cfg, int* d_next_key, int* d_status,
+                 int* d_new_key, void* stream) {
+  if (P <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->scratch.ensure(mutate_scratch_bytes(P)));
+  CK(launch_mutate(d_nodes, d_conns, d_keys, P, d_active, cfg, ctx->sh, d_next_key, d_status, ctx->scratch.p,
+                   ctx->scratch.cap, d_new_key, static_cast<cudaStream_t>(stream), &ctx->launches));
+  return 0;
+}
+
+int fnb_mutate(fnb_ctx* ctx, double* pop_nodes, double* pop_conns, int P, const uint32_t* keys,
+               const fnb_mutation_config* cfg, int* next_key) {
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (P <= 0) return 0;
+  CK(cudaSetDevice(ctx->device));
+  const size_t nb = sizeof(double) * ctx->L.N * kNodeCols * size_t(P);
+  const size_t cb = sizeof(double) * ctx->L.C * kConnCols * size_t(P);
+  CK(ctx->nodes.ensure(nb));
+  CK(ctx->conns.ensure(cb));
+  // misc: keys [4P] | status [P] | new_key [P] | next_key [2]
+  CK(ctx->misc.ensure(sizeof(uint32_t) * 4 * size_t(P) + sizeof(int) * (2 * size_t(P) + 2) + 64));
+  uint32_t* d_keys = static_cast<uint32_t*>(ctx->misc.p);
+  int* d_status = reinterpret_cast<int*>(d_keys + 4 * size_t(P));
+  int* d_newk = d_status + P;
+  int* d_nk = d_newk + P;
+  const int nk2[2] = {*next_key, 0};
+  CK(cudaMemcpyAsync(ctx->nodes.p, pop_nodes, nb, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->conns.p, pop_conns, cb, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d_keys, keys, sizeof(uint32_t) * 4 * size_t(P), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d_nk, nk2, sizeof(nk2), cudaMemcpyHostToDevice, ctx->stream));
+  int st = fnb_mutate_d(ctx, static_cast<double*>(ctx->nodes.p), static_cast<double*>(ctx->conns.p), P, d_keys,
+                        nullptr, cfg, d_nk, d_status, d_newk, ctx->stream);
+  if (st) return st;
+  std::vector<int> status(static_cast<size_t>(P)), newk(static_cast<size_t>(P));
+  CK(cudaMemcpyAsync(status.data(), d_status, sizeof(int) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(newk.data(), d_newk, sizeof(int) * P, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int bad = -1;
+  for (int i = 0; i < P; ++i)
+    if (status[size_t(i)]) { bad = i; break; }
+  const int done = bad < 0 ? P : bad;  // genomes [0, done) keep their mutation
+  const size_t nrow = size_t(ctx->L.N) * kNodeCols, crow = size_t(ctx->L.C) * kConnCols;
+  if (done > 0) {
+    CK(cudaMemcpyAsync(pop_nodes, ctx->nodes.p, sizeof(double) * nrow * done, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(pop_conns, ctx->conns.p, sizeof(double) * crow * done, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  // table state after slots [0, done] (the failing slot assigned before throwing)
+  int nk = *next_key;
+  for (int i = 0; i <= (bad < 0 ? P - 1 : bad); ++i)
+    if (newk[size_t(i)] >= 0) nk = std::max(nk, newk[size_t(i)] + 1);
+  *next_key = nk;
+  if (bad >= 0) {
+    const int code = status[size_t(bad)] - 1;
+    return set_err(ctx, code, code == FNB_E_DUPLICATE_KEY ? "node key collides with the innovation counter"
+                                                           : "mutation failed",
+                   bad);
+  }
+  return 0;
+}
+
+}  // extern "C"
