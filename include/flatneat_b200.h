@@ -88,7 +88,24 @@ typedef struct fnb_distance_config {
   double compatibility_disjoint, compatibility_homologous;
 } fnb_distance_config;
 
+/* NeatConfig (Table 4 / Appendix C defaults in the Python
+ * mirror).  Input keys must be 0..I-1 and output keys I..I+O-1. */
+typedef struct fnb_neat_config {
+  int pop_size;
+  int max_species;              /* <= 32 */
+  double compatibility_threshold;
+  int species_elitism;
+  int max_stagnation;
+  int genome_elitism;
+  double survival_threshold;
+  double spawn_number_change_rate;
+  int output_activation;        /* registry id given to output nodes at init */
+  fnb_mutation_config mutation;
+  fnb_distance_config distance;
+} fnb_neat_config;
+
 typedef struct fnb_ctx fnb_ctx;
+typedef struct fnb_evolver fnb_evolver;
 
 /* ---- context --------------------------------------------------------- */
 int fnb_abi_version(void);
@@ -187,6 +204,33 @@ int fnb_check_nets_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns,
 int fnb_forward_d(fnb_ctx* ctx, const void* d_nets, int P, const float* d_X, const float* d_Y,
                   int batch, int fitness_kind, double fitness_offset, double* d_fitness,
                   double* d_out, void* stream);
+
+/* ---- the generation loop (PAPER Algorithm 1) -------------
+ * An evolver owns a device-resident population of cfg->pop_size genomes, the
+ * species state (<= 32 species), the fitness vector and the innovation
+ * counter.  Semantics are the frozen restatement oracle/evolution.c (rules
+ * E1-E5 in DESIGN.md): evaluate -> step (speciate, update_stagnation,
+ * compute_spawn_counts, reproduce) -> next generation. */
+int fnb_evolver_create(fnb_ctx* ctx, const fnb_neat_config* cfg, uint64_t seed, fnb_evolver** out);
+void fnb_evolver_destroy(fnb_evolver* ev);
+int fnb_evolver_init_population(fnb_evolver* ev);  /* initialize_population */
+int fnb_evolver_set_population(fnb_evolver* ev, const double* pop_nodes, const double* pop_conns);
+int fnb_evolver_get_population(fnb_evolver* ev, double* pop_nodes, double* pop_conns);
+int fnb_evolver_set_fitness(fnb_evolver* ev, const double* fitness);  /* inject (parity tests) */
+int fnb_evolver_get_fitness(fnb_evolver* ev, double* fitness);
+/* transform + forward + fitness of the current population */
+int fnb_evolver_evaluate(fnb_evolver* ev, const double* inputs, const double* targets, int batch,
+                         int fitness_kind, double fitness_offset);
+int fnb_evolver_evaluate_d(fnb_evolver* ev, const float* d_X, const float* d_Y, int batch, int fitness_kind,
+                           double fitness_offset);
+int fnb_evolver_step(fnb_evolver* ev);
+/* species arrays have room for 32 entries; species_of[pop_size] may be NULL */
+int fnb_evolver_species(fnb_evolver* ev, int* count, int* ids, int* sizes, int* spawn, double* best,
+                        int* stagnation, int* species_of);
+int fnb_evolver_state(fnb_evolver* ev, int* generation, int* next_key);
+/* device pointers of the current population / fitness and the evolver's stream */
+int fnb_evolver_device_state(fnb_evolver* ev, double** d_nodes, double** d_conns, double** d_fitness,
+                             void** stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@
  *     the species_elitism best (max fitness desc, ties lower id); at least
  *     one species always survives.
  *  E4 spawn: rank r_i of (fitness asc, index asc) normalised r/(P-1);
- *     species mean (member index order); target = P * af/sum(af); clamp to
+ *     species mean = exact integer rank sum / ((P-1) n_j); target = P * af/sum(af); clamp to
  *     old +- round(rate*old); rescale to P; largest remainder (ties lower
  *     id); raise to genome_elitism, taking surplus from the largest
  *     allocation (ties highest id).
@@ -271,21 +271,28 @@ void fo_compute_spawn(const fo_neat_cfg* cfg, const double* fitness,
                       const int* species_of, fo_species* s) {
   const int P = cfg->pop_size;
   const int S = s->count;
+  /* rank r_i of (fitness asc, index asc); the species mean of r_i/(P-1) is
+   * formed from the EXACT integer rank sum, so the value does not depend on
+   * summation order: af_j = double(sum r_i) / (double(P-1) * double(n_j)). */
   fi_t* ord = (fi_t*)malloc(sizeof(fi_t) * (size_t)P);
-  double* rn = (double*)malloc(sizeof(double) * (size_t)P);
+  long long* rk = (long long*)malloc(sizeof(long long) * (size_t)P);
   for (int i = 0; i < P; ++i) { ord[i].f = fitness[i]; ord[i].i = i; }
   qsort(ord, (size_t)P, sizeof(fi_t), fi_asc);
-  for (int r = 0; r < P; ++r) rn[ord[r].i] = (double)r / (double)(P - 1);
+  for (int r = 0; r < P; ++r) rk[ord[r].i] = r;
+  long long* rsum = (long long*)calloc((size_t)S, sizeof(long long));
   double* af = (double*)calloc((size_t)S, sizeof(double));
   int* cnt = (int*)calloc((size_t)S, sizeof(int));
   for (int i = 0; i < P; ++i) {
     const int j = species_of[i];
     if (j < 0) continue;
-    af[j] += rn[i];
+    rsum[j] += rk[i];
     cnt[j]++;
   }
   double total = 0.0;
-  for (int j = 0; j < S; ++j) { af[j] = af[j] / (double)cnt[j]; total += af[j]; }
+  for (int j = 0; j < S; ++j) {
+    af[j] = (double)rsum[j] / ((double)(P - 1) * (double)cnt[j]);
+    total += af[j];
+  }
   double* nw = (double*)malloc(sizeof(double) * (size_t)S);
   double sum_new = 0.0;
   for (int j = 0; j < S; ++j) {
@@ -329,7 +336,7 @@ void fo_compute_spawn(const fo_neat_cfg* cfg, const double* fitness,
     s->spawn[b]--;
     --tot;
   }
-  free(ord); free(rn); free(af); free(cnt); free(nw); free(frac);
+  free(ord); free(rk); free(rsum); free(af); free(cnt); free(nw); free(frac);
 }
 
 int fo_reproduce(const fo_shape* sh, const fo_schema* sc, const fo_neat_cfg* cfg,

@@ -39,6 +39,14 @@ class fnb_distance_config(C.Structure):
     _fields_ = [("compatibility_disjoint", C.c_double), ("compatibility_homologous", C.c_double)]
 
 
+class fnb_neat_config(C.Structure):
+    _fields_ = [("pop_size", C.c_int), ("max_species", C.c_int), ("compatibility_threshold", C.c_double),
+                ("species_elitism", C.c_int), ("max_stagnation", C.c_int), ("genome_elitism", C.c_int),
+                ("survival_threshold", C.c_double), ("spawn_number_change_rate", C.c_double),
+                ("output_activation", C.c_int), ("mutation", fnb_mutation_config),
+                ("distance", fnb_distance_config)]
+
+
 VP = C.c_void_p
 DP = C.POINTER(C.c_double)
 IP = C.POINTER(C.c_int32)
@@ -69,6 +77,19 @@ SIGNATURES = {
     "fnb_crossover_d": (C.c_int, [VP, VP, VP, VP, VP, VP, C.c_int, VP, VP, VP]),
     "fnb_mutate": (C.c_int, [VP, DP, DP, C.c_int, U32P, C.POINTER(fnb_mutation_config), C.POINTER(C.c_int)]),
     "fnb_mutate_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.POINTER(fnb_mutation_config), VP, VP, VP, VP]),
+    "fnb_evolver_create": (C.c_int, [VP, C.POINTER(fnb_neat_config), C.c_uint64, C.POINTER(VP)]),
+    "fnb_evolver_destroy": (None, [VP]),
+    "fnb_evolver_init_population": (C.c_int, [VP]),
+    "fnb_evolver_set_population": (C.c_int, [VP, DP, DP]),
+    "fnb_evolver_get_population": (C.c_int, [VP, DP, DP]),
+    "fnb_evolver_set_fitness": (C.c_int, [VP, DP]),
+    "fnb_evolver_get_fitness": (C.c_int, [VP, DP]),
+    "fnb_evolver_evaluate": (C.c_int, [VP, DP, DP, C.c_int, C.c_int, C.c_double]),
+    "fnb_evolver_evaluate_d": (C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_double]),
+    "fnb_evolver_step": (C.c_int, [VP]),
+    "fnb_evolver_species": (C.c_int, [VP, IP, IP, IP, IP, DP, IP, IP]),
+    "fnb_evolver_state": (C.c_int, [VP, IP, IP]),
+    "fnb_evolver_device_state": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)]),
     "fnb_stream_draws_d": (C.c_int, [VP, VP, C.c_int, C.c_int, C.c_int, C.c_uint64, VP, VP]),
     "fnb_split_keys_d": (C.c_int, [VP, U32P, C.c_uint64, C.c_int, VP, VP]),
 }

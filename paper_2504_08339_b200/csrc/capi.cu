@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "fnb_common.cuh"
+#include "ctx_internal.cuh"
 
 namespace fnb {
 // host launchers (transform.cu / forward.cu)
@@ -39,37 +40,7 @@ const char* errc_name(int c) {  // errors.hpp:33-57
   return (c >= 0 && c < 20) ? names[c] : "unknown";
 }
 
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  cudaError_t ensure(size_t bytes) {
-    if (bytes <= cap) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-    cudaError_t e = cudaMalloc(&p, bytes);
-    if (e == cudaSuccess) cap = bytes;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-  }
-};
-
 }  // namespace
-
-struct fnb_ctx {
-  int device = 0;
-  DevShape sh{};
-  NetLayout L{0, 0, 0, 0};
-  std::string err;
-  int err_index = -1;
-  long long launches = 0;
-  cudaStream_t stream = nullptr;
-  DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc, scratch;
-};
 
 static int fnb_cuda_fail_ctx(fnb_ctx* ctx, cudaError_t e, const char* what) {
   if (ctx) {

@@ -64,11 +64,16 @@ __global__ void k_rep_tables(const double* __restrict__ rn, const double* __rest
 __global__ void __launch_bounds__(128)
 k_distance(const double* __restrict__ nodes, const double* __restrict__ conns, int P,
            const double* __restrict__ rn, const double* __restrict__ rc, int S, RepTables t, int N, int C,
-           double cd, double ch, double* __restrict__ out) {
+           double cd, double ch, double* __restrict__ out, const int* __restrict__ only_unassigned,
+           const int* __restrict__ after_founder) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= P) return;
+  // speciation rounds only need genomes still without a species (and, for a
+  // founding round, after the founder): skip the rest without touching HBM
+  if (only_unassigned && only_unassigned[g] >= 0) return;
+  if (after_founder && (after_founder[0] < 0 || g <= after_founder[0])) return;
   int16_t* match = reinterpret_cast<int16_t*>(smem_raw) + size_t(warp) * S * (N + C);
   const double* gn = nodes + size_t(g) * N * kNodeCols;
   const double* gc = conns + size_t(g) * C * kConnCols;
@@ -147,9 +152,22 @@ k_distance(const double* __restrict__ nodes, const double* __restrict__ conns, i
 }
 
 // ---- host launcher -----------------------------------------------------------
+cudaError_t launch_distance_masked(const double* nodes, const double* conns, int P, const double* rn,
+                                   const double* rc, int S, int N, int C, double cd, double ch, double* out,
+                                   void* scratch, size_t scratch_bytes, const int* only_unassigned,
+                                   const int* after_founder, cudaStream_t st);
+
 cudaError_t launch_distance(const double* nodes, const double* conns, int P, const double* rn, const double* rc,
                             int S, int N, int C, double cd, double ch, double* out, void* scratch,
                             size_t scratch_bytes, cudaStream_t st) {
+  return launch_distance_masked(nodes, conns, P, rn, rc, S, N, C, cd, ch, out, scratch, scratch_bytes, nullptr,
+                                nullptr, st);
+}
+
+cudaError_t launch_distance_masked(const double* nodes, const double* conns, int P, const double* rn,
+                                   const double* rc, int S, int N, int C, double cd, double ch, double* out,
+                                   void* scratch, size_t scratch_bytes, const int* only_unassigned,
+                                   const int* after_founder, cudaStream_t st) {
   if (S <= 0 || P <= 0) return cudaSuccess;
   RepTables t;
   t.Hn = table_capacity(N);
@@ -170,7 +188,8 @@ cudaError_t launch_distance(const double* nodes, const double* conns, int P, con
   const size_t smem = per_warp * warps;
   e = cudaFuncSetAttribute(k_distance, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  k_distance<<<(P + warps - 1) / warps, 32 * warps, smem, st>>>(nodes, conns, P, rn, rc, S, t, N, C, cd, ch, out);
+  k_distance<<<(P + warps - 1) / warps, 32 * warps, smem, st>>>(nodes, conns, P, rn, rc, S, t, N, C, cd, ch, out,
+                                                                only_unassigned, after_founder);
   return cudaGetLastError();
 }
 

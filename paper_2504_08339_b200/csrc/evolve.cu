@@ -1,0 +1,870 @@
+// evolve.cu -- the NEAT generation loop on the device (
+// PAPER Algorithm 1): initialize_population, speciate, update_stagnation,
+// compute_spawn_counts and reproduce, held bit-exact to the frozen CPU
+// restatement oracle/evolution.c (the reference ships no code for these
+// stages; its rules E1-E5 are listed there and in DESIGN.md).
+//
+// Everything population-sized is a kernel over genomes or children; the
+// species bookkeeping (<= 32 species) runs in single-thread kernels so it
+// never leaves the device:
+//   speciate   K3 distances to the old representatives -> first match;
+//              founding rounds (min unassigned index via atomicMin, founder
+//              copied to a representative slot, K3 of the still-unassigned
+//              genomes against it); nearest-representative overflow;
+//              new representative = member closest to the old one (two-pass
+//              atomicMin on (distance bits, index)); empty species dropped.
+//   stagnate   per-species max fitness (atomicMax on order-preserving bits),
+//              counter update, species_elitism protection, compaction.
+//   spawn      fitness ranks by a stable radix sort (CUB), exact integer
+//              rank sums per species, then the clamp / rescale / largest-
+//              remainder / elitism arithmetic on one thread.
+//   reproduce  members ordered (fitness desc, index asc) by two stable radix
+//              sorts, per-slot parent selection from the split(0) stream,
+//              K5 crossover (elites are self-crossovers = exact copies), K6/K7
+//              mutation with one slot-ordered innovation table.
+#include <climits>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "fnb_common.cuh"
+#include "glibc_math.cuh"
+#include "philox.cuh"
+
+namespace fnb {
+
+constexpr int kMaxSpecies = 32;
+
+struct SpeciesDev {
+  int count, next_id, old_count;
+  int founder;       // current founding round: founder index or -1
+  int round_j;       // species index created by the current round
+  int cand;          // min unassigned index candidate
+  int id[kMaxSpecies];
+  double best[kMaxSpecies];
+  int stag[kMaxSpecies];
+  int size[kMaxSpecies];
+  int spawn[kMaxSpecies];
+  int soff[kMaxSpecies + 1];  // child slot offsets
+  int moff[kMaxSpecies + 1];  // member offsets in the sorted member list
+  int remap[kMaxSpecies];
+  unsigned long long mxbits[kMaxSpecies];
+  unsigned long long dmin[kMaxSpecies];
+  int argmin[kMaxSpecies];
+  long long rsum[kMaxSpecies];
+  int cnt[kMaxSpecies];
+  int total_spawn;
+  int error;
+};
+
+struct NeatCfg {  // == fnb_neat_config
+  int pop_size, max_species;
+  double threshold;
+  int species_elitism, max_stagnation, genome_elitism;
+  double survival, spawn_rate;
+  int output_activation;
+};
+
+__device__ __forceinline__ unsigned long long ordered_bits(double x) {  // monotone in x; -0 == +0
+  x = __dadd_rn(x, 0.0);
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_ordered(unsigned long long o) {
+  const unsigned long long u = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+  return __longlong_as_double((long long)u);
+}
+
+// ---- initialize_population (oracle E1) ------------------------
+__global__ void k_init_population(double* nodes, double* conns, int P, int N, int C, int I, int O, Key4 init_key,
+                                  double bm, double bs, double rm, double rs, double wm, double ws, int default_agg,
+                                  int default_act, int out_act) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= P) return;
+  double* n = nodes + size_t(g) * N * kNodeCols;
+  double* c = conns + size_t(g) * C * kConnCols;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  for (int i = lane; i < N * kNodeCols; i += 32) n[i] = nan;
+  for (int i = lane; i < C * kConnCols; i += 32) c[i] = nan;
+  __syncwarp();
+  if (lane != 0) return;
+  Stream s(key_split(init_key, uint64_t(g)));
+  const int hidden = I + O;
+  for (int i = 0; i < I; ++i) {
+    double* row = n + i * kNodeCols;
+    row[0] = double(i); row[1] = 0.0; row[2] = 1.0; row[3] = double(default_agg); row[4] = double(default_act);
+  }
+  for (int r = I; r <= hidden; ++r) {
+    double* row = n + r * kNodeCols;
+    row[0] = double(r);
+    const double a0 = s.uniform(), a1 = s.uniform();
+    row[1] = glibc::normal_from_uniforms(a0, a1, bm, bs);
+    const double b0 = s.uniform(), b1 = s.uniform();
+    row[2] = glibc::normal_from_uniforms(b0, b1, rm, rs);
+    row[3] = double(default_agg);
+    row[4] = double(r < hidden ? out_act : default_act);
+  }
+  for (int r = 0; r < I + O; ++r) {
+    double* row = c + r * kConnCols;
+    row[0] = double(r < I ? r : hidden);
+    row[1] = double(r < I ? hidden : r);
+    row[2] = 1.0;
+    const double a0 = s.uniform(), a1 = s.uniform();
+    row[3] = glibc::normal_from_uniforms(a0, a1, wm, ws);
+  }
+}
+
+// copy genome `src` (or *src_dev when src < 0) into dst
+__global__ void k_copy_genome(const double* sn, const double* sc, const int* src_dev, int src, double* dn, double* dc,
+                              int N, int C) {
+  const int s = src >= 0 ? src : *src_dev;
+  if (s < 0) return;
+  const double* a = sn + size_t(s) * N * kNodeCols;
+  const double* b = sc + size_t(s) * C * kConnCols;
+  for (int i = threadIdx.x; i < N * kNodeCols; i += blockDim.x) dn[i] = a[i];
+  for (int i = threadIdx.x; i < C * kConnCols; i += blockDim.x) dc[i] = b[i];
+}
+
+// ---- speciate (oracle E2) -------------------------------------------------------
+__global__ void k_spec_begin(SpeciesDev* sd) {
+  sd->old_count = sd->count;
+  for (int j = 0; j < kMaxSpecies; ++j) {
+    sd->dmin[j] = ~0ull;
+    sd->argmin[j] = INT_MAX;
+    sd->size[j] = 0;
+  }
+}
+
+__global__ void k_assign_first(const double* __restrict__ d, int P, int S_old, double th, int* species_of) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  int a = -1;
+  for (int j = 0; j < S_old; ++j)
+    if (d[size_t(i) * S_old + j] < th) { a = j; break; }
+  species_of[i] = a;
+}
+
+__global__ void k_round_reset(SpeciesDev* sd) { sd->cand = INT_MAX; }
+
+__global__ void k_min_unassigned(const int* species_of, int P, SpeciesDev* sd) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P && species_of[i] < 0) atomicMin(&sd->cand, i);
+}
+
+// founder commit + copies of the founder into its representative slot and
+// the round buffer (one block)
+__global__ void k_found(SpeciesDev* sd, int max_species, int* species_of, const double* pn, const double* pc,
+                        double* rep_n, double* rep_c, double* round_n, double* round_c, int N, int C) {
+  __shared__ int f, j;
+  if (threadIdx.x == 0) {
+    f = -1;
+    j = -1;
+    if (sd->cand != INT_MAX && sd->count < max_species) {
+      f = sd->cand;
+      j = sd->count++;
+      sd->id[j] = sd->next_id++;
+      sd->best[j] = -INFINITY;
+      sd->stag[j] = 0;
+      species_of[f] = j;
+    }
+    sd->founder = f;
+    sd->round_j = j;
+  }
+  __syncthreads();
+  if (f < 0) return;
+  const double* a = pn + size_t(f) * N * kNodeCols;
+  const double* b = pc + size_t(f) * C * kConnCols;
+  for (int i = threadIdx.x; i < N * kNodeCols; i += blockDim.x) {
+    rep_n[size_t(j) * N * kNodeCols + i] = a[i];
+    round_n[i] = a[i];
+  }
+  for (int i = threadIdx.x; i < C * kConnCols; i += blockDim.x) {
+    rep_c[size_t(j) * C * kConnCols + i] = b[i];
+    round_c[i] = b[i];
+  }
+}
+
+__global__ void k_join_round(const double* __restrict__ d, int P, double th, const SpeciesDev* sd, int* species_of) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = sd->founder;
+  if (i >= P || f < 0 || i <= f || species_of[i] >= 0) return;
+  if (d[i] < th) species_of[i] = sd->round_j;
+}
+
+__global__ void k_nearest(const double* __restrict__ d, int P, int stride, const SpeciesDev* sd, int* species_of) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P || species_of[i] >= 0) return;
+  int best = 0;
+  double bd = 0.0;
+  for (int j = 0; j < sd->count; ++j) {
+    const double x = d[size_t(i) * stride + j];
+    if (j == 0 || x < bd) { bd = x; best = j; }
+  }
+  species_of[i] = best;
+}
+
+__global__ void k_rep_min(const double* __restrict__ d, int P, int S_old, const int* species_of, SpeciesDev* sd,
+                          int pass) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int j = species_of[i];
+  if (j < 0 || j >= S_old) return;
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d[size_t(i) * S_old + j]);  // d >= 0
+  if (pass == 0) atomicMin(&sd->dmin[j], b);
+  else if (b == sd->dmin[j]) atomicMin(&sd->argmin[j], i);
+}
+
+// new representatives of old species: one block per species
+__global__ void k_rep_copy(const SpeciesDev* sd, const double* pn, const double* pc, double* rep_n, double* rep_c,
+                           int N, int C) {
+  const int j = blockIdx.x;
+  if (j >= sd->old_count) return;
+  const int m = sd->argmin[j];
+  if (m == INT_MAX) return;
+  for (int i = threadIdx.x; i < N * kNodeCols; i += blockDim.x)
+    rep_n[size_t(j) * N * kNodeCols + i] = pn[size_t(m) * N * kNodeCols + i];
+  for (int i = threadIdx.x; i < C * kConnCols; i += blockDim.x)
+    rep_c[size_t(j) * C * kConnCols + i] = pc[size_t(m) * C * kConnCols + i];
+}
+
+__global__ void k_sizes(const int* species_of, int P, SpeciesDev* sd) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P && species_of[i] >= 0) atomicAdd(&sd->size[species_of[i]], 1);
+}
+
+__global__ void k_mark_nonempty(SpeciesDev* sd) {
+  for (int j = 0; j < sd->count; ++j) sd->remap[j] = sd->size[j] > 0 ? 1 : -1;
+}
+
+// compaction driven by remap[j] in {1 keep, -1 drop}: rewrites remap to the
+// new index and moves every field and representative (new <= old: forward)
+__global__ void k_apply_compaction(SpeciesDev* sd, double* rep_n, double* rep_c, int N, int C) {
+  __shared__ int S;
+  if (threadIdx.x == 0) {
+    S = sd->count;
+    int k = 0;
+    for (int j = 0; j < S; ++j) sd->remap[j] = sd->remap[j] > 0 ? k++ : -1;
+  }
+  __syncthreads();
+  for (int j = 0; j < S; ++j) {
+    const int t = sd->remap[j];
+    if (t < 0 || t == j) continue;
+    for (int i = threadIdx.x; i < N * kNodeCols; i += blockDim.x)
+      rep_n[size_t(t) * N * kNodeCols + i] = rep_n[size_t(j) * N * kNodeCols + i];
+    for (int i = threadIdx.x; i < C * kConnCols; i += blockDim.x)
+      rep_c[size_t(t) * C * kConnCols + i] = rep_c[size_t(j) * C * kConnCols + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sd->id[t] = sd->id[j];
+      sd->best[t] = sd->best[j];
+      sd->stag[t] = sd->stag[j];
+      sd->size[t] = sd->size[j];
+      sd->spawn[t] = sd->spawn[j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int j = 0; j < S; ++j) k += sd->remap[j] >= 0;
+    sd->count = k;
+  }
+}
+
+__global__ void k_remap(int* species_of, int P, const SpeciesDev* sd) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P && species_of[i] >= 0) species_of[i] = sd->remap[species_of[i]];
+}
+
+// ---- update_stagnation (oracle E3) --------------------------------------------------
+__global__ void k_stag_begin(SpeciesDev* sd) {
+  for (int j = 0; j < kMaxSpecies; ++j) sd->mxbits[j] = 0ull;
+}
+__global__ void k_species_max(const double* fitness, const int* species_of, int P, SpeciesDev* sd) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P && species_of[i] >= 0) atomicMax(&sd->mxbits[species_of[i]], ordered_bits(fitness[i]));
+}
+__global__ void k_stagnation(SpeciesDev* sd, int species_elitism, int max_stagnation) {
+  const int S = sd->count;
+  if (S <= 0) return;
+  double mx[kMaxSpecies];
+  for (int j = 0; j < S; ++j) mx[j] = from_ordered(sd->mxbits[j]);
+  for (int j = 0; j < S; ++j) {
+    if (mx[j] > sd->best[j]) { sd->best[j] = mx[j]; sd->stag[j] = 0; }
+    else sd->stag[j] += 1;
+  }
+  int prot[kMaxSpecies];
+  for (int j = 0; j < S; ++j) {
+    int better = 0;
+    for (int q = 0; q < S; ++q)
+      if (mx[q] > mx[j] || (mx[q] == mx[j] && q < j)) ++better;
+    prot[j] = better < species_elitism;
+  }
+  int survivors = 0;
+  for (int j = 0; j < S; ++j) survivors += (prot[j] || sd->stag[j] <= max_stagnation);
+  if (survivors == 0) {
+    int b = 0;
+    for (int j = 1; j < S; ++j)
+      if (mx[j] > mx[b]) b = j;
+    prot[b] = 1;
+  }
+  for (int j = 0; j < S; ++j) sd->remap[j] = (!prot[j] && sd->stag[j] > max_stagnation) ? -1 : 1;
+}
+__global__ void k_remap_or_drop(int* species_of, int P, const SpeciesDev* sd) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P && species_of[i] >= 0) species_of[i] = sd->remap[species_of[i]];
+}
+
+// ---- compute_spawn_counts (oracle E4) ------------------------------------------------
+__global__ void k_fit_keys(const double* fitness, int P, unsigned long long* asc, unsigned long long* desc, int* idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const unsigned long long o = ordered_bits(fitness[i]);
+  asc[i] = o;
+  desc[i] = ~o;
+  idx[i] = i;
+}
+__global__ void k_rank_sums(const int* sorted_idx, int P, const int* species_of, SpeciesDev* sd) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P) return;
+  const int i = sorted_idx[r];
+  const int j = species_of[i];
+  if (j < 0) return;
+  atomicAdd(reinterpret_cast<unsigned long long*>(&sd->rsum[j]), (unsigned long long)r);
+  atomicAdd(&sd->cnt[j], 1);
+}
+__global__ void k_spawn_begin(SpeciesDev* sd) {
+  for (int j = 0; j < kMaxSpecies; ++j) { sd->rsum[j] = 0; sd->cnt[j] = 0; }
+}
+__global__ void k_spawn(SpeciesDev* sd, int P, double rate, int genome_elitism) {
+  const int S = sd->count;
+  double af[kMaxSpecies], nw[kMaxSpecies], frac[kMaxSpecies];
+  double total = 0.0;
+  for (int j = 0; j < S; ++j) {
+    af[j] = __ddiv_rn(double(sd->rsum[j]), __dmul_rn(double(P - 1), double(sd->cnt[j])));
+    total = __dadd_rn(total, af[j]);
+  }
+  double sum_new = 0.0;
+  for (int j = 0; j < S; ++j) {
+    const double target = total > 0.0 ? __dmul_rn(__ddiv_rn(af[j], total), double(P)) : __ddiv_rn(double(P), double(S));
+    const double old = double(sd->cnt[j]);
+    const double md = round(__dmul_rn(rate, old));
+    double v = target;
+    if (v < __dsub_rn(old, md)) v = __dsub_rn(old, md);
+    if (v > __dadd_rn(old, md)) v = __dadd_rn(old, md);
+    nw[j] = v;
+    sum_new = __dadd_rn(sum_new, v);
+  }
+  int assigned = 0;
+  for (int j = 0; j < S; ++j) {
+    const double sc = sum_new > 0.0 ? __ddiv_rn(__dmul_rn(nw[j], double(P)), sum_new) : __ddiv_rn(double(P), double(S));
+    const double fl = floor(sc);
+    sd->spawn[j] = int(fl);
+    frac[j] = __dsub_rn(sc, fl);
+    assigned += sd->spawn[j];
+  }
+  int rem = P - assigned;
+  while (rem > 0) {
+    int b = -1;
+    for (int j = 0; j < S; ++j)
+      if (frac[j] >= 0.0 && (b < 0 || frac[j] > frac[b])) b = j;
+    if (b < 0) {
+      for (int j = 0; j < S && rem > 0; ++j, --rem) sd->spawn[j]++;
+      break;
+    }
+    sd->spawn[b]++;
+    frac[b] = -1.0;
+    --rem;
+  }
+  int tot = 0;
+  for (int j = 0; j < S; ++j) {
+    if (sd->spawn[j] < genome_elitism) sd->spawn[j] = genome_elitism;
+    tot += sd->spawn[j];
+  }
+  while (tot > P) {
+    int b = -1;
+    for (int j = 0; j < S; ++j)
+      if (sd->spawn[j] > genome_elitism && (b < 0 || sd->spawn[j] >= sd->spawn[b])) b = j;
+    if (b < 0) break;
+    sd->spawn[b]--;
+    --tot;
+  }
+  int so = 0, mo = 0;
+  for (int j = 0; j < S; ++j) {
+    sd->soff[j] = so;
+    sd->moff[j] = mo;
+    so += sd->spawn[j];
+    mo += sd->cnt[j];
+    sd->size[j] = sd->cnt[j];
+  }
+  sd->soff[S] = so;
+  sd->moff[S] = mo;
+  sd->total_spawn = so;
+  sd->error = so == P ? 0 : 1;
+}
+
+// ---- reproduce (oracle E5) -----------------------------------------------------------------
+__global__ void k_species_keys(const int* sorted_idx, int P, const int* species_of, int* skey) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P) return;
+  const int j = species_of[sorted_idx[r]];
+  skey[r] = j < 0 ? kMaxSpecies : j;
+}
+
+__global__ void k_reproduce_plan(const SpeciesDev* sd, const int* members, const double* fitness, int P, Key4 gen_key,
+                                 int genome_elitism, double survival, int* fit_idx, int* oth_idx, uint32_t* xkeys,
+                                 uint32_t* mkeys, uint8_t* active) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P) return;
+  const int S = sd->count;
+  int j = 0;
+  while (j + 1 < S && sd->soff[j + 1] <= c) ++j;
+  const int k = c - sd->soff[j];
+  const int m = sd->size[j];
+  const int* mem = members + sd->moff[j];
+  int n_elite = genome_elitism;
+  if (n_elite > sd->spawn[j]) n_elite = sd->spawn[j];
+  if (n_elite > m) n_elite = m;
+  if (k < n_elite) {  // elite: exact copy (self-crossover), not mutated
+    fit_idx[c] = oth_idx[c] = mem[k];
+    for (int q = 0; q < 4; ++q) { xkeys[4 * c + q] = 0u; mkeys[4 * c + q] = 0u; }
+    active[c] = 0;
+    return;
+  }
+  int pool = int(ceil(__dmul_rn(survival, double(m))));
+  if (pool < 1) pool = 1;
+  if (pool > m) pool = m;
+  const Key4 ck = key_split(gen_key, uint64_t(c));
+  Stream sel(key_split(ck, 0));
+  const int a = mem[int(sel.below(uint64_t(pool)))];
+  const int b = mem[int(sel.below(uint64_t(pool)))];
+  const bool a_fit = fitness[a] > fitness[b] || (fitness[a] == fitness[b] && a <= b);
+  fit_idx[c] = a_fit ? a : b;
+  oth_idx[c] = a_fit ? b : a;
+  const Key4 xk = key_split(ck, 1), mk = key_split(ck, 2);
+  for (int q = 0; q < 4; ++q) { xkeys[4 * c + q] = xk.w[q]; mkeys[4 * c + q] = mk.w[q]; }
+  active[c] = 1;
+}
+
+// ---- host-side launchers used by capi.cu ------------------------------------------------------
+cudaError_t launch_distance_masked(const double* nodes, const double* conns, int P, const double* rn,
+                                   const double* rc, int S, int N, int C, double cd, double ch, double* out,
+                                   void* scratch, size_t scratch_bytes, const int* only_unassigned,
+                                   const int* after_founder, cudaStream_t st);
+size_t distance_scratch_bytes(int S, int N, int C);
+cudaError_t launch_crossover(const double* nodes, const double* conns, const int32_t* fit, const int32_t* oth,
+                             const uint32_t* keys, int n, int N, int C, double* cn, double* cc, cudaStream_t st);
+size_t mutate_scratch_bytes(int n);
+cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, int n, const uint8_t* active,
+                          const fnb_mutation_config* m, const DevShape& sh, int* d_next_key, int* d_status,
+                          void* scratch, size_t scratch_bytes, int* d_new_key_out, cudaStream_t st,
+                          long long* launches);
+
+struct Evolver {
+  NeatCfg cfg;
+  fnb_mutation_config mut;
+  fnb_distance_config dist;
+  DevShape sh;
+  uint64_t seed = 0;
+  int generation = 0;
+  int P = 0, N = 0, C = 0;
+  int host_species = 0;  // mirror of sd->count, refreshed at the end of a step
+  cudaStream_t st = nullptr;
+  long long* launches = nullptr;
+  // device buffers
+  double *pn[2] = {nullptr, nullptr}, *pc[2] = {nullptr, nullptr};
+  int cur = 0;
+  double* fitness = nullptr;
+  double *rep_n = nullptr, *rep_c = nullptr, *round_n = nullptr, *round_c = nullptr;
+  double *dmat = nullptr, *dround = nullptr;
+  int* species_of = nullptr;
+  SpeciesDev* sd = nullptr;
+  unsigned long long *kasc = nullptr, *kdesc = nullptr, *ktmp = nullptr;
+  int *idx = nullptr, *idx_sorted = nullptr, *idx_tmp = nullptr, *skey = nullptr, *skey_tmp = nullptr;
+  int *fit_idx = nullptr, *oth_idx = nullptr, *status = nullptr, *next_key = nullptr;
+  uint32_t *xkeys = nullptr, *mkeys = nullptr;
+  uint8_t* active = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+
+  size_t gn() const { return size_t(N) * kNodeCols; }
+  size_t gc() const { return size_t(C) * kConnCols; }
+
+  cudaError_t alloc() {
+    cudaError_t e = cudaSuccess;
+    auto A = [&](auto** p, size_t bytes) {
+      if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    };
+    for (int b = 0; b < 2; ++b) {
+      A(&pn[b], sizeof(double) * gn() * P);
+      A(&pc[b], sizeof(double) * gc() * P);
+    }
+    A(&fitness, sizeof(double) * P);
+    A(&rep_n, sizeof(double) * gn() * kMaxSpecies);
+    A(&rep_c, sizeof(double) * gc() * kMaxSpecies);
+    A(&round_n, sizeof(double) * gn());
+    A(&round_c, sizeof(double) * gc());
+    A(&dmat, sizeof(double) * size_t(P) * 2 * kMaxSpecies);  // [old reps | overflow vs all reps]
+    A(&dround, sizeof(double) * size_t(P));
+    A(&species_of, sizeof(int) * P);
+    A(&sd, sizeof(SpeciesDev));
+    A(&kasc, 8 * size_t(P));
+    A(&kdesc, 8 * size_t(P));
+    A(&ktmp, 8 * size_t(P));
+    A(&idx, 4 * size_t(P));
+    A(&idx_sorted, 4 * size_t(P));
+    A(&idx_tmp, 4 * size_t(P));
+    A(&skey, 4 * size_t(P));
+    A(&skey_tmp, 4 * size_t(P));
+    A(&fit_idx, 4 * size_t(P));
+    A(&oth_idx, 4 * size_t(P));
+    A(&status, 4 * size_t(P));
+    A(&next_key, 8);
+    A(&xkeys, 16 * size_t(P));
+    A(&mkeys, 16 * size_t(P));
+    A(&active, size_t(P));
+    if (e != cudaSuccess) return e;
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b1, kasc, ktmp, idx, idx_tmp, P);
+    cub::DeviceRadixSort::SortPairs(nullptr, b2, skey, skey_tmp, idx, idx_tmp, P, 0, 6);
+    cub_bytes = std::max(b1, b2);
+    A(&cub_tmp, cub_bytes);
+    scratch_bytes = std::max(distance_scratch_bytes(kMaxSpecies, N, C), mutate_scratch_bytes(P));
+    A(&scratch, scratch_bytes);
+    if (e != cudaSuccess) return e;
+    // representatives start as empty genomes (never read before founded)
+    e = cudaMemsetAsync(rep_n, 0xff, sizeof(double) * gn() * kMaxSpecies, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(rep_c, 0xff, sizeof(double) * gc() * kMaxSpecies, st);
+    SpeciesDev z{};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sd, &z, sizeof(z), cudaMemcpyHostToDevice, st);
+    const int nk[2] = {sh.I + sh.O + 1, 0};  // InnovationTable(first_key = I + O + 1)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(next_key, nk, sizeof(nk), cudaMemcpyHostToDevice, st);
+    return e;
+  }
+
+  void release() {
+    void* ps[] = {pn[0], pn[1], pc[0], pc[1], fitness, rep_n, rep_c, round_n, round_c, dmat, dround, species_of, sd,
+                  kasc, kdesc, ktmp, idx, idx_sorted, idx_tmp, skey, skey_tmp, fit_idx, oth_idx, status, next_key,
+                  xkeys, mkeys, active, cub_tmp, scratch};
+    for (void* p : ps)
+      if (p) cudaFree(p);
+  }
+
+  cudaError_t init_population() {
+    const Key4 root = key_from_seed(seed);
+    k_init_population<<<(P + 3) / 4, 128, 0, st>>>(pn[cur], pc[cur], P, N, C, sh.I, sh.O, key_split(root, 0),
+                                                   mut.bias.init_mean, mut.bias.init_std, mut.response.init_mean,
+                                                   mut.response.init_std, mut.weight.init_mean, mut.weight.init_std,
+                                                   sh.default_agg, sh.default_act, cfg.output_activation);
+    ++*launches;
+    return cudaGetLastError();
+  }
+
+  // speciate -> update_stagnation -> compute_spawn_counts -> reproduce
+  cudaError_t step(int* host_error) {
+    const int T = 256, B = (P + T - 1) / T;
+    const double th = cfg.threshold;
+    const double* n = pn[cur];
+    const double* c = pc[cur];
+    cudaError_t e;
+    const int S_old = host_species;
+    // ---- speciate
+    k_spec_begin<<<1, 1, 0, st>>>(sd);
+    if (S_old > 0) {
+      e = launch_distance_masked(n, c, P, rep_n, rep_c, S_old, N, C, dist.compatibility_disjoint,
+                                 dist.compatibility_homologous, dmat, scratch, scratch_bytes, nullptr, nullptr, st);
+      if (e != cudaSuccess) return e;
+    }
+    k_assign_first<<<B, T, 0, st>>>(dmat, P, S_old, th, species_of);
+    for (int r = S_old; r < cfg.max_species; ++r) {
+      k_round_reset<<<1, 1, 0, st>>>(sd);
+      k_min_unassigned<<<B, T, 0, st>>>(species_of, P, sd);
+      k_found<<<1, 256, 0, st>>>(sd, cfg.max_species, species_of, n, c, rep_n, rep_c, round_n, round_c, N, C);
+      e = launch_distance_masked(n, c, P, round_n, round_c, 1, N, C, dist.compatibility_disjoint,
+                                 dist.compatibility_homologous, dround, scratch, scratch_bytes, species_of,
+                                 &sd->founder, st);
+      if (e != cudaSuccess) return e;
+      k_join_round<<<B, T, 0, st>>>(dround, P, th, sd, species_of);
+      *launches += 6;
+    }
+    e = launch_distance_masked(n, c, P, rep_n, rep_c, cfg.max_species, N, C, dist.compatibility_disjoint,
+                               dist.compatibility_homologous, dmat + size_t(P) * S_old, scratch, scratch_bytes,
+                               species_of, nullptr, st);
+    if (e != cudaSuccess) return e;
+    k_nearest<<<B, T, 0, st>>>(dmat + size_t(P) * S_old, P, cfg.max_species, sd, species_of);
+    if (S_old > 0) {
+      k_rep_min<<<B, T, 0, st>>>(dmat, P, S_old, species_of, sd, 0);
+      k_rep_min<<<B, T, 0, st>>>(dmat, P, S_old, species_of, sd, 1);
+      k_rep_copy<<<S_old, 256, 0, st>>>(sd, n, c, rep_n, rep_c, N, C);
+    }
+    k_sizes<<<B, T, 0, st>>>(species_of, P, sd);
+    k_mark_nonempty<<<1, 1, 0, st>>>(sd);
+    k_apply_compaction<<<1, 256, 0, st>>>(sd, rep_n, rep_c, N, C);
+    k_remap<<<B, T, 0, st>>>(species_of, P, sd);
+    // ---- update_stagnation
+    k_stag_begin<<<1, 1, 0, st>>>(sd);
+    k_species_max<<<B, T, 0, st>>>(fitness, species_of, P, sd);
+    k_stagnation<<<1, 1, 0, st>>>(sd, cfg.species_elitism, cfg.max_stagnation);
+    k_apply_compaction<<<1, 256, 0, st>>>(sd, rep_n, rep_c, N, C);
+    k_remap_or_drop<<<B, T, 0, st>>>(species_of, P, sd);
+    // ---- compute_spawn_counts: ranks by a stable ascending radix sort
+    k_fit_keys<<<B, T, 0, st>>>(fitness, P, kasc, kdesc, idx);
+    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
+    if (e != cudaSuccess) return e;
+    k_spawn_begin<<<1, 1, 0, st>>>(sd);
+    k_rank_sums<<<B, T, 0, st>>>(idx_sorted, P, species_of, sd);
+    k_spawn<<<1, 1, 0, st>>>(sd, P, cfg.spawn_rate, cfg.genome_elitism);
+    // ---- reproduce: members by (fitness desc, index asc), then by species
+    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kdesc, ktmp, idx, idx_tmp, P, 0, 64, st);
+    if (e != cudaSuccess) return e;
+    k_species_keys<<<B, T, 0, st>>>(idx_tmp, P, species_of, skey);
+    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, skey, skey_tmp, idx_tmp, idx_sorted, P, 0, 6, st);
+    if (e != cudaSuccess) return e;
+    const Key4 gen_key = key_split(key_split(key_from_seed(seed), 1), uint64_t(generation));
+    k_reproduce_plan<<<B, T, 0, st>>>(sd, idx_sorted, fitness, P, gen_key, cfg.genome_elitism, cfg.survival, fit_idx,
+                                      oth_idx, xkeys, mkeys, active);
+    *launches += 24;
+    e = launch_crossover(n, c, fit_idx, oth_idx, xkeys, P, N, C, pn[cur ^ 1], pc[cur ^ 1], st);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    e = launch_mutate(pn[cur ^ 1], pc[cur ^ 1], mkeys, P, active, &mut, sh, next_key, status, scratch, scratch_bytes,
+                      nullptr, st, launches);
+    if (e != cudaSuccess) return e;
+    // step status: spawn total and per-child mutation status
+    int err_spawn = 0, count = 0;
+    e = cudaMemcpyAsync(&err_spawn, &sd->error, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&count, &sd->count, sizeof(int), cudaMemcpyDeviceToHost, st);
+    std::vector<int> stv(static_cast<size_t>(P));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(stv.data(), status, sizeof(int) * P, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    *host_error = err_spawn ? -2 : -1;
+    if (!err_spawn)
+      for (int i = 0; i < P; ++i)
+        if (stv[size_t(i)]) { *host_error = i; break; }
+    host_species = count;
+    cur ^= 1;
+    ++generation;
+    return cudaSuccess;
+  }
+};
+
+}  // namespace fnb
+
+// =================================================================================
+// C ABI: fnb_evolver_* (include/flatneat_b200.h)
+// =================================================================================
+#include "ctx_internal.cuh"
+
+struct fnb_evolver {
+  fnb_ctx* ctx = nullptr;
+  fnb::Evolver ev;
+  DevBuf nets, X, Y;
+};
+
+namespace fnb {
+int launch_forward(const void* nets, NetLayout L, int P, const float* X, const float* Y, int B, int fit_kind,
+                   double offset, double* fitness, double* out, double* partial_buf, size_t partial_cap,
+                   int uniform_agg, int uniform_act, cudaStream_t st, long long* launches);
+size_t forward_partial_needed(NetLayout L, int P, int B);
+cudaError_t launch_transform(const double* n, const double* c, int P, uint8_t* nets, const NetLayout& L,
+                             const DevShape& sh, cudaStream_t st);
+}  // namespace fnb
+
+#define EV_CK(expr)                                                         \
+  do {                                                                      \
+    cudaError_t e_ = (expr);                                                \
+    if (e_ != cudaSuccess) return fnb_cuda_error(ev->ctx, e_, #expr);       \
+  } while (0)
+
+extern "C" {
+
+int fnb_evolver_create(fnb_ctx* ctx, const fnb_neat_config* cfg, uint64_t seed, fnb_evolver** out) {
+  if (!ctx || !cfg || !out) return 1 + FNB_E_CONFIG_ERROR;
+  *out = nullptr;
+  const fnb::DevShape& sh = ctx->sh;
+  if (cfg->pop_size < 2 || cfg->max_species < 1 || cfg->max_species > fnb::kMaxSpecies ||
+      cfg->survival_threshold <= 0.0 || cfg->survival_threshold > 1.0 ||
+      cfg->max_species * cfg->genome_elitism > cfg->pop_size)
+    return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "invalid NeatConfig", -1);
+  if (sh.I + sh.O + 1 > sh.N || sh.I + sh.O > sh.C)
+    return fnb_set_error(ctx, FNB_E_LIMITS_TOO_SMALL, "limits cannot hold the minimal genome", -1);
+  for (int i = 0; i < sh.I; ++i)
+    if (sh.input_keys[i] != i) return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "input keys must be 0..I-1", -1);
+  for (int o = 0; o < sh.O; ++o)
+    if (sh.output_keys[o] != sh.I + o)
+      return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "output keys must be I..I+O-1", -1);
+  if (cfg->output_activation < 0 || cfg->output_activation >= sh.n_act)
+    return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "output activation id out of range", -1);
+  auto* e = new fnb_evolver();
+  e->ctx = ctx;
+  fnb::Evolver& v = e->ev;
+  v.cfg = fnb::NeatCfg{cfg->pop_size, cfg->max_species, cfg->compatibility_threshold, cfg->species_elitism,
+                       cfg->max_stagnation, cfg->genome_elitism, cfg->survival_threshold,
+                       cfg->spawn_number_change_rate, cfg->output_activation};
+  v.mut = cfg->mutation;
+  v.dist = cfg->distance;
+  v.sh = sh;
+  v.seed = seed;
+  v.P = cfg->pop_size;
+  v.N = sh.N;
+  v.C = sh.C;
+  v.st = ctx->stream;
+  v.launches = &ctx->launches;
+  cudaSetDevice(ctx->device);
+  cudaError_t err = v.alloc();
+  if (err == cudaSuccess) err = cudaStreamSynchronize(v.st);
+  if (err != cudaSuccess) {
+    v.release();
+    delete e;
+    return fnb_cuda_error(ctx, err, "evolver allocation");
+  }
+  *out = e;
+  return 0;
+}
+
+void fnb_evolver_destroy(fnb_evolver* ev) {
+  if (!ev) return;
+  cudaSetDevice(ev->ctx->device);
+  ev->ev.release();
+  ev->nets.release();
+  ev->X.release();
+  ev->Y.release();
+  delete ev;
+}
+
+int fnb_evolver_init_population(fnb_evolver* ev) {
+  cudaSetDevice(ev->ctx->device);
+  EV_CK(ev->ev.init_population());
+  EV_CK(cudaStreamSynchronize(ev->ev.st));
+  return 0;
+}
+
+int fnb_evolver_set_population(fnb_evolver* ev, const double* nodes, const double* conns) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  EV_CK(cudaMemcpyAsync(v.pn[v.cur], nodes, sizeof(double) * v.gn() * v.P, cudaMemcpyHostToDevice, v.st));
+  EV_CK(cudaMemcpyAsync(v.pc[v.cur], conns, sizeof(double) * v.gc() * v.P, cudaMemcpyHostToDevice, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  return 0;
+}
+
+int fnb_evolver_get_population(fnb_evolver* ev, double* nodes, double* conns) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  if (nodes) EV_CK(cudaMemcpyAsync(nodes, v.pn[v.cur], sizeof(double) * v.gn() * v.P, cudaMemcpyDeviceToHost, v.st));
+  if (conns) EV_CK(cudaMemcpyAsync(conns, v.pc[v.cur], sizeof(double) * v.gc() * v.P, cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  return 0;
+}
+
+int fnb_evolver_set_fitness(fnb_evolver* ev, const double* fitness) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  EV_CK(cudaMemcpyAsync(v.fitness, fitness, sizeof(double) * v.P, cudaMemcpyHostToDevice, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  return 0;
+}
+
+int fnb_evolver_get_fitness(fnb_evolver* ev, double* fitness) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  EV_CK(cudaMemcpyAsync(fitness, v.fitness, sizeof(double) * v.P, cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  return 0;
+}
+
+// transform + forward + fused fitness of the current population (device data)
+int fnb_evolver_evaluate_d(fnb_evolver* ev, const float* d_X, const float* d_Y, int batch, int fitness_kind,
+                           double fitness_offset) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  cudaSetDevice(ctx->device);
+  EV_CK(ev->nets.ensure(ctx->L.bytes * size_t(v.P)));
+  EV_CK(fnb::launch_transform(v.pn[v.cur], v.pc[v.cur], v.P, static_cast<uint8_t*>(ev->nets.p), ctx->L, ctx->sh,
+                              v.st));
+  ctx->launches++;
+  EV_CK(ctx->partial.ensure(fnb::forward_partial_needed(ctx->L, v.P, batch)));
+  if (fnb::launch_forward(ev->nets.p, ctx->L, v.P, d_X, d_Y, batch, fitness_kind, fitness_offset, v.fitness, nullptr,
+                          static_cast<double*>(ctx->partial.p), ctx->partial.cap,
+                          ctx->sh.n_agg == 1 ? int(ctx->sh.agg[0]) : -1, ctx->sh.n_act == 1 ? int(ctx->sh.act[0]) : -1,
+                          v.st, &ctx->launches))
+    return fnb_cuda_error(ctx, cudaGetLastError(), "forward launch");
+  return 0;
+}
+
+// host-data variant: inputs / targets as FP64 host arrays (B x I, B x O)
+int fnb_evolver_evaluate(fnb_evolver* ev, const double* X, const double* Y, int batch, int fitness_kind,
+                         double fitness_offset) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  cudaSetDevice(ctx->device);
+  const size_t nx = size_t(batch) * ctx->sh.I, ny = size_t(batch) * ctx->sh.O;
+  std::vector<float> xf(nx), yf(ny);
+  for (size_t i = 0; i < nx; ++i) xf[i] = float(X[i]);
+  for (size_t i = 0; i < ny; ++i) yf[i] = float(Y[i]);
+  EV_CK(ev->X.ensure(sizeof(float) * nx + 16));
+  EV_CK(ev->Y.ensure(sizeof(float) * ny + 16));
+  EV_CK(cudaMemcpyAsync(ev->X.p, xf.data(), sizeof(float) * nx, cudaMemcpyHostToDevice, v.st));
+  EV_CK(cudaMemcpyAsync(ev->Y.p, yf.data(), sizeof(float) * ny, cudaMemcpyHostToDevice, v.st));
+  int st = fnb_evolver_evaluate_d(ev, static_cast<float*>(ev->X.p), static_cast<float*>(ev->Y.p), batch,
+                                  fitness_kind, fitness_offset);
+  if (st) return st;
+  EV_CK(cudaStreamSynchronize(v.st));
+  return 0;
+}
+
+int fnb_evolver_step(fnb_evolver* ev) {
+  cudaSetDevice(ev->ctx->device);
+  int err = -1;
+  EV_CK(ev->ev.step(&err));
+  if (err == -2) return fnb_set_error(ev->ctx, FNB_E_EVAL_ERROR, "spawn counts do not sum to pop_size", -1);
+  if (err >= 0) return fnb_set_error(ev->ctx, FNB_E_DUPLICATE_KEY, "mutation failed in child slot", err);
+  return 0;
+}
+
+int fnb_evolver_species(fnb_evolver* ev, int* count, int* ids, int* sizes, int* spawn, double* best, int* stagnation,
+                        int* species_of) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  fnb::SpeciesDev h;
+  EV_CK(cudaMemcpyAsync(&h, v.sd, sizeof(h), cudaMemcpyDeviceToHost, v.st));
+  if (species_of) EV_CK(cudaMemcpyAsync(species_of, v.species_of, sizeof(int) * v.P, cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  if (count) *count = h.count;
+  for (int j = 0; j < h.count; ++j) {
+    if (ids) ids[j] = h.id[j];
+    if (sizes) sizes[j] = h.size[j];
+    if (spawn) spawn[j] = h.spawn[j];
+    if (best) best[j] = h.best[j];
+    if (stagnation) stagnation[j] = h.stag[j];
+  }
+  return 0;
+}
+
+int fnb_evolver_state(fnb_evolver* ev, int* generation, int* next_key) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  int nk[2] = {0, 0};
+  EV_CK(cudaMemcpyAsync(nk, v.next_key, sizeof(nk), cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  if (generation) *generation = v.generation;
+  if (next_key) *next_key = nk[0];
+  return 0;
+}
+
+int fnb_evolver_device_state(fnb_evolver* ev, double** d_nodes, double** d_conns, double** d_fitness,
+                             void** stream) {
+  fnb::Evolver& v = ev->ev;
+  if (d_nodes) *d_nodes = v.pn[v.cur];
+  if (d_conns) *d_conns = v.pc[v.cur];
+  if (d_fitness) *d_fitness = v.fitness;
+  if (stream) *stream = v.st;
+  return 0;
+}
+
+}  // extern "C"

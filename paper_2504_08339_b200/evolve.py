@@ -1,0 +1,178 @@
+"""The generation loop (SPEC.md:328-424 `evolution`; PAPER Algorithm 1) on the device.
+
+NeatConfig mirrors SPEC's NeatConfig with the paper's Appendix C defaults
+(PAPER.md:1030-1060).  Evolver wraps fnb_evolver_* (include/flatneat_b200.h):
+the population, species state, fitness and innovation counter all stay in
+HBM; each `step()` runs speciate -> update_stagnation -> compute_spawn_counts
+-> reproduce as device kernels.  `evolve()` is SPEC's evolve(problem, cfg,
+key): evaluate, stop at the fitness target BEFORE reproducing, step.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _native as N
+from .api import (FIT_NEG_MSE, AttributeSchema, DistanceConfig, Engine, FlatneatError, GenomeLimits,
+                  MutationConfig, _dp)
+
+
+@dataclass
+class NeatConfig:
+    """SPEC.md:333-336 with Appendix C defaults."""
+    pop_size: int = 1000
+    max_species: int = 10
+    compatibility_threshold: float = 3.5
+    species_elitism: int = 2
+    max_stagnation: int = 15
+    genome_elitism: int = 2
+    survival_threshold: float = 0.2
+    spawn_number_change_rate: float = 0.5
+    output_activation: int = 0
+    mutation: MutationConfig = field(default_factory=MutationConfig)
+    distance: DistanceConfig = field(default_factory=DistanceConfig)
+    fitness_target: float = float("inf")
+    generation_limit: int = 100
+
+    def to_c(self) -> N.fnb_neat_config:
+        return N.fnb_neat_config(self.pop_size, self.max_species, self.compatibility_threshold, self.species_elitism,
+                                 self.max_stagnation, self.genome_elitism, self.survival_threshold,
+                                 self.spawn_number_change_rate, self.output_activation, self.mutation.to_c(),
+                                 self.distance.to_c())
+
+
+@dataclass
+class RunStats:
+    """one record per completed generation."""
+    generation: int
+    best: float
+    mean: float
+    std: float
+    species_count: int
+    elapsed_ms: float
+
+
+class Evolver:
+    def __init__(self, engine: Engine, cfg: NeatConfig, seed: int):
+        self.engine = engine
+        self.cfg = cfg
+        self.seed = seed
+        self._lib = N.lib()
+        h = C.c_void_p()
+        c = cfg.to_c()
+        st = self._lib.fnb_evolver_create(engine._h, C.byref(c), C.c_uint64(seed), C.byref(h))
+        if st:
+            raise FlatneatError(st, self._lib.fnb_last_error(engine._h).decode())
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.fnb_evolver_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, st):
+        if st:
+            raise FlatneatError(st, self._lib.fnb_last_error(self.engine._h).decode(),
+                                int(self._lib.fnb_last_error_index(self.engine._h)))
+
+    # -- population ------------------------------------------------------------
+    def init_population(self):
+        self._raise(self._lib.fnb_evolver_init_population(self._h))
+
+    def population(self):
+        P, L = self.cfg.pop_size, self.engine.limits
+        n = np.empty((P, L.max_nodes, 5))
+        c = np.empty((P, L.max_conns, 4))
+        self._raise(self._lib.fnb_evolver_get_population(self._h, _dp(n), _dp(c)))
+        return n, c
+
+    def set_population(self, nodes, conns):
+        n = np.ascontiguousarray(nodes, dtype=np.float64)
+        c = np.ascontiguousarray(conns, dtype=np.float64)
+        self._raise(self._lib.fnb_evolver_set_population(self._h, _dp(n), _dp(c)))
+
+    # -- fitness ----------------------------------------------------------------
+    def evaluate(self, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0):
+        x = np.ascontiguousarray(X, dtype=np.float64)
+        y = np.ascontiguousarray(Y, dtype=np.float64)
+        self._raise(self._lib.fnb_evolver_evaluate(self._h, _dp(x), _dp(y), x.shape[0], kind, offset))
+
+    def evaluate_d(self, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0):
+        self._raise(self._lib.fnb_evolver_evaluate_d(self._h, X.data_ptr(), Y.data_ptr(), X.shape[0], kind, offset))
+
+    def fitness(self) -> np.ndarray:
+        f = np.empty(self.cfg.pop_size)
+        self._raise(self._lib.fnb_evolver_get_fitness(self._h, _dp(f)))
+        return f
+
+    def set_fitness(self, fitness):
+        f = np.ascontiguousarray(fitness, dtype=np.float64)
+        self._raise(self._lib.fnb_evolver_set_fitness(self._h, _dp(f)))
+
+    # -- generation ---------------------------------------------------------------
+    def step(self):
+        self._raise(self._lib.fnb_evolver_step(self._h))
+
+    def species(self):
+        cnt = C.c_int(0)
+        ids = np.zeros(32, dtype=np.int32)
+        sizes = np.zeros(32, dtype=np.int32)
+        spawn = np.zeros(32, dtype=np.int32)
+        best = np.zeros(32)
+        stag = np.zeros(32, dtype=np.int32)
+        sof = np.zeros(self.cfg.pop_size, dtype=np.int32)
+        ip = lambda a: a.ctypes.data_as(N.IP)
+        self._raise(self._lib.fnb_evolver_species(self._h, C.byref(cnt), ip(ids), ip(sizes), ip(spawn), _dp(best),
+                                                  ip(stag), ip(sof)))
+        k = cnt.value
+        return dict(count=k, ids=ids[:k], sizes=sizes[:k], spawn=spawn[:k], best=best[:k], stagnation=stag[:k],
+                    species_of=sof)
+
+    def state(self):
+        g, nk = C.c_int(0), C.c_int(0)
+        self._raise(self._lib.fnb_evolver_state(self._h, C.byref(g), C.byref(nk)))
+        return g.value, nk.value
+
+    def device_state(self):
+        n, c, f, s = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self._raise(self._lib.fnb_evolver_device_state(self._h, C.byref(n), C.byref(c), C.byref(f), C.byref(s)))
+        return n.value, c.value, f.value, s.value
+
+
+def evolve(engine: Engine, cfg: NeatConfig, seed: int, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0,
+           on_generation: Optional[Callable[[RunStats], None]] = None):
+    """evaluate -> check target -> speciate/stagnate/spawn/reproduce.
+    Returns (best genome (nodes, conns), best fitness, [RunStats])."""
+    ev = Evolver(engine, cfg, seed)
+    ev.init_population()
+    stats: List[RunStats] = []
+    best = (None, -np.inf)
+    for gen in range(cfg.generation_limit):
+        t0 = time.perf_counter()
+        ev.evaluate(X, Y, kind, offset)
+        fit = ev.fitness()
+        i = int(np.argmax(fit))  # lowest index on ties
+        if fit[i] > best[1]:
+            n, c = ev.population()
+            best = ((n[i].copy(), c[i].copy()), float(fit[i]))
+        done = fit[i] >= cfg.fitness_target
+        if not done:
+            ev.step()
+        rs = RunStats(gen, float(fit[i]), float(fit.mean()), float(fit.std()), ev.species()["count"],
+                      (time.perf_counter() - t0) * 1e3)
+        stats.append(rs)
+        if on_generation:
+            on_generation(rs)
+        if done:
+            break
+    return best[0], best[1], stats

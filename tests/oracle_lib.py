@@ -180,10 +180,12 @@ class Problem:
         return len(self.output_keys)
 
     def c(self) -> Shape:
-        self._ik = np.asarray(self.input_keys, dtype=np.int32)
-        self._ok = np.asarray(self.output_keys, dtype=np.int32)
-        return Shape(self.max_nodes, self.max_conns, len(self.input_keys), len(self.output_keys),
-                     ptr(self._ik, I32P), ptr(self._ok, I32P))
+        ik = np.asarray(self.input_keys, dtype=np.int32)
+        ok = np.asarray(self.output_keys, dtype=np.int32)
+        s = Shape(self.max_nodes, self.max_conns, len(self.input_keys), len(self.output_keys),
+                  ptr(ik, I32P), ptr(ok, I32P))
+        s._keep = (ik, ok)  # the key arrays live as long as the struct
+        return s
 
     def empty_pop(self, P: int):
         return (np.full((P, self.max_nodes, 5), np.nan), np.full((P, self.max_conns, 4), np.nan))
@@ -405,3 +407,66 @@ def mutate_population(prob, schema, pop_nodes, pop_conns, keys: np.ndarray, cfg:
     nk = t.next_key
     lib.fo_innov_free(C.byref(t))
     return st, bad, nk, nodes, conns
+
+
+# ---------------------------------------------------------------------------
+# Evolution restatement driver (oracle/evolution.c)
+# ---------------------------------------------------------------------------
+
+def neat_cfg(pop_size, max_species=10, threshold=3.5, species_elitism=2, max_stagnation=15, genome_elitism=2,
+             survival=0.2, spawn_rate=0.5, output_activation=0, mutation=None, cd=1.0, ch=0.5) -> NeatCfg:
+    return NeatCfg(pop_size, max_species, threshold, species_elitism, max_stagnation, genome_elitism, survival,
+                   spawn_rate, output_activation, mutation if mutation is not None else mut_cfg(), DistCfg(cd, ch))
+
+
+class OracleEvolution:
+    """The frozen CPU generation loop: speciate -> stagnation -> spawn -> reproduce."""
+
+    def __init__(self, prob: Problem, schema: SchemaSpec, cfg: NeatCfg, seed: int):
+        self.prob, self.schema, self.cfg, self.seed = prob, schema, cfg, seed
+        self._sh, self._sc = prob.c(), schema.c()
+        lib = oracle()
+        lib.fo_species_init.argtypes = [C.POINTER(Species), C.POINTER(Shape), C.c_int]
+        lib.fo_speciate.argtypes = [C.POINTER(Shape), C.POINTER(NeatCfg), F64P, F64P, C.POINTER(Species), I32P]
+        lib.fo_update_stagnation.argtypes = [C.POINTER(NeatCfg), F64P, C.POINTER(Species), I32P]
+        lib.fo_compute_spawn.argtypes = [C.POINTER(NeatCfg), F64P, I32P, C.POINTER(Species)]
+        self.species = Species()
+        lib.fo_species_init(C.byref(self.species), C.byref(self._sh), cfg.max_species)
+        P = cfg.pop_size
+        self.nodes, self.conns = prob.empty_pop(P)
+        self.innov = InnovTable()
+        lib.fo_innov_init(C.byref(self.innov), prob.num_inputs + prob.num_outputs + 1)
+        self.generation = 0
+        self.species_of = np.zeros(P, dtype=np.int32)
+
+    def init_population(self):
+        st = oracle().fo_initialize_population(C.byref(self._sh), C.byref(self._sc), C.byref(self.cfg),
+                                               C.c_uint64(self.seed), ptr(self.nodes, F64P), ptr(self.conns, F64P))
+        assert st == 0, st
+
+    def step(self, fitness: np.ndarray):
+        lib = oracle()
+        P = self.cfg.pop_size
+        f = np.ascontiguousarray(fitness, dtype=np.float64)
+        lib.fo_speciate(C.byref(self._sh), C.byref(self.cfg), ptr(self.nodes, F64P), ptr(self.conns, F64P),
+                        C.byref(self.species), ptr(self.species_of, I32P))
+        lib.fo_update_stagnation(C.byref(self.cfg), ptr(f, F64P), C.byref(self.species), ptr(self.species_of, I32P))
+        lib.fo_compute_spawn(C.byref(self.cfg), ptr(f, F64P), ptr(self.species_of, I32P), C.byref(self.species))
+        lib.fo_innov_next_generation(C.byref(self.innov))
+        nn, nc = self.prob.empty_pop(P)
+        pa = np.zeros(P, dtype=np.int32)
+        pb = np.zeros(P, dtype=np.int32)
+        st = lib.fo_reproduce(C.byref(self._sh), C.byref(self._sc), C.byref(self.cfg), ptr(self.nodes, F64P),
+                              ptr(self.conns, F64P), ptr(f, F64P), ptr(self.species_of, I32P),
+                              C.byref(self.species), C.c_uint64(self.seed), self.generation, C.byref(self.innov),
+                              ptr(nn, F64P), ptr(nc, F64P), ptr(pa, I32P), ptr(pb, I32P))
+        assert st == 0, st
+        self.nodes, self.conns = nn, nc
+        self.generation += 1
+
+    def species_view(self):
+        s = self.species
+        k = s.count
+        return dict(count=k, ids=np.array([s.id[j] for j in range(k)]), spawn=np.array([s.spawn[j] for j in range(k)]),
+                    best=np.array([s.best_fitness[j] for j in range(k)]),
+                    stagnation=np.array([s.stagnation[j] for j in range(k)]))

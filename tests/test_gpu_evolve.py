@@ -1,0 +1,91 @@
+"""The device generation loop vs the frozen CPU restatement (oracle/evolution.c).
+
+SPEC-only stages have no reference code ("parity unpinned"),
+so the bar is bit-exact equality with the restatement, which itself is built
+on oracle functions pinned to the reference.  Both sides receive the SAME
+fitness vector each generation: the device evaluates it, the
+CPU loop is handed a copy.  Checked every generation: the whole population
+(node and connection tensors, bit for bit), species ids / spawn counts /
+best fitness / stagnation counters, and the innovation counter.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as ol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fnb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_08339_b200 as m
+    return m
+
+
+def _mut(fnb, kw):
+    m = fnb.MutationConfig()
+    for k, v in kw.items():
+        setattr(m, k, fnb.AttrMutation(*v) if isinstance(v, tuple) else v)
+    return m
+
+
+CASES = [
+    # (name, pop, limits, threshold, max_species, max_stagnation, mutation overrides, generations)
+    ("default", 200, (24, 80), 3.5, 10, 15, {}, 12),
+    ("many-species", 240, (24, 80), 0.6, 10, 15, dict(node_add=0.5, conn_add=0.6), 12),
+    ("stagnation", 160, (20, 60), 0.8, 6, 1, dict(node_delete=0.2, conn_delete=0.2), 12),
+    ("overflow", 120, (20, 60), 0.05, 4, 3, dict(activation_replace_rate=0.2), 10),
+]
+
+
+@pytest.mark.parametrize("name,P,limits,th,ms,stag,mkw,G", CASES)
+def test_generation_loop_bit_exact(fnb, name, P, limits, th, ms, stag, mkw, G):
+    from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+    from paper_2504_08339_b200.synthetic import regression_dataset
+    schema_acts = ["tanh", "sigmoid", "identity"]
+    prob = ol.Problem(limits[0], limits[1], [0, 1, 2], [3])
+    schema = ol.SchemaSpec(schema_acts, ["sum", "product"])
+    eng = fnb.Engine(fnb.GenomeLimits(*limits), [0, 1, 2], [3], fnb.AttributeSchema(schema_acts, ["sum", "product"]))
+    cfg = NeatConfig(pop_size=P, max_species=ms, compatibility_threshold=th, max_stagnation=stag,
+                     mutation=_mut(fnb, mkw), output_activation=1)
+    ev = Evolver(eng, cfg, seed=2024)
+    ocfg = ol.neat_cfg(P, max_species=ms, threshold=th, max_stagnation=stag, output_activation=1,
+                       mutation=ol.mut_cfg(**mkw))
+    orc = ol.OracleEvolution(prob, schema, ocfg, seed=2024)
+    ev.init_population()
+    orc.init_population()
+    gn, gc = ev.population()
+    np.testing.assert_array_equal(gn, orc.nodes)
+    np.testing.assert_array_equal(gc, orc.conns)
+    X, Y = regression_dataset(64, 3, 1, seed=5)
+    for g in range(G):
+        ev.evaluate(X, Y)
+        fit = ev.fitness()
+        orc.step(fit)
+        ev.step()
+        gn, gc = ev.population()
+        np.testing.assert_array_equal(gn, orc.nodes, err_msg=f"{name} gen {g} nodes")
+        np.testing.assert_array_equal(gc, orc.conns, err_msg=f"{name} gen {g} conns")
+        sp, so = ev.species(), orc.species_view()
+        assert sp["count"] == so["count"], (name, g)
+        np.testing.assert_array_equal(sp["ids"], so["ids"])
+        np.testing.assert_array_equal(sp["spawn"], so["spawn"])
+        np.testing.assert_array_equal(sp["best"], so["best"])
+        np.testing.assert_array_equal(sp["stagnation"], so["stagnation"])
+        assert ev.state()[1] == orc.innov.next_key, (name, g)
+        assert int(np.sum(sp["spawn"])) == P
+
+
+def test_xor_evolves(fnb):
+    """SPEC.md:441-449 shape: XOR with a bias input; fitness 4 - SSE rises."""
+    from paper_2504_08339_b200.evolve import NeatConfig, evolve
+    from paper_2504_08339_b200.synthetic import xor_dataset
+    eng = fnb.Engine(fnb.GenomeLimits(16, 32), [0, 1, 2], [3], fnb.AttributeSchema(["sigmoid", "tanh"], ["sum"]))
+    X, Y = xor_dataset(bias_input=True)
+    cfg = NeatConfig(pop_size=1000, generation_limit=60, fitness_target=3.9)
+    best, fit, stats = evolve(eng, cfg, seed=0, X=X, Y=Y, kind=fnb.FIT_OFFSET_SSE, offset=4.0)
+    assert stats[-1].best >= stats[0].best
+    assert fit > 3.0
