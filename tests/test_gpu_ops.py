@@ -117,3 +117,15 @@ def test_crossover_identical_parents(fnb):
     cn, cc = _engine(fnb, prob, schema).crossover(nodes, conns, nodes, conns, ck)
     np.testing.assert_array_equal(cn, nodes)
     np.testing.assert_array_equal(cc, conns)
+
+
+def test_cpp_dropin_header(fnb):
+    """include/flatneat/gpu.hpp used with the reference's own C++ types and
+    functions (tests/cpp/test_gpu_hpp.cpp, built by __graft_entry__.build())."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "_bin", "test_gpu_hpp")
+    if not os.path.exists(exe):
+        pytest.skip("test_gpu_hpp not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "gpu.hpp parity ok" in r.stdout, r.stdout + r.stderr
