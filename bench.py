@@ -124,6 +124,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-generations", action="store_true")
     ap.add_argument("--spt", type=int, default=0, help="forward columns per thread (tuning; 0 = auto)")
     args = ap.parse_args()
 
@@ -239,6 +240,40 @@ def main():
     h2d = nodes_h.nbytes + conns_h.nbytes + X_h.nbytes + Y_h.nbytes
     d2h = fit_h.nbytes
 
+    # ---- generations/s: evaluate + speciate/stagnate/spawn/reproduce on the device ----
+    gen = None
+    if not args.no_generations:
+        from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+        ev = Evolver(eng, NeatConfig(pop_size=P_SHARD), seed=1000 + rank)
+        ev.set_population(nodes_h, conns_h)
+        es = torch.cuda.ExternalStream(ev.device_state()[3])
+        g_warm, g_steps = max(3, args.warmup), max(5, args.steps)
+        gms, ems = [], []
+        launches_g0 = 0
+        for it in range(g_warm + g_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if it == g_warm:
+                launches_g0 = eng.launch_count
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(es)
+            ev.evaluate_d(X, Y)
+            e1.record(es)
+            ev.step()
+            e2.record(es)
+            es.synchronize()
+            if it >= g_warm:
+                gms.append(e0.elapsed_time(e2))
+                ems.append(e0.elapsed_time(e1))
+        sp = ev.species()
+        gen = {"generations_per_s": 1e3 / float(np.mean(gms)), "ms_per_generation": float(np.mean(gms)),
+               "evaluate_ms": float(np.mean(ems)), "evolve_step_ms": float(np.mean(gms) - np.mean(ems)),
+               "generations_timed": g_steps, "species": int(sp["count"]),
+               "launches_per_generation": (eng.launch_count - launches_g0) / g_steps,
+               "note": "pop 10k per GPU, C2 shapes; step = speciate+stagnation+spawn+reproduce (K3,K5,K6,K7 + "
+                       "selection), fitness from the fused forward; per-GPU replicas at N>1"}
+        ev.close()
+
     # ---- roofline for the dominant kernel (K2 forward) ----
     n_en = int(np.sum(conns_h[:, :, 2] == 1.0))
     n_ops = int(np.sum(~np.isnan(nodes_h[:, :, 0]))) - P_SHARD * NI
@@ -278,6 +313,8 @@ def main():
                                   "frac": smem_bytes / fwd_s / 1e12 / smem_peak}},
             "clocks": clocks,
         }
+        if gen is not None:
+            line["generations"] = gen
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

@@ -228,6 +228,8 @@ int fnb_evolver_step(fnb_evolver* ev);
 int fnb_evolver_species(fnb_evolver* ev, int* count, int* ids, int* sizes, int* spawn, double* best,
                         int* stagnation, int* species_of);
 int fnb_evolver_state(fnb_evolver* ev, int* generation, int* next_key);
+/* InnovationTable::reserve_up_to for a population loaded with set_population */
+int fnb_evolver_set_next_key(fnb_evolver* ev, int next_key);
 /* device pointers of the current population / fitness and the evolver's stream */
 int fnb_evolver_device_state(fnb_evolver* ev, double** d_nodes, double** d_conns, double** d_fitness,
                              void** stream);

@@ -89,6 +89,7 @@ SIGNATURES = {
     "fnb_evolver_step": (C.c_int, [VP]),
     "fnb_evolver_species": (C.c_int, [VP, IP, IP, IP, IP, DP, IP, IP]),
     "fnb_evolver_state": (C.c_int, [VP, IP, IP]),
+    "fnb_evolver_set_next_key": (C.c_int, [VP, C.c_int]),
     "fnb_evolver_device_state": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)]),
     "fnb_stream_draws_d": (C.c_int, [VP, VP, C.c_int, C.c_int, C.c_int, C.c_uint64, VP, VP]),
     "fnb_split_keys_d": (C.c_int, [VP, U32P, C.c_uint64, C.c_int, VP, VP]),

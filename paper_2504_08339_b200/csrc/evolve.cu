@@ -857,6 +857,15 @@ int fnb_evolver_state(fnb_evolver* ev, int* generation, int* next_key) {
   return 0;
 }
 
+int fnb_evolver_set_next_key(fnb_evolver* ev, int next_key) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  const int nk[2] = {next_key, 0};
+  EV_CK(cudaMemcpyAsync(v.next_key, nk, sizeof(nk), cudaMemcpyHostToDevice, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  return 0;
+}
+
 int fnb_evolver_device_state(fnb_evolver* ev, double** d_nodes, double** d_conns, double** d_fitness,
                              void** stream) {
   fnb::Evolver& v = ev->ev;

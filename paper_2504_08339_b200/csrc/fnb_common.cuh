@@ -37,7 +37,8 @@ struct NetHeader {          // 32 B
   int16_t n_ops;            // non-input rows in order
   int16_t n_edges;          // enabled edges feeding ops
   int16_t n_rec;            // forward records
-  int32_t pad1, pad2;
+  int32_t n_slots;          // forward value slots (liveness-shared); slot n_slots = zero row
+  int32_t pad2;
 };
 static_assert(sizeof(NetHeader) == 32, "header");
 

@@ -133,13 +133,14 @@ struct FwdParams {
   double* out;          // [P][B][O] or null
   double* partial;      // [P][chunks] when gridDim.y > 1
   size_t group_smem;    // bytes per group
+  int rows_lo, rows_hi; // this pass evaluates genomes needing rows_lo < n_slots+1 <= rows_hi value rows
 };
 
-__host__ __device__ inline size_t fwd_group_smem(int N, int C, int I, int O, int T, int spt) {
+__host__ __device__ inline size_t fwd_group_smem(int N, int C, int I, int O, int T, int spt, int rows) {
   size_t b = align16(size_t(max_records(N, C) + 1) * sizeof(SRec));  // + zero sentinel
   b += align16(size_t(I + O) * sizeof(uint32_t));
   b += 8 * sizeof(double);                                  // reduction scratch (T/32 <= 8 warps)
-  b += size_t(N + 1) * size_t(T) * spt * sizeof(float);     // node values + zero row
+  b += size_t(rows) * size_t(T) * spt * sizeof(float);      // value slots + zero slot
   return align16(b);
 }
 
@@ -163,8 +164,13 @@ k_forward(FwdParams p) {
   const uint32_t row_bytes = uint32_t(TC) * 4u;
   const uint32_t vb = uint32_t(__cvta_generic_to_shared(v)) + uint32_t(j) * SPT * 4u;  // my columns
 
-  const bool live = grp < p.groups && g < p.P;
-  int n_rec = 0;
+  bool live = grp < p.groups && g < p.P;
+  int n_rec = 0, n_slots = 0;
+  if (live) {  // genomes whose live values need more slots go to the overflow pass
+    const NetHeader* hd = reinterpret_cast<const NetHeader*>(p.nets + size_t(g) * L.bytes);
+    n_slots = hd->n_slots;
+    live = n_slots + 1 > p.rows_lo && n_slots + 1 <= p.rows_hi;
+  }
   if (live) {
     const uint8_t* net = p.nets + size_t(g) * L.bytes;
     n_rec = reinterpret_cast<const NetHeader*>(net)->n_rec;
@@ -184,7 +190,7 @@ k_forward(FwdParams p) {
     float z[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) z[k] = 0.0f;
-    sts<SPT>(vb + (uint32_t(L.N) << row_shift), z);  // the all-zero pad row
+    sts<SPT>(vb + (uint32_t(n_slots) << row_shift), z);  // the all-zero pad slot
   }
   __syncthreads();
 
@@ -319,9 +325,11 @@ k_forward(FwdParams p) {
 }
 
 __global__ void k_fitness_finalize(const double* __restrict__ partial, int chunks, int P, int B, int O,
-                                   int fit_kind, double offset, double* __restrict__ fitness) {
+                                   int fit_kind, double offset, double* __restrict__ fitness,
+                                   const uint8_t* __restrict__ nets, size_t stride, int rows_hi) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P) return;
+  if (reinterpret_cast<const NetHeader*>(nets + size_t(g) * stride)->n_slots + 1 > rows_hi) return;  // overflow pass
   double sse = 0.0;
   for (int c = 0; c < chunks; ++c) sse += partial[size_t(g) * chunks + c];
   fitness[g] = fit_kind == FNB_FIT_NEG_MSE ? -(sse / (double(B) * double(O))) : offset - sse;
@@ -338,25 +346,29 @@ __global__ void k_to_float(const double* __restrict__ src, float* __restrict__ d
 // ---- host launchers --------------------------------------------------------
 
 struct FwdConfig {
-  int T, spt, block, groups, chunks, grid_x;
+  int T, spt, block, groups, chunks, grid_x, rows;
   size_t group_smem, cta_smem;
 };
 
-static int g_force_spt = 0;  // tuning override (fnb_set_forward_spt)
+static int g_force_spt = 0;       // tuning override (fnb_set_forward_spt)
+static int g_rows_pct = 62;       // main-pass slot capacity, % of max_nodes + 1
 
-static FwdConfig fwd_config(const NetLayout& L, int P, int B) {
+// Launch geometry for `rows` value rows per column (slots + the zero slot).
+static FwdConfig fwd_config(const NetLayout& L, int P, int B, int rows, bool single_chunk) {
   FwdConfig c{};
+  c.rows = rows;
   // columns per group: cover the batch, at most 256, shrinking until a
-  // group fits ~72 KB (3 resident CTAs per SM)
+  // group fits ~72 KB (>= 3 resident CTAs per SM)
   int cols = 1;
   while (cols < B && cols < 256) cols <<= 1;
   int spt = g_force_spt ? g_force_spt : (cols >= 128 ? 2 : 1);
-  while (cols > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, std::max(1, cols / spt), spt) > 72 * 1024) cols >>= 1;
+  while (cols > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, std::max(1, cols / spt), spt, rows) > 72 * 1024)
+    cols >>= 1;
   spt = std::min(spt, cols);
   const int T = std::max(1, cols / spt);
   c.spt = spt;
   c.T = T;
-  c.group_smem = fwd_group_smem(L.N, L.C, L.I, L.O, T, spt);
+  c.group_smem = fwd_group_smem(L.N, L.C, L.I, L.O, T, spt, rows);
   // groups per CTA: up to 256 threads and ~96 KB of shared memory
   int groups = std::max(1, 256 / T);
   while (groups > 1 && c.group_smem * groups > 96 * 1024) groups >>= 1;
@@ -367,14 +379,19 @@ static FwdConfig fwd_config(const NetLayout& L, int P, int B) {
   const int tiles = (B + T * spt - 1) / (T * spt);
   const int target = 4 * 148;  // >= 4 CTAs per SM before splitting samples
   c.chunks = 1;
-  if (c.grid_x < target) c.chunks = std::min(tiles, (target + c.grid_x - 1) / c.grid_x);
+  if (!single_chunk && c.grid_x < target) c.chunks = std::min(tiles, (target + c.grid_x - 1) / c.grid_x);
   return c;
 }
 
+static int main_rows(const NetLayout& L) {
+  return std::min(L.N + 1, std::max(16, ((L.N + 1) * g_rows_pct + 99) / 100));
+}
+
 void set_forward_spt(int spt) { g_force_spt = (spt == 1 || spt == 2 || spt == 4) ? spt : 0; }
+void set_forward_rows_pct(int pct) { g_rows_pct = (pct >= 10 && pct <= 100) ? pct : 62; }
 
 size_t forward_partial_needed(NetLayout L, int P, int B) {
-  const FwdConfig c = fwd_config(L, P, B);
+  const FwdConfig c = fwd_config(L, P, B, main_rows(L), false);
   return sizeof(double) * size_t(P) * size_t(c.chunks) + 16;
 }
 
@@ -411,12 +428,29 @@ static cudaError_t launch_spt(const FwdConfig& c, const FwdParams& p, int agg, i
   return launch_k<SPT, -1, -1>(c, p, st);
 }
 
+static cudaError_t launch_pass(const FwdConfig& c, FwdParams p, int rows_lo, int agg, int act, cudaStream_t st) {
+  if (c.cta_smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  p.T = c.T;
+  p.groups = c.groups;
+  p.group_smem = c.group_smem;
+  p.rows_lo = rows_lo;
+  p.rows_hi = c.rows;
+  switch (c.spt) {
+    case 4: return launch_spt<4>(c, p, agg, act, st);
+    case 2: return launch_spt<2>(c, p, agg, act, st);
+    default: return launch_spt<1>(c, p, agg, act, st);
+  }
+}
+
+// Two passes: genomes whose live values fit the main slot capacity (almost
+// all), then -- over the same grid, exiting immediately for the rest -- the
+// few that need up to max_nodes + 1 rows.
 // uniform_agg / uniform_act: the single registry entry, or -1 for mixed schemas
 int launch_forward(const void* nets, NetLayout L, int P, const float* X, const float* Y, int B, int fit_kind,
                    double offset, double* fitness, double* out, double* partial_buf, size_t partial_cap,
                    int uniform_agg, int uniform_act, cudaStream_t st, long long* launches) {
-  const FwdConfig c = fwd_config(L, P, B);
-  if (c.cta_smem > 227 * 1024) return 1;
+  const int rows_main = main_rows(L);
+  const FwdConfig c = fwd_config(L, P, B, rows_main, false);
   FwdParams p;
   p.nets = static_cast<const uint8_t*>(nets);
   p.L = L;
@@ -424,27 +458,23 @@ int launch_forward(const void* nets, NetLayout L, int P, const float* X, const f
   p.X = X;
   p.Y = Y;
   p.B = B;
-  p.T = c.T;
-  p.groups = c.groups;
   p.fit_kind = fit_kind;
   p.fit_offset = offset;
   p.fitness = fitness;
   p.out = out;
   p.partial = partial_buf;
-  p.group_smem = c.group_smem;
   if (c.chunks > 1 && fit_kind != FNB_FIT_NONE && sizeof(double) * size_t(P) * c.chunks > partial_cap) return 1;
-  cudaError_t e;
-  switch (c.spt) {
-    case 4: e = launch_spt<4>(c, p, uniform_agg, uniform_act, st); break;
-    case 2: e = launch_spt<2>(c, p, uniform_agg, uniform_act, st); break;
-    default: e = launch_spt<1>(c, p, uniform_agg, uniform_act, st); break;
-  }
-  if (e != cudaSuccess) return 1;
+  if (launch_pass(c, p, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
   ++*launches;
   if (c.chunks > 1 && fit_kind != FNB_FIT_NONE) {
     k_fitness_finalize<<<(P + 255) / 256, 256, 0, st>>>(partial_buf, c.chunks, P, B, L.O, fit_kind, offset,
-                                                         fitness);
+                                                         fitness, p.nets, L.bytes, rows_main);
     if (cudaGetLastError() != cudaSuccess) return 1;
+    ++*launches;
+  }
+  if (rows_main < L.N + 1) {
+    const FwdConfig co = fwd_config(L, P, B, L.N + 1, true);
+    if (launch_pass(co, p, rows_main, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
     ++*launches;
   }
   return 0;

@@ -266,9 +266,14 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     return;
   }
 
-  // ---- 6. forward records: ops in topological order, skipping input rows
-  //         (network.hpp:252-254); each op = max(1, ceil(fanin/4)) records
-  Rec* grec = reinterpret_cast<Rec*>(net + L.ops_off);
+  // ---- 6a. ops in topological order, skipping input rows (network.hpp:252-254):
+  //          op index and record base per row; each op = max(1, ceil(fanin/4))
+  //          records.  (rank / row_of_rank / R / sorted_key are free after
+  //          Kahn and reused as opos / slot_of / last_use / fanin.)
+  uint16_t* opos = s.rank;
+  uint16_t* slot_of = s.row_of_rank;
+  int* last_use = s.R;
+  int* fanin = s.sorted_key;
   int op_base = 0, rec_base = 0, edge_total = 0;
   for (int p0 = 0; p0 < count; p0 += 32) {
     const int p = p0 + lane;
@@ -291,35 +296,95 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
       const int te = __shfl_up_sync(kFull, incl_e, d);
       if (lane >= d) { incl += t; incl_e += te; }
     }
-    const int rb = rec_base + incl - nrec;
     if (is_op) {
-      RecHeader h;
-      h.bias = float(nrow[row * kNodeCols + kBias]);
-      h.resp = float(nrow[row * kNodeCols + kResp]);
-      h.dst = uint16_t(row);
-      h.act = sh.act[int(nrow[row * kNodeCols + kAct])];
-      h.agg = sh.agg[int(nrow[row * kNodeCols + kAgg])];
-      h.fanin = uint16_t(ne);
-      for (int k = 0; k < nrec; ++k) {
-        h.cnt = uint8_t(min(kRecSlots, ne - k * kRecSlots > 0 ? ne - k * kRecSlots : 0));
-        h.flags = uint8_t((k == 0 ? kRecFirst : 0) | (k == nrec - 1 ? kRecLast : 0));
-        grec[rb + k].h = h;
-      }
-      Edge z;  // pad slots of the last record: zero weight, all-zero row N
-      z.w = 0.0f;
-      z.src = uint16_t(N);
-      z.conn_row = 0xffff;
-      for (int q = ne; q < nrec * kRecSlots; ++q) grec[rb + q / kRecSlots].slot[q % kRecSlots] = z;
-      s.ebeg[row] = uint16_t(rb);
+      opos[row] = uint16_t(op_base + __popc(m & ((1u << lane) - 1u)));
+      s.ebeg[row] = uint16_t(rec_base + incl - nrec);
+      fanin[row] = ne;
     }
     op_base += __popc(m);
     rec_base += __shfl_sync(kFull, incl, 31);
     edge_total += __shfl_sync(kFull, incl_e, 31);
   }
+  // ---- 6b. last consumer (op index) of every value; outputs live to the end
+  for (int r = lane; r < N; r += 32) last_use[r] = -1;
   __syncwarp();
+  for (int i = lane; i < sh.O; i += 32) last_use[out_rows[i]] = 0x7fffffff;
+  __syncwarp();
+  for (int r = lane; r < C; r += 32) {
+    const int dst = s.cdst[r];
+    if (dst < 0 || (s.flags[dst] & 2)) continue;
+    atomicMax(&last_use[s.csrc[r]], int(opos[dst]));
+  }
+  __syncwarp();
+  // ---- 6c. value slots: linear-scan allocation over the op order, a slot is
+  //          released after its value's last consumer (lane 0, <= 255 values)
+  int n_slots = 0;
+  if (lane == 0) {
+    uint32_t used[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto alloc = [&]() {
+      int w = 0;
+      while (used[w] == 0xffffffffu) ++w;
+      const int b = __ffs(~used[w]) - 1;
+      used[w] |= 1u << b;
+      const int sl = w * 32 + b;
+      n_slots = max(n_slots, sl + 1);
+      return sl;
+    };
+    auto release = [&](int sl) { used[sl >> 5] &= ~(1u << (sl & 31)); };
+    for (int r = 0; r < N; ++r) slot_of[r] = 0xffff;
+    for (int i = 0; i < sh.I; ++i) {
+      const int r = in_rows[i];
+      if (slot_of[r] == 0xffff) slot_of[r] = uint16_t(alloc());
+    }
+    int k = 0;
+    for (int p = 0; p < count; ++p) {
+      const int row = s.order[p];
+      if (s.flags[row] & 2) continue;
+      for (int w = 0; w < W; ++w) {  // sources whose last consumer is this op
+        uint32_t bits = s.pred[row * W + w];
+        while (bits) {
+          const int src = w * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (last_use[src] == k) release(slot_of[src]);
+        }
+      }
+      const int sl = alloc();
+      slot_of[row] = uint16_t(sl);
+      if (last_use[row] < 0) release(sl);  // written, never read
+      ++k;
+    }
+  }
+  n_slots = __shfl_sync(kFull, n_slots, 0);
+  __syncwarp();
+  // ---- 6d. record headers; pad slots read the zero slot n_slots
+  Rec* grec = reinterpret_cast<Rec*>(net + L.ops_off);
+  for (int p = lane; p < count; p += 32) {
+    const int row = s.order[p];
+    if (s.flags[row] & 2) continue;
+    const int ne = fanin[row];
+    const int nrec = ne == 0 ? 1 : (ne + kRecSlots - 1) / kRecSlots;
+    const int rb = s.ebeg[row];
+    RecHeader h;
+    h.bias = float(nrow[row * kNodeCols + kBias]);
+    h.resp = float(nrow[row * kNodeCols + kResp]);
+    h.dst = slot_of[row];
+    h.act = sh.act[int(nrow[row * kNodeCols + kAct])];
+    h.agg = sh.agg[int(nrow[row * kNodeCols + kAgg])];
+    h.fanin = uint16_t(ne);
+    for (int k = 0; k < nrec; ++k) {
+      h.cnt = uint8_t(min(kRecSlots, ne - k * kRecSlots > 0 ? ne - k * kRecSlots : 0));
+      h.flags = uint8_t((k == 0 ? kRecFirst : 0) | (k == nrec - 1 ? kRecLast : 0));
+      grec[rb + k].h = h;
+    }
+    Edge z;  // pad slots of the last record: zero weight, the zero slot
+    z.w = 0.0f;
+    z.src = uint16_t(n_slots);
+    z.conn_row = 0xffff;
+    for (int q = ne; q < nrec * kRecSlots; ++q) grec[rb + q / kRecSlots].slot[q % kRecSlots] = z;
+  }
 
   // ---- 7. edges: the i-th predecessor (ascending source row) of an op goes
-  //         to slot i%4 of its record i/4
+  //         to slot i%4 of its record i/4, reading the source's value slot
   for (int r = lane; r < C; r += 32) {
     const int dst = s.cdst[r];
     if (dst < 0 || (s.flags[dst] & 2)) continue;
@@ -334,11 +399,16 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     }
     Edge e;
     e.w = float(crow[r * kConnCols + kW]);
-    e.src = uint16_t(src);
+    e.src = slot_of[src];
     e.conn_row = uint16_t(r);
     grec[s.ebeg[dst] + below / kRecSlots].slot[below % kRecSlots] = e;
   }
+  __syncwarp();
+  // ---- 8. input / output rows become value slots for the forward
+  for (int i = lane; i < sh.I; i += 32) in_rows[i] = slot_of[in_rows[i]];
+  for (int i = lane; i < sh.O; i += 32) out_rows[i] = slot_of[out_rows[i]];
   if (lane == 0) {
+    reinterpret_cast<NetHeader*>(net)->n_slots = n_slots;
     NetHeader* h = reinterpret_cast<NetHeader*>(net);
     h->status = 0;
     h->err_kind = kErrNone;

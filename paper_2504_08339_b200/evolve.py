@@ -97,9 +97,13 @@ class Evolver:
         return n, c
 
     def set_population(self, nodes, conns):
+        """Load a population; the innovation counter moves above its largest key."""
         n = np.ascontiguousarray(nodes, dtype=np.float64)
         c = np.ascontiguousarray(conns, dtype=np.float64)
         self._raise(self._lib.fnb_evolver_set_population(self._h, _dp(n), _dp(c)))
+        keys = n[:, :, 0]
+        top = int(np.nanmax(keys)) + 1 if np.any(~np.isnan(keys)) else 0
+        self._raise(self._lib.fnb_evolver_set_next_key(self._h, max(top, self.state()[1])))
 
     # -- fitness ----------------------------------------------------------------
     def evaluate(self, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0):
