@@ -177,21 +177,40 @@ __global__ void k7_advance(int* next_key) { next_key[0] += next_key[1]; }
 
 // ---------------------------------------------------------------------------
 // apply_node_split + mutate_rest (ops.hpp:222-361)
+//
+// The child's keys and flags are staged in shared memory (and kept in step
+// with every structural edit lane 0 makes to the HBM rows), so each scan
+// and each lane-0 stream step is a shared-memory access, not an L2 trip.
+// The long attribute stream split(5) is produced 64 draws at a time by the
+// whole warp (one Philox block per lane) and walked warp-uniformly.
 // ---------------------------------------------------------------------------
 struct MutSmem {
-  unsigned long long* nkeys;  // node key -> first row
+  unsigned long long* nkeys;  // marker table: node key -> first row
   int* nrows;
-  unsigned long long* ckeys;  // conn pair -> first row
+  unsigned long long* ckeys;  // marker table: conn pair -> first row
   int* crows;
   uint32_t* reach;            // [N][W]: rows reachable (>= 1 enabled edge) from row
   uint32_t* act_n;            // [2N] bias / response actions of node rows
   uint32_t* act_c;            // [C] weight actions
+  int* nkey;                  // [N] node key (rows)
+  int* cin;                   // [C]
+  int* cout;                  // [C]
+  int* list_a;                // [N] scratch lists (keys / targets / sorted)
+  int* list_b;                // [N]
+  unsigned long long* dbuf;   // [64] stream draws
+  uint8_t* nflag;             // [N] bit0 non-empty, bit1 input, bit2 output
+  uint8_t* cflag;             // [C] bit0 non-empty, bit1 enabled
+  int8_t* new_agg;            // [N] -1 or replacement id
+  int8_t* new_act;            // [N]
 };
 
 __host__ __device__ inline size_t mut_smem_bytes(int N, int C) {
   const int W = (N + 31) / 32;
-  return size_t(table_capacity(N)) * 12 + size_t(table_capacity(C)) * 12 + size_t(N) * W * 4 +
-         size_t(2 * N + C) * 4 + 64;
+  size_t b = size_t(table_capacity(N)) * 12 + size_t(table_capacity(C)) * 12;
+  b += size_t(N) * W * 4 + size_t(2 * N + C) * 4;  // reach, actions
+  b += size_t(N) * 4 * 3 + size_t(C) * 4 * 2;      // nkey, list_a, list_b, cin, cout
+  b += 64 * 8 + size_t(N) * 3 + size_t(C) + 64;    // dbuf, flags, new ids, slack
+  return align16(b);
 }
 
 __device__ inline MutSmem mut_carve(uint8_t* p, int N, int C) {
@@ -199,11 +218,21 @@ __device__ inline MutSmem mut_carve(uint8_t* p, int N, int C) {
   const int Hn = table_capacity(N), Hc = table_capacity(C), W = (N + 31) / 32;
   s.nkeys = reinterpret_cast<unsigned long long*>(p); p += size_t(Hn) * 8;
   s.ckeys = reinterpret_cast<unsigned long long*>(p); p += size_t(Hc) * 8;
+  s.dbuf = reinterpret_cast<unsigned long long*>(p); p += 64 * 8;
   s.nrows = reinterpret_cast<int*>(p); p += size_t(Hn) * 4;
   s.crows = reinterpret_cast<int*>(p); p += size_t(Hc) * 4;
   s.reach = reinterpret_cast<uint32_t*>(p); p += size_t(N) * W * 4;
   s.act_n = reinterpret_cast<uint32_t*>(p); p += size_t(2 * N) * 4;
-  s.act_c = reinterpret_cast<uint32_t*>(p);
+  s.act_c = reinterpret_cast<uint32_t*>(p); p += size_t(C) * 4;
+  s.nkey = reinterpret_cast<int*>(p); p += size_t(N) * 4;
+  s.list_a = reinterpret_cast<int*>(p); p += size_t(N) * 4;
+  s.list_b = reinterpret_cast<int*>(p); p += size_t(N) * 4;
+  s.cin = reinterpret_cast<int*>(p); p += size_t(C) * 4;
+  s.cout = reinterpret_cast<int*>(p); p += size_t(C) * 4;
+  s.nflag = p; p += N;
+  s.cflag = p; p += C;
+  s.new_agg = reinterpret_cast<int8_t*>(p); p += N;
+  s.new_act = reinterpret_cast<int8_t*>(p);
   return s;
 }
 
@@ -213,19 +242,23 @@ __device__ __forceinline__ bool is_key_in(int key, const int* ks, int n) {
   return false;
 }
 
-// attribute action code: bit0-1 kind (0 none, 1 add normal(0,power), 2 replace
-// normal(init)), bits 2.. = stream position of the normal's first draw
-__device__ __forceinline__ uint32_t scalar_action(Stream& s, double rate, double replace) {
-  const double u = s.uniform();  // mutate_scalar, ops.hpp:281-289
-  if (u < rate || u < rate + replace) {
-    const uint32_t pos = uint32_t(s.position());
-    s.next_u64();
-    s.next_u64();
-    return (pos << 2) | (u < rate ? 1u : 2u);
-  }
-  return 0u;
+__device__ __forceinline__ void stage_node(MutSmem& sm, const double* n, int r, const DevShape& sh) {
+  const double k = n[r * kNodeCols + kKey];
+  if (isnan(k)) { sm.nflag[r] = 0; sm.nkey[r] = 0; return; }
+  const int key = int(k);
+  sm.nkey[r] = key;
+  sm.nflag[r] = uint8_t(1 | (is_key_in(key, sh.input_keys, sh.I) ? 2 : 0) | (is_key_in(key, sh.output_keys, sh.O) ? 4 : 0));
+}
+__device__ __forceinline__ void stage_conn(MutSmem& sm, const double* c, int r) {
+  const double2 a = *reinterpret_cast<const double2*>(c + r * kConnCols);
+  if (isnan(a.x)) { sm.cflag[r] = 0; sm.cin[r] = 0; sm.cout[r] = 0; return; }
+  sm.cin[r] = int(a.x);
+  sm.cout[r] = int(a.y);
+  sm.cflag[r] = uint8_t(1 | (c[r * kConnCols + kEn] == 1.0 ? 2 : 0));
 }
 
+// attribute action code: bit0-1 kind (0 none, 1 add normal(0,power), 2 replace
+// normal(init)), bits 2.. = stream position of the normal's first draw
 __device__ __forceinline__ double apply_scalar(double v, uint32_t a, const Key4& k, double power, double mean,
                                                double sd) {
   if ((a & 3u) == 0) return v;
@@ -234,6 +267,44 @@ __device__ __forceinline__ double apply_scalar(double v, uint32_t a, const Key4&
   if ((a & 3u) == 1) return __dadd_rn(v, glibc::normal_from_uniforms(u0, u1, 0.0, power));
   return glibc::normal_from_uniforms(u0, u1, mean, sd);
 }
+
+// split(5) stream, 64 draws per refill, walked identically by every lane
+struct ChunkStream {
+  Key4 key;
+  uint64_t pos = 0, base = ~0ull;
+  unsigned long long* buf;
+  __device__ __forceinline__ uint64_t at(uint64_t q) {
+    if (base == ~0ull || q < base || q >= base + 64) {
+      base = q & ~63ull;
+      __syncwarp();
+      const int lane = threadIdx.x & 31;
+      uint32_t b[4];
+      stream_block(key, (base >> 1) + uint64_t(lane), b);
+      buf[2 * lane] = (uint64_t(b[3]) << 32) | b[2];
+      buf[2 * lane + 1] = (uint64_t(b[1]) << 32) | b[0];
+      __syncwarp();
+    }
+    return buf[q - base];
+  }
+  __device__ __forceinline__ uint64_t next() { return at(pos++); }
+  __device__ __forceinline__ double uniform() { return u64_to_uniform(next()); }
+  __device__ __forceinline__ int index(int n) {  // below(n), rng.hpp:99-106
+    const uint64_t mx = ~0ull, limit = mx - ((mx % uint64_t(n)) + 1) % uint64_t(n);
+    uint64_t x = next();
+    while (x > limit) x = next();
+    return int(x % uint64_t(n));
+  }
+  // mutate_scalar (ops.hpp:281-289): record the action, consume its draws
+  __device__ __forceinline__ uint32_t scalar(double rate, double replace) {
+    const double u = uniform();
+    if (u < rate || u < rate + replace) {
+      const uint32_t a = (uint32_t(pos) << 2) | (u < rate ? 1u : 2u);
+      pos += 2;
+      return a;
+    }
+    return 0u;
+  }
+};
 
 __global__ void __launch_bounds__(128)
 k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
@@ -253,57 +324,53 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
   double* cc = conns + size_t(c) * C * kConnCols;
   const Key4 key = load_key(keys, c);
   const int Hn = table_capacity(N), Hc = table_capacity(C), W = (N + 31) / 32;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
   int st = 0;
-  auto node_key_at = [&](int r) { return int(n[r * kNodeCols + kKey]); };
+  for (int r = lane; r < N; r += 32) stage_node(sm, n, r, sh);
+  for (int r = lane; r < C; r += 32) stage_conn(sm, cc, r);
+  __syncwarp();
+  auto n_live = [&](int q) { return (sm.nflag[q] & 1) != 0; };
+  auto c_live = [&](int q) { return (sm.cflag[q] & 1) != 0; };
 
   // ---- apply_node_split (ops.hpp:222-243)
   if (plan_flag[c]) {
     const unsigned long long pr = plan_pair[c];
     const int in_key = int(uint32_t(pr >> 32)), out_key = int(uint32_t(pr));
-    const int r = warp_first(C, [&](int q) {
-      return !row_empty_c(cc, q) && int(cc[q * kConnCols + kIn]) == in_key && int(cc[q * kConnCols + kOut]) == out_key;
-    });
+    const int r = warp_first(C, [&](int q) { return c_live(q) && sm.cin[q] == in_key && sm.cout[q] == out_key; });
     if (r >= 0) {
-      const double old_w = cc[r * kConnCols + kW];
       const int nk = new_key[c];
-      double bias = 0.0, resp = 0.0;
+      const bool dup = warp_first(N, [&](int q) { return n_live(q) && sm.nkey[q] == nk; }) >= 0;
+      const int nr = warp_first(N, [&](int q) { return !n_live(q); });
+      const int cr0 = warp_first(C, [&](int q) { return !c_live(q); });
+      const int cr1 = cr0 < 0 ? -1 : warp_first(C, [&](int q) { return q > cr0 && !c_live(q); });
       if (lane == 0) {
+        const double old_w = cc[r * kConnCols + kW];
         cc[r * kConnCols + kEn] = 0.0;
-        Stream s(key_split(key, 1));
-        const double a0 = s.uniform(), a1 = s.uniform(), b0 = s.uniform(), b1 = s.uniform();
-        bias = glibc::normal_from_uniforms(a0, a1, cfg.b_mean, cfg.b_std);
-        resp = glibc::normal_from_uniforms(b0, b1, cfg.r_mean, cfg.r_std);
-      }
-      __syncwarp();
-      // add_node (ops.hpp:19-27): duplicate key, then first empty row
-      const bool dup = warp_first(N, [&](int q) { return !row_empty_n(n, q) && node_key_at(q) == nk; }) >= 0;
-      const int nr = warp_first(N, [&](int q) { return row_empty_n(n, q); });
-      if (dup) st = 1 + FNB_E_DUPLICATE_KEY;
-      else if (nr < 0) st = 1 + FNB_E_GENOME_FULL;
-      if (!st) {
-        if (lane == 0) {
+        sm.cflag[r] = 1;
+        if (dup) st = 1 + FNB_E_DUPLICATE_KEY;          // add_node (ops.hpp:19-27)
+        else if (nr < 0) st = 1 + FNB_E_GENOME_FULL;
+        else if (cr1 < 0) st = 1 + FNB_E_GENOME_FULL;   // add_conn x2 (ops.hpp:46-58)
+        if (!st) {
+          Stream s(key_split(key, 1));
+          const double a0 = s.uniform(), a1 = s.uniform(), b0 = s.uniform(), b1 = s.uniform();
           double* row = n + nr * kNodeCols;
           row[kKey] = double(nk);
-          row[kBias] = bias;
-          row[kResp] = resp;
+          row[kBias] = glibc::normal_from_uniforms(a0, a1, cfg.b_mean, cfg.b_std);
+          row[kResp] = glibc::normal_from_uniforms(b0, b1, cfg.r_mean, cfg.r_std);
           row[kAgg] = double(cfg.default_agg);
           row[kAct] = double(cfg.default_act);
-        }
-        __syncwarp();
-        // add_conn x2 (ops.hpp:46-58): endpoints exist, pairs are new, first empty row
-        for (int e = 0; e < 2 && !st; ++e) {
-          const int cr = warp_first(C, [&](int q) { return row_empty_c(cc, q); });
-          if (cr < 0) { st = 1 + FNB_E_GENOME_FULL; break; }
-          if (lane == 0) {
-            double* row = cc + cr * kConnCols;
-            row[kIn] = double(e == 0 ? in_key : nk);
-            row[kOut] = double(e == 0 ? nk : out_key);
-            row[kEn] = 1.0;
-            row[kW] = e == 0 ? 1.0 : old_w;
-          }
-          __syncwarp();
+          double* c0 = cc + cr0 * kConnCols;
+          c0[kIn] = double(in_key); c0[kOut] = double(nk); c0[kEn] = 1.0; c0[kW] = 1.0;
+          double* c1 = cc + cr1 * kConnCols;
+          c1[kIn] = double(nk); c1[kOut] = double(out_key); c1[kEn] = 1.0; c1[kW] = old_w;
+          sm.nkey[nr] = nk;
+          sm.nflag[nr] = uint8_t(1 | (is_key_in(nk, sh.input_keys, sh.I) ? 2 : 0) | (is_key_in(nk, sh.output_keys, sh.O) ? 4 : 0));
+          sm.cin[cr0] = in_key; sm.cout[cr0] = nk; sm.cflag[cr0] = 3;
+          sm.cin[cr1] = nk; sm.cout[cr1] = out_key; sm.cflag[cr1] = 3;
         }
       }
+      st = __shfl_sync(kFullMask, st, 0);
+      __syncwarp();
     }
   }
 
@@ -313,27 +380,37 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
     int coin = 0;
     if (lane == 0) coin = s.coin(cfg.conn_add);
     coin = __shfl_sync(kFullMask, coin, 0);
-    const int free_row = coin ? warp_first(C, [&](int q) { return row_empty_c(cc, q); }) : -1;
+    const int free_row = coin ? warp_first(C, [&](int q) { return !c_live(q); }) : -1;
     if (free_row >= 0) {
-      auto is_target = [&](int q) { return !row_empty_n(n, q) && !is_key_in(node_key_at(q), sh.input_keys, sh.I); };
-      const int nk = warp_count(N, [&](int q) { return !row_empty_n(n, q); });
-      const int nt = warp_count(N, is_target);
+      // keys[] (node keys, row order) and targets[] (non-input keys, row order)
+      int nk = 0, nt = 0;
+      for (int r0 = 0; r0 < N; r0 += 32) {
+        const int q = r0 + lane;
+        const bool live = q < N && n_live(q);
+        const bool tgt = live && !(sm.nflag[q] & 2);
+        const unsigned bl = __ballot_sync(kFullMask, live), bt = __ballot_sync(kFullMask, tgt);
+        const unsigned below = (1u << lane) - 1u;
+        if (live) sm.list_a[nk + __popc(bl & below)] = sm.nkey[q];
+        if (tgt) sm.list_b[nt + __popc(bt & below)] = sm.nkey[q];
+        nk += __popc(bl);
+        nt += __popc(bt);
+      }
       if (nk > 0 && nt > 0) {
-        // marker tables and the enabled-edge reachability closure (by row)
         for (int i = lane; i < Hn; i += 32) { sm.nkeys[i] = kEmptyKey; sm.nrows[i] = INT_MAX; }
         for (int i = lane; i < Hc; i += 32) { sm.ckeys[i] = kEmptyKey; sm.crows[i] = INT_MAX; }
         for (int i = lane; i < N * W; i += 32) sm.reach[i] = 0u;
         __syncwarp();
         for (int q = lane; q < N; q += 32)
-          if (!row_empty_n(n, q)) table_insert(sm.nkeys, sm.nrows, Hn - 1, node_key(n[q * kNodeCols]), q);
+          if (n_live(q)) table_insert(sm.nkeys, sm.nrows, Hn - 1, uint32_t(sm.nkey[q]), q);
         for (int q = lane; q < C; q += 32)
-          if (!row_empty_c(cc, q))
-            table_insert(sm.ckeys, sm.crows, Hc - 1, conn_key(cc[q * kConnCols + kIn], cc[q * kConnCols + kOut]), q);
+          if (c_live(q))
+            table_insert(sm.ckeys, sm.crows, Hc - 1,
+                         (static_cast<unsigned long long>(uint32_t(sm.cin[q])) << 32) | uint32_t(sm.cout[q]), q);
         __syncwarp();
         for (int q = lane; q < C; q += 32) {
-          if (row_empty_c(cc, q) || cc[q * kConnCols + kEn] != 1.0) continue;
-          const int a = table_find(sm.nkeys, sm.nrows, Hn - 1, node_key(cc[q * kConnCols + kIn]));
-          const int b = table_find(sm.nkeys, sm.nrows, Hn - 1, node_key(cc[q * kConnCols + kOut]));
+          if (sm.cflag[q] != 3) continue;  // enabled edges only (ops.hpp:106)
+          const int a = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(sm.cin[q]));
+          const int b = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(sm.cout[q]));
           if (a >= 0 && b >= 0) atomicOr(&sm.reach[a * W + (b >> 5)], 1u << (b & 31));
         }
         __syncwarp();
@@ -345,69 +422,55 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
         }
         // legal(from, to): pair absent and !creates_cycle (ops.hpp:93-111, 261-263)
         auto legal = [&](int from, int to) {
-          if (table_find(sm.ckeys, sm.crows, Hc - 1, conn_key(double(from), double(to))) >= 0) return false;
+          const unsigned long long pk = (static_cast<unsigned long long>(uint32_t(from)) << 32) | uint32_t(to);
+          if (table_find(sm.ckeys, sm.crows, Hc - 1, pk) >= 0) return false;
           if (from == to) return false;
-          const int rt = table_find(sm.nkeys, sm.nrows, Hn - 1, node_key(double(to)));
-          const int rf = table_find(sm.nkeys, sm.nrows, Hn - 1, node_key(double(from)));
+          const int rt = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(to));
+          const int rf = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(from));
           if (rt < 0 || rf < 0) return true;
           return !((sm.reach[rt * W + (rf >> 5)] >> (rf & 31)) & 1u);
         };
         int found = 0, pf = 0, pt = 0;
         if (lane == 0) {
           for (int probe = 0; probe < 16 && !found; ++probe) {
-            const int ki = s.index(nk), ti = s.index(nt);
-            // keys[] / targets[] are node keys in row order
-            int from = 0, to = 0;
-            for (int q = 0, seen = 0; q < N; ++q)
-              if (!row_empty_n(n, q) && seen++ == ki) { from = node_key_at(q); break; }
-            for (int q = 0, seen = 0; q < N; ++q)
-              if (!row_empty_n(n, q) && !is_key_in(node_key_at(q), sh.input_keys, sh.I) && seen++ == ti) {
-                to = node_key_at(q);
-                break;
-              }
+            const int from = sm.list_a[s.index(nk)];
+            const int to = sm.list_b[s.index(nt)];
             if (legal(from, to)) { found = 1; pf = from; pt = to; }
           }
         }
         found = __shfl_sync(kFullMask, found, 0);
         if (!found) {
           // deterministic fallback: sorted keys x sorted targets, from-major
-          // (ops.hpp:271-278).  Sorted position of a row = rank of its key.
-          int* sk = reinterpret_cast<int*>(sm.act_c);  // scratch: sorted keys / targets
+          // (ops.hpp:271-278); sorted position = rank of (key, list index)
+          int* sk = reinterpret_cast<int*>(sm.act_c);
           int* stg = sk + N;
-          for (int q = lane; q < N; q += 32) {
-            if (row_empty_n(n, q)) continue;
-            const int kq = node_key_at(q);
-            int rk = 0, rt = 0;
-            for (int p = 0; p < N; ++p) {
-              if (row_empty_n(n, p)) continue;
-              const int kp = node_key_at(p);
-              const bool before = kp < kq || (kp == kq && p < q);
-              rk += before;
-              if (!is_key_in(kp, sh.input_keys, sh.I)) rt += before;
-            }
+          __syncwarp();
+          for (int q = lane; q < nk; q += 32) {
+            const int kq = sm.list_a[q];
+            int rk = 0;
+            for (int p = 0; p < nk; ++p) rk += sm.list_a[p] < kq || (sm.list_a[p] == kq && p < q);
             sk[rk] = kq;
-            if (!is_key_in(kq, sh.input_keys, sh.I)) stg[rt] = kq;
+          }
+          for (int q = lane; q < nt; q += 32) {
+            const int kq = sm.list_b[q];
+            int rt = 0;
+            for (int p = 0; p < nt; ++p) rt += sm.list_b[p] < kq || (sm.list_b[p] == kq && p < q);
+            stg[rt] = kq;
           }
           __syncwarp();
-          // count legal candidates per `from` (lane-strided), prefix in order
           int total = 0;
           for (int f0 = 0; f0 < nk; f0 += 32) {
             const int f = f0 + lane;
             int cnt = 0;
             if (f < nk)
               for (int t = 0; t < nt; ++t) cnt += legal(sk[f], stg[t]);
-            int incl = cnt;
-            for (int d = 1; d < 32; d <<= 1) {
-              const int v = __shfl_up_sync(kFullMask, incl, d);
-              if (lane >= d) incl += v;
-            }
-            total += __shfl_sync(kFullMask, incl, 31);
+            for (int d = 16; d > 0; d >>= 1) cnt += __shfl_down_sync(kFullMask, cnt, d);
+            total += __shfl_sync(kFullMask, cnt, 0);
           }
           if (total > 0) {
             int idx = 0;
-            if (lane == 0) idx = s.index(total);
-            idx = __shfl_sync(kFullMask, idx, 0);
             if (lane == 0) {
+              idx = s.index(total);
               for (int f = 0; f < nk && !found; ++f)
                 for (int t = 0; t < nt; ++t)
                   if (legal(sk[f], stg[t]) && idx-- == 0) { found = 1; pf = sk[f]; pt = stg[t]; break; }
@@ -416,19 +479,18 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
           }
           __syncwarp();
         }
-        if (found) {
-          pf = __shfl_sync(kFullMask, pf, 0);
-          pt = __shfl_sync(kFullMask, pt, 0);
-          if (lane == 0) {
-            const double u0 = s.uniform(), u1 = s.uniform();
-            double* row = cc + free_row * kConnCols;
-            row[kIn] = double(pf);
-            row[kOut] = double(pt);
-            row[kEn] = 1.0;
-            row[kW] = glibc::normal_from_uniforms(u0, u1, cfg.w_mean, cfg.w_std);
-          }
-          __syncwarp();
+        if (found && lane == 0) {
+          const double u0 = s.uniform(), u1 = s.uniform();
+          double* row = cc + free_row * kConnCols;
+          row[kIn] = double(pf);
+          row[kOut] = double(pt);
+          row[kEn] = 1.0;
+          row[kW] = glibc::normal_from_uniforms(u0, u1, cfg.w_mean, cfg.w_std);
+          sm.cin[free_row] = pf;
+          sm.cout[free_row] = pt;
+          sm.cflag[free_row] = 3;
         }
+        __syncwarp();
       }
     }
   }
@@ -440,27 +502,24 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
     if (lane == 0) coin = s.coin(cfg.node_delete);
     coin = __shfl_sync(kFullMask, coin, 0);
     if (coin) {
-      auto hidden = [&](int q) {
-        if (row_empty_n(n, q)) return false;
-        const int k = node_key_at(q);
-        return !is_key_in(k, sh.input_keys, sh.I) && !is_key_in(k, sh.output_keys, sh.O);
-      };
+      auto hidden = [&](int q) { return sm.nflag[q] == 1; };  // non-empty, neither input nor output
       const int nh = warp_count(N, hidden);
       if (nh > 0) {
         int idx = 0;
         if (lane == 0) idx = s.index(nh);
         idx = __shfl_sync(kFullMask, idx, 0);
-        const int rr = warp_kth(N, idx, hidden);
-        const int dk = node_key_at(rr);
+        const int dk = sm.nkey[warp_kth(N, idx, hidden)];
         // remove_node (ops.hpp:30-44): first row with the key, then cascade
-        const int rm = warp_first(N, [&](int q) { return !row_empty_n(n, q) && node_key_at(q) == dk; });
+        const int rm = warp_first(N, [&](int q) { return n_live(q) && sm.nkey[q] == dk; });
         __syncwarp();
-        if (lane == 0)
-          for (int a = 0; a < kNodeCols; ++a) n[rm * kNodeCols + a] = __longlong_as_double(0x7ff8000000000000ll);
+        if (lane == 0) {
+          for (int a = 0; a < kNodeCols; ++a) n[rm * kNodeCols + a] = nan;
+          sm.nflag[rm] = 0;
+        }
         for (int q = lane; q < C; q += 32) {
-          if (row_empty_c(cc, q)) continue;
-          if (int(cc[q * kConnCols + kIn]) == dk || int(cc[q * kConnCols + kOut]) == dk)
-            for (int a = 0; a < kConnCols; ++a) cc[q * kConnCols + a] = __longlong_as_double(0x7ff8000000000000ll);
+          if (!c_live(q) || (sm.cin[q] != dk && sm.cout[q] != dk)) continue;
+          for (int a = 0; a < kConnCols; ++a) cc[q * kConnCols + a] = nan;
+          sm.cflag[q] = 0;
         }
         __syncwarp();
       }
@@ -474,48 +533,58 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
     if (lane == 0) coin = s.coin(cfg.conn_delete);
     coin = __shfl_sync(kFullMask, coin, 0);
     if (coin) {
-      auto live = [&](int q) { return !row_empty_c(cc, q); };
-      const int nr = warp_count(C, live);
+      const int nr = warp_count(C, c_live);
       if (nr > 0) {
         int idx = 0;
         if (lane == 0) idx = s.index(nr);
         idx = __shfl_sync(kFullMask, idx, 0);
-        const int rr = warp_kth(C, idx, live);
-        const int a = int(cc[rr * kConnCols + kIn]), b = int(cc[rr * kConnCols + kOut]);
-        const int rm = warp_first(C, [&](int q) {
-          return !row_empty_c(cc, q) && int(cc[q * kConnCols + kIn]) == a && int(cc[q * kConnCols + kOut]) == b;
-        });
+        const int rr = warp_kth(C, idx, c_live);
+        const int a = sm.cin[rr], b = sm.cout[rr];
+        const int rm = warp_first(C, [&](int q) { return c_live(q) && sm.cin[q] == a && sm.cout[q] == b; });
         __syncwarp();
-        if (lane == 0)
-          for (int k = 0; k < kConnCols; ++k) cc[rm * kConnCols + k] = __longlong_as_double(0x7ff8000000000000ll);
+        if (lane == 0) {
+          for (int k = 0; k < kConnCols; ++k) cc[rm * kConnCols + k] = nan;
+          sm.cflag[rm] = 0;
+        }
         __syncwarp();
       }
     }
   }
 
-  // ---- attributes (ops.hpp:338-359): lane 0 walks split(5), all lanes apply
+  // ---- attributes (ops.hpp:338-359): every lane walks split(5) identically
+  //      over shared-memory draws; then all lanes apply the normals
   if (!st) {
     const Key4 k5 = key_split(key, 5);
-    if (lane == 0) {
-      Stream s(k5);
-      for (int q = 0; q < N; ++q) {
-        sm.act_n[2 * q] = 0u;
-        sm.act_n[2 * q + 1] = 0u;
-        if (row_empty_n(n, q)) continue;
-        if (is_key_in(node_key_at(q), sh.input_keys, sh.I)) continue;
-        sm.act_n[2 * q] = scalar_action(s, cfg.b_rate, cfg.b_replace);
-        sm.act_n[2 * q + 1] = scalar_action(s, cfg.r_rate, cfg.r_replace);
-        if (cfg.agg_rate > 0.0 && s.coin(cfg.agg_rate)) n[q * kNodeCols + kAgg] = double(s.index(cfg.n_agg));
-        if (cfg.act_rate > 0.0 && s.coin(cfg.act_rate)) n[q * kNodeCols + kAct] = double(s.index(cfg.n_act));
+    ChunkStream cs;
+    cs.key = k5;
+    cs.buf = sm.dbuf;
+    for (int q = 0; q < N; ++q) {
+      uint32_t ab = 0u, ar = 0u;
+      int ag = -1, ac = -1;
+      if (sm.nflag[q] & 1 && !(sm.nflag[q] & 2)) {
+        ab = cs.scalar(cfg.b_rate, cfg.b_replace);
+        ar = cs.scalar(cfg.r_rate, cfg.r_replace);
+        if (cfg.agg_rate > 0.0 && cs.uniform() < cfg.agg_rate) ag = cs.index(cfg.n_agg);
+        if (cfg.act_rate > 0.0 && cs.uniform() < cfg.act_rate) ac = cs.index(cfg.n_act);
       }
-      for (int q = 0; q < C; ++q)
-        sm.act_c[q] = row_empty_c(cc, q) ? 0u : scalar_action(s, cfg.w_rate, cfg.w_replace);
+      if (lane == 0) {
+        sm.act_n[2 * q] = ab;
+        sm.act_n[2 * q + 1] = ar;
+        sm.new_agg[q] = int8_t(ag);
+        sm.new_act[q] = int8_t(ac);
+      }
+    }
+    for (int q = 0; q < C; ++q) {
+      const uint32_t aw = (sm.cflag[q] & 1) ? cs.scalar(cfg.w_rate, cfg.w_replace) : 0u;
+      if (lane == 0) sm.act_c[q] = aw;
     }
     __syncwarp();
     for (int q = lane; q < N; q += 32) {
       const uint32_t ab = sm.act_n[2 * q], ar = sm.act_n[2 * q + 1];
       if (ab) n[q * kNodeCols + kBias] = apply_scalar(n[q * kNodeCols + kBias], ab, k5, cfg.b_power, cfg.b_mean, cfg.b_std);
       if (ar) n[q * kNodeCols + kResp] = apply_scalar(n[q * kNodeCols + kResp], ar, k5, cfg.r_power, cfg.r_mean, cfg.r_std);
+      if (sm.new_agg[q] >= 0) n[q * kNodeCols + kAgg] = double(sm.new_agg[q]);
+      if (sm.new_act[q] >= 0) n[q * kNodeCols + kAct] = double(sm.new_act[q]);
     }
     for (int q = lane; q < C; q += 32) {
       const uint32_t aw = sm.act_c[q];

@@ -68,21 +68,26 @@ __host__ __device__ __forceinline__ uint64_t stream_u64_at(const Key4& k, uint64
 // uniform() = (u64 >> 11) * 2^-53 (rng.hpp:90-92); coin(p) = uniform < p
 __host__ __device__ __forceinline__ double u64_to_uniform(uint64_t x) { return double(x >> 11) * 0x1.0p-53; }
 
-// Sequential stream with a one-block buffer (rng.hpp:77-134).
+// Sequential stream with a one-block buffer (rng.hpp:77-134).  The block is
+// kept as its two u64 halves so no array is indexed dynamically (registers,
+// not local memory, on the device).
 struct Stream {
   Key4 key;
   uint64_t block;
-  uint32_t buf[4];
-  int avail;
-  __host__ __device__ explicit Stream(const Key4& k) : key(k), block(0), buf{0, 0, 0, 0}, avail(0) {}
+  uint64_t first, second;  // draw order within the current block
+  int avail;               // u32 words left, as in the reference (4, 2, 0)
+  __host__ __device__ explicit Stream(const Key4& k) : key(k), block(0), first(0), second(0), avail(0) {}
   __host__ __device__ __forceinline__ uint64_t next_u64() {
     if (avail == 0) {
-      stream_block(key, block, buf);
+      uint32_t b[4];
+      stream_block(key, block, b);
       ++block;
+      first = (uint64_t(b[3]) << 32) | b[2];
+      second = (uint64_t(b[1]) << 32) | b[0];
       avail = 4;
     }
     avail -= 2;
-    return (uint64_t(buf[avail + 1]) << 32) | buf[avail];
+    return avail == 2 ? first : second;
   }
   __host__ __device__ __forceinline__ double uniform() { return u64_to_uniform(next_u64()); }
   __host__ __device__ __forceinline__ bool coin(double p) { return uniform() < p; }
