@@ -223,6 +223,14 @@ int fnb_evolver_evaluate(fnb_evolver* ev, const double* inputs, const double* ta
                          int fitness_kind, double fitness_offset);
 int fnb_evolver_evaluate_d(fnb_evolver* ev, const float* d_X, const float* d_Y, int batch, int fitness_kind,
                            double fitness_offset);
+/* a rank's shard [lo, hi): fitness of those genomes into d_fitness_out[hi-lo] */
+int fnb_evolver_evaluate_range_d(fnb_evolver* ev, int lo, int hi, const float* d_X, const float* d_Y, int batch,
+                                 int fitness_kind, double fitness_offset, double* d_fitness_out);
+/* device-to-device fitness injection (ordered on the evolver stream) */
+int fnb_evolver_set_fitness_d(fnb_evolver* ev, const double* d_fitness);
+/* population checksum (nodes, conns as 64-bit words: sum w_i*(2i+1) mod 2^64,
+   xor next_key << 32, xor generation): replicas of one run agree bit for bit */
+int fnb_evolver_checksum(fnb_evolver* ev, uint64_t* out);
 int fnb_evolver_step(fnb_evolver* ev);
 /* species arrays have room for 32 entries; species_of[pop_size] may be NULL */
 int fnb_evolver_species(fnb_evolver* ev, int* count, int* ids, int* sizes, int* spawn, double* best,

@@ -87,6 +87,9 @@ SIGNATURES = {
     "fnb_evolver_evaluate": (C.c_int, [VP, DP, DP, C.c_int, C.c_int, C.c_double]),
     "fnb_evolver_evaluate_d": (C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_double]),
     "fnb_evolver_step": (C.c_int, [VP]),
+    "fnb_evolver_evaluate_range_d": (C.c_int, [VP, C.c_int, C.c_int, VP, VP, C.c_int, C.c_int, C.c_double, VP]),
+    "fnb_evolver_set_fitness_d": (C.c_int, [VP, VP]),
+    "fnb_evolver_checksum": (C.c_int, [VP, C.POINTER(C.c_uint64)]),
     "fnb_evolver_species": (C.c_int, [VP, IP, IP, IP, IP, DP, IP, IP]),
     "fnb_evolver_state": (C.c_int, [VP, IP, IP]),
     "fnb_evolver_set_next_key": (C.c_int, [VP, C.c_int]),

@@ -857,6 +857,68 @@ int fnb_evolver_state(fnb_evolver* ev, int* generation, int* next_key) {
   return 0;
 }
 
+// evaluate genomes [lo, hi) only, writing d_fitness_out[0 .. hi-lo) (a rank's
+// shard of the population in the multi-GPU loop)
+int fnb_evolver_evaluate_range_d(fnb_evolver* ev, int lo, int hi, const float* d_X, const float* d_Y, int batch,
+                                 int fitness_kind, double fitness_offset, double* d_fitness_out) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  if (lo < 0 || hi > v.P || lo > hi) return fnb_set_error(ctx, FNB_E_SHAPE_MISMATCH, "bad genome range", -1);
+  const int n = hi - lo;
+  if (n == 0) return 0;
+  cudaSetDevice(ctx->device);
+  EV_CK(ev->nets.ensure(ctx->L.bytes * size_t(n)));
+  EV_CK(fnb::launch_transform(v.pn[v.cur] + size_t(lo) * v.gn(), v.pc[v.cur] + size_t(lo) * v.gc(), n,
+                              static_cast<uint8_t*>(ev->nets.p), ctx->L, ctx->sh, v.st));
+  ctx->launches++;
+  EV_CK(ctx->partial.ensure(fnb::forward_partial_needed(ctx->L, n, batch)));
+  if (fnb::launch_forward(ev->nets.p, ctx->L, n, d_X, d_Y, batch, fitness_kind, fitness_offset, d_fitness_out,
+                          nullptr, static_cast<double*>(ctx->partial.p), ctx->partial.cap,
+                          ctx->sh.n_agg == 1 ? int(ctx->sh.agg[0]) : -1, ctx->sh.n_act == 1 ? int(ctx->sh.act[0]) : -1,
+                          v.st, &ctx->launches))
+    return fnb_cuda_error(ctx, cudaGetLastError(), "forward launch");
+  return 0;
+}
+
+// population checksum: sum over 64-bit words w_i * (2i + 1) mod 2^64 (order
+// independent, so deterministic under atomics); replicas compare it
+__global__ void k_checksum(const unsigned long long* __restrict__ a, size_t n, size_t base,
+                           unsigned long long* out) {
+  unsigned long long s = 0;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    s += a[i] * (2ull * (base + i) + 1ull);
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_down_sync(0xffffffffu, s, d);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+int fnb_evolver_checksum(fnb_evolver* ev, uint64_t* out) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  cudaSetDevice(ctx->device);
+  EV_CK(ctx->partial.ensure(16));
+  unsigned long long* d = static_cast<unsigned long long*>(ctx->partial.p);
+  EV_CK(cudaMemsetAsync(d, 0, 8, v.st));
+  const size_t nn = v.gn() * v.P, nc = v.gc() * v.P;
+  k_checksum<<<4 * 148, 256, 0, v.st>>>(reinterpret_cast<const unsigned long long*>(v.pn[v.cur]), nn, 0, d);
+  k_checksum<<<4 * 148, 256, 0, v.st>>>(reinterpret_cast<const unsigned long long*>(v.pc[v.cur]), nc, nn, d);
+  ctx->launches += 2;
+  uint64_t h = 0;
+  int nk = 0;
+  EV_CK(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaMemcpyAsync(&nk, v.next_key, sizeof(int), cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  *out = h ^ (uint64_t(uint32_t(nk)) << 32) ^ uint64_t(uint32_t(v.generation));
+  return 0;
+}
+
+// device-to-device fitness injection on the evolver stream (after a gather)
+int fnb_evolver_set_fitness_d(fnb_evolver* ev, const double* d_fitness) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  EV_CK(cudaMemcpyAsync(v.fitness, d_fitness, sizeof(double) * v.P, cudaMemcpyDeviceToDevice, v.st));
+  return 0;
+}
+
 int fnb_evolver_set_next_key(fnb_evolver* ev, int next_key) {
   fnb::Evolver& v = ev->ev;
   cudaSetDevice(ev->ctx->device);

@@ -131,7 +131,8 @@ struct FwdParams {
   double fit_offset;
   double* fitness;      // [P] or null
   double* out;          // [P][B][O] or null
-  double* partial;      // [P][chunks] when gridDim.y > 1
+  double* partial;      // [P][units]: squared error of each 32-sample unit
+  int units;            // ceil(B / 32)
   size_t group_smem;    // bytes per group
   int rows_lo, rows_hi; // this pass evaluates genomes needing rows_lo < n_slots+1 <= rows_hi value rows
 };
@@ -139,7 +140,6 @@ struct FwdParams {
 __host__ __device__ inline size_t fwd_group_smem(int N, int C, int I, int O, int T, int spt, int rows) {
   size_t b = align16(size_t(max_records(N, C) + 1) * sizeof(SRec));  // + zero sentinel
   b += align16(size_t(I + O) * sizeof(uint32_t));
-  b += 8 * sizeof(double);                                  // reduction scratch (T/32 <= 8 warps)
   b += size_t(rows) * size_t(T) * spt * sizeof(float);      // value slots + zero slot
   return align16(b);
 }
@@ -156,9 +156,7 @@ k_forward(FwdParams p) {
   uint8_t* base = smem_raw + size_t(grp < p.groups ? grp : 0) * p.group_smem;
   SRec* s_rec = reinterpret_cast<SRec*>(base);
   uint32_t* s_io = reinterpret_cast<uint32_t*>(base + align16(size_t(max_records(L.N, L.C) + 1) * sizeof(SRec)));
-  double* s_red = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(s_io) +
-                                            align16(size_t(L.I + L.O) * sizeof(uint32_t)));
-  uint8_t* v = reinterpret_cast<uint8_t*>(s_red) + 8 * sizeof(double);
+  uint8_t* v = reinterpret_cast<uint8_t*>(s_io) + align16(size_t(L.I + L.O) * sizeof(uint32_t));
   const int TC = T * SPT;                                 // columns per tile
   const uint32_t row_shift = uint32_t(__ffs(TC * 4) - 1);  // v row stride = TC*4 bytes (a power of two)
   const uint32_t row_bytes = uint32_t(TC) * 4u;
@@ -195,7 +193,13 @@ k_forward(FwdParams p) {
   __syncthreads();
 
   const int I = L.I, O = L.O;
-  double err = 0.0;
+  // fitness units: 32 consecutive samples, reduced by an adjacent-pair tree
+  // (in-thread over SPT, then shfl_xor over the unit's lanes); samples >= B
+  // add exact zeros, so a unit's sum depends on neither T, SPT, the chunking
+  // nor the population it is evaluated with
+  const int ulanes = min(32 / SPT, T);
+  const int lane = threadIdx.x & 31;
+  const unsigned gmask = T >= 32 ? 0xffffffffu : (((1u << T) - 1u) << (lane & ~(T - 1)));
   // sample tiles of this CTA's y-chunk; dead groups (g >= P) run zero tiles
   // but stay resident for the warp-synchronous reduction below
   const int tiles = (p.B + TC - 1) / TC;
@@ -286,7 +290,10 @@ k_forward(FwdParams p) {
       }
       cur.a = s_rec[r + 1].a;
     }
-    // outputs + fitness epilogue
+    // outputs + fitness epilogue: per-sample squared error, outputs in order
+    double e[SPT];
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) e[k] = 0.0;
     for (int o = 0; o < O; ++o) {
       float val[SPT];
       lds_pred<SPT>(true, vb + s_io[I + o], val);
@@ -297,41 +304,29 @@ k_forward(FwdParams p) {
         if (p.out) p.out[(size_t(g) * p.B + s) * O + o] = double(val[k]);
         if (p.fit_kind != FNB_FIT_NONE) {
           const double d = double(__ldg(p.Y + size_t(s) * O + o)) - double(val[k]);
-          err += d * d;
+          e[k] += d * d;
         }
       }
     }
-  }
-  if (p.fit_kind == FNB_FIT_NONE) return;
-  // deterministic group reduction: shuffle tree within warps, then ordered
-  // sum of warp partials.
-  const int width = T < 32 ? T : 32;
-  for (int d = width >> 1; d > 0; d >>= 1) err += __shfl_down_sync(0xffffffffu, err, d, width);
-  if (T > 32) {  // every thread of the CTA (dead groups included) reaches here
-    if ((j & 31) == 0) s_red[j >> 5] = err;
-    __syncthreads();
-    if (j == 0) {
-      err = 0.0;
-      for (int w = 0; w < T / 32; ++w) err += s_red[w];
-    }
-  }
-  if (j == 0 && live) {
-    if (gridDim.y > 1) {
-      p.partial[size_t(g) * gridDim.y + blockIdx.y] = err;
-    } else {
-      p.fitness[g] = p.fit_kind == FNB_FIT_NEG_MSE ? -(err / (double(p.B) * double(O))) : p.fit_offset - err;
+    if (p.fit_kind != FNB_FIT_NONE) {
+      double u;
+      if constexpr (SPT == 1) u = e[0];
+      else if constexpr (SPT == 2) u = e[0] + e[1];
+      else u = (e[0] + e[1]) + (e[2] + e[3]);
+      for (int m = 1; m < ulanes; m <<= 1) u += __shfl_xor_sync(gmask, u, m);
+      if ((j & (ulanes - 1)) == 0 && s0 < p.B) p.partial[size_t(g) * p.units + (s0 >> 5)] = u;
     }
   }
 }
 
-__global__ void k_fitness_finalize(const double* __restrict__ partial, int chunks, int P, int B, int O,
-                                   int fit_kind, double offset, double* __restrict__ fitness,
-                                   const uint8_t* __restrict__ nets, size_t stride, int rows_hi) {
+// fitness = ordered sum of the 32-sample units (network.hpp's evaluate loop
+// order is restated in tests/ with a tolerance; the device order is fixed)
+__global__ void k_fitness_finalize(const double* __restrict__ partial, int units, int P, int B, int O,
+                                   int fit_kind, double offset, double* __restrict__ fitness) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P) return;
-  if (reinterpret_cast<const NetHeader*>(nets + size_t(g) * stride)->n_slots + 1 > rows_hi) return;  // overflow pass
   double sse = 0.0;
-  for (int c = 0; c < chunks; ++c) sse += partial[size_t(g) * chunks + c];
+  for (int c = 0; c < units; ++c) sse += partial[size_t(g) * units + c];
   fitness[g] = fit_kind == FNB_FIT_NEG_MSE ? -(sse / (double(B) * double(O))) : offset - sse;
 }
 
@@ -390,9 +385,10 @@ static int main_rows(const NetLayout& L) {
 void set_forward_spt(int spt) { g_force_spt = (spt == 1 || spt == 2 || spt == 4) ? spt : 0; }
 void set_forward_rows_pct(int pct) { g_rows_pct = (pct >= 10 && pct <= 100) ? pct : 62; }
 
-size_t forward_partial_needed(NetLayout L, int P, int B) {
-  const FwdConfig c = fwd_config(L, P, B, main_rows(L), false);
-  return sizeof(double) * size_t(P) * size_t(c.chunks) + 16;
+static int fitness_units(int B) { return (B + 31) / 32; }
+
+size_t forward_partial_needed(NetLayout, int P, int B) {
+  return sizeof(double) * size_t(P) * size_t(fitness_units(B)) + 16;
 }
 
 cudaError_t launch_to_float(const double* src, float* dst, size_t n, int* bad, cudaStream_t st) {
@@ -463,18 +459,19 @@ int launch_forward(const void* nets, NetLayout L, int P, const float* X, const f
   p.fitness = fitness;
   p.out = out;
   p.partial = partial_buf;
-  if (c.chunks > 1 && fit_kind != FNB_FIT_NONE && sizeof(double) * size_t(P) * c.chunks > partial_cap) return 1;
+  p.units = fitness_units(B);
+  const bool fit = fit_kind != FNB_FIT_NONE;
+  if (fit && sizeof(double) * size_t(P) * p.units > partial_cap) return 1;
   if (launch_pass(c, p, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
   ++*launches;
-  if (c.chunks > 1 && fit_kind != FNB_FIT_NONE) {
-    k_fitness_finalize<<<(P + 255) / 256, 256, 0, st>>>(partial_buf, c.chunks, P, B, L.O, fit_kind, offset,
-                                                         fitness, p.nets, L.bytes, rows_main);
-    if (cudaGetLastError() != cudaSuccess) return 1;
-    ++*launches;
-  }
   if (rows_main < L.N + 1) {
     const FwdConfig co = fwd_config(L, P, B, L.N + 1, true);
     if (launch_pass(co, p, rows_main, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
+    ++*launches;
+  }
+  if (fit) {
+    k_fitness_finalize<<<(P + 255) / 256, 256, 0, st>>>(partial_buf, p.units, P, B, L.O, fit_kind, offset, fitness);
+    if (cudaGetLastError() != cudaSuccess) return 1;
     ++*launches;
   }
   return 0;

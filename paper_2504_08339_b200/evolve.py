@@ -114,6 +114,31 @@ class Evolver:
     def evaluate_d(self, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0):
         self._raise(self._lib.fnb_evolver_evaluate_d(self._h, X.data_ptr(), Y.data_ptr(), X.shape[0], kind, offset))
 
+    def evaluate_range_d(self, lo: int, hi: int, X, Y, out, kind: int = FIT_NEG_MSE, offset: float = 0.0):
+        """Fitness of genomes [lo, hi) into the device FP64 tensor `out` (hi-lo),
+        on the evolver stream -- one rank's shard in the multi-GPU loop."""
+        if out.numel() < hi - lo or out.dtype != torch_float64():
+            raise ValueError("out must be a float64 device tensor of at least hi-lo elements")
+        self._raise(self._lib.fnb_evolver_evaluate_range_d(self._h, lo, hi, X.data_ptr(), Y.data_ptr(), X.shape[0],
+                                                           kind, offset, out.data_ptr()))
+
+    def set_fitness_d(self, fitness):
+        """Device-to-device copy of a full FP64 fitness vector (pop_size)."""
+        if fitness.numel() < self.cfg.pop_size or fitness.dtype != torch_float64():
+            raise ValueError("fitness must be a float64 device tensor of pop_size elements")
+        self._raise(self._lib.fnb_evolver_set_fitness_d(self._h, fitness.data_ptr()))
+
+    def checksum(self) -> int:
+        """Population checksum (include/flatneat_b200.h fnb_evolver_checksum)."""
+        h = C.c_uint64(0)
+        self._raise(self._lib.fnb_evolver_checksum(self._h, C.byref(h)))
+        return h.value
+
+    def stream_handle(self) -> int:
+        """The evolver's CUDA stream (cudaStream_t as int) -- every evolver
+        kernel runs on it; wrap with torch.cuda.ExternalStream to order torch work."""
+        return self.device_state()[3]
+
     def fitness(self) -> np.ndarray:
         f = np.empty(self.cfg.pop_size)
         self._raise(self._lib.fnb_evolver_get_fitness(self._h, _dp(f)))
@@ -151,6 +176,11 @@ class Evolver:
         n, c, f, s = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         self._raise(self._lib.fnb_evolver_device_state(self._h, C.byref(n), C.byref(c), C.byref(f), C.byref(s)))
         return n.value, c.value, f.value, s.value
+
+
+def torch_float64():
+    import torch
+    return torch.float64
 
 
 def evolve(engine: Engine, cfg: NeatConfig, seed: int, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0,
