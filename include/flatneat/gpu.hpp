@@ -97,6 +97,19 @@ class Context {
     return r;
   }
 
+  // transform + forward + fused fitness: fitness_kind is
+  // FNB_FIT_NEG_MSE (func-fit) or FNB_FIT_OFFSET_SSE (xor, `offset` - SSE)
+  std::vector<double> evaluate(const PopulationTensors& pop, std::span<const double> inputs,
+                               std::span<const double> targets, int batch, int fitness_kind = FNB_FIT_NEG_MSE,
+                               double offset = 0.0) {
+    if (int(inputs.size()) != batch * int(in_.size()) || int(targets.size()) != batch * int(out_.size()))
+      raise(Errc::shape_mismatch, "input / target matrix is not batch x num_inputs / num_outputs");
+    std::vector<double> fit(std::size_t(pop.pop_size));
+    check(fnb_evaluate(ctx_, pop.pop_nodes.data(), pop.pop_conns.data(), pop.pop_size, inputs.data(),
+                       targets.data(), batch, fitness_kind, offset, fit.data()));
+    return fit;
+  }
+
   // distance(genome_p, rep_s) (ops.hpp:415) for a population x representatives
   std::vector<double> distance(const PopulationTensors& pop, const PopulationTensors& reps,
                                const DistanceConfig& cfg = {}) {
