@@ -8,9 +8,9 @@
 // species bookkeeping (<= 32 species) runs in single-thread kernels so it
 // never leaves the device:
 //   speciate   K3 distances to the old representatives -> first match;
-//              founding rounds (min unassigned index via atomicMin, founder
-//              copied to a representative slot, K3 of the still-unassigned
-//              genomes against it); nearest-representative overflow;
+//              founding rounds in one cooperative kernel (founder = lowest
+//              unassigned index, K3 of the still-unassigned genomes against
+//              it, one grid barrier per round); nearest-representative overflow;
 //              new representative = member closest to the old one (two-pass
 //              atomicMin on (distance bits, index)); empty species dropped.
 //   stagnate   per-species max fitness (atomicMax on order-preserving bits),
@@ -18,30 +18,32 @@
 //   spawn      fitness ranks by a stable radix sort (CUB), exact integer
 //              rank sums per species, then the clamp / rescale / largest-
 //              remainder / elitism arithmetic on one thread.
-//   reproduce  members ordered (fitness desc, index asc) by two stable radix
-//              sorts, per-slot parent selection from the split(0) stream,
+//   reproduce  members ordered (fitness desc, index asc) from the ranking
+//              sort (equal-key groups reversed) and a 6-bit species sort, per-slot parent selection from the split(0) stream,
 //              K5 crossover (elites are self-crossovers = exact copies), K6/K7
 //              mutation with one slot-ordered innovation table.
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 
+#include "distance_warp.cuh"
 #include "fnb_common.cuh"
 #include "glibc_math.cuh"
 #include "philox.cuh"
 
 namespace fnb {
 
+namespace cg = cooperative_groups;
 constexpr int kMaxSpecies = 32;
 
 struct SpeciesDev {
   int count, next_id, old_count;
-  int founder;       // current founding round: founder index or -1
-  int round_j;       // species index created by the current round
-  int cand;          // min unassigned index candidate
+  int rcand[kMaxSpecies + 1];  // fused founding rounds: founder of round r (INT_MAX = none)
   int id[kMaxSpecies];
   double best[kMaxSpecies];
   int stag[kMaxSpecies];
@@ -131,6 +133,7 @@ __global__ void k_copy_genome(const double* sn, const double* sc, const int* src
 // ---- speciate (oracle E2) -------------------------------------------------------
 __global__ void k_spec_begin(SpeciesDev* sd) {
   sd->old_count = sd->count;
+  for (int j = 0; j <= kMaxSpecies; ++j) sd->rcand[j] = INT_MAX;
   for (int j = 0; j < kMaxSpecies; ++j) {
     sd->dmin[j] = ~0ull;
     sd->argmin[j] = INT_MAX;
@@ -147,51 +150,93 @@ __global__ void k_assign_first(const double* __restrict__ d, int P, int S_old, d
   species_of[i] = a;
 }
 
-__global__ void k_round_reset(SpeciesDev* sd) { sd->cand = INT_MAX; }
+// All founding rounds in one cooperative launch (oracle E2, the rounds of
+// founder search, founder commit, K3 against the founder and the join fused):
+// round r's founder f is the lowest unassigned genome; it founds species
+// j = S_old + r, and every unassigned genome after it whose distance to it is
+// below the threshold joins.  Genomes that stay unassigned atomicMin the
+// next round's founder, so no separate minimum pass is needed; each CTA
+// builds the founder's marker tables in its own shared memory, so the only
+// grid-wide barrier is one per round.  Rounds end, grid-uniformly, when no
+// genome is left or max_species is reached.  Distances are distance_warp's
+// (bit-identical to k_distance).
+__global__ void __launch_bounds__(128) k_found_rounds(SpeciesDev* sd, int S_old, int max_species, int* species_of,
+                                                      const double* __restrict__ pn, const double* __restrict__ pc,
+                                                      double* rep_n, double* rep_c, int P, int N, int C, double th,
+                                                      double cd, double ch, int Hn, int Hc) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  unsigned long long* nk = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned long long* ck = nk + Hn;
+  int* nr = reinterpret_cast<int*>(ck + Hc);
+  int* cr = nr + Hn;
+  int* counts = cr + Hc;                                          // 2 ints (+2 pad)
+  double* dist_w = reinterpret_cast<double*>(counts + 4);         // one per warp
+  const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int16_t* match = reinterpret_cast<int16_t*>(dist_w + warps) + size_t(warp) * (N + C);
+  const int gw = blockIdx.x * warps + warp, nw = gridDim.x * warps;
+  const size_t gn = size_t(N) * kNodeCols, gc = size_t(C) * kConnCols;
 
-__global__ void k_min_unassigned(const int* species_of, int P, SpeciesDev* sd) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P && species_of[i] < 0) atomicMin(&sd->cand, i);
-}
-
-// founder commit + copies of the founder into its representative slot and
-// the round buffer (one block)
-__global__ void k_found(SpeciesDev* sd, int max_species, int* species_of, const double* pn, const double* pc,
-                        double* rep_n, double* rep_c, double* round_n, double* round_c, int N, int C) {
-  __shared__ int f, j;
-  if (threadIdx.x == 0) {
-    f = -1;
-    j = -1;
-    if (sd->cand != INT_MAX && sd->count < max_species) {
-      f = sd->cand;
-      j = sd->count++;
-      sd->id[j] = sd->next_id++;
-      sd->best[j] = -INFINITY;
-      sd->stag[j] = 0;
-      species_of[f] = j;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x)
+    if (__ldcg(species_of + i) < 0) atomicMin(&sd->rcand[0], i);
+  grid.sync();
+  for (int r = 0; S_old + r < max_species; ++r) {
+    const int f = __ldcg(&sd->rcand[r]);
+    if (f == INT_MAX) break;
+    const int j = S_old + r;
+    const double* fn = pn + size_t(f) * gn;
+    const double* fc = pc + size_t(f) * gc;
+    if (blockIdx.x == 0) {  // commit the species and its representative
+      if (threadIdx.x == 0) {
+        sd->count = j + 1;
+        sd->id[j] = sd->next_id++;
+        sd->best[j] = -INFINITY;
+        sd->stag[j] = 0;
+        species_of[f] = j;
+      }
+      for (size_t i = threadIdx.x; i < gn; i += blockDim.x) rep_n[size_t(j) * gn + i] = fn[i];
+      for (size_t i = threadIdx.x; i < gc; i += blockDim.x) rep_c[size_t(j) * gc + i] = fc[i];
     }
-    sd->founder = f;
-    sd->round_j = j;
-  }
-  __syncthreads();
-  if (f < 0) return;
-  const double* a = pn + size_t(f) * N * kNodeCols;
-  const double* b = pc + size_t(f) * C * kConnCols;
-  for (int i = threadIdx.x; i < N * kNodeCols; i += blockDim.x) {
-    rep_n[size_t(j) * N * kNodeCols + i] = a[i];
-    round_n[i] = a[i];
-  }
-  for (int i = threadIdx.x; i < C * kConnCols; i += blockDim.x) {
-    rep_c[size_t(j) * C * kConnCols + i] = b[i];
-    round_c[i] = b[i];
+    rep_table_build(fn, fc, N, C, nk, nr, Hn, ck, cr, Hc, counts);
+    const RepTables t{nk, nr, ck, cr, counts, Hn, Hc};
+    for (int g = gw; g < P; g += nw) {
+      if (g <= f || __ldcg(species_of + g) >= 0) continue;  // warp-uniform
+      distance_warp(pn + size_t(g) * gn, pc + size_t(g) * gc, fn, fc, 1, t, N, C, cd, ch, match, dist_w + warp);
+      __syncwarp();
+      if (lane == 0) {
+        if (dist_w[warp] < th) species_of[g] = j;
+        else atomicMin(&sd->rcand[r + 1], g);
+      }
+      __syncwarp();
+    }
+    grid.sync();
   }
 }
 
-__global__ void k_join_round(const double* __restrict__ d, int P, double th, const SpeciesDev* sd, int* species_of) {
+// Members by (fitness descending, index ascending) from the ascending stable
+// sort (keys desc = ~asc): the equal-key group [lo, hi) of position i moves
+// to [P - hi, P - lo), keeping its (index-ascending) order -- replaces a
+// second 64-bit radix sort with two binary searches per element.
+__global__ void k_desc_from_asc(const unsigned long long* __restrict__ keys, const int* __restrict__ idx, int P,
+                                int* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int f = sd->founder;
-  if (i >= P || f < 0 || i <= f || species_of[i] >= 0) return;
-  if (d[i] < th) species_of[i] = sd->round_j;
+  if (i >= P) return;
+  const unsigned long long k = keys[i];
+  int a = 0, b = i;  // lo = first position with key >= k
+  while (a < b) {
+    const int m = (a + b) >> 1;
+    if (keys[m] < k) a = m + 1;
+    else b = m;
+  }
+  const int lo = a;
+  a = i + 1;
+  b = P;  // hi = first position with key > k
+  while (a < b) {
+    const int m = (a + b) >> 1;
+    if (keys[m] <= k) a = m + 1;
+    else b = m;
+  }
+  out[(P - a) + (i - lo)] = idx[i];
 }
 
 __global__ void k_nearest(const double* __restrict__ d, int P, int stride, const SpeciesDev* sd, int* species_of) {
@@ -477,8 +522,8 @@ struct Evolver {
   double *pn[2] = {nullptr, nullptr}, *pc[2] = {nullptr, nullptr};
   int cur = 0;
   double* fitness = nullptr;
-  double *rep_n = nullptr, *rep_c = nullptr, *round_n = nullptr, *round_c = nullptr;
-  double *dmat = nullptr, *dround = nullptr;
+  double *rep_n = nullptr, *rep_c = nullptr;
+  double* dmat = nullptr;
   int* species_of = nullptr;
   SpeciesDev* sd = nullptr;
   unsigned long long *kasc = nullptr, *kdesc = nullptr, *ktmp = nullptr;
@@ -506,10 +551,7 @@ struct Evolver {
     A(&fitness, sizeof(double) * P);
     A(&rep_n, sizeof(double) * gn() * kMaxSpecies);
     A(&rep_c, sizeof(double) * gc() * kMaxSpecies);
-    A(&round_n, sizeof(double) * gn());
-    A(&round_c, sizeof(double) * gc());
     A(&dmat, sizeof(double) * size_t(P) * 2 * kMaxSpecies);  // [old reps | overflow vs all reps]
-    A(&dround, sizeof(double) * size_t(P));
     A(&species_of, sizeof(int) * P);
     A(&sd, sizeof(SpeciesDev));
     A(&kasc, 8 * size_t(P));
@@ -547,7 +589,7 @@ struct Evolver {
   }
 
   void release() {
-    void* ps[] = {pn[0], pn[1], pc[0], pc[1], fitness, rep_n, rep_c, round_n, round_c, dmat, dround, species_of, sd,
+    void* ps[] = {pn[0], pn[1], pc[0], pc[1], fitness, rep_n, rep_c, dmat, species_of, sd,
                   kasc, kdesc, ktmp, idx, idx_sorted, idx_tmp, skey, skey_tmp, fit_idx, oth_idx, status, next_key,
                   xkeys, mkeys, active, cub_tmp, scratch};
     for (void* p : ps)
@@ -562,6 +604,32 @@ struct Evolver {
                                                    sh.default_agg, sh.default_act, cfg.output_activation);
     ++*launches;
     return cudaGetLastError();
+  }
+
+  int coop_blocks = 0;  // co-resident CTAs of k_found_rounds (cooperative launch bound)
+
+  cudaError_t launch_found_rounds(int S_old, const double* n, const double* c) {
+    int Hn = table_capacity(N), Hc = table_capacity(C);
+    const int block = 128;
+    const size_t smem = size_t(Hn + Hc) * 12 + 16 + (block / 32) * 8 + (block / 32) * size_t(N + C) * 2;
+    cudaError_t e = cudaFuncSetAttribute(k_found_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    if (coop_blocks == 0) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_found_rounds, block, smem);
+      if (e != cudaSuccess) return e;
+      coop_blocks = std::max(1, per_sm * sms);
+    }
+    int grid = std::max(1, std::min(coop_blocks, (P + block / 32 - 1) / (block / 32)));
+    int ms = cfg.max_species;
+    double th = cfg.threshold, cd = dist.compatibility_disjoint, ch = dist.compatibility_homologous;
+    int p = P, nn = N, cc = C;
+    void* args[] = {&sd, &S_old, &ms, &species_of, &n, &c, &rep_n, &rep_c, &p, &nn, &cc, &th, &cd, &ch, &Hn, &Hc};
+    ++*launches;
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_found_rounds), dim3(grid), dim3(block), args, smem,
+                                       st);
   }
 
   // speciate -> update_stagnation -> compute_spawn_counts -> reproduce
@@ -580,16 +648,10 @@ struct Evolver {
       if (e != cudaSuccess) return e;
     }
     k_assign_first<<<B, T, 0, st>>>(dmat, P, S_old, th, species_of);
-    for (int r = S_old; r < cfg.max_species; ++r) {
-      k_round_reset<<<1, 1, 0, st>>>(sd);
-      k_min_unassigned<<<B, T, 0, st>>>(species_of, P, sd);
-      k_found<<<1, 256, 0, st>>>(sd, cfg.max_species, species_of, n, c, rep_n, rep_c, round_n, round_c, N, C);
-      e = launch_distance_masked(n, c, P, round_n, round_c, 1, N, C, dist.compatibility_disjoint,
-                                 dist.compatibility_homologous, dround, scratch, scratch_bytes, species_of,
-                                 &sd->founder, st);
+    *launches += 2;
+    if (S_old < cfg.max_species) {
+      e = launch_found_rounds(S_old, n, c);
       if (e != cudaSuccess) return e;
-      k_join_round<<<B, T, 0, st>>>(dround, P, th, sd, species_of);
-      *launches += 6;
     }
     e = launch_distance_masked(n, c, P, rep_n, rep_c, cfg.max_species, N, C, dist.compatibility_disjoint,
                                dist.compatibility_homologous, dmat + size_t(P) * S_old, scratch, scratch_bytes,
@@ -619,8 +681,7 @@ struct Evolver {
     k_rank_sums<<<B, T, 0, st>>>(idx_sorted, P, species_of, sd);
     k_spawn<<<1, 1, 0, st>>>(sd, P, cfg.spawn_rate, cfg.genome_elitism);
     // ---- reproduce: members by (fitness desc, index asc), then by species
-    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kdesc, ktmp, idx, idx_tmp, P, 0, 64, st);
-    if (e != cudaSuccess) return e;
+    k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp);
     k_species_keys<<<B, T, 0, st>>>(idx_tmp, P, species_of, skey);
     e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, skey, skey_tmp, idx_tmp, idx_sorted, P, 0, 6, st);
     if (e != cudaSuccess) return e;

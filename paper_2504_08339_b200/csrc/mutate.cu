@@ -181,8 +181,9 @@ __global__ void k7_advance(int* next_key) { next_key[0] += next_key[1]; }
 // The child's keys and flags are staged in shared memory (and kept in step
 // with every structural edit lane 0 makes to the HBM rows), so each scan
 // and each lane-0 stream step is a shared-memory access, not an L2 trip.
-// The long attribute stream split(5) is produced 64 draws at a time by the
-// whole warp (one Philox block per lane) and walked warp-uniformly.
+// The long attribute stream split(5) is evaluated by the whole warp (one
+// Philox block per lane) into per-position decision words; lane 0 chases the
+// positions the walk actually visits (AttrDecider).
 // ---------------------------------------------------------------------------
 struct MutSmem {
   unsigned long long* nkeys;  // marker table: node key -> first row
@@ -197,7 +198,7 @@ struct MutSmem {
   int* cout;                  // [C]
   int* list_a;                // [N] scratch lists (keys / targets / sorted)
   int* list_b;                // [N]
-  unsigned long long* dbuf;   // [64] stream draws
+  unsigned long long* dbuf;   // [64] scratch (with the tables: the S5 decision window)
   uint8_t* nflag;             // [N] bit0 non-empty, bit1 input, bit2 output
   uint8_t* cflag;             // [C] bit0 non-empty, bit1 enabled
   int8_t* new_agg;            // [N] -1 or replacement id
@@ -268,41 +269,42 @@ __device__ __forceinline__ double apply_scalar(double v, uint32_t a, const Key4&
   return glibc::normal_from_uniforms(u0, u1, mean, sd);
 }
 
-// split(5) stream, 64 draws per refill, walked identically by every lane
-struct ChunkStream {
-  Key4 key;
-  uint64_t pos = 0, base = ~0ull;
-  unsigned long long* buf;
-  __device__ __forceinline__ uint64_t at(uint64_t q) {
-    if (base == ~0ull || q < base || q >= base + 64) {
-      base = q & ~63ull;
-      __syncwarp();
-      const int lane = threadIdx.x & 31;
-      uint32_t b[4];
-      stream_block(key, (base >> 1) + uint64_t(lane), b);
-      buf[2 * lane] = (uint64_t(b[3]) << 32) | b[2];
-      buf[2 * lane + 1] = (uint64_t(b[1]) << 32) | b[0];
-      __syncwarp();
-    }
-    return buf[q - base];
+// Every decision the split(5) attribute walk can take at one stream position,
+// from that position's draw x (u = uniform(x)):
+//   bits 0-1  bias:   u < rate, u < rate + replace   (mutate_scalar, ops.hpp:281-289)
+//   bits 2-3  resp:   same
+//   bits 4-5  weight: same
+//   bit 6/7   u < aggregation / activation replace rate (the coins)
+//   bit 8/9   x accepted by below(n_agg) / below(n_act) (rng.hpp:99-106)
+//   bits 10-12 / 13-15  x % n_agg / x % n_act (registries hold <= 8)
+struct AttrDecider {
+  static constexpr int kBias = 0, kResp = 2, kWeight = 4, kAggCoin = 6, kActCoin = 7, kAggAcc = 8, kActAcc = 9,
+                       kAggVal = 10, kActVal = 13;
+  double b_rate, b_sum, r_rate, r_sum, w_rate, w_sum, agg_rate, act_rate;
+  uint64_t lim_agg, lim_act, n_agg, n_act;
+  __device__ explicit AttrDecider(const MutCfgDev& c)
+      : b_rate(c.b_rate), b_sum(c.b_rate + c.b_replace), r_rate(c.r_rate), r_sum(c.r_rate + c.r_replace),
+        w_rate(c.w_rate), w_sum(c.w_rate + c.w_replace), agg_rate(c.agg_rate), act_rate(c.act_rate),
+        n_agg(uint64_t(max(1, c.n_agg))), n_act(uint64_t(max(1, c.n_act))) {
+    const uint64_t mx = ~0ull;
+    lim_agg = mx - ((mx % n_agg) + 1) % n_agg;
+    lim_act = mx - ((mx % n_act) + 1) % n_act;
   }
-  __device__ __forceinline__ uint64_t next() { return at(pos++); }
-  __device__ __forceinline__ double uniform() { return u64_to_uniform(next()); }
-  __device__ __forceinline__ int index(int n) {  // below(n), rng.hpp:99-106
-    const uint64_t mx = ~0ull, limit = mx - ((mx % uint64_t(n)) + 1) % uint64_t(n);
-    uint64_t x = next();
-    while (x > limit) x = next();
-    return int(x % uint64_t(n));
+  __device__ __forceinline__ uint16_t operator()(uint64_t x) const {
+    const double u = u64_to_uniform(x);
+    uint32_t f = uint32_t(u < b_rate) | uint32_t(u < b_sum) << 1 | uint32_t(u < r_rate) << 2 |
+                 uint32_t(u < r_sum) << 3 | uint32_t(u < w_rate) << 4 | uint32_t(u < w_sum) << 5 |
+                 uint32_t(u < agg_rate) << 6 | uint32_t(u < act_rate) << 7 | uint32_t(x <= lim_agg) << 8 |
+                 uint32_t(x <= lim_act) << 9;
+    if (agg_rate > 0.0) f |= mod_small(x, uint32_t(n_agg)) << 10;
+    if (act_rate > 0.0) f |= mod_small(x, uint32_t(n_act)) << 13;
+    return uint16_t(f);
   }
-  // mutate_scalar (ops.hpp:281-289): record the action, consume its draws
-  __device__ __forceinline__ uint32_t scalar(double rate, double replace) {
-    const double u = uniform();
-    if (u < rate || u < rate + replace) {
-      const uint32_t a = (uint32_t(pos) << 2) | (u < rate ? 1u : 2u);
-      pos += 2;
-      return a;
-    }
-    return 0u;
+  // x % n for n <= 8 with 32-bit remainders: x = hi * 2^32 + lo
+  __device__ __forceinline__ static uint32_t mod_small(uint64_t x, uint32_t n) {
+    const uint32_t hi = uint32_t(x >> 32), lo = uint32_t(x);
+    const uint32_t r32 = (0u - n) % n;  // 2^32 mod n
+    return ((hi % n) * r32 + lo % n) % n;
   }
 };
 
@@ -551,32 +553,67 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
     }
   }
 
-  // ---- attributes (ops.hpp:338-359): every lane walks split(5) identically
-  //      over shared-memory draws; then all lanes apply the normals
+  // ---- attributes (ops.hpp:338-359).  The split(5) walk is sequential (a
+  //      scalar consumes 1 or 3 draws depending on its own draw), so: all
+  //      lanes first evaluate every decision the walk could take at every
+  //      stream position of a window that covers the worst case (one 16-bit
+  //      word per position, in the marker tables' dead shared memory); lane 0
+  //      then chases the positions, a few instructions per decision; all
+  //      lanes finally apply the normals.  Positions past the window (only
+  //      reachable through below() rejections) are evaluated directly.
   if (!st) {
     const Key4 k5 = key_split(key, 5);
-    ChunkStream cs;
-    cs.key = k5;
-    cs.buf = sm.dbuf;
-    for (int q = 0; q < N; ++q) {
-      uint32_t ab = 0u, ar = 0u;
-      int ag = -1, ac = -1;
-      if (sm.nflag[q] & 1 && !(sm.nflag[q] & 2)) {
-        ab = cs.scalar(cfg.b_rate, cfg.b_replace);
-        ar = cs.scalar(cfg.r_rate, cfg.r_replace);
-        if (cfg.agg_rate > 0.0 && cs.uniform() < cfg.agg_rate) ag = cs.index(cfg.n_agg);
-        if (cfg.act_rate > 0.0 && cs.uniform() < cfg.act_rate) ac = cs.index(cfg.n_act);
-      }
-      if (lane == 0) {
+    uint16_t* dw = reinterpret_cast<uint16_t*>(sm.nkeys);  // nkeys..crows are contiguous and free here
+    const int cap = int((size_t(Hn) * 12 + size_t(Hc) * 12 + 64 * 8) / 2) & ~1;
+    int nn = 0, nc = 0;
+    for (int q = lane; q < N; q += 32) nn += (sm.nflag[q] & 3) == 1;
+    for (int q = lane; q < C; q += 32) nc += sm.cflag[q] & 1;
+    nn = __reduce_add_sync(kFullMask, nn);
+    nc = __reduce_add_sync(kFullMask, nc);
+    const int per_node = 6 + (cfg.agg_rate > 0.0 ? 2 : 0) + (cfg.act_rate > 0.0 ? 2 : 0);
+    const int need = min(cap, (nn * per_node + nc * 3 + 1) & ~1);
+    const AttrDecider dec(cfg);
+    for (int b = lane; 2 * b < need; b += 32) {
+      uint32_t w[4];
+      stream_block(k5, uint64_t(b), w);
+      dw[2 * b] = dec((uint64_t(w[3]) << 32) | w[2]);
+      dw[2 * b + 1] = dec((uint64_t(w[1]) << 32) | w[0]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      uint32_t p = 0;
+      auto word = [&](uint32_t q) -> uint32_t { return q < uint32_t(need) ? dw[q] : dec(stream_u64_at(k5, q)); };
+      // mutate_scalar (ops.hpp:281-289): action code, the normal's draws skipped
+      auto scalar = [&](int sh) -> uint32_t {
+        const uint32_t f = (word(p++) >> sh) & 3u;
+        if (!f) return 0u;
+        const uint32_t a = (p << 2) | ((f & 1u) ? 1u : 2u);
+        p += 2;
+        return a;
+      };
+      auto index = [&](int acc_bit, int val_shift) -> int {  // below(n), rng.hpp:99-106
+        for (;;) {
+          const uint32_t f = word(p++);
+          if ((f >> acc_bit) & 1u) return int((f >> val_shift) & 7u);
+        }
+      };
+      for (int q = 0; q < N; ++q) {
+        uint32_t ab = 0u, ar = 0u;
+        int ag = -1, ac = -1;
+        if ((sm.nflag[q] & 3) == 1) {
+          ab = scalar(AttrDecider::kBias);
+          ar = scalar(AttrDecider::kResp);
+          if (cfg.agg_rate > 0.0 && ((word(p++) >> AttrDecider::kAggCoin) & 1u))
+            ag = index(AttrDecider::kAggAcc, AttrDecider::kAggVal);
+          if (cfg.act_rate > 0.0 && ((word(p++) >> AttrDecider::kActCoin) & 1u))
+            ac = index(AttrDecider::kActAcc, AttrDecider::kActVal);
+        }
         sm.act_n[2 * q] = ab;
         sm.act_n[2 * q + 1] = ar;
         sm.new_agg[q] = int8_t(ag);
         sm.new_act[q] = int8_t(ac);
       }
-    }
-    for (int q = 0; q < C; ++q) {
-      const uint32_t aw = (sm.cflag[q] & 1) ? cs.scalar(cfg.w_rate, cfg.w_replace) : 0u;
-      if (lane == 0) sm.act_c[q] = aw;
+      for (int q = 0; q < C; ++q) sm.act_c[q] = (sm.cflag[q] & 1) ? scalar(AttrDecider::kWeight) : 0u;
     }
     __syncwarp();
     for (int q = lane; q < N; q += 32) {
