@@ -24,6 +24,7 @@ struct TfSmem {
   int* sorted_key;      // [N]
   int* R;               // [N] enabled rows per destination
   uint32_t* pred;       // [N * W]
+  uint32_t* die;        // [N * W] rows whose last consumer is op k (by op index)
   uint16_t* row_of_rank;// [N]
   uint16_t* rank;       // [N]
   uint16_t* order;      // [N]
@@ -38,7 +39,7 @@ __host__ __device__ inline size_t tf_smem_bytes(int N, int C, int W) {
   b += align16(size_t(N) * 8);           // kr
   b += align16(size_t(N) * 4);           // sorted_key
   b += align16(size_t(N) * 4);           // R
-  b += align16(size_t(N) * W * 4);       // pred
+  b += align16(size_t(N) * W * 4) * 2;   // pred, die
   b += align16(size_t(N) * 2) * 4;       // row_of_rank, rank, order, ebeg
   b += align16(size_t(N));               // flags
   b += align16(size_t(C) * 2) * 2;       // csrc, cdst
@@ -51,6 +52,7 @@ __device__ inline TfSmem tf_carve(uint8_t* p, int N, int C, int W) {
   s.sorted_key = reinterpret_cast<int*>(p); p += align16(size_t(N) * 4);
   s.R = reinterpret_cast<int*>(p); p += align16(size_t(N) * 4);
   s.pred = reinterpret_cast<uint32_t*>(p); p += align16(size_t(N) * W * 4);
+  s.die = reinterpret_cast<uint32_t*>(p); p += align16(size_t(N) * W * 4);
   s.row_of_rank = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
   s.rank = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
   s.order = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
@@ -306,7 +308,12 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     edge_total += __shfl_sync(kFull, incl_e, 31);
   }
   // ---- 6b. last consumer (op index) of every value; outputs live to the end
-  for (int r = lane; r < N; r += 32) last_use[r] = -1;
+  for (int r = lane; r < N; r += 32) {
+    last_use[r] = -1;
+    slot_of[r] = 0xffff;
+#pragma unroll
+    for (int w = 0; w < W; ++w) s.die[r * W + w] = 0u;
+  }
   __syncwarp();
   for (int i = lane; i < sh.O; i += 32) last_use[out_rows[i]] = 0x7fffffff;
   __syncwarp();
@@ -316,22 +323,39 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     atomicMax(&last_use[s.csrc[r]], int(opos[dst]));
   }
   __syncwarp();
-  // ---- 6c. value slots: linear-scan allocation over the op order, a slot is
-  //          released after its value's last consumer (lane 0, <= 255 values)
+  // values dying at each op, as row bitmasks indexed by op
+  for (int r = lane; r < N; r += 32) {
+    const int k = last_use[r];
+    if (k >= 0 && k < 0x7fffffff) atomicOr(&s.die[k * W + (r >> 5)], 1u << (r & 31));
+  }
+  __syncwarp();
+  // ---- 6c. value slots: linear scan over the op order, lowest free slot
+  //          (slots = max live values); lane 0 touches each value once.  The
+  //          free mask is a W-word register array indexed only by unrolled
+  //          compile-time loops (no local memory).
   int n_slots = 0;
   if (lane == 0) {
-    uint32_t used[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t used[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) used[w] = 0u;
     auto alloc = [&]() {
-      int w = 0;
-      while (used[w] == 0xffffffffu) ++w;
-      const int b = __ffs(~used[w]) - 1;
-      used[w] |= 1u << b;
-      const int sl = w * 32 + b;
+      int sl = -1;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (sl < 0 && used[w] != 0xffffffffu) {
+          const int b = __ffs(~used[w]) - 1;
+          used[w] |= 1u << b;
+          sl = w * 32 + b;
+        }
+      }
       n_slots = max(n_slots, sl + 1);
       return sl;
     };
-    auto release = [&](int sl) { used[sl >> 5] &= ~(1u << (sl & 31)); };
-    for (int r = 0; r < N; ++r) slot_of[r] = 0xffff;
+    auto release = [&](int sl) {
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        if (w == (sl >> 5)) used[w] &= ~(1u << (sl & 31));
+    };
     for (int i = 0; i < sh.I; ++i) {
       const int r = in_rows[i];
       if (slot_of[r] == 0xffff) slot_of[r] = uint16_t(alloc());
@@ -340,12 +364,12 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     for (int p = 0; p < count; ++p) {
       const int row = s.order[p];
       if (s.flags[row] & 2) continue;
-      for (int w = 0; w < W; ++w) {  // sources whose last consumer is this op
-        uint32_t bits = s.pred[row * W + w];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint32_t bits = s.die[k * W + w];
         while (bits) {
-          const int src = w * 32 + __ffs(bits) - 1;
+          release(slot_of[w * 32 + __ffs(bits) - 1]);
           bits &= bits - 1;
-          if (last_use[src] == k) release(slot_of[src]);
         }
       }
       const int sl = alloc();
