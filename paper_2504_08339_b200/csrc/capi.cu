@@ -23,6 +23,7 @@ int launch_forward(const void* nets, NetLayout L, int P, const float* X, const f
                    size_t partial_cap, int uniform_agg, int uniform_act, cudaStream_t st, long long* launches);
 size_t forward_partial_needed(NetLayout L, int P, int B);
 void set_forward_spt(int spt);
+void set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb);
 cudaError_t launch_to_float(const double* src, float* dst, size_t n, int* bad, cudaStream_t st);
 }  // namespace fnb
 
@@ -122,6 +123,9 @@ int fnb_last_error_index(const fnb_ctx* ctx) { return ctx ? ctx->err_index : -1;
 size_t fnb_net_bytes(const fnb_ctx* ctx) { return ctx ? ctx->L.bytes : 0; }
 long long fnb_launch_count(const fnb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 void fnb_set_forward_spt(int spt) { set_forward_spt(spt); }
+void fnb_set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb) {
+  set_forward_tuning(spt, max_cols, rows_pct, group_kb);
+}
 
 // ---- device layer ------------------------------------------------------
 

@@ -347,6 +347,8 @@ struct FwdConfig {
 
 static int g_force_spt = 0;       // tuning override (fnb_set_forward_spt)
 static int g_rows_pct = 62;       // main-pass slot capacity, % of max_nodes + 1
+static int g_max_cols = 256;      // sample columns per genome group (tile width)
+static int g_group_kb = 72;       // shared-memory budget of one genome group
 
 // Launch geometry for `rows` value rows per column (slots + the zero slot).
 static FwdConfig fwd_config(const NetLayout& L, int P, int B, int rows, bool single_chunk) {
@@ -355,9 +357,9 @@ static FwdConfig fwd_config(const NetLayout& L, int P, int B, int rows, bool sin
   // columns per group: cover the batch, at most 256, shrinking until a
   // group fits ~72 KB (>= 3 resident CTAs per SM)
   int cols = 1;
-  while (cols < B && cols < 256) cols <<= 1;
+  while (cols < B && cols < g_max_cols) cols <<= 1;
   int spt = g_force_spt ? g_force_spt : (cols >= 128 ? 2 : 1);
-  while (cols > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, std::max(1, cols / spt), spt, rows) > 72 * 1024)
+  while (cols > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, std::max(1, cols / spt), spt, rows) > size_t(g_group_kb) * 1024)
     cols >>= 1;
   spt = std::min(spt, cols);
   const int T = std::max(1, cols / spt);
@@ -384,6 +386,12 @@ static int main_rows(const NetLayout& L) {
 
 void set_forward_spt(int spt) { g_force_spt = (spt == 1 || spt == 2 || spt == 4) ? spt : 0; }
 void set_forward_rows_pct(int pct) { g_rows_pct = (pct >= 10 && pct <= 100) ? pct : 62; }
+void set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb) {
+  set_forward_spt(spt);
+  set_forward_rows_pct(rows_pct);
+  g_max_cols = (max_cols >= 32 && max_cols <= 1024 && (max_cols & (max_cols - 1)) == 0) ? max_cols : 256;
+  g_group_kb = (group_kb >= 8 && group_kb <= 220) ? group_kb : 72;
+}
 
 static int fitness_units(int B) { return (B + 31) / 32; }
 

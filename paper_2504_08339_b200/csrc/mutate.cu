@@ -308,6 +308,82 @@ struct AttrDecider {
   }
 };
 
+// The connection-weight part of the split(5) walk in parallel.  Each live
+// connection is one mutate_scalar: at its position p it consumes p and, when
+// the weight bits of word p trigger, the two draws of a normal.  As an
+// automaton over positions the state is "draws still to skip" (0, 1, 2), so:
+// every lane folds its chunk of [p0, p0 + 3m) into a 3-entry state map, a warp
+// scan of map compositions gives each chunk's incoming state, a scan of visit
+// counts gives each visit's connection index, and the k-th visit's action
+// goes to the k-th live row.  Returns false (nothing written) when the walk
+// could leave the decision window.
+__device__ __forceinline__ uint32_t map_at(uint32_t m, uint32_t s) { return (m >> (2 * s)) & 3u; }
+
+__device__ bool conn_walk(const uint16_t* dw, uint32_t need, uint32_t p0, int m, uint32_t* tmp,
+                          const uint8_t* cflag, uint32_t* act_c, int C) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t span = 3u * uint32_t(m);
+  if (p0 + span > need) return false;
+  const uint32_t L = (span + 31) / 32;
+  const uint32_t lo = min(p0 + span, p0 + uint32_t(lane) * L), hi = min(p0 + span, lo + L);
+  auto bits = [&](uint32_t p) { return (uint32_t(dw[p]) >> AttrDecider::kWeight) & 3u; };
+  // pass 1: this chunk's map of start state -> end state
+  uint32_t s0 = 0, s1 = 1, s2 = 2;
+  for (uint32_t p = lo; p < hi; ++p) {
+    const uint32_t t = bits(p) ? 2u : 0u;
+    s0 = s0 ? s0 - 1 : t;
+    s1 = s1 ? s1 - 1 : t;
+    s2 = s2 ? s2 - 1 : t;
+  }
+  uint32_t f = s0 | (s1 << 2) | (s2 << 4);
+  for (int d = 1; d < 32; d <<= 1) {  // inclusive scan: F_l = f_l o F_{l-1}
+    const uint32_t g = __shfl_up_sync(kFullMask, f, d);
+    if (lane >= d) f = map_at(f, map_at(g, 0)) | (map_at(f, map_at(g, 1)) << 2) | (map_at(f, map_at(g, 2)) << 4);
+  }
+  const uint32_t prev = __shfl_up_sync(kFullMask, f, 1);
+  const uint32_t s_in = lane == 0 ? 0u : map_at(prev, 0);
+  // pass 2: visits in this chunk, exclusive prefix -> first connection index
+  uint32_t s = s_in;
+  int cnt = 0;
+  for (uint32_t p = lo; p < hi; ++p) {
+    if (s == 0) {
+      ++cnt;
+      s = bits(p) ? 2u : 0u;
+    } else {
+      --s;
+    }
+  }
+  int incl = cnt;
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(kFullMask, incl, d);
+    if (lane >= d) incl += v;
+  }
+  // pass 3: action codes by visit index
+  int k = incl - cnt;
+  s = s_in;
+  for (uint32_t p = lo; p < hi; ++p) {
+    if (s == 0) {
+      const uint32_t b = bits(p);
+      if (k < m) tmp[k] = b ? (((p + 1) << 2) | ((b & 1u) ? 1u : 2u)) : 0u;
+      ++k;
+      s = b ? 2u : 0u;
+    } else {
+      --s;
+    }
+  }
+  __syncwarp();
+  // k-th live row <- k-th visit
+  int before = 0;
+  for (int r0 = 0; r0 < C; r0 += 32) {
+    const int q = r0 + lane;
+    const bool live = q < C && (cflag[q] & 1);
+    const unsigned bl = __ballot_sync(kFullMask, live);
+    if (q < C) act_c[q] = live ? tmp[before + __popc(bl & ((1u << lane) - 1u))] : 0u;
+    before += __popc(bl);
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(128)
 k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
                int n_children, const uint8_t* __restrict__ active, int N, int C, MutCfgDev cfg, DevShape sh,
@@ -580,9 +656,10 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
       dw[2 * b + 1] = dec((uint64_t(w[1]) << 32) | w[0]);
     }
     __syncwarp();
-    if (lane == 0) {
+    uint32_t p_nodes_end = 0;
+    if (lane == 0) {  // node attributes: lane 0 chases the decision words
       uint32_t p = 0;
-      auto word = [&](uint32_t q) -> uint32_t { return q < uint32_t(need) ? dw[q] : dec(stream_u64_at(k5, q)); };
+      auto word =[&](uint32_t q) -> uint32_t { return q < uint32_t(need) ? dw[q] : dec(stream_u64_at(k5, q)); };
       // mutate_scalar (ops.hpp:281-289): action code, the normal's draws skipped
       auto scalar = [&](int sh) -> uint32_t {
         const uint32_t f = (word(p++) >> sh) & 3u;
@@ -613,7 +690,29 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
         sm.new_agg[q] = int8_t(ag);
         sm.new_act[q] = int8_t(ac);
       }
-      for (int q = 0; q < C; ++q) sm.act_c[q] = (sm.cflag[q] & 1) ? scalar(AttrDecider::kWeight) : 0u;
+      p_nodes_end = p;
+    }
+    // connection weights: nc scalars from position p0, walked in parallel
+    // (conn_walk); the sequential chase is kept for windows that are too short
+    const uint32_t p0 = __shfl_sync(kFullMask, p_nodes_end, 0);
+    uint32_t* tmp = reinterpret_cast<uint32_t*>(dw + ((need + 1) & ~1));  // [nc] codes by visit index
+    const bool tmp_fits = uint32_t((need + 1) & ~1) * 2u + 4u * uint32_t(nc) <= uint32_t(cap) * 2u;
+    if (!tmp_fits || !conn_walk(dw, uint32_t(need), p0, nc, tmp, sm.cflag, sm.act_c, C)) {
+      if (lane == 0) {
+        uint32_t p = p0;
+        for (int q = 0; q < C; ++q) {
+          uint32_t a = 0u;
+          if (sm.cflag[q] & 1) {
+            const uint32_t f = ((p < uint32_t(need) ? dw[p] : dec(stream_u64_at(k5, p))) >> AttrDecider::kWeight) & 3u;
+            ++p;
+            if (f) {
+              a = (p << 2) | ((f & 1u) ? 1u : 2u);
+              p += 2;
+            }
+          }
+          sm.act_c[q] = a;
+        }
+      }
     }
     __syncwarp();
     for (int q = lane; q < N; q += 32) {

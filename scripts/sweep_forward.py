@@ -1,0 +1,74 @@
+"""Sweep the K2 launch geometry (fnb_set_forward_tuning) on the bench workload.
+
+Every configuration must reproduce the default configuration's fitness bit
+for bit (the 32-sample fitness units make the FP64 sums independent of the
+geometry); the script asserts that, then prints the fastest configurations.
+
+    python scripts/sweep_forward.py > gpurun_out/sweep.txt
+"""
+import itertools
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2504_08339_b200 as fnb  # noqa: E402
+from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population  # noqa: E402
+
+
+def main():
+    P, N, C, B, NI, NO = 10_000, 64, 256, 1024, 4, 1
+    dev = torch.device("cuda", 0)
+    nodes_h, conns_h = synthetic_population(P, N, C, 0.75, NI, NO, seed=1000)
+    X_h, Y_h = regression_dataset(B, NI, NO, seed=0)
+    eng = fnb.Engine(fnb.GenomeLimits(N, C), list(range(NI)), list(range(NI, NI + NO)), fnb.AttributeSchema())
+    nodes, conns = torch.from_numpy(nodes_h).to(dev), torch.from_numpy(conns_h).to(dev)
+    X = torch.from_numpy(X_h.astype(np.float32)).to(dev)
+    Y = torch.from_numpy(Y_h.astype(np.float32)).to(dev)
+    nets = eng.alloc_nets(P)
+    st = torch.cuda.current_stream()
+    eng.transform_d(nodes, conns, nets, st)
+    fit = torch.empty(P, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    lib = fnb._native.lib()
+
+    def run(reps=10):
+        eng.forward_d(nets, P, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=st)
+        ms = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            eng.forward_d(nets, P, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=st)
+            b.record(st)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        return float(np.median(ms))
+
+    lib.fnb_set_forward_tuning(0, 0, 0, 0)
+    base_ms = run()
+    base_fit = fit.clone()
+    res = []
+    for spt, cols, pct, kb in itertools.product((1, 2, 4), (64, 128, 256, 512), (45, 55, 62, 75, 100), (48, 72, 96)):
+        lib.fnb_set_forward_tuning(spt, cols, pct, kb)
+        try:
+            ms = run()
+        except Exception as e:  # geometry that does not fit is reported, not fatal
+            res.append({"spt": spt, "cols": cols, "pct": pct, "kb": kb, "error": str(e)[:80]})
+            continue
+        same = bool(torch.equal(fit, base_fit))
+        res.append({"spt": spt, "cols": cols, "pct": pct, "kb": kb, "ms": ms, "bit_equal": same})
+        assert same, ("fitness bits changed with the launch geometry", spt, cols, pct, kb)
+    lib.fnb_set_forward_tuning(0, 0, 0, 0)
+    ok = sorted([r for r in res if "ms" in r], key=lambda r: r["ms"])
+    print(json.dumps({"default_ms": base_ms, "best": ok[:12], "errors": [r for r in res if "error" in r][:5],
+                      "n": len(res)}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
