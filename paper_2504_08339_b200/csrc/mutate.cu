@@ -15,9 +15,11 @@
 //                   split(4) connection delete, split(5) attribute pass.
 // Row scans (first empty row, k-th enabled row, cascades) are warp ballots;
 // every RngStream is owned by lane 0 so its draws are consumed in exactly
-// the reference order.  The attribute pass walks the split(5) stream on
-// lane 0 recording where each normal() starts, then all lanes evaluate the
-// glibc-exact normals (glibc_math.cuh) and apply them.
+// the reference order.  The attribute pass evaluates every decision of the
+// split(5) stream per position in parallel (AttrDecider), walks the node
+// attributes on lane 0 and the connection weights as a warp-parallel
+// automaton (conn_walk), then all lanes evaluate the glibc-exact normals
+// (glibc_math.cuh) and apply them.
 #include <climits>
 
 #include "fnb_common.cuh"
