@@ -123,7 +123,7 @@ long long fnb_launch_count(const fnb_ctx* ctx);
 void fnb_set_forward_spt(int spt);
 /* tuning knobs of the forward launch geometry (process-wide; 0 = default):
  * spt columns per thread (1/2/4), max_cols sample columns per genome group
- * (power of two, default 256), rows_pct main-pass value-slot capacity in % of
+ * (power of two, default 128), rows_pct main-pass value-slot capacity in % of
  * max_nodes + 1 (default 62), group_kb shared-memory budget per genome group
  * (default 72).  Fitness bits do not depend on any of them. */
 void fnb_set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb);

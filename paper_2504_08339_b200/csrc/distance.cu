@@ -5,13 +5,10 @@
 // linear scan and accumulates the attribute differences sequentially.  Here:
 //   * each representative gets an open-addressing marker table once
 //     (k_rep_tables), so every lookup is ~1 probe instead of an O(C) scan;
-//   * phase A (all 32 lanes, rows strided): markers of the genome are looked
-//     up in all S tables, the matched rows kept in shared memory;
-//   * phase B (lane s = representative s): the sequential FP64 sums run in
-//     exactly g1 row order with separately rounded ops (__dadd_rn & co, no
-//     FMA contraction), so the result equals the reference bit for bit
-//     (7% of random pairs are bitwise asymmetric -- SURVEY.md H4 -- so the
-//     argument order distance(genome, representative) is kept).
+//   * rows in chunks of 32 (one per lane, coalesced): each lane computes its
+//     row's term against every representative into a shared tile, then lane
+//     s adds the chunk in row order -- the reference's sequential FP64 sum
+//     with separately rounded ops, bit for bit (distance_warp.cuh).
 #include "distance_warp.cuh"
 
 namespace fnb {
@@ -44,9 +41,9 @@ k_distance(const double* __restrict__ nodes, const double* __restrict__ conns, i
   // founding round, after the founder): skip the rest without touching HBM
   if (only_unassigned && only_unassigned[g] >= 0) return;
   if (after_founder && (after_founder[0] < 0 || g <= after_founder[0])) return;
-  int16_t* match = reinterpret_cast<int16_t*>(smem_raw) + size_t(warp) * S * (N + C);
+  double* tile = reinterpret_cast<double*>(smem_raw) + size_t(warp) * S * 33;
   distance_warp(nodes + size_t(g) * N * kNodeCols, conns + size_t(g) * C * kConnCols, rn, rc, S, t, N, C, cd, ch,
-                match, out + size_t(g) * S);
+                tile, out + size_t(g) * S);
 }
 
 // ---- host launcher -----------------------------------------------------------
@@ -80,7 +77,7 @@ cudaError_t launch_distance_masked(const double* nodes, const double* conns, int
   k_rep_tables<<<S, 256, 0, st>>>(rn, rc, N, C, t);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t per_warp = size_t(S) * (N + C) * sizeof(int16_t);
+  const size_t per_warp = size_t(S) * 33 * sizeof(double);
   int warps = 4;
   while (warps > 1 && per_warp * warps > 96 * 1024) warps >>= 1;
   const size_t smem = per_warp * warps;

@@ -46,73 +46,81 @@ __device__ inline void rep_table_build(const double* __restrict__ n, const doubl
   __syncthreads();
 }
 
-// One warp: distance(genome (gn, gc), rep s) for s < S.  `match` is this
-// warp's S * (N + C) int16 scratch (shared memory).
-//   phase A (all 32 lanes, rows strided): markers looked up in all S tables;
-//   phase B (lane s = representative s): the sequential FP64 sums in exactly
-//   g1 row order with separately rounded ops (__dadd_rn & co, no FMA
-//   contraction), so the result equals the reference bit for bit (7% of
-//   random pairs are bitwise asymmetric -- SURVEY.md H4 -- so the argument
-//   order distance(genome, representative) is kept).
+// One warp: distance(genome (gn, gc), rep s) for s < S (<= 32); lane s
+// writes out[s].  `tile` is this warp's S * 33 doubles of shared memory.
+// Rows go in chunks of 32, one row per lane (coalesced genome reads): each
+// lane looks its row's marker up in every representative's table and writes
+// the row's term for rep s -- node (|db| + |dr| + [agg!=] + [act!=]) / 4,
+// connection |dw| / 1, separately rounded (__dadd_rn & co, no contraction),
+// +0.0 when unmatched -- into tile[s][row]; then lane s adds the chunk's 32
+// terms in row order.  Adding +0.0 for an unmatched row is exact (every term
+// is >= +0 and the sums start at +0), so each sum is the reference's g1
+// row-order sum bit for bit (ops.hpp:428-441, 454-463).  The argument order
+// distance(genome, representative) is kept: 7% of random pairs are bitwise
+// asymmetric.
 __device__ inline void distance_warp(const double* __restrict__ gn, const double* __restrict__ gc,
                                      const double* __restrict__ rn, const double* __restrict__ rc, int S,
-                                     const RepTables& t, int N, int C, double cd, double ch, int16_t* match,
+                                     const RepTables& t, int N, int C, double cd, double ch, double* tile,
                                      double* out) {
   const int lane = threadIdx.x & 31;
-  int n1 = 0, c1 = 0;
+  int n1 = 0, c1 = 0, mn = 0, mc = 0;
+  double sum_n = 0.0, sum_c = 0.0;
   for (int r0 = 0; r0 < N; r0 += 32) {
     const int r = r0 + lane;
-    const double k = r < N ? gn[r * kNodeCols + kKey] : __longlong_as_double(0x7ff8000000000000ll);
+    const double* a = gn + size_t(r) * kNodeCols;
+    const double k = r < N ? a[kKey] : __longlong_as_double(0x7ff8000000000000ll);
     const bool ne = !isnan(k);
     n1 += __popc(__ballot_sync(0xffffffffu, ne));
-    if (r < N)
-      for (int s = 0; s < S; ++s)
-        match[s * (N + C) + r] = int16_t(
-            ne ? table_find(t.nkeys + size_t(s) * t.Hn, t.nrows + size_t(s) * t.Hn, t.Hn - 1, node_key(k)) : -1);
+    for (int s = 0; s < S; ++s) {
+      const int q = ne ? table_find(t.nkeys + size_t(s) * t.Hn, t.nrows + size_t(s) * t.Hn, t.Hn - 1, node_key(k)) : -1;
+      double v = 0.0;
+      if (q >= 0) {
+        const double* b = rn + size_t(s) * N * kNodeCols + size_t(q) * kNodeCols;
+        double d = __dadd_rn(fabs(__dsub_rn(a[kBias], b[kBias])), fabs(__dsub_rn(a[kResp], b[kResp])));
+        d = __dadd_rn(d, a[kAgg] != b[kAgg] ? 1.0 : 0.0);
+        d = __dadd_rn(d, a[kAct] != b[kAct] ? 1.0 : 0.0);
+        v = __ddiv_rn(d, 4.0);
+      }
+      const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
+      if (lane == s) mn += m;
+      tile[s * 33 + lane] = v;
+    }
+    __syncwarp();
+    if (lane < S) {
+      const int n = min(32, N - r0);
+      for (int i = 0; i < n; ++i) sum_n = __dadd_rn(sum_n, tile[lane * 33 + i]);
+    }
+    __syncwarp();
   }
   for (int r0 = 0; r0 < C; r0 += 32) {
     const int r = r0 + lane;
-    double in = __longlong_as_double(0x7ff8000000000000ll), o = 0.0;
+    double in = __longlong_as_double(0x7ff8000000000000ll), o = 0.0, w = 0.0;
     if (r < C) {
-      const double2 a = *reinterpret_cast<const double2*>(gc + r * kConnCols);
-      in = a.x;
-      o = a.y;
+      const double2 x = *reinterpret_cast<const double2*>(gc + size_t(r) * kConnCols);
+      in = x.x;
+      o = x.y;
     }
     const bool ne = !isnan(in);
+    if (ne) w = gc[size_t(r) * kConnCols + kW];
     c1 += __popc(__ballot_sync(0xffffffffu, ne));
-    if (r < C) {
-      const unsigned long long key = ne ? conn_key(in, o) : 0ull;
-      for (int s = 0; s < S; ++s)
-        match[s * (N + C) + N + r] =
-            int16_t(ne ? table_find(t.ckeys + size_t(s) * t.Hc, t.crows + size_t(s) * t.Hc, t.Hc - 1, key) : -1);
+    const unsigned long long key = ne ? conn_key(in, o) : 0ull;
+    for (int s = 0; s < S; ++s) {
+      const int q = ne ? table_find(t.ckeys + size_t(s) * t.Hc, t.crows + size_t(s) * t.Hc, t.Hc - 1, key) : -1;
+      double v = 0.0;
+      if (q >= 0) v = __ddiv_rn(fabs(__dsub_rn(w, rc[size_t(s) * C * kConnCols + size_t(q) * kConnCols + kW])), 1.0);
+      const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
+      if (lane == s) mc += m;
+      tile[s * 33 + lane] = v;
     }
+    __syncwarp();
+    if (lane < S) {
+      const int n = min(32, C - r0);
+      for (int i = 0; i < n; ++i) sum_c = __dadd_rn(sum_c, tile[lane * 33 + i]);
+    }
+    __syncwarp();
   }
-  __syncwarp();
-
-  // phase B: lane s accumulates rep s in g1 row order (ops.hpp:428-441, 454-463)
-  for (int s = lane; s < S; s += 32) {
-    const int16_t* m = match + s * (N + C);
-    const double* rnode = rn + size_t(s) * N * kNodeCols;
-    const double* rconn = rc + size_t(s) * C * kConnCols;
-    int mn = 0, mc = 0;
-    double sum_n = 0.0, sum_c = 0.0;
-    for (int r = 0; r < N; ++r) {
-      const int q = m[r];
-      if (q < 0) continue;
-      ++mn;
-      const double* a = gn + r * kNodeCols;
-      const double* b = rnode + q * kNodeCols;
-      double d = __dadd_rn(fabs(__dsub_rn(a[kBias], b[kBias])), fabs(__dsub_rn(a[kResp], b[kResp])));
-      d = __dadd_rn(d, a[kAgg] != b[kAgg] ? 1.0 : 0.0);
-      d = __dadd_rn(d, a[kAct] != b[kAct] ? 1.0 : 0.0);
-      sum_n = __dadd_rn(sum_n, __ddiv_rn(d, 4.0));
-    }
-    for (int r = 0; r < C; ++r) {
-      const int q = m[N + r];
-      if (q < 0) continue;
-      ++mc;
-      sum_c = __dadd_rn(sum_c, __ddiv_rn(fabs(__dsub_rn(gc[r * kConnCols + kW], rconn[q * kConnCols + kW])), 1.0));
-    }
+  if (lane < S) {
+    const int s = lane;
     const int n2 = t.counts[2 * s], c2 = t.counts[2 * s + 1];
     double total = 0.0;
     {

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(128) k_found_rounds(SpeciesDev* sd, int S_old,
   int* counts = cr + Hc;                                          // 2 ints (+2 pad)
   double* dist_w = reinterpret_cast<double*>(counts + 4);         // one per warp
   const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int16_t* match = reinterpret_cast<int16_t*>(dist_w + warps) + size_t(warp) * (N + C);
+  double* tile = dist_w + warps + size_t(warp) * 33;  // distance_warp scratch (S = 1)
   const int gw = blockIdx.x * warps + warp, nw = gridDim.x * warps;
   const size_t gn = size_t(N) * kNodeCols, gc = size_t(C) * kConnCols;
 
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(128) k_found_rounds(SpeciesDev* sd, int S_old,
     const RepTables t{nk, nr, ck, cr, counts, Hn, Hc};
     for (int g = gw; g < P; g += nw) {
       if (g <= f || __ldcg(species_of + g) >= 0) continue;  // warp-uniform
-      distance_warp(pn + size_t(g) * gn, pc + size_t(g) * gc, fn, fc, 1, t, N, C, cd, ch, match, dist_w + warp);
+      distance_warp(pn + size_t(g) * gn, pc + size_t(g) * gc, fn, fc, 1, t, N, C, cd, ch, tile, dist_w + warp);
       __syncwarp();
       if (lane == 0) {
         if (dist_w[warp] < th) species_of[g] = j;
@@ -611,7 +611,7 @@ struct Evolver {
   cudaError_t launch_found_rounds(int S_old, const double* n, const double* c) {
     int Hn = table_capacity(N), Hc = table_capacity(C);
     const int block = 128;
-    const size_t smem = size_t(Hn + Hc) * 12 + 16 + (block / 32) * 8 + (block / 32) * size_t(N + C) * 2;
+    const size_t smem = size_t(Hn + Hc) * 12 + 16 + (block / 32) * 8 + (block / 32) * 33 * 8;
     cudaError_t e = cudaFuncSetAttribute(k_found_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     if (coop_blocks == 0) {

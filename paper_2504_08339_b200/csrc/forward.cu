@@ -347,7 +347,7 @@ struct FwdConfig {
 
 static int g_force_spt = 0;       // tuning override (fnb_set_forward_spt)
 static int g_rows_pct = 62;       // main-pass slot capacity, % of max_nodes + 1
-static int g_max_cols = 256;      // sample columns per genome group (tile width)
+static int g_max_cols = 128;      // sample columns per genome group (tile width; swept, scripts/sweep_forward.py)
 static int g_group_kb = 72;       // shared-memory budget of one genome group
 
 // Launch geometry for `rows` value rows per column (slots + the zero slot).
@@ -389,7 +389,7 @@ void set_forward_rows_pct(int pct) { g_rows_pct = (pct >= 10 && pct <= 100) ? pc
 void set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb) {
   set_forward_spt(spt);
   set_forward_rows_pct(rows_pct);
-  g_max_cols = (max_cols >= 32 && max_cols <= 1024 && (max_cols & (max_cols - 1)) == 0) ? max_cols : 256;
+  g_max_cols = (max_cols >= 32 && max_cols <= 1024 && (max_cols & (max_cols - 1)) == 0) ? max_cols : 128;
   g_group_kb = (group_kb >= 8 && group_kb <= 220) ? group_kb : 72;
 }
 
