@@ -160,6 +160,32 @@ def c5_distance(dev, stream, flush, reps: int = 5):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}}
 
 
+def c3_cppn(eng, nets, dev, stream, flush, reps: int = 3):
+    """C3: the pop-10k C2 networks as CPPNs queried over a
+    256 x 256 grid (x, y, r, bias) = 65,536 queries per genome, image-MSE
+    fitness fused into the forward (outputs never materialised)."""
+    import torch
+    import paper_2504_08339_b200 as fnb
+    from paper_2504_08339_b200.synthetic import cppn_dataset
+    Xh, Yh = cppn_dataset(256)
+    X = torch.from_numpy(Xh.astype(np.float32)).to(dev)
+    Y = torch.from_numpy(Yh.astype(np.float32)).to(dev)
+    fit = torch.empty(P_SHARD, dtype=torch.float64, device=dev)
+    eng.forward_d(nets, P_SHARD, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=stream)
+    ms = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.forward_d(nets, P_SHARD, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = float(np.median(ms)) / 1e3
+    return {"workload": "C3 CPPN: pop 10k (C2 networks), 256x256 grid = 65,536 queries per genome, image MSE",
+            "forward_ms": t * 1e3, "evals_per_s": P_SHARD * Xh.shape[0] / t}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -168,7 +194,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-generations", action="store_true")
-    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (pop 100k) K3 distance roofline")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C3 (CPPN) and C5 (pop 100k K3 distance) measurements")
     ap.add_argument("--spt", type=int, default=0, help="forward columns per thread (tuning; 0 = auto)")
     args = ap.parse_args()
 
@@ -334,6 +360,7 @@ def main():
                        "max over ranks"}
         ev.close()
 
+    c3 = c3_cppn(eng, nets, dev, stream, flush) if not args.no_c5 else None
     c5 = None
     if not args.no_c5:
         c5 = c5_distance(dev, stream, flush)
@@ -381,6 +408,8 @@ def main():
             line["generations"] = gen
         if c5 is not None:
             line["c5_distance"] = c5
+        if c3 is not None:
+            line["c3_cppn"] = c3
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

@@ -24,6 +24,7 @@
 //              mutation with one slot-ordered innovation table.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -59,6 +60,8 @@ struct SpeciesDev {
   int cnt[kMaxSpecies];
   int total_spawn;
   int error;
+  int generation;    // the step's generation (keys split(1).split(generation)); graph replays read it here
+  int first_bad;     // lowest child whose mutation failed (INT_MAX = none)
 };
 
 struct NeatCfg {  // == fnb_neat_config
@@ -134,6 +137,7 @@ __global__ void k_copy_genome(const double* sn, const double* sc, const int* src
 __global__ void k_spec_begin(SpeciesDev* sd) {
   sd->old_count = sd->count;
   for (int j = 0; j <= kMaxSpecies; ++j) sd->rcand[j] = INT_MAX;
+  sd->first_bad = INT_MAX;
   for (int j = 0; j < kMaxSpecies; ++j) {
     sd->dmin[j] = ~0ull;
     sd->argmin[j] = INT_MAX;
@@ -458,7 +462,14 @@ __global__ void k_species_keys(const int* sorted_idx, int P, const int* species_
   skey[r] = j < 0 ? kMaxSpecies : j;
 }
 
-__global__ void k_reproduce_plan(const SpeciesDev* sd, const int* members, const double* fitness, int P, Key4 gen_key,
+__global__ void k_gen_advance(SpeciesDev* sd) { ++sd->generation; }
+
+__global__ void k_first_bad(const int* status, int P, SpeciesDev* sd) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P && status[i]) atomicMin(&sd->first_bad, i);
+}
+
+__global__ void k_reproduce_plan(const SpeciesDev* sd, const int* members, const double* fitness, int P, Key4 root1,
                                  int genome_elitism, double survival, int* fit_idx, int* oth_idx, uint32_t* xkeys,
                                  uint32_t* mkeys, uint8_t* active) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -481,7 +492,7 @@ __global__ void k_reproduce_plan(const SpeciesDev* sd, const int* members, const
   int pool = int(ceil(__dmul_rn(survival, double(m))));
   if (pool < 1) pool = 1;
   if (pool > m) pool = m;
-  const Key4 ck = key_split(gen_key, uint64_t(c));
+  const Key4 ck = key_split(key_split(root1, uint64_t(sd->generation)), uint64_t(c));
   Stream sel(key_split(ck, 0));
   const int a = mem[int(sel.below(uint64_t(pool)))];
   const int b = mem[int(sel.below(uint64_t(pool)))];
@@ -589,6 +600,7 @@ struct Evolver {
   }
 
   void release() {
+    release_graphs();
     void* ps[] = {pn[0], pn[1], pc[0], pc[1], fitness, rep_n, rep_c, dmat, species_of, sd,
                   kasc, kdesc, ktmp, idx, idx_sorted, idx_tmp, skey, skey_tmp, fit_idx, oth_idx, status, next_key,
                   xkeys, mkeys, active, cub_tmp, scratch};
@@ -632,8 +644,75 @@ struct Evolver {
                                        st);
   }
 
-  // speciate -> update_stagnation -> compute_spawn_counts -> reproduce
+  // One generation step = enqueue_step() (all kernels, no host sync) and a
+  // 12-byte status read.  The kernel sequence depends only on (S_old, cur),
+  // so it is captured once per pair as a CUDA graph and replayed; the
+  // generation number the keys need lives in SpeciesDev.  FNB_STEP_GRAPH=0
+  // (or a failed capture) runs the same sequence eagerly.
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    long long n_launches = 0;
+  };
+  StepGraph graphs[kMaxSpecies + 1][2];
+  bool use_graphs = true;
+
   cudaError_t step(int* host_error) {
+    cudaError_t e = cudaSuccess;
+    if (use_graphs) {
+      StepGraph& g = graphs[host_species][cur];
+      if (!g.exec) {
+        const long long before = *launches;
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+          const cudaError_t ee = enqueue_step();
+          e = cudaStreamEndCapture(st, &graph);
+          if (ee != cudaSuccess) e = ee;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        g.n_launches = *launches - before;
+        *launches = before;
+        if (e != cudaSuccess) {  // e.g. a capture-unsupported launch: stay eager
+          g.exec = nullptr;
+          use_graphs = false;
+          cudaGetLastError();
+        }
+      }
+      if (use_graphs) {
+        e = cudaGraphLaunch(g.exec, st);
+        if (e != cudaSuccess) return e;
+        *launches += g.n_launches;
+      }
+    }
+    if (!use_graphs) {
+      e = enqueue_step();
+      if (e != cudaSuccess) return e;
+    }
+    int stat[3] = {0, 0, INT_MAX};  // error, count, first_bad
+    e = cudaMemcpyAsync(&stat[0], &sd->error, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&stat[1], &sd->count, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&stat[2], &sd->first_bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    *host_error = stat[0] ? -2 : (stat[2] == INT_MAX ? -1 : stat[2]);
+    host_species = stat[1];
+    cur ^= 1;
+    ++generation;
+    return cudaSuccess;
+  }
+
+  void release_graphs() {
+    for (auto& row : graphs)
+      for (auto& g : row)
+        if (g.exec) {
+          cudaGraphExecDestroy(g.exec);
+          g.exec = nullptr;
+        }
+  }
+
+  // speciate -> update_stagnation -> compute_spawn_counts -> reproduce
+  cudaError_t enqueue_step() {
     const int T = 256, B = (P + T - 1) / T;
     const double th = cfg.threshold;
     const double* n = pn[cur];
@@ -685,8 +764,8 @@ struct Evolver {
     k_species_keys<<<B, T, 0, st>>>(idx_tmp, P, species_of, skey);
     e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, skey, skey_tmp, idx_tmp, idx_sorted, P, 0, 6, st);
     if (e != cudaSuccess) return e;
-    const Key4 gen_key = key_split(key_split(key_from_seed(seed), 1), uint64_t(generation));
-    k_reproduce_plan<<<B, T, 0, st>>>(sd, idx_sorted, fitness, P, gen_key, cfg.genome_elitism, cfg.survival, fit_idx,
+    const Key4 root1 = key_split(key_from_seed(seed), 1);
+    k_reproduce_plan<<<B, T, 0, st>>>(sd, idx_sorted, fitness, P, root1, cfg.genome_elitism, cfg.survival, fit_idx,
                                       oth_idx, xkeys, mkeys, active);
     *launches += 24;
     e = launch_crossover(n, c, fit_idx, oth_idx, xkeys, P, N, C, pn[cur ^ 1], pc[cur ^ 1], st);
@@ -695,22 +774,10 @@ struct Evolver {
     e = launch_mutate(pn[cur ^ 1], pc[cur ^ 1], mkeys, P, active, &mut, sh, next_key, status, scratch, scratch_bytes,
                       nullptr, st, launches);
     if (e != cudaSuccess) return e;
-    // step status: spawn total and per-child mutation status
-    int err_spawn = 0, count = 0;
-    e = cudaMemcpyAsync(&err_spawn, &sd->error, sizeof(int), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&count, &sd->count, sizeof(int), cudaMemcpyDeviceToHost, st);
-    std::vector<int> stv(static_cast<size_t>(P));
-    if (e == cudaSuccess) e = cudaMemcpyAsync(stv.data(), status, sizeof(int) * P, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return e;
-    *host_error = err_spawn ? -2 : -1;
-    if (!err_spawn)
-      for (int i = 0; i < P; ++i)
-        if (stv[size_t(i)]) { *host_error = i; break; }
-    host_species = count;
-    cur ^= 1;
-    ++generation;
-    return cudaSuccess;
+    k_first_bad<<<B, T, 0, st>>>(status, P, sd);
+    k_gen_advance<<<1, 1, 0, st>>>(sd);
+    *launches += 2;
+    return cudaGetLastError();
   }
 };
 
@@ -775,6 +842,7 @@ int fnb_evolver_create(fnb_ctx* ctx, const fnb_neat_config* cfg, uint64_t seed, 
   v.N = sh.N;
   v.C = sh.C;
   v.st = ctx->stream;
+  if (const char* g = std::getenv("FNB_STEP_GRAPH")) v.use_graphs = std::string(g) != "0";
   v.launches = &ctx->launches;
   cudaSetDevice(ctx->device);
   cudaError_t err = v.alloc();

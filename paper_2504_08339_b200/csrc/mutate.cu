@@ -183,9 +183,8 @@ __global__ void k7_advance(int* next_key) { next_key[0] += next_key[1]; }
 // The child's keys and flags are staged in shared memory (and kept in step
 // with every structural edit lane 0 makes to the HBM rows), so each scan
 // and each lane-0 stream step is a shared-memory access, not an L2 trip.
-// The long attribute stream split(5) is evaluated by the whole warp (one
-// Philox block per lane) into per-position decision words; lane 0 chases the
-// positions the walk actually visits (AttrDecider).
+// The attribute pass split(5) runs afterwards in its own kernel
+// (k_mutate_attrs) with a small footprint.
 // ---------------------------------------------------------------------------
 struct MutSmem {
   unsigned long long* nkeys;  // marker table: node key -> first row
@@ -193,26 +192,22 @@ struct MutSmem {
   unsigned long long* ckeys;  // marker table: conn pair -> first row
   int* crows;
   uint32_t* reach;            // [N][W]: rows reachable (>= 1 enabled edge) from row
-  uint32_t* act_n;            // [2N] bias / response actions of node rows
-  uint32_t* act_c;            // [C] weight actions
+  int* sbuf;                  // [2N] S2 fallback: sorted keys / targets
   int* nkey;                  // [N] node key (rows)
   int* cin;                   // [C]
   int* cout;                  // [C]
   int* list_a;                // [N] scratch lists (keys / targets / sorted)
   int* list_b;                // [N]
-  unsigned long long* dbuf;   // [64] scratch (with the tables: the S5 decision window)
   uint8_t* nflag;             // [N] bit0 non-empty, bit1 input, bit2 output
   uint8_t* cflag;             // [C] bit0 non-empty, bit1 enabled
-  int8_t* new_agg;            // [N] -1 or replacement id
-  int8_t* new_act;            // [N]
 };
 
 __host__ __device__ inline size_t mut_smem_bytes(int N, int C) {
   const int W = (N + 31) / 32;
   size_t b = size_t(table_capacity(N)) * 12 + size_t(table_capacity(C)) * 12;
-  b += size_t(N) * W * 4 + size_t(2 * N + C) * 4;  // reach, actions
+  b += size_t(N) * W * 4 + size_t(2 * N) * 4;      // reach, sbuf
   b += size_t(N) * 4 * 3 + size_t(C) * 4 * 2;      // nkey, list_a, list_b, cin, cout
-  b += 64 * 8 + size_t(N) * 3 + size_t(C) + 64;    // dbuf, flags, new ids, slack
+  b += size_t(N) + size_t(C) + 64;                 // flags, slack
   return align16(b);
 }
 
@@ -221,21 +216,17 @@ __device__ inline MutSmem mut_carve(uint8_t* p, int N, int C) {
   const int Hn = table_capacity(N), Hc = table_capacity(C), W = (N + 31) / 32;
   s.nkeys = reinterpret_cast<unsigned long long*>(p); p += size_t(Hn) * 8;
   s.ckeys = reinterpret_cast<unsigned long long*>(p); p += size_t(Hc) * 8;
-  s.dbuf = reinterpret_cast<unsigned long long*>(p); p += 64 * 8;
   s.nrows = reinterpret_cast<int*>(p); p += size_t(Hn) * 4;
   s.crows = reinterpret_cast<int*>(p); p += size_t(Hc) * 4;
   s.reach = reinterpret_cast<uint32_t*>(p); p += size_t(N) * W * 4;
-  s.act_n = reinterpret_cast<uint32_t*>(p); p += size_t(2 * N) * 4;
-  s.act_c = reinterpret_cast<uint32_t*>(p); p += size_t(C) * 4;
+  s.sbuf = reinterpret_cast<int*>(p); p += size_t(2 * N) * 4;
   s.nkey = reinterpret_cast<int*>(p); p += size_t(N) * 4;
   s.list_a = reinterpret_cast<int*>(p); p += size_t(N) * 4;
   s.list_b = reinterpret_cast<int*>(p); p += size_t(N) * 4;
   s.cin = reinterpret_cast<int*>(p); p += size_t(C) * 4;
   s.cout = reinterpret_cast<int*>(p); p += size_t(C) * 4;
   s.nflag = p; p += N;
-  s.cflag = p; p += C;
-  s.new_agg = reinterpret_cast<int8_t*>(p); p += N;
-  s.new_act = reinterpret_cast<int8_t*>(p);
+  s.cflag = p;
   return s;
 }
 
@@ -262,7 +253,7 @@ __device__ __forceinline__ void stage_conn(MutSmem& sm, const double* c, int r) 
 
 // attribute action code: bit0-1 kind (0 none, 1 add normal(0,power), 2 replace
 // normal(init)), bits 2.. = stream position of the normal's first draw
-__device__ __forceinline__ double apply_scalar(double v, uint32_t a, const Key4& k, double power, double mean,
+__device__ __noinline__ double apply_scalar(double v, uint32_t a, const Key4& k, double power, double mean,
                                                double sd) {
   if ((a & 3u) == 0) return v;
   const uint64_t pos = a >> 2;
@@ -316,13 +307,13 @@ struct AttrDecider {
 // automaton over positions the state is "draws still to skip" (0, 1, 2), so:
 // every lane folds its chunk of [p0, p0 + 3m) into a 3-entry state map, a warp
 // scan of map compositions gives each chunk's incoming state, a scan of visit
-// counts gives each visit's connection index, and the k-th visit's action
-// goes to the k-th live row.  Returns false (nothing written) when the walk
-// could leave the decision window.
+// counts gives each visit's connection index k, and the lane that finds
+// visit k applies its normal to the k-th live row.  Returns false (nothing
+// written) when the walk could leave the decision window.
 __device__ __forceinline__ uint32_t map_at(uint32_t m, uint32_t s) { return (m >> (2 * s)) & 3u; }
 
-__device__ bool conn_walk(const uint16_t* dw, uint32_t need, uint32_t p0, int m, uint32_t* tmp,
-                          const uint8_t* cflag, uint32_t* act_c, int C) {
+__device__ bool conn_walk(const uint16_t* dw, uint32_t need, uint32_t p0, int m, const int16_t* live_row,
+                          double* cc, const Key4& k5, const MutCfgDev& cfg) {
   const int lane = threadIdx.x & 31;
   const uint32_t span = 3u * uint32_t(m);
   if (p0 + span > need) return false;
@@ -360,28 +351,21 @@ __device__ bool conn_walk(const uint16_t* dw, uint32_t need, uint32_t p0, int m,
     const int v = __shfl_up_sync(kFullMask, incl, d);
     if (lane >= d) incl += v;
   }
-  // pass 3: action codes by visit index
+  // pass 3: apply the triggered normals of this chunk's visits
   int k = incl - cnt;
   s = s_in;
   for (uint32_t p = lo; p < hi; ++p) {
     if (s == 0) {
       const uint32_t b = bits(p);
-      if (k < m) tmp[k] = b ? (((p + 1) << 2) | ((b & 1u) ? 1u : 2u)) : 0u;
+      if (b && k < m) {
+        double* w = cc + size_t(live_row[k]) * kConnCols + kW;
+        *w = apply_scalar(*w, ((p + 1) << 2) | ((b & 1u) ? 1u : 2u), k5, cfg.w_power, cfg.w_mean, cfg.w_std);
+      }
       ++k;
       s = b ? 2u : 0u;
     } else {
       --s;
     }
-  }
-  __syncwarp();
-  // k-th live row <- k-th visit
-  int before = 0;
-  for (int r0 = 0; r0 < C; r0 += 32) {
-    const int q = r0 + lane;
-    const bool live = q < C && (cflag[q] & 1);
-    const unsigned bl = __ballot_sync(kFullMask, live);
-    if (q < C) act_c[q] = live ? tmp[before + __popc(bl & ((1u << lane) - 1u))] : 0u;
-    before += __popc(bl);
   }
   return true;
 }
@@ -522,7 +506,7 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
         if (!found) {
           // deterministic fallback: sorted keys x sorted targets, from-major
           // (ops.hpp:271-278); sorted position = rank of (key, list index)
-          int* sk = reinterpret_cast<int*>(sm.act_c);
+          int* sk = sm.sbuf;
           int* stg = sk + N;
           __syncwarp();
           for (int q = lane; q < nk; q += 32) {
@@ -631,105 +615,133 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
     }
   }
 
-  // ---- attributes (ops.hpp:338-359).  The split(5) walk is sequential (a
-  //      scalar consumes 1 or 3 draws depending on its own draw), so: all
-  //      lanes first evaluate every decision the walk could take at every
-  //      stream position of a window that covers the worst case (one 16-bit
-  //      word per position, in the marker tables' dead shared memory); lane 0
-  //      then chases the positions, a few instructions per decision; all
-  //      lanes finally apply the normals.  Positions past the window (only
-  //      reachable through below() rejections) are evaluated directly.
-  if (!st) {
-    const Key4 k5 = key_split(key, 5);
-    uint16_t* dw = reinterpret_cast<uint16_t*>(sm.nkeys);  // nkeys..crows are contiguous and free here
-    const int cap = int((size_t(Hn) * 12 + size_t(Hc) * 12 + 64 * 8) / 2) & ~1;
-    int nn = 0, nc = 0;
-    for (int q = lane; q < N; q += 32) nn += (sm.nflag[q] & 3) == 1;
-    for (int q = lane; q < C; q += 32) nc += sm.cflag[q] & 1;
-    nn = __reduce_add_sync(kFullMask, nn);
-    nc = __reduce_add_sync(kFullMask, nc);
-    const int per_node = 6 + (cfg.agg_rate > 0.0 ? 2 : 0) + (cfg.act_rate > 0.0 ? 2 : 0);
-    const int need = min(cap, (nn * per_node + nc * 3 + 1) & ~1);
-    const AttrDecider dec(cfg);
-    for (int b = lane; 2 * b < need; b += 32) {
-      uint32_t w[4];
-      stream_block(k5, uint64_t(b), w);
-      dw[2 * b] = dec((uint64_t(w[3]) << 32) | w[2]);
-      dw[2 * b + 1] = dec((uint64_t(w[1]) << 32) | w[0]);
+  if (lane == 0) status[c] = st;
+}
+
+// ---------------------------------------------------------------------------
+// attributes (ops.hpp:338-359), one warp per child after the structural pass.
+// The split(5) walk is sequential (a scalar consumes 1 or 3 draws depending on
+// its own draw), so: all lanes first evaluate every decision the walk could
+// take at every stream position of a window that covers the worst case (one
+// 16-bit word per position, AttrDecider); lane 0 chases the node attributes
+// through the words; the connection weights are walked as a warp-parallel
+// automaton (conn_walk) that applies their normals; all lanes finally apply
+// the node normals.  Positions past the window (only reachable through
+// below() rejections) are evaluated directly from the stream.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline int attr_per_node(const MutCfgDev& cfg) {
+  return 6 + (cfg.agg_rate > 0.0 ? 2 : 0) + (cfg.act_rate > 0.0 ? 2 : 0);
+}
+__host__ __device__ inline int attr_window(int N, int C, int per_node) { return (per_node * N + 3 * C + 1) & ~1; }
+__host__ __device__ inline size_t attr_smem_bytes(int N, int C, int win) {
+  return align16(size_t(win) * 2) + align16(size_t(C) * 2) + align16(size_t(2 * N) * 4) + align16(size_t(2 * N)) +
+         align16(size_t(N));
+}
+
+__global__ void __launch_bounds__(256)
+k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
+               int n_children, const uint8_t* __restrict__ active, const int* __restrict__ status, int N, int C,
+               MutCfgDev cfg, DevShape sh, int win, size_t smem_per_warp) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (c >= n_children) return;
+  if ((active && !active[c]) || status[c]) return;
+  uint8_t* p8 = smem_raw + size_t(warp) * smem_per_warp;
+  uint16_t* dw = reinterpret_cast<uint16_t*>(p8); p8 += align16(size_t(win) * 2);
+  int16_t* live_row = reinterpret_cast<int16_t*>(p8); p8 += align16(size_t(C) * 2);
+  uint32_t* act_n = reinterpret_cast<uint32_t*>(p8); p8 += align16(size_t(2 * N) * 4);
+  int8_t* new_id = reinterpret_cast<int8_t*>(p8); p8 += align16(size_t(2 * N));  // [q] agg, [N + q] act
+  uint8_t* hid = p8;                                                              // [N] mutable node row
+  double* n = nodes + size_t(c) * N * kNodeCols;
+  double* cc = conns + size_t(c) * C * kConnCols;
+  const Key4 k5 = key_split(load_key(keys, c), 5);
+
+  // rows of the structurally final child: mutable nodes, live connections
+  int nn = 0, nc = 0;
+  for (int r0 = 0; r0 < N; r0 += 32) {
+    const int r = r0 + lane;
+    bool h = false;
+    if (r < N) {
+      const double k = n[r * kNodeCols + kKey];
+      h = !isnan(k) && !is_key_in(int(k), sh.input_keys, sh.I);
+      hid[r] = h;
     }
-    __syncwarp();
-    uint32_t p_nodes_end = 0;
-    if (lane == 0) {  // node attributes: lane 0 chases the decision words
-      uint32_t p = 0;
-      auto word =[&](uint32_t q) -> uint32_t { return q < uint32_t(need) ? dw[q] : dec(stream_u64_at(k5, q)); };
-      // mutate_scalar (ops.hpp:281-289): action code, the normal's draws skipped
-      auto scalar = [&](int sh) -> uint32_t {
-        const uint32_t f = (word(p++) >> sh) & 3u;
-        if (!f) return 0u;
-        const uint32_t a = (p << 2) | ((f & 1u) ? 1u : 2u);
+    nn += __popc(__ballot_sync(kFullMask, h));
+  }
+  for (int r0 = 0; r0 < C; r0 += 32) {
+    const int r = r0 + lane;
+    const bool live = r < C && !isnan(cc[r * kConnCols + kIn]);
+    const unsigned bl = __ballot_sync(kFullMask, live);
+    if (live) live_row[nc + __popc(bl & ((1u << lane) - 1u))] = int16_t(r);
+    nc += __popc(bl);
+  }
+  const int need = min(win, (nn * attr_per_node(cfg) + nc * 3 + 1) & ~1);
+  const AttrDecider dec(cfg);
+  for (int b = lane; 2 * b < need; b += 32) {
+    uint32_t w[4];
+    stream_block(k5, uint64_t(b), w);
+    dw[2 * b] = dec((uint64_t(w[3]) << 32) | w[2]);
+    dw[2 * b + 1] = dec((uint64_t(w[1]) << 32) | w[0]);
+  }
+  __syncwarp();
+  uint32_t p_nodes_end = 0;
+  if (lane == 0) {  // node attributes: lane 0 chases the decision words in row order
+    uint32_t p = 0;
+    auto word = [&](uint32_t q) -> uint32_t { return q < uint32_t(need) ? dw[q] : dec(stream_u64_at(k5, q)); };
+    auto scalar = [&](int sh_) -> uint32_t {  // mutate_scalar (ops.hpp:281-289): action code
+      const uint32_t f = (word(p++) >> sh_) & 3u;
+      if (!f) return 0u;
+      const uint32_t a = (p << 2) | ((f & 1u) ? 1u : 2u);
+      p += 2;
+      return a;
+    };
+    auto index = [&](int acc_bit, int val_shift) -> int {  // below(n), rng.hpp:99-106
+      for (;;) {
+        const uint32_t f = word(p++);
+        if ((f >> acc_bit) & 1u) return int((f >> val_shift) & 7u);
+      }
+    };
+    for (int q = 0; q < N; ++q) {
+      uint32_t ab = 0u, ar = 0u;
+      int ag = -1, ac = -1;
+      if (hid[q]) {
+        ab = scalar(AttrDecider::kBias);
+        ar = scalar(AttrDecider::kResp);
+        if (cfg.agg_rate > 0.0 && ((word(p++) >> AttrDecider::kAggCoin) & 1u))
+          ag = index(AttrDecider::kAggAcc, AttrDecider::kAggVal);
+        if (cfg.act_rate > 0.0 && ((word(p++) >> AttrDecider::kActCoin) & 1u))
+          ac = index(AttrDecider::kActAcc, AttrDecider::kActVal);
+      }
+      act_n[2 * q] = ab;
+      act_n[2 * q + 1] = ar;
+      new_id[q] = int8_t(ag);
+      new_id[N + q] = int8_t(ac);
+    }
+    p_nodes_end = p;
+  }
+  // connection weights from p0 (warp-parallel; lane-0 chase if the window is short)
+  const uint32_t p0 = __shfl_sync(kFullMask, p_nodes_end, 0);
+  if (!conn_walk(dw, uint32_t(need), p0, nc, live_row, cc, k5, cfg) && lane == 0) {
+    uint32_t p = p0;
+    for (int k = 0; k < nc; ++k) {
+      const uint32_t f = ((p < uint32_t(need) ? dw[p] : dec(stream_u64_at(k5, p))) >> AttrDecider::kWeight) & 3u;
+      ++p;
+      if (f) {
+        double* w = cc + size_t(live_row[k]) * kConnCols + kW;
+        *w = apply_scalar(*w, (p << 2) | ((f & 1u) ? 1u : 2u), k5, cfg.w_power, cfg.w_mean, cfg.w_std);
         p += 2;
-        return a;
-      };
-      auto index = [&](int acc_bit, int val_shift) -> int {  // below(n), rng.hpp:99-106
-        for (;;) {
-          const uint32_t f = word(p++);
-          if ((f >> acc_bit) & 1u) return int((f >> val_shift) & 7u);
-        }
-      };
-      for (int q = 0; q < N; ++q) {
-        uint32_t ab = 0u, ar = 0u;
-        int ag = -1, ac = -1;
-        if ((sm.nflag[q] & 3) == 1) {
-          ab = scalar(AttrDecider::kBias);
-          ar = scalar(AttrDecider::kResp);
-          if (cfg.agg_rate > 0.0 && ((word(p++) >> AttrDecider::kAggCoin) & 1u))
-            ag = index(AttrDecider::kAggAcc, AttrDecider::kAggVal);
-          if (cfg.act_rate > 0.0 && ((word(p++) >> AttrDecider::kActCoin) & 1u))
-            ac = index(AttrDecider::kActAcc, AttrDecider::kActVal);
-        }
-        sm.act_n[2 * q] = ab;
-        sm.act_n[2 * q + 1] = ar;
-        sm.new_agg[q] = int8_t(ag);
-        sm.new_act[q] = int8_t(ac);
       }
-      p_nodes_end = p;
-    }
-    // connection weights: nc scalars from position p0, walked in parallel
-    // (conn_walk); the sequential chase is kept for windows that are too short
-    const uint32_t p0 = __shfl_sync(kFullMask, p_nodes_end, 0);
-    uint32_t* tmp = reinterpret_cast<uint32_t*>(dw + ((need + 1) & ~1));  // [nc] codes by visit index
-    const bool tmp_fits = uint32_t((need + 1) & ~1) * 2u + 4u * uint32_t(nc) <= uint32_t(cap) * 2u;
-    if (!tmp_fits || !conn_walk(dw, uint32_t(need), p0, nc, tmp, sm.cflag, sm.act_c, C)) {
-      if (lane == 0) {
-        uint32_t p = p0;
-        for (int q = 0; q < C; ++q) {
-          uint32_t a = 0u;
-          if (sm.cflag[q] & 1) {
-            const uint32_t f = ((p < uint32_t(need) ? dw[p] : dec(stream_u64_at(k5, p))) >> AttrDecider::kWeight) & 3u;
-            ++p;
-            if (f) {
-              a = (p << 2) | ((f & 1u) ? 1u : 2u);
-              p += 2;
-            }
-          }
-          sm.act_c[q] = a;
-        }
-      }
-    }
-    __syncwarp();
-    for (int q = lane; q < N; q += 32) {
-      const uint32_t ab = sm.act_n[2 * q], ar = sm.act_n[2 * q + 1];
-      if (ab) n[q * kNodeCols + kBias] = apply_scalar(n[q * kNodeCols + kBias], ab, k5, cfg.b_power, cfg.b_mean, cfg.b_std);
-      if (ar) n[q * kNodeCols + kResp] = apply_scalar(n[q * kNodeCols + kResp], ar, k5, cfg.r_power, cfg.r_mean, cfg.r_std);
-      if (sm.new_agg[q] >= 0) n[q * kNodeCols + kAgg] = double(sm.new_agg[q]);
-      if (sm.new_act[q] >= 0) n[q * kNodeCols + kAct] = double(sm.new_act[q]);
-    }
-    for (int q = lane; q < C; q += 32) {
-      const uint32_t aw = sm.act_c[q];
-      if (aw) cc[q * kConnCols + kW] = apply_scalar(cc[q * kConnCols + kW], aw, k5, cfg.w_power, cfg.w_mean, cfg.w_std);
     }
   }
-  if (lane == 0) status[c] = st;
+  __syncwarp();
+  for (int q = lane; q < N; q += 32) {
+    const uint32_t ab = act_n[2 * q], ar = act_n[2 * q + 1];
+    if (ab) n[q * kNodeCols + kBias] = apply_scalar(n[q * kNodeCols + kBias], ab, k5, cfg.b_power, cfg.b_mean, cfg.b_std);
+    if (ar) n[q * kNodeCols + kResp] = apply_scalar(n[q * kNodeCols + kResp], ar, k5, cfg.r_power, cfg.r_mean, cfg.r_std);
+    if (new_id[q] >= 0) n[q * kNodeCols + kAgg] = double(new_id[q]);
+    if (new_id[N + q] >= 0) n[q * kNodeCols + kAct] = double(new_id[N + q]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -779,7 +791,15 @@ cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, in
   if (e != cudaSuccess) return e;
   k_mutate_apply<<<(n + warps - 1) / warps, 32 * warps, per_warp * warps, st>>>(
       nodes, conns, keys, n, active, N, C, cfg, sh, flag, pair, newk, d_status, per_warp);
-  *launches += 7;
+  const int win = attr_window(N, C, attr_per_node(cfg));
+  const size_t aw = attr_smem_bytes(N, C, win);
+  int awarps = 8;
+  while (awarps > 1 && aw * awarps > 96 * 1024) awarps >>= 1;
+  e = cudaFuncSetAttribute(k_mutate_attrs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(aw * awarps));
+  if (e != cudaSuccess) return e;
+  k_mutate_attrs<<<(n + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nodes, conns, keys, n, active, d_status,
+                                                                             N, C, cfg, sh, win, aw);
+  *launches += 8;
   return cudaGetLastError();
 }
 

@@ -73,3 +73,16 @@ def xor_dataset(bias_input: bool = False):
         X = np.concatenate([X, np.ones((4, 1))], axis=1)
     Y = np.array([[0], [1], [1], [0]], dtype=np.float64)
     return X, Y
+
+
+def cppn_dataset(side: int = 256):
+    """C3: CPPN queries over a side x side grid -- inputs
+    (x, y, r = sqrt(x^2 + y^2), bias = 1) with x, y in [-1, 1] -- and a fixed
+    target image (concentric rings) for the image-MSE fitness.  Returns
+    (X [side^2, 4], Y [side^2, 1]) as float64."""
+    t = np.linspace(-1.0, 1.0, side)
+    yy, xx = np.meshgrid(t, t, indexing="ij")
+    r = np.sqrt(xx * xx + yy * yy)
+    X = np.stack([xx.ravel(), yy.ravel(), r.ravel(), np.ones(side * side)], axis=1)
+    Y = (0.5 + 0.5 * np.cos(8.0 * np.pi * r)).reshape(-1, 1)
+    return X, Y
