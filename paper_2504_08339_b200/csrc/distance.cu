@@ -13,18 +13,14 @@
 
 namespace fnb {
 
-__host__ inline size_t rep_tables_bytes(int S, int N, int C) {
-  const size_t hn = size_t(table_capacity(N)), hc = size_t(table_capacity(C));
-  return size_t(S) * (hn * 12 + hc * 12 + 8) + 64;
-}
+__host__ inline size_t rep_tables_bytes(int S, int N, int C) { return size_t(S) * rep_table_bytes_one(N, C) + 64; }
 
 // one CTA per representative
 __global__ void k_rep_tables(const double* __restrict__ rn, const double* __restrict__ rc, int N, int C,
                              RepTables t) {
   const int s = blockIdx.x;
-  rep_table_build(rn + size_t(s) * N * kNodeCols, rc + size_t(s) * C * kConnCols, N, C, t.nkeys + size_t(s) * t.Hn,
-                  t.nrows + size_t(s) * t.Hn, t.Hn, t.ckeys + size_t(s) * t.Hc, t.crows + size_t(s) * t.Hc, t.Hc,
-                  t.counts + 2 * s);
+  rep_table_build(rn + size_t(s) * N * kNodeCols, rc + size_t(s) * C * kConnCols, N, C, t.n + size_t(s) * t.Hn, t.Hn,
+                  t.c + size_t(s) * t.Hc, t.crow + size_t(s) * t.Hc, t.Hc, t.counts + 2 * s);
 }
 
 // one warp per genome
@@ -42,7 +38,7 @@ k_distance(const double* __restrict__ nodes, const double* __restrict__ conns, i
   if (only_unassigned && only_unassigned[g] >= 0) return;
   if (after_founder && (after_founder[0] < 0 || g <= after_founder[0])) return;
   double* tile = reinterpret_cast<double*>(smem_raw) + size_t(warp) * S * 33;
-  distance_warp(nodes + size_t(g) * N * kNodeCols, conns + size_t(g) * C * kConnCols, rn, rc, S, t, N, C, cd, ch,
+  distance_warp(nodes + size_t(g) * N * kNodeCols, conns + size_t(g) * C * kConnCols, rn, S, t, N, C, cd, ch,
                 tile, out + size_t(g) * S);
 }
 
@@ -68,10 +64,10 @@ cudaError_t launch_distance_masked(const double* nodes, const double* conns, int
   t.Hn = table_capacity(N);
   t.Hc = table_capacity(C);
   uint8_t* p = static_cast<uint8_t*>(scratch);
-  t.nkeys = reinterpret_cast<unsigned long long*>(p); p += size_t(S) * t.Hn * 8;
-  t.ckeys = reinterpret_cast<unsigned long long*>(p); p += size_t(S) * t.Hc * 8;
-  t.nrows = reinterpret_cast<int*>(p); p += size_t(S) * t.Hn * 4;
-  t.crows = reinterpret_cast<int*>(p); p += size_t(S) * t.Hc * 4;
+  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  t.n = reinterpret_cast<NSlot*>(p); p += size_t(S) * t.Hn * sizeof(NSlot);
+  t.c = reinterpret_cast<CSlot*>(p); p += size_t(S) * t.Hc * sizeof(CSlot);
+  t.crow = reinterpret_cast<int*>(p); p += size_t(S) * t.Hc * 4;
   t.counts = reinterpret_cast<int*>(p); p += size_t(S) * 8;
   if (size_t(p - static_cast<uint8_t*>(scratch)) > scratch_bytes) return cudaErrorInvalidValue;
   k_rep_tables<<<S, 256, 0, st>>>(rn, rc, N, C, t);
