@@ -66,8 +66,10 @@ def main():
         assert same, ("fitness bits changed with the launch geometry", spt, cols, pct, kb)
     lib.fnb_set_forward_tuning(0, 0, 0, 0)
     ok = sorted([r for r in res if "ms" in r], key=lambda r: r["ms"])
-    print(json.dumps({"default_ms": base_ms, "best": ok[:12], "errors": [r for r in res if "error" in r][:5],
-                      "n": len(res)}, indent=1))
+    best_by_spt = {spt: min((r for r in ok if r["spt"] == spt), key=lambda r: r["ms"], default=None)
+                   for spt in (1, 2, 4)}
+    print(json.dumps({"default_ms": base_ms, "best": ok[:12], "best_by_spt": best_by_spt,
+                      "errors": [r for r in res if "error" in r][:5], "n": len(res)}, indent=1))
 
 
 if __name__ == "__main__":
