@@ -10,97 +10,51 @@
 
 namespace fnb {
 
-constexpr int kLookupBatch = 8;  // representatives whose first probes are issued together
-
-// Representative tables: open addressing, power-of-two capacity, hash_key
-// (keytable.cuh).  A slot is 16 bytes so one load answers a probe:
-//   node slot  {key, lowest row}          (attributes read from the rep row)
-//   conn slot  {key, weight of the lowest row holding the pair}
-// (the reference's find_* scans return the first matching row,
-// genome.hpp:195-210).  A row's probe start is the same in every
-// representative's table, so lookups for several representatives are issued
-// together.
-struct NSlot {
-  unsigned long long key;
-  int row;
-  int pad;
-};
-struct CSlot {
-  unsigned long long key;
-  double w;
-};
-static_assert(sizeof(NSlot) == 16 && sizeof(CSlot) == 16, "16-byte table slots");
-
 struct RepTables {
-  NSlot* n;      // [S][Hn]
-  CSlot* c;      // [S][Hc]
-  int* crow;     // [S][Hc] build scratch: lowest conn row per slot
-  int* counts;   // [S][2] non-empty node / conn rows
+  unsigned long long* nkeys;  // [S][Hn]
+  int* nrows;
+  unsigned long long* ckeys;  // [S][Hc]
+  int* crows;
+  int* counts;                // [S][2] non-empty node / conn rows
   int Hn, Hc;
+  // connection-key Bloom filters (one hash bit per key), [S][1 << fw_log2]
+  // words; k_distance reads a shared-memory copy.  null = no filter.
+  const uint32_t* filt;
+  int fw_log2;
 };
 
-__host__ __device__ inline size_t rep_table_bytes_one(int N, int C) {
-  return size_t(table_capacity(N)) * sizeof(NSlot) + size_t(table_capacity(C)) * (sizeof(CSlot) + 4) + 16;
+// filter bit of a key: the hash's high bits (the tables probe from the low
+// bits), so a miss in the filter is a miss in the table
+__device__ __forceinline__ uint32_t filter_bit(unsigned long long key, int fw_log2) {
+  return hash_key(key) >> (32 - (fw_log2 + 5));
 }
+__device__ __forceinline__ bool filter_has(const uint32_t* f, uint32_t b) { return (f[b >> 5] >> (b & 31)) & 1u; }
 
-// Marker tables of one representative (n, c) by the whole CTA (global or
-// shared memory).  Ends with __syncthreads().
+// Marker tables of one representative (n, c) by the whole CTA.  Ends with
+// __syncthreads(); `counts` receives the non-empty node / conn row counts.
 __device__ inline void rep_table_build(const double* __restrict__ n, const double* __restrict__ c, int N, int C,
-                                       NSlot* ns, int Hn, CSlot* cs, int* crow, int Hc, int* counts) {
+                                       unsigned long long* nk, int* nr, int Hn, unsigned long long* ck, int* cr,
+                                       int Hc, int* counts) {
   __shared__ int cnt[2];
-  for (int i = threadIdx.x; i < Hn; i += blockDim.x) ns[i] = NSlot{kEmptyKey, 0x7fffffff, 0};
-  for (int i = threadIdx.x; i < Hc; i += blockDim.x) {
-    cs[i] = CSlot{kEmptyKey, 0.0};
-    crow[i] = 0x7fffffff;
-  }
+  for (int i = threadIdx.x; i < Hn; i += blockDim.x) { nk[i] = kEmptyKey; nr[i] = 0x7fffffff; }
+  for (int i = threadIdx.x; i < Hc; i += blockDim.x) { ck[i] = kEmptyKey; cr[i] = 0x7fffffff; }
   if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
   __syncthreads();
   for (int r = threadIdx.x; r < N; r += blockDim.x) {
     const double k = n[r * kNodeCols + kKey];
     if (isnan(k)) continue;
-    const unsigned long long key = node_key(k);
-    uint32_t s = hash_key(key) & uint32_t(Hn - 1);
-    for (;;) {
-      const unsigned long long prev = atomicCAS(&ns[s].key, kEmptyKey, key);
-      if (prev == kEmptyKey || prev == key) {
-        atomicMin(&ns[s].row, r);
-        break;
-      }
-      s = (s + 1) & uint32_t(Hn - 1);
-    }
+    table_insert(nk, nr, Hn - 1, node_key(k), r);
     atomicAdd(&cnt[0], 1);
   }
   for (int r = threadIdx.x; r < C; r += blockDim.x) {
     const double in = c[r * kConnCols + kIn];
     if (isnan(in)) continue;
-    const unsigned long long key = conn_key(in, c[r * kConnCols + kOut]);
-    uint32_t s = hash_key(key) & uint32_t(Hc - 1);
-    for (;;) {
-      const unsigned long long prev = atomicCAS(&cs[s].key, kEmptyKey, key);
-      if (prev == kEmptyKey || prev == key) {
-        atomicMin(&crow[s], r);
-        break;
-      }
-      s = (s + 1) & uint32_t(Hc - 1);
-    }
+    table_insert(ck, cr, Hc - 1, conn_key(in, c[r * kConnCols + kOut]), r);
     atomicAdd(&cnt[1], 1);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < Hc; i += blockDim.x)
-    if (cs[i].key != kEmptyKey) cs[i].w = c[crow[i] * kConnCols + kW];
   if (threadIdx.x < 2) counts[threadIdx.x] = cnt[threadIdx.x];
   __syncthreads();
-}
-
-// continue a probe sequence whose first slot `x` (at `pos`) was already loaded
-template <class Slot>
-__device__ __forceinline__ bool probe_rest(const Slot* tab, uint32_t mask, uint32_t pos, unsigned long long key,
-                                           Slot& x) {
-  while (x.key != key && x.key != kEmptyKey) {
-    pos = (pos + 1) & mask;
-    x = tab[pos];
-  }
-  return x.key == key;
 }
 
 // One warp: distance(genome (gn, gc), rep s) for s < S (<= 32); lane s
@@ -116,7 +70,7 @@ __device__ __forceinline__ bool probe_rest(const Slot* tab, uint32_t mask, uint3
 // distance(genome, representative) is kept: 7% of random pairs are bitwise
 // asymmetric.
 __device__ inline void distance_warp(const double* __restrict__ gn, const double* __restrict__ gc,
-                                     const double* __restrict__ rn, int S,
+                                     const double* __restrict__ rn, const double* __restrict__ rc, int S,
                                      const RepTables& t, int N, int C, double cd, double ch, double* tile,
                                      double* out) {
   const int lane = threadIdx.x & 31;
@@ -128,31 +82,19 @@ __device__ inline void distance_warp(const double* __restrict__ gn, const double
     const double k = r < N ? a[kKey] : __longlong_as_double(0x7ff8000000000000ll);
     const bool ne = !isnan(k);
     n1 += __popc(__ballot_sync(0xffffffffu, ne));
-    const unsigned long long key = ne ? node_key(k) : 0ull;
-    const uint32_t h = hash_key(key) & uint32_t(t.Hn - 1);
-    for (int s0 = 0; s0 < S; s0 += kLookupBatch) {
-      NSlot x[kLookupBatch];
-#pragma unroll
-      for (int i = 0; i < kLookupBatch; ++i)
-        if (ne && s0 + i < S) x[i] = t.n[size_t(s0 + i) * t.Hn + h];
-#pragma unroll
-      for (int i = 0; i < kLookupBatch; ++i) {
-        const int s = s0 + i;
-        if (s >= S) break;  // warp-uniform
-        int q = -1;
-        if (ne && probe_rest(t.n + size_t(s) * t.Hn, uint32_t(t.Hn - 1), h, key, x[i])) q = x[i].row;
-        double v = 0.0;
-        if (q >= 0) {
-          const double* b = rn + size_t(s) * N * kNodeCols + size_t(q) * kNodeCols;
-          double d = __dadd_rn(fabs(__dsub_rn(a[kBias], b[kBias])), fabs(__dsub_rn(a[kResp], b[kResp])));
-          d = __dadd_rn(d, a[kAgg] != b[kAgg] ? 1.0 : 0.0);
-          d = __dadd_rn(d, a[kAct] != b[kAct] ? 1.0 : 0.0);
-          v = __ddiv_rn(d, 4.0);
-        }
-        const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
-        if (lane == s) mn += m;
-        tile[s * 33 + lane] = v;
+    for (int s = 0; s < S; ++s) {
+      const int q = ne ? table_find(t.nkeys + size_t(s) * t.Hn, t.nrows + size_t(s) * t.Hn, t.Hn - 1, node_key(k)) : -1;
+      double v = 0.0;
+      if (q >= 0) {
+        const double* b = rn + size_t(s) * N * kNodeCols + size_t(q) * kNodeCols;
+        double d = __dadd_rn(fabs(__dsub_rn(a[kBias], b[kBias])), fabs(__dsub_rn(a[kResp], b[kResp])));
+        d = __dadd_rn(d, a[kAgg] != b[kAgg] ? 1.0 : 0.0);
+        d = __dadd_rn(d, a[kAct] != b[kAct] ? 1.0 : 0.0);
+        v = __ddiv_rn(d, 4.0);
       }
+      const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
+      if (lane == s) mn += m;
+      tile[s * 33 + lane] = v;
     }
     __syncwarp();
     if (lane < S) {
@@ -173,22 +115,15 @@ __device__ inline void distance_warp(const double* __restrict__ gn, const double
     if (ne) w = gc[size_t(r) * kConnCols + kW];
     c1 += __popc(__ballot_sync(0xffffffffu, ne));
     const unsigned long long key = ne ? conn_key(in, o) : 0ull;
-    const uint32_t h = hash_key(key) & uint32_t(t.Hc - 1);
-    for (int s0 = 0; s0 < S; s0 += kLookupBatch) {
-      CSlot x[kLookupBatch];
-#pragma unroll
-      for (int i = 0; i < kLookupBatch; ++i)
-        if (ne && s0 + i < S) x[i] = t.c[size_t(s0 + i) * t.Hc + h];
-#pragma unroll
-      for (int i = 0; i < kLookupBatch; ++i) {
-        const int s = s0 + i;
-        if (s >= S) break;  // warp-uniform
-        const bool hit = ne && probe_rest(t.c + size_t(s) * t.Hc, uint32_t(t.Hc - 1), h, key, x[i]);
-        const double v = hit ? __ddiv_rn(fabs(__dsub_rn(w, x[i].w)), 1.0) : 0.0;
-        const int m = __popc(__ballot_sync(0xffffffffu, hit));
-        if (lane == s) mc += m;
-        tile[s * 33 + lane] = v;
-      }
+    const uint32_t fb = filter_bit(key, t.fw_log2);
+    for (int s = 0; s < S; ++s) {
+      const bool maybe = ne && (!t.filt || filter_has(t.filt + (size_t(s) << t.fw_log2), fb));
+      const int q = maybe ? table_find(t.ckeys + size_t(s) * t.Hc, t.crows + size_t(s) * t.Hc, t.Hc - 1, key) : -1;
+      double v = 0.0;
+      if (q >= 0) v = __ddiv_rn(fabs(__dsub_rn(w, rc[size_t(s) * C * kConnCols + size_t(q) * kConnCols + kW])), 1.0);
+      const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
+      if (lane == s) mc += m;
+      tile[s * 33 + lane] = v;
     }
     __syncwarp();
     if (lane < S) {

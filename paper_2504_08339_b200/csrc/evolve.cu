@@ -170,10 +170,11 @@ __global__ void __launch_bounds__(128) k_found_rounds(SpeciesDev* sd, int S_old,
                                                       double cd, double ch, int Hn, int Hc) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  NSlot* ns = reinterpret_cast<NSlot*>(smem_raw);
-  CSlot* cs = reinterpret_cast<CSlot*>(ns + Hn);
-  int* crow = reinterpret_cast<int*>(cs + Hc);
-  int* counts = crow + Hc;                                        // 2 ints (+2 pad)
+  unsigned long long* nk = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned long long* ck = nk + Hn;
+  int* nr = reinterpret_cast<int*>(ck + Hc);
+  int* cr = nr + Hn;
+  int* counts = cr + Hc;                                          // 2 ints (+2 pad)
   double* dist_w = reinterpret_cast<double*>(counts + 4);         // one per warp
   const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* tile = dist_w + warps + size_t(warp) * 33;  // distance_warp scratch (S = 1)
@@ -200,11 +201,11 @@ __global__ void __launch_bounds__(128) k_found_rounds(SpeciesDev* sd, int S_old,
       for (size_t i = threadIdx.x; i < gn; i += blockDim.x) rep_n[size_t(j) * gn + i] = fn[i];
       for (size_t i = threadIdx.x; i < gc; i += blockDim.x) rep_c[size_t(j) * gc + i] = fc[i];
     }
-    rep_table_build(fn, fc, N, C, ns, Hn, cs, crow, Hc, counts);
-    const RepTables t{ns, cs, crow, counts, Hn, Hc};
+    rep_table_build(fn, fc, N, C, nk, nr, Hn, ck, cr, Hc, counts);
+    const RepTables t{nk, nr, ck, cr, counts, Hn, Hc, nullptr, 0};
     for (int g = gw; g < P; g += nw) {
       if (g <= f || __ldcg(species_of + g) >= 0) continue;  // warp-uniform
-      distance_warp(pn + size_t(g) * gn, pc + size_t(g) * gc, fn, 1, t, N, C, cd, ch, tile, dist_w + warp);
+      distance_warp(pn + size_t(g) * gn, pc + size_t(g) * gc, fn, fc, 1, t, N, C, cd, ch, tile, dist_w + warp);
       __syncwarp();
       if (lane == 0) {
         if (dist_w[warp] < th) species_of[g] = j;
@@ -622,8 +623,7 @@ struct Evolver {
   cudaError_t launch_found_rounds(int S_old, const double* n, const double* c) {
     int Hn = table_capacity(N), Hc = table_capacity(C);
     const int block = 128;
-    const size_t smem = size_t(Hn) * sizeof(NSlot) + size_t(Hc) * (sizeof(CSlot) + 4) + 16 + (block / 32) * 8 +
-                        (block / 32) * 33 * 8;
+    const size_t smem = size_t(Hn + Hc) * 12 + 16 + (block / 32) * 8 + (block / 32) * 33 * 8;
     cudaError_t e = cudaFuncSetAttribute(k_found_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     if (coop_blocks == 0) {
