@@ -301,6 +301,12 @@ struct AttrDecider {
   }
 };
 
+// decision word of a position past the window (only below() rejections get
+// there); out of line so the hot chase compiles to a plain branch
+__device__ __noinline__ uint32_t slow_word(const Key4& k5, uint32_t q, const AttrDecider& dec) {
+  return dec(stream_u64_at(k5, q));
+}
+
 // The connection-weight part of the split(5) walk in parallel.  Each live
 // connection is one mutate_scalar: at its position p it consumes p and, when
 // the weight bits of word p trigger, the two draws of a normal.  As an
@@ -688,7 +694,7 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   uint32_t p_nodes_end = 0;
   if (lane == 0) {  // node attributes: lane 0 chases the decision words in row order
     uint32_t p = 0;
-    auto word = [&](uint32_t q) -> uint32_t { return q < uint32_t(need) ? dw[q] : dec(stream_u64_at(k5, q)); };
+    auto word = [&](uint32_t q) -> uint32_t { return q < uint32_t(need) ? uint32_t(dw[q]) : slow_word(k5, q, dec); };
     auto scalar = [&](int sh_) -> uint32_t {  // mutate_scalar (ops.hpp:281-289): action code
       const uint32_t f = (word(p++) >> sh_) & 3u;
       if (!f) return 0u;
@@ -725,7 +731,7 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   if (!conn_walk(dw, uint32_t(need), p0, nc, live_row, cc, k5, cfg) && lane == 0) {
     uint32_t p = p0;
     for (int k = 0; k < nc; ++k) {
-      const uint32_t f = ((p < uint32_t(need) ? dw[p] : dec(stream_u64_at(k5, p))) >> AttrDecider::kWeight) & 3u;
+      const uint32_t f = ((p < uint32_t(need) ? uint32_t(dw[p]) : slow_word(k5, p, dec)) >> AttrDecider::kWeight) & 3u;
       ++p;
       if (f) {
         double* w = cc + size_t(live_row[k]) * kConnCols + kW;
