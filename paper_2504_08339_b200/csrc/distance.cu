@@ -15,18 +15,19 @@
 
 namespace fnb {
 
-// Bloom filter words per representative (log2): about 32 bits per connection
-// key (false positives ~3%), within a 48 KB shared-memory budget for S reps.
+// Bloom filter words per representative (log2): about 16 bits per connection
+// key (false positives ~6%), within a 24 KB shared-memory budget for S reps
+// (the rest of the SM's shared memory keeps the warps in flight).
 __host__ inline int filter_words_log2(int S, int C) {
   int lg = 5;  // 32 words = 1024 bits minimum
-  while (lg < 11 && (size_t(1) << (lg + 5)) < size_t(32) * C) ++lg;
-  while (lg > 5 && size_t(S) * (size_t(4) << lg) > 48 * 1024) --lg;
+  while (lg < 11 && (size_t(1) << (lg + 5)) < size_t(16) * C) ++lg;
+  while (lg > 5 && size_t(S) * (size_t(4) << lg) > 24 * 1024) --lg;
   return lg;
 }
 
 __host__ inline size_t rep_tables_bytes(int S, int N, int C) {
   const size_t hn = size_t(table_capacity(N)), hc = size_t(table_capacity(C));
-  return size_t(S) * (hn * 12 + hc * 12 + 8 + (size_t(4) << filter_words_log2(S, C))) + 64;
+  return size_t(S) * (hn * 12 + hc * 20 + 8 + (size_t(4) << filter_words_log2(S, C))) + 64;
 }
 
 // one CTA per representative: marker tables + the connection-key filter
@@ -43,8 +44,8 @@ __global__ void k_rep_tables(const double* __restrict__ rn, const double* __rest
     const uint32_t b = filter_bit(conn_key(in, cr[r * kConnCols + kOut]), t.fw_log2);
     atomicOr(&f[b >> 5], 1u << (b & 31));
   }
-  rep_table_build(rn + size_t(s) * N * kNodeCols, rc + size_t(s) * C * kConnCols, N, C, t.nkeys + size_t(s) * t.Hn,
-                  t.nrows + size_t(s) * t.Hn, t.Hn, t.ckeys + size_t(s) * t.Hc, t.crows + size_t(s) * t.Hc, t.Hc,
+  rep_table_build(rn + size_t(s) * N * kNodeCols, cr, N, C, t.nkeys + size_t(s) * t.Hn, t.nrows + size_t(s) * t.Hn,
+                  t.Hn, t.ckeys + size_t(s) * t.Hc, t.crows + size_t(s) * t.Hc, t.cw + size_t(s) * t.Hc, t.Hc,
                   t.counts + 2 * s);
 }
 
@@ -101,6 +102,7 @@ cudaError_t launch_distance_masked(const double* nodes, const double* conns, int
   t.nkeys = reinterpret_cast<unsigned long long*>(p); p += size_t(S) * t.Hn * 8;
   t.ckeys = reinterpret_cast<unsigned long long*>(p); p += size_t(S) * t.Hc * 8;
   t.nrows = reinterpret_cast<int*>(p); p += size_t(S) * t.Hn * 4;
+  t.cw = reinterpret_cast<double*>(p); p += size_t(S) * t.Hc * 8;
   t.crows = reinterpret_cast<int*>(p); p += size_t(S) * t.Hc * 4;
   t.counts = reinterpret_cast<int*>(p); p += size_t(S) * 8;
   t.fw_log2 = filter_words_log2(S, C);

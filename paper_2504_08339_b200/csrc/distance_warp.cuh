@@ -15,6 +15,7 @@ struct RepTables {
   int* nrows;
   unsigned long long* ckeys;  // [S][Hc]
   int* crows;
+  double* cw;                 // [S][Hc] weight of the slot's (lowest) row: a hit needs no row load
   int* counts;                // [S][2] non-empty node / conn rows
   int Hn, Hc;
   // connection-key Bloom filters (one hash bit per key), [S][1 << fw_log2]
@@ -30,11 +31,23 @@ __device__ __forceinline__ uint32_t filter_bit(unsigned long long key, int fw_lo
 }
 __device__ __forceinline__ bool filter_has(const uint32_t* f, uint32_t b) { return (f[b >> 5] >> (b & 31)) & 1u; }
 
+constexpr int kLookupBatch = 8;  // representatives whose first probes are issued together
+
+// slot of `key` in a table whose first probe (at `pos`) already returned k0
+__device__ __forceinline__ int probe_from(const unsigned long long* keys, int mask, uint32_t pos,
+                                          unsigned long long k0, unsigned long long key) {
+  while (k0 != key && k0 != kEmptyKey) {
+    pos = (pos + 1) & uint32_t(mask);
+    k0 = keys[pos];
+  }
+  return k0 == key ? int(pos) : -1;
+}
+
 // Marker tables of one representative (n, c) by the whole CTA.  Ends with
 // __syncthreads(); `counts` receives the non-empty node / conn row counts.
 __device__ inline void rep_table_build(const double* __restrict__ n, const double* __restrict__ c, int N, int C,
                                        unsigned long long* nk, int* nr, int Hn, unsigned long long* ck, int* cr,
-                                       int Hc, int* counts) {
+                                       double* cw, int Hc, int* counts) {
   __shared__ int cnt[2];
   for (int i = threadIdx.x; i < Hn; i += blockDim.x) { nk[i] = kEmptyKey; nr[i] = 0x7fffffff; }
   for (int i = threadIdx.x; i < Hc; i += blockDim.x) { ck[i] = kEmptyKey; cr[i] = 0x7fffffff; }
@@ -53,6 +66,7 @@ __device__ inline void rep_table_build(const double* __restrict__ n, const doubl
     atomicAdd(&cnt[1], 1);
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < Hc; i += blockDim.x) cw[i] = ck[i] != kEmptyKey ? c[cr[i] * kConnCols + kW] : 0.0;
   if (threadIdx.x < 2) counts[threadIdx.x] = cnt[threadIdx.x];
   __syncthreads();
 }
@@ -82,19 +96,31 @@ __device__ inline void distance_warp(const double* __restrict__ gn, const double
     const double k = r < N ? a[kKey] : __longlong_as_double(0x7ff8000000000000ll);
     const bool ne = !isnan(k);
     n1 += __popc(__ballot_sync(0xffffffffu, ne));
-    for (int s = 0; s < S; ++s) {
-      const int q = ne ? table_find(t.nkeys + size_t(s) * t.Hn, t.nrows + size_t(s) * t.Hn, t.Hn - 1, node_key(k)) : -1;
-      double v = 0.0;
-      if (q >= 0) {
-        const double* b = rn + size_t(s) * N * kNodeCols + size_t(q) * kNodeCols;
-        double d = __dadd_rn(fabs(__dsub_rn(a[kBias], b[kBias])), fabs(__dsub_rn(a[kResp], b[kResp])));
-        d = __dadd_rn(d, a[kAgg] != b[kAgg] ? 1.0 : 0.0);
-        d = __dadd_rn(d, a[kAct] != b[kAct] ? 1.0 : 0.0);
-        v = __ddiv_rn(d, 4.0);
+    const unsigned long long key = ne ? node_key(k) : 0ull;
+    const uint32_t h = hash_key(key) & uint32_t(t.Hn - 1);
+    for (int s0 = 0; s0 < S; s0 += kLookupBatch) {
+      unsigned long long k0[kLookupBatch];
+#pragma unroll
+      for (int i = 0; i < kLookupBatch; ++i)  // first probes of several reps in flight
+        k0[i] = (ne && s0 + i < S) ? t.nkeys[size_t(s0 + i) * t.Hn + h] : kEmptyKey;
+#pragma unroll
+      for (int i = 0; i < kLookupBatch; ++i) {
+        const int s = s0 + i;
+        if (s >= S) break;  // warp-uniform
+        const int slot = ne ? probe_from(t.nkeys + size_t(s) * t.Hn, t.Hn - 1, h, k0[i], key) : -1;
+        const int q = slot >= 0 ? t.nrows[size_t(s) * t.Hn + slot] : -1;
+        double v = 0.0;
+        if (q >= 0) {
+          const double* b = rn + size_t(s) * N * kNodeCols + size_t(q) * kNodeCols;
+          double d = __dadd_rn(fabs(__dsub_rn(a[kBias], b[kBias])), fabs(__dsub_rn(a[kResp], b[kResp])));
+          d = __dadd_rn(d, a[kAgg] != b[kAgg] ? 1.0 : 0.0);
+          d = __dadd_rn(d, a[kAct] != b[kAct] ? 1.0 : 0.0);
+          v = __ddiv_rn(d, 4.0);
+        }
+        const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
+        if (lane == s) mn += m;
+        tile[s * 33 + lane] = v;
       }
-      const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
-      if (lane == s) mn += m;
-      tile[s * 33 + lane] = v;
     }
     __syncwarp();
     if (lane < S) {
@@ -116,14 +142,27 @@ __device__ inline void distance_warp(const double* __restrict__ gn, const double
     c1 += __popc(__ballot_sync(0xffffffffu, ne));
     const unsigned long long key = ne ? conn_key(in, o) : 0ull;
     const uint32_t fb = filter_bit(key, t.fw_log2);
-    for (int s = 0; s < S; ++s) {
-      const bool maybe = ne && (!t.filt || filter_has(t.filt + (size_t(s) << t.fw_log2), fb));
-      const int q = maybe ? table_find(t.ckeys + size_t(s) * t.Hc, t.crows + size_t(s) * t.Hc, t.Hc - 1, key) : -1;
-      double v = 0.0;
-      if (q >= 0) v = __ddiv_rn(fabs(__dsub_rn(w, rc[size_t(s) * C * kConnCols + size_t(q) * kConnCols + kW])), 1.0);
-      const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
-      if (lane == s) mc += m;
-      tile[s * 33 + lane] = v;
+    const uint32_t h = hash_key(key) & uint32_t(t.Hc - 1);
+    for (int s0 = 0; s0 < S; s0 += kLookupBatch) {
+      unsigned long long k0[kLookupBatch];
+      uint32_t maybe = 0u;
+#pragma unroll
+      for (int i = 0; i < kLookupBatch; ++i) {  // filter tests, then first probes in flight
+        const int s = s0 + i;
+        const bool m = ne && s < S && (!t.filt || filter_has(t.filt + (size_t(s) << t.fw_log2), fb));
+        maybe |= uint32_t(m) << i;
+        k0[i] = m ? t.ckeys[size_t(s) * t.Hc + h] : kEmptyKey;
+      }
+#pragma unroll
+      for (int i = 0; i < kLookupBatch; ++i) {
+        const int s = s0 + i;
+        if (s >= S) break;  // warp-uniform
+        const int slot = ((maybe >> i) & 1u) ? probe_from(t.ckeys + size_t(s) * t.Hc, t.Hc - 1, h, k0[i], key) : -1;
+        const double v = slot >= 0 ? __ddiv_rn(fabs(__dsub_rn(w, t.cw[size_t(s) * t.Hc + slot])), 1.0) : 0.0;
+        const int m = __popc(__ballot_sync(0xffffffffu, slot >= 0));
+        if (lane == s) mc += m;
+        tile[s * 33 + lane] = v;
+      }
     }
     __syncwarp();
     if (lane < S) {

@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(128) k_found_rounds(SpeciesDev* sd, int S_old,
   extern __shared__ __align__(16) uint8_t smem_raw[];
   unsigned long long* nk = reinterpret_cast<unsigned long long*>(smem_raw);
   unsigned long long* ck = nk + Hn;
-  int* nr = reinterpret_cast<int*>(ck + Hc);
+  double* cw = reinterpret_cast<double*>(ck + Hc);
+  int* nr = reinterpret_cast<int*>(cw + Hc);
   int* cr = nr + Hn;
   int* counts = cr + Hc;                                          // 2 ints (+2 pad)
   double* dist_w = reinterpret_cast<double*>(counts + 4);         // one per warp
@@ -201,8 +202,8 @@ __global__ void __launch_bounds__(128) k_found_rounds(SpeciesDev* sd, int S_old,
       for (size_t i = threadIdx.x; i < gn; i += blockDim.x) rep_n[size_t(j) * gn + i] = fn[i];
       for (size_t i = threadIdx.x; i < gc; i += blockDim.x) rep_c[size_t(j) * gc + i] = fc[i];
     }
-    rep_table_build(fn, fc, N, C, nk, nr, Hn, ck, cr, Hc, counts);
-    const RepTables t{nk, nr, ck, cr, counts, Hn, Hc, nullptr, 0};
+    rep_table_build(fn, fc, N, C, nk, nr, Hn, ck, cr, cw, Hc, counts);
+    const RepTables t{nk, nr, ck, cr, cw, counts, Hn, Hc, nullptr, 0};
     for (int g = gw; g < P; g += nw) {
       if (g <= f || __ldcg(species_of + g) >= 0) continue;  // warp-uniform
       distance_warp(pn + size_t(g) * gn, pc + size_t(g) * gc, fn, fc, 1, t, N, C, cd, ch, tile, dist_w + warp);
@@ -623,7 +624,7 @@ struct Evolver {
   cudaError_t launch_found_rounds(int S_old, const double* n, const double* c) {
     int Hn = table_capacity(N), Hc = table_capacity(C);
     const int block = 128;
-    const size_t smem = size_t(Hn + Hc) * 12 + 16 + (block / 32) * 8 + (block / 32) * 33 * 8;
+    const size_t smem = size_t(Hn) * 12 + size_t(Hc) * 20 + 16 + (block / 32) * 8 + (block / 32) * 33 * 8;
     cudaError_t e = cudaFuncSetAttribute(k_found_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     if (coop_blocks == 0) {

@@ -107,16 +107,6 @@ __device__ __forceinline__ void lds_pred(bool p, uint32_t addr, float (&x)[SPT])
   }
 }
 template <int SPT>
-__device__ __forceinline__ void lds(uint32_t addr, float (&x)[SPT]) {
-  if constexpr (SPT == 1) {
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(addr));
-  } else if constexpr (SPT == 2) {
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x[0]), "=f"(x[1]) : "r"(addr));
-  } else {
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]) : "r"(addr));
-  }
-}
-template <int SPT>
 __device__ __forceinline__ void sts(uint32_t addr, const float (&x)[SPT]) {
   if constexpr (SPT == 1) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(x[0]));
@@ -240,45 +230,6 @@ k_forward(FwdParams p) {
       const bool first = (meta >> 11) & 1u;
       const bool last = (meta >> 12) & 1u;
       const int agg = AGG >= 0 ? AGG : int((meta >> 16) & 3u);
-      if constexpr (AGG == FNB_AGG_SUM) {
-        // {sum} specialisation: exactly cnt value loads and FMA steps per
-        // record (cnt is uniform across a genome group, so the switch does
-        // not diverge for T >= 32): no pad slots, no zeroing, no predicates;
-        // the accumulator is reset after each finalize instead of per record.
-        float x0[SPT], x1[SPT], x2[SPT], x3[SPT];
-        switch (cnt) {
-          case 4:
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4440) * row_bytes, x0);
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4441) * row_bytes, x1);
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4442) * row_bytes, x2);
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4443) * row_bytes, x3);
-#pragma unroll
-            for (int k = 0; k < SPT; ++k)
-              acc[k] = fmaf(cur.w.w, x3[k], fmaf(cur.w.z, x2[k], fmaf(cur.w.y, x1[k], fmaf(cur.w.x, x0[k], acc[k]))));
-            break;
-          case 3:
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4440) * row_bytes, x0);
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4441) * row_bytes, x1);
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4442) * row_bytes, x2);
-#pragma unroll
-            for (int k = 0; k < SPT; ++k)
-              acc[k] = fmaf(cur.w.z, x2[k], fmaf(cur.w.y, x1[k], fmaf(cur.w.x, x0[k], acc[k])));
-            break;
-          case 2:
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4440) * row_bytes, x0);
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4441) * row_bytes, x1);
-#pragma unroll
-            for (int k = 0; k < SPT; ++k) acc[k] = fmaf(cur.w.y, x1[k], fmaf(cur.w.x, x0[k], acc[k]));
-            break;
-          case 1:
-            lds<SPT>(vb + __byte_perm(srcs, 0u, 0x4440) * row_bytes, x0);
-#pragma unroll
-            for (int k = 0; k < SPT; ++k) acc[k] = fmaf(cur.w.x, x0[k], acc[k]);
-            break;
-          default:
-            break;
-        }
-      } else {
       float x0[SPT], x1[SPT], x2[SPT], x3[SPT];
 #pragma unroll
       for (int k = 0; k < SPT; ++k) x0[k] = x1[k] = x2[k] = x3[k] = 0.0f;
@@ -321,7 +272,6 @@ k_forward(FwdParams p) {
           }
         }
       }
-      }
       cur.w = s_rec[r + 1].w;
       if (last) {
         if (agg == FNB_AGG_MEAN) {
@@ -337,10 +287,6 @@ k_forward(FwdParams p) {
         for (int k = 0; k < SPT; ++k)
           y[k] = act_apply<ACT>(int((meta >> 13) & 7u), fmaf(cur.a.y, acc[k], cur.a.x));
         sts<SPT>(vb + ((meta & 0xffu) << row_shift), y);
-        if constexpr (AGG == FNB_AGG_SUM) {
-#pragma unroll
-          for (int k = 0; k < SPT; ++k) acc[k] = 0.0f;
-        }
       }
       cur.a = s_rec[r + 1].a;
     }
