@@ -176,41 +176,64 @@ __host__ __device__ __forceinline__ double taylor_sin_fma(double a, double da) {
   return GM_ADD(a, t);
 }
 
-// __cos_fma for finite 0 <= x < 105414350 (the RngStream domain is [0, 2*pi))
+// __cos_fma for finite 0 <= x < 105414350 (the RngStream domain is [0, 2*pi)).
+// Every argument range only prepares (a, da, kernel, sign) -- the same
+// rounded operations as s_sin.c's branches -- and the three kernels each have
+// one call site, so a warp whose lanes fall in different ranges runs at most
+// do_cos + do_sin (+ the rare Taylor case) instead of one kernel copy per range.
 __host__ __device__ inline double cos(double x) {
   const uint32_t k = uint32_t(bits(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e400000u) return 1.0;
-  if (k < 0x3feb6000u) return do_cos_fma(fabs(x), x < 0.0 ? -0.0 : 0.0);
-  if (k < 0x400368fdu) {
+  double a, da;
+  int kern;  // 0 do_cos(a, da), 1 do_sin(a, da), 2 taylor_sin(a, da)
+  bool neg = false;
+  if (k < 0x3feb6000u) {
+    a = fabs(x);
+    da = x < 0.0 ? -0.0 : 0.0;
+    kern = 0;
+  } else if (k < 0x400368fdu) {
     const double y = GM_SUB(FNB_LIBM_HP0, fabs(x));
-    const double a = GM_ADD(y, FNB_LIBM_HP1);
-    const double da = GM_ADD(GM_SUB(y, a), FNB_LIBM_HP1);
-    if (fabs(a) < FNB_LIBM_SMALL) return taylor_sin_fma(a, da);
-    return do_sin_fma(a, a <= 0.0 ? -da : da);
+    a = GM_ADD(y, FNB_LIBM_HP1);
+    da = GM_ADD(GM_SUB(y, a), FNB_LIBM_HP1);
+    if (fabs(a) < FNB_LIBM_SMALL) {
+      kern = 2;
+    } else {
+      kern = 1;
+      if (a <= 0.0) da = -da;
+    }
+  } else {  // reduce_sincos
+    const double t = GM_FMA(x, FNB_LIBM_HPINV, FNB_LIBM_TOINT);
+    const double xn = GM_SUB(t, FNB_LIBM_TOINT);
+    const int n = int(uint32_t(bits(t)) & 3u);
+    double y = GM_FMA(-xn, FNB_LIBM_MP1, x);
+    y = GM_FMA(-xn, FNB_LIBM_MP2, y);
+    const double t2 = GM_FMA(-xn, FNB_LIBM_PP3, y);
+    double db = GM_SUB(y, t2);
+    db = GM_FMA(-xn, FNB_LIBM_PP3, db);
+    const double b = GM_FMA(-xn, FNB_LIBM_PP4, t2);
+    double e = GM_SUB(t2, b);
+    e = GM_FMA(-xn, FNB_LIBM_PP4, e);
+    db = GM_ADD(db, e);
+    if ((n & 1) == 0) {  // do_sincos(b, db, n + 1) -> do_cos
+      a = fabs(b);
+      da = b < 0.0 ? -db : db;
+      kern = 0;
+    } else if (fabs(b) < FNB_LIBM_SMALL) {
+      a = b;
+      da = db;
+      kern = 2;
+    } else {
+      a = b;
+      da = b <= 0.0 ? -db : db;
+      kern = 1;
+    }
+    neg = ((n + 1) & 2) != 0;
   }
-  // reduce_sincos
-  const double t = GM_FMA(x, FNB_LIBM_HPINV, FNB_LIBM_TOINT);
-  const double xn = GM_SUB(t, FNB_LIBM_TOINT);
-  const int n = int(uint32_t(bits(t)) & 3u);
-  double y = GM_FMA(-xn, FNB_LIBM_MP1, x);
-  y = GM_FMA(-xn, FNB_LIBM_MP2, y);
-  const double t2 = GM_FMA(-xn, FNB_LIBM_PP3, y);
-  double db = GM_SUB(y, t2);
-  db = GM_FMA(-xn, FNB_LIBM_PP3, db);
-  const double b = GM_FMA(-xn, FNB_LIBM_PP4, t2);
-  double e = GM_SUB(t2, b);
-  e = GM_FMA(-xn, FNB_LIBM_PP4, e);
-  db = GM_ADD(db, e);
   double res;
-  if ((n & 1) == 0) {  // do_sincos(b, db, n + 1) -> do_cos
-    const double ab = fabs(b);
-    res = do_cos_fma(ab, b < 0.0 ? -db : db);
-  } else if (fabs(b) < FNB_LIBM_SMALL) {
-    res = taylor_sin_fma(b, db);
-  } else {
-    res = do_sin_fma(b, b <= 0.0 ? -db : db);
-  }
-  return ((n + 1) & 2) ? -res : res;
+  if (kern == 0) res = do_cos_fma(a, da);
+  else if (kern == 1) res = do_sin_fma(a, da);
+  else res = taylor_sin_fma(a, da);
+  return neg ? -res : res;
 }
 
 // RngStream::normal from its two uniforms (rng.hpp:111-116): u1 = 1 - U0,
