@@ -34,6 +34,21 @@ P_SHARD, N_MAX, C_MAX, FILL, BATCH, NI, NO = 10_000, 64, 256, 0.75, 1024, 4, 1
 WORKLOAD = "C2 func-regression: pop 10k per GPU, B=1024, N_max=64, C_max=256, fill 0.75, tanh/sum"
 
 
+def ncu_traffic(name: str):
+    """DRAM bytes per launch of a kernel from the newest committed ncu summary
+    (profiles/*_ncu_summary.json, scripts/ncu_summary.py), or (None, None)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f)).get(name)
+        except Exception:
+            continue
+        if d and "dram_read" in d:
+            return d["dram_read"] + d.get("dram_write", 0.0), os.path.relpath(f, ROOT)
+    return None, None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -151,12 +166,14 @@ def c5_distance(dev, stream, flush, reps: int = 5):
     alg = P5 * (40 * N5 + 32 * C5) + P5 * S5 * 8  # canonical genome bytes + distances out
     peak = peaks().get("hbm_gbs") or 7700.0
     achieved = alg / t / 1e9
+    c5_traffic, c5_src = ncu_traffic("k3_distance_c5")
     del nodes5, conns5
     return {"workload": "C5 K3 distance: pop 100k, N128/C1024, S=10 reps, fill 0.75 (2k distinct genomes tiled)",
             "ms": t * 1e3, "genomes_per_s": P5 / t,
             "roofline": {"kernel": "k_rep_tables + k_distance (K3)", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "algorithmic_bytes_per_launch": alg,
+                         "algorithmic_bytes_per_launch": alg, "traffic": c5_traffic,
+                         "traffic_source": c5_src,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}}
 
 
@@ -366,6 +383,7 @@ def main():
         c5 = c5_distance(dev, stream, flush)
 
     # ---- roofline for the dominant kernel (K2 forward) ----
+    k2_traffic, k2_traffic_src = ncu_traffic("k2_forward_main_pass")
     n_en = int(np.sum(conns_h[:, :, 2] == 1.0))
     n_ops = int(np.sum(~np.isnan(nodes_h[:, :, 0]))) - P_SHARD * NI
     flops = 2.0 * BATCH * (n_en + n_ops)          # FMA per enabled edge + resp*agg+bias per node
@@ -398,7 +416,8 @@ def main():
             "kernels": {"transform_plus_forward_ms": ms_per_step, "forward_ms": fwd_s * 1e3,
                         "transform_ms": ms_per_step - fwd_s * 1e3},
             "roofline": {"kernel": "k_forward (K2)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
-                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": k2_traffic,
+                         "traffic_source": k2_traffic_src,
                          "peak_source": "nominal FP32 FMA peak at MEASURED_PEAKS sm_max_mhz (no measured FP32 peak)",
                          "smem": {"achieved_TBps": smem_bytes / fwd_s / 1e12, "peak_TBps": smem_peak,
                                   "frac": smem_bytes / fwd_s / 1e12 / smem_peak}},
