@@ -102,7 +102,7 @@ __device__ inline void distance_warp(const double* __restrict__ gn, const double
       unsigned long long k0[kLookupBatch];
 #pragma unroll
       for (int i = 0; i < kLookupBatch; ++i)  // first probes of several reps in flight
-        k0[i] = (ne && s0 + i < S) ? t.nkeys[size_t(s0 + i) * t.Hn + h] : kEmptyKey;
+        k0[i] = (ne && s0 + i < S) ? t.nkeys[uint32_t(s0 + i) * uint32_t(t.Hn) + h] : kEmptyKey;
 #pragma unroll
       for (int i = 0; i < kLookupBatch; ++i) {
         const int s = s0 + i;
@@ -115,7 +115,7 @@ __device__ inline void distance_warp(const double* __restrict__ gn, const double
           double d = __dadd_rn(fabs(__dsub_rn(a[kBias], b[kBias])), fabs(__dsub_rn(a[kResp], b[kResp])));
           d = __dadd_rn(d, a[kAgg] != b[kAgg] ? 1.0 : 0.0);
           d = __dadd_rn(d, a[kAct] != b[kAct] ? 1.0 : 0.0);
-          v = __ddiv_rn(d, 4.0);
+          v = __dmul_rn(d, 0.25);  // == d / 4.0 exactly (both correctly rounded d/4)
         }
         const int m = __popc(__ballot_sync(0xffffffffu, q >= 0));
         if (lane == s) mn += m;
@@ -151,14 +151,15 @@ __device__ inline void distance_warp(const double* __restrict__ gn, const double
         const int s = s0 + i;
         const bool m = ne && s < S && (!t.filt || filter_has(t.filt + (size_t(s) << t.fw_log2), fb));
         maybe |= uint32_t(m) << i;
-        k0[i] = m ? t.ckeys[size_t(s) * t.Hc + h] : kEmptyKey;
+        k0[i] = m ? t.ckeys[uint32_t(s) * uint32_t(t.Hc) + h] : kEmptyKey;
       }
 #pragma unroll
       for (int i = 0; i < kLookupBatch; ++i) {
         const int s = s0 + i;
         if (s >= S) break;  // warp-uniform
         const int slot = ((maybe >> i) & 1u) ? probe_from(t.ckeys + size_t(s) * t.Hc, t.Hc - 1, h, k0[i], key) : -1;
-        const double v = slot >= 0 ? __ddiv_rn(fabs(__dsub_rn(w, t.cw[size_t(s) * t.Hc + slot])), 1.0) : 0.0;
+        // |dw| / 1.0 == |dw| exactly (IEEE division by one)
+        const double v = slot >= 0 ? fabs(__dsub_rn(w, t.cw[uint32_t(s) * uint32_t(t.Hc) + uint32_t(slot)])) : 0.0;
         const int m = __popc(__ballot_sync(0xffffffffu, slot >= 0));
         if (lane == s) mc += m;
         tile[s * 33 + lane] = v;
