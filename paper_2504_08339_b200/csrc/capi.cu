@@ -1,6 +1,7 @@
 // capi.cu -- extern "C" boundary (include/flatneat_b200.h): contexts, the
 // synchronous host layer mirroring the reference free functions, and the
 // asynchronous device layer.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -114,7 +115,12 @@ void fnb_ctx_destroy(fnb_ctx* ctx) {
   for (DevBuf* b : {&ctx->nodes, &ctx->conns, &ctx->nets, &ctx->X, &ctx->Y, &ctx->fit, &ctx->out,
                     &ctx->partial, &ctx->misc, &ctx->scratch})
     b->release();
+  ctx->flags.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) {
+    cudaStreamDestroy(ctx->copy_stream);
+    for (auto& e : ctx->chunk_ev) cudaEventDestroy(e);
+  }
   delete ctx;
 }
 
@@ -260,25 +266,23 @@ int fnb_transform(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns
   return 0;
 }
 
-static int upload_floats(fnb_ctx* ctx, DevBuf& dst, const double* src, size_t n, bool check_finite) {
-  // doubles go up as-is and are narrowed on the device (no host-side pass)
-  CK(dst.ensure(n * sizeof(float) + n * sizeof(double) + 16));
-  double* d_tmp = reinterpret_cast<double*>(static_cast<uint8_t*>(dst.p) + ((n * sizeof(float) + 15) & ~size_t(15)));
-  CK(cudaMemcpyAsync(d_tmp, src, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-  CK(ctx->misc.ensure(sizeof(int) * size_t(ctx->L.N + 8)));
-  int* d_bad = static_cast<int*>(ctx->misc.p);
-  CK(cudaMemsetAsync(d_bad, 0, sizeof(int), ctx->stream));
-  CK(launch_to_float(d_tmp, static_cast<float*>(dst.p), n, d_bad, ctx->stream));
-  ctx->launches++;
-  if (check_finite) {
-    int bad = 0;
-    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    if (bad) return set_err(ctx, FNB_E_NON_FINITE_INPUT, "input not finite", 0);  // network.hpp:245-246
-  }
+// Lazily created copy stream + chunk events of the host-layer pipeline.
+static int ensure_pipeline(fnb_ctx* ctx) {
+  if (ctx->copy_stream) return 0;
+  CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : ctx->chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return 0;
 }
 
+// Host-buffer evaluation (batch_forward network.hpp:294-330 + the fitness of
+// SPEC.md:441-458).  The population crosses PCIe in chunks on copy_stream;
+// chunk k is transformed (K1) and evaluated (K2) on the compute stream as
+// soon as its copy lands, so the transfer of chunk k+1 overlaps the kernels
+// of chunk k.  Per-genome fitness is partition invariant (forward.cu), so
+// the chunking does not change a bit of the result.  Errors are collected on
+// the device and read once at the end, in the reference's order: the lowest
+// failing genome's transform error (network.hpp:122-220), then a non-finite
+// input (network.hpp:245-246).
 static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
                          const double* inputs, const double* targets, int batch, int kind, double offset,
                          double* fitness_out, double* out) {
@@ -286,30 +290,83 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
   ctx->err_index = -1;
   if (P <= 0) return 0;
   CK(cudaSetDevice(ctx->device));
-  int st = upload_pop(ctx, pop_nodes, pop_conns, P);
-  if (!st) st = transform_and_check(ctx, P);
-  if (!st) st = upload_floats(ctx, ctx->X, inputs, size_t(batch) * ctx->L.I, true);
-  if (!st && kind != FNB_FIT_NONE) st = upload_floats(ctx, ctx->Y, targets, size_t(batch) * ctx->L.O, false);
-  if (st) return st;
+  if (int st = ensure_pipeline(ctx)) return st;
+  const int N = ctx->L.N, Cm = ctx->L.C, O = ctx->L.O;
+  const size_t nrow = sizeof(double) * size_t(N) * kNodeCols, crow = sizeof(double) * size_t(Cm) * kConnCols;
+  CK(ctx->nodes.ensure(nrow * size_t(P)));
+  CK(ctx->conns.ensure(crow * size_t(P)));
+  CK(ctx->nets.ensure(ctx->L.bytes * size_t(P)));
+  CK(ctx->flags.ensure(4 * sizeof(int)));
+  int* d_flags = static_cast<int*>(ctx->flags.p);  // [0] first failing genome, [1] non-finite X, [2] Y
+  static const int kInit[4] = {0x7fffffff, 0, 0, 0};
+  CK(cudaMemcpyAsync(d_flags, kInit, sizeof(kInit), cudaMemcpyHostToDevice, ctx->stream));
+  // X and Y go up as doubles and are narrowed on the device
+  auto up = [&](DevBuf& dst, const double* src, size_t n, int* bad) -> int {
+    CK(dst.ensure(n * sizeof(float) + n * sizeof(double) + 16));
+    double* d_tmp = reinterpret_cast<double*>(static_cast<uint8_t*>(dst.p) + ((n * sizeof(float) + 15) & ~size_t(15)));
+    CK(cudaMemcpyAsync(d_tmp, src, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_to_float(d_tmp, static_cast<float*>(dst.p), n, bad, ctx->stream));
+    ctx->launches++;
+    return 0;
+  };
+  if (int st = up(ctx->X, inputs, size_t(batch) * ctx->L.I, d_flags + 1)) return st;
+  if (kind != FNB_FIT_NONE)
+    if (int st = up(ctx->Y, targets, size_t(batch) * O, d_flags + 2)) return st;
   double* d_out = nullptr;
   double* d_fit = nullptr;
   if (out) {
-    CK(ctx->out.ensure(sizeof(double) * size_t(P) * batch * ctx->L.O));
+    CK(ctx->out.ensure(sizeof(double) * size_t(P) * batch * O));
     d_out = static_cast<double*>(ctx->out.p);
   }
   if (kind != FNB_FIT_NONE) {
     CK(ctx->fit.ensure(sizeof(double) * size_t(P)));
     d_fit = static_cast<double*>(ctx->fit.p);
   }
-  st = fnb_forward_d(ctx, ctx->nets.p, P, static_cast<float*>(ctx->X.p),
-                     kind != FNB_FIT_NONE ? static_cast<float*>(ctx->Y.p) : nullptr, batch, kind, offset, d_fit,
-                     d_out, ctx->stream);
-  if (st) return st;
+  // ~8 MB chunks (enough to keep the copy engine streaming), at most kMaxChunks
+  const size_t total = (nrow + crow) * size_t(P);
+  const int chunks = int(std::max<size_t>(
+      1, std::min<size_t>(std::min<size_t>(fnb_ctx::kMaxChunks, size_t(P)), total / (size_t(8) << 20))));
+  auto lo_of = [&](int k) { return int((long long)P * k / chunks); };
+  // the copies must not overwrite buffers still read by earlier work on the compute stream
+  CK(cudaEventRecord(ctx->chunk_ev[fnb_ctx::kMaxChunks], ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[fnb_ctx::kMaxChunks], 0));
+  uint8_t* dn = static_cast<uint8_t*>(ctx->nodes.p);
+  uint8_t* dc = static_cast<uint8_t*>(ctx->conns.p);
+  for (int k = 0; k < chunks; ++k) {
+    const size_t lo = size_t(lo_of(k)), n = size_t(lo_of(k + 1)) - lo;
+    CK(cudaMemcpyAsync(dn + lo * nrow, reinterpret_cast<const uint8_t*>(pop_nodes) + lo * nrow, n * nrow,
+                       cudaMemcpyHostToDevice, ctx->copy_stream));
+    CK(cudaMemcpyAsync(dc + lo * crow, reinterpret_cast<const uint8_t*>(pop_conns) + lo * crow, n * crow,
+                       cudaMemcpyHostToDevice, ctx->copy_stream));
+    CK(cudaEventRecord(ctx->chunk_ev[k], ctx->copy_stream));
+  }
+  uint8_t* nets = static_cast<uint8_t*>(ctx->nets.p);
+  for (int k = 0; k < chunks; ++k) {
+    const int lo = lo_of(k), n = lo_of(k + 1) - lo;
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[k], 0));
+    int st = fnb_transform_d(ctx, reinterpret_cast<const double*>(dn + size_t(lo) * nrow),
+                             reinterpret_cast<const double*>(dc + size_t(lo) * crow), n,
+                             nets + size_t(lo) * ctx->L.bytes, ctx->stream);
+    if (st) return st;
+    // genomes that failed K1 carry no records: K2 runs them as empty programs
+    st = fnb_forward_d(ctx, nets + size_t(lo) * ctx->L.bytes, n, static_cast<float*>(ctx->X.p),
+                       kind != FNB_FIT_NONE ? static_cast<float*>(ctx->Y.p) : nullptr, batch, kind, offset,
+                       d_fit ? d_fit + lo : nullptr, d_out ? d_out + size_t(lo) * batch * O : nullptr, ctx->stream);
+    if (st) return st;
+  }
+  CK(launch_first_error(nets, ctx->L.bytes, P, d_flags, ctx->stream));
+  ctx->launches++;
+  int flags[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(flags, d_flags, sizeof(flags), cudaMemcpyDeviceToHost, ctx->stream));
   if (out)
-    CK(cudaMemcpyAsync(out, d_out, sizeof(double) * size_t(P) * batch * ctx->L.O, cudaMemcpyDeviceToHost,
-                       ctx->stream));
-  if (fitness_out) CK(cudaMemcpyAsync(fitness_out, d_fit, sizeof(double) * size_t(P), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(out, d_out, sizeof(double) * size_t(P) * batch * O, cudaMemcpyDeviceToHost, ctx->stream));
+  if (fitness_out)
+    CK(cudaMemcpyAsync(fitness_out, d_fit, sizeof(double) * size_t(P), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  if (flags[0] != 0x7fffffff)  // rebuild the reference's message for the lowest failing genome
+    return fnb_check_nets_d(ctx, reinterpret_cast<const double*>(dn), reinterpret_cast<const double*>(dc), nets, P,
+                            ctx->stream);
+  if (flags[1]) return set_err(ctx, FNB_E_NON_FINITE_INPUT, "input not finite", 0);  // network.hpp:245-246
   return 0;
 }
 

@@ -32,7 +32,12 @@ struct fnb_ctx {
   int err_index = -1;
   long long launches = 0;
   cudaStream_t stream = nullptr;
-  DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc, scratch;
+  // host-layer pipeline: population chunks go up on copy_stream while the
+  // previous chunk is transformed and evaluated on `stream`
+  cudaStream_t copy_stream = nullptr;
+  static constexpr int kMaxChunks = 16;
+  cudaEvent_t chunk_ev[kMaxChunks + 1] = {};
+  DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc, scratch, flags;
 };
 
 // errors.hpp:33-57

@@ -166,3 +166,37 @@ def test_known_answers(fnb):
     c[0, 0] = [0, 1, 1, 0.5]
     out = _engine(fnb, prob, schema).batch_forward(n, c, np.array([[1.0]])).values
     assert abs(out[0, 0, 0] - 0.5370495669980353) < 1e-6
+
+
+def test_pipelined_host_path_chunks(fnb):
+    """fnb_evaluate streams the population up in chunks (capi.cu evaluate_impl):
+    3000 C2 genomes = 32 MB -> 4 chunks.  Fitness must equal the one-shot
+    device path bit for bit (partition-invariant units), and a transform error
+    in a late chunk must still be reported for the lowest failing genome."""
+    import torch
+    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
+    P = 3000
+    nodes, conns = synthetic_population(P, 64, 256, fill=0.75, seed=21)
+    X, Y = regression_dataset(256, seed=2)
+    prob = ol.Problem(64, 256, [0, 1, 2, 3], [4])
+    eng = _engine(fnb, prob, ol.SchemaSpec())
+    fit = eng.evaluate(nodes, conns, X, Y, fnb.FIT_NEG_MSE)
+    dev = torch.device("cuda", 0)
+    dn, dc = torch.from_numpy(nodes).to(dev), torch.from_numpy(conns).to(dev)
+    nets = eng.alloc_nets(P)
+    st = torch.cuda.current_stream()
+    eng.transform_d(dn, dc, nets, st)
+    f_d = torch.empty(P, dtype=torch.float64, device=dev)
+    eng.forward_d(nets, P, torch.from_numpy(X.astype(np.float32)).to(dev),
+                  torch.from_numpy(Y.astype(np.float32)).to(dev), fnb.FIT_NEG_MSE, 0.0, fitness=f_d, stream=st)
+    torch.cuda.synchronize()
+    assert np.array_equal(fit, f_d.cpu().numpy())
+    # a dangling endpoint in genome 2900 (last chunk) and 2950: 2900 is reported
+    bad_c = conns.copy()
+    for g in (2950, 2900):
+        bad_c[g, 0, 1] = 9999.0
+    with pytest.raises(fnb.FlatneatError) as ei:
+        eng.evaluate(nodes, bad_c, X, Y, fnb.FIT_NEG_MSE)
+    assert ei.value.index == 2900 and ei.value.code == "dangling_endpoint"
+    # the context recovers: the next call is clean and identical
+    assert np.array_equal(eng.evaluate(nodes, conns, X, Y, fnb.FIT_NEG_MSE), fit)
