@@ -421,7 +421,7 @@ int fnb_distance_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, i
   CK(launch_distance(d_nodes, d_conns, P, d_rep_nodes, d_rep_conns, S, ctx->L.N, ctx->L.C,
                      cfg->compatibility_disjoint, cfg->compatibility_homologous, d_out, ctx->scratch.p,
                      ctx->scratch.cap, static_cast<cudaStream_t>(stream)));
-  ctx->launches += 2;
+  ctx->launches += kDistanceLaunches;
   return 0;
 }
 

@@ -671,9 +671,23 @@ struct Evolver {
           if (ee != cudaSuccess) e = ee;
         }
         if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, graph, 0);
-        if (graph) cudaGraphDestroy(graph);
         g.n_launches = *launches - before;
         *launches = before;
+        if (e == cudaSuccess) {  // exact: the kernel nodes the capture recorded
+          size_t n = 0;
+          if (cudaGraphGetNodes(graph, nullptr, &n) == cudaSuccess) {
+            std::vector<cudaGraphNode_t> nodes(n);
+            long long k = 0;
+            if (n && cudaGraphGetNodes(graph, nodes.data(), &n) == cudaSuccess) {
+              for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType t;
+                if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+              }
+              g.n_launches = k;
+            }
+          }
+        }
+        if (graph) cudaGraphDestroy(graph);
         if (e != cudaSuccess) {  // e.g. a capture-unsupported launch: stay eager
           g.exec = nullptr;
           use_graphs = false;
@@ -728,7 +742,7 @@ struct Evolver {
       if (e != cudaSuccess) return e;
     }
     k_assign_first<<<B, T, 0, st>>>(dmat, P, S_old, th, species_of);
-    *launches += 2;
+    *launches += 2 + (S_old > 0 ? kDistanceLaunches : 0);
     if (S_old < cfg.max_species) {
       e = launch_found_rounds(S_old, n, c);
       if (e != cudaSuccess) return e;
@@ -768,7 +782,7 @@ struct Evolver {
     const Key4 root1 = key_split(key_from_seed(seed), 1);
     k_reproduce_plan<<<B, T, 0, st>>>(sd, idx_sorted, fitness, P, root1, cfg.genome_elitism, cfg.survival, fit_idx,
                                       oth_idx, xkeys, mkeys, active);
-    *launches += 24;
+    *launches += 22 + kDistanceLaunches;
     e = launch_crossover(n, c, fit_idx, oth_idx, xkeys, P, N, C, pn[cur ^ 1], pc[cur ^ 1], st);
     if (e != cudaSuccess) return e;
     ++*launches;

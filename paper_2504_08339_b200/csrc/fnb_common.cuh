@@ -81,6 +81,9 @@ struct Rec {                // 48 B
 static_assert(sizeof(RecHeader) == 16 && sizeof(Rec) == 48, "record");
 __host__ __device__ inline int max_records(int N, int C) { return N + (C + kRecSlots - 1) / kRecSlots; }
 
+// kernels one K3 distance call launches (distance.cu: 6 union-table build kernels + k_distance)
+constexpr int kDistanceLaunches = 7;
+
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct NetLayout {

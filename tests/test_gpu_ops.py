@@ -129,3 +129,68 @@ def test_cpp_dropin_header(fnb):
         pytest.skip("test_gpu_hpp not built (needs /root/reference at build time)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "gpu.hpp parity ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_distance_union_tables_edge_cases(fnb):
+    """K3's merged representative tables (distance.cu): 32 representatives
+    (the ABI maximum), C5 row limits, and duplicated markers -- a repeated
+    connection / node key in a representative resolves to its FIRST row, as
+    the reference's linear find_conn / find_node do (genome.hpp:195-210)."""
+    from paper_2504_08339_b200.synthetic import synthetic_population
+    schema = ol.SchemaSpec()
+    prob = ol.Problem(128, 1024, [0, 1, 2, 3], [4])
+    nodes, conns = synthetic_population(72, 128, 1024, fill=0.75, seed=77)
+    reps_n, reps_c = nodes[40:72].copy(), conns[40:72].copy()
+    gn, gc = nodes[:40].copy(), conns[:40].copy()
+    # share markers: genome i copies half of rep (i % 32)'s connections
+    for i in range(40):
+        gc[i, :384] = reps_c[i % 32, :384]
+        gc[i, :384, 3] += 0.25 * i
+    # duplicates: rep 3 repeats row 10 with another weight after its rows;
+    # genome 5 repeats its own row 7; rep 6 repeats a node key
+    reps_c[3, 900] = reps_c[3, 10]
+    reps_c[3, 900, 3] = 123.0
+    gc[5, 901] = gc[5, 7]
+    reps_n[6, 120] = reps_n[6, 9]
+    reps_n[6, 120, 1] = -7.0
+    got = _engine(fnb, prob, schema).distance(gn, gc, reps_n, reps_c)
+    use_ref = ol.ref_available()
+    for p in range(gn.shape[0]):
+        for s in range(32):
+            want = ol.distance(prob, gn[p], gc[p], reps_n[s], reps_c[s], use_ref=use_ref)
+            assert got[p, s] == want, (p, s, got[p, s], want)
+    # one representative, and an empty population slice, go through the same path
+    one = _engine(fnb, prob, schema).distance(gn[:3], gc[:3], reps_n[:1], reps_c[:1])
+    for p in range(3):
+        assert one[p, 0] == ol.distance(prob, gn[p], gc[p], reps_n[0], reps_c[0], use_ref=use_ref)
+
+
+@pytest.mark.parametrize("variant", ["compact", "full_codes", "full_species"])
+def test_distance_image_formats(fnb, variant):
+    """K3's image formats (distance.cu): the compact one (S <= 16, small-integer
+    agg / act codes) and the full one -- forced by a representative whose agg
+    is not a small integer, or by more than 16 representatives -- give the
+    reference's distances bit for bit, including genomes whose own agg / act
+    are not small integers (code 0xFFFF)."""
+    from paper_2504_08339_b200.synthetic import synthetic_population
+    schema = ol.SchemaSpec(["tanh", "identity", "sigmoid"], ["sum", "product"])
+    prob = ol.Problem(64, 256, [0, 1, 2, 3], [4])
+    nodes, conns = synthetic_population(60, 64, 256, fill=0.75, n_act=3, n_agg=2, seed=404)
+    S = 20 if variant == "full_species" else 10
+    reps_n, reps_c = nodes[40:40 + S].copy(), conns[40:40 + S].copy()
+    gn, gc = nodes[:40].copy(), conns[:40].copy()
+    for i in range(40):  # shared markers with perturbed weights / attributes
+        gc[i, :100] = reps_c[i % S, :100]
+        gc[i, :100, 3] *= 1.0 + 0.01 * i
+        gn[i, 5:20, 3] = (gn[i, 5:20, 3] + i) % 2
+    gn[3, 7, 3] = 1.5        # a genome agg that is not a small integer
+    gn[4, 8, 4] = 70000.0    # ... and a large act
+    gn[5, 9, 3] = -0.0       # -0.0 == 0.0
+    if variant == "full_codes":
+        reps_n[2, 6, 3] = 2.5
+    got = _engine(fnb, prob, schema).distance(gn, gc, reps_n, reps_c)
+    use_ref = ol.ref_available()
+    for p in range(gn.shape[0]):
+        for s in range(S):
+            want = ol.distance(prob, gn[p], gc[p], reps_n[s], reps_c[s], use_ref=use_ref)
+            assert got[p, s] == want, (variant, p, s, got[p, s], want)
