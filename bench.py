@@ -203,6 +203,48 @@ def c3_cppn(eng, nets, dev, stream, flush, reps: int = 3):
             "forward_ms": t * 1e3, "evals_per_s": P_SHARD * Xh.shape[0] / t}
 
 
+def c4_hyperneat(dev, stream, flush, reps: int = 3):
+    """C4: pop 4k CPPNs (N32/C128) queried at the 28 x 8
+    substrate connections, each policy run for 1000 steps of the synthetic
+    27-obs / 8-act linear dynamics.  One step = K1 + K2 (224 queries per
+    CPPN) + the rollout kernel."""
+    import torch
+    import paper_2504_08339_b200 as fnb
+    from paper_2504_08339_b200.synthetic import CPPN_ACTS, cppn_population, hyper_dynamics
+    P4 = 4000
+    nodes_h, conns_h = cppn_population(P4, 32, 128, seed=4)
+    A, B, s0 = hyper_dynamics(seed=4)
+    eng4 = fnb.Engine(fnb.GenomeLimits(32, 128), [0, 1, 2, 3, 4], [5], fnb.AttributeSchema(CPPN_ACTS, ["sum"]),
+                      device=dev.index)
+    cfg = fnb.HyperConfig()
+    nodes, conns = torch.from_numpy(nodes_h).to(dev), torch.from_numpy(conns_h).to(dev)
+    f32 = lambda x: torch.from_numpy(x.astype(np.float32)).to(dev)
+    dA, dB, ds0 = f32(A), f32(B), f32(s0)
+    nets = eng4.alloc_nets(P4)
+    fit = torch.empty(P4, dtype=torch.float64, device=dev)
+
+    def run():
+        eng4.transform_d(nodes, conns, nets, stream)
+        eng4.hyper_evaluate_d(nets, P4, cfg, dA, dB, ds0, fit, stream=stream)
+
+    run()
+    ms = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        run()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = float(np.median(ms)) / 1e3
+    Q = (cfg.num_obs + 1) * cfg.num_act
+    return {"workload": "C4 HyperNEAT: pop 4k CPPNs (N32/C128), 28x8 substrate queries, 27-obs/8-act policy, "
+                        "1000-step linear-dynamics rollout",
+            "ms": t * 1e3, "policy_steps_per_s": P4 * cfg.steps / t, "cppn_evals_per_s": P4 * Q / t,
+            "generations_equiv_per_s": 1.0 / t}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -211,7 +253,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-generations", action="store_true")
-    ap.add_argument("--no-c5", action="store_true", help="skip the C3 (CPPN) and C5 (pop 100k K3 distance) measurements")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C3 (CPPN), C4 (HyperNEAT) and C5 (pop 100k K3 distance) measurements")
     ap.add_argument("--spt", type=int, default=0, help="forward columns per thread (tuning; 0 = auto)")
     args = ap.parse_args()
 
@@ -380,6 +422,7 @@ def main():
         ev.close()
 
     c3 = c3_cppn(eng, nets, dev, stream, flush) if not args.no_c5 else None
+    c4 = c4_hyperneat(dev, stream, flush) if not args.no_c5 else None
     c5 = None
     if not args.no_c5:
         c5 = c5_distance(dev, stream, flush)
@@ -432,6 +475,8 @@ def main():
             line["c5_distance"] = c5
         if c3 is not None:
             line["c3_cppn"] = c3
+        if c4 is not None:
+            line["c4_hyperneat"] = c4
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

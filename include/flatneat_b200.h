@@ -211,6 +211,30 @@ int fnb_forward_d(fnb_ctx* ctx, const void* d_nets, int P, const float* d_X, con
                   int batch, int fitness_kind, double fitness_offset, double* d_fitness,
                   double* d_out, void* stream);
 
+/* ---- BASELINE config 4: HyperNEAT ---------------------
+ * The context's genomes are CPPNs with 5 inputs (x1, y1, x2, y2, bias) and 1
+ * output.  Each CPPN is queried at the (num_obs + 1) x num_act substrate
+ * connections (query q = j * (num_obs + 1) + i), its outputs become policy
+ * weights (clamp to [-1, 1], |y| < weight_threshold -> 0, else rescaled to
+ * max_weight), and the policy a = tanh(W [s, 1]) drives s' = A s + B a for
+ * `steps` steps from s0; fitness = mean reward
+ * -(|s'|^2 / num_obs) - act_cost |a|^2 / num_act.  A is num_obs x num_obs,
+ * B num_obs x num_act (row-major); dynamics run in FP32, reward sums in FP64.
+ * No reference code exists for this config: oracle/hyperneat.c
+ * is the repo's FP64 restatement. */
+typedef struct fnb_hyper_config {
+  int num_obs, num_act, steps;        /* num_obs <= 31, num_act <= 32 */
+  double weight_threshold, max_weight, act_cost;
+} fnb_hyper_config;
+/* host layer: genomes and dynamics from host memory; weights_out
+ * ([P][num_act][num_obs+1] floats) may be NULL */
+int fnb_hyper_evaluate(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
+                       const fnb_hyper_config* cfg, const double* A, const double* B, const double* s0,
+                       double* fitness_out, float* weights_out);
+/* device layer: transformed CPPNs (fnb_transform_d), FP32 dynamics on the device */
+int fnb_hyper_evaluate_d(fnb_ctx* ctx, const void* d_nets, int P, const fnb_hyper_config* cfg, const float* d_A,
+                         const float* d_B, const float* d_s0, double* d_fitness, float* d_weights, void* stream);
+
 /* ---- the generation loop (PAPER Algorithm 1) -------------
  * An evolver owns a device-resident population of cfg->pop_size genomes, the
  * species state (<= 32 species), the fitness vector and the innovation

@@ -219,6 +219,17 @@ int fo_reproduce(const fo_shape* sh, const fo_schema* sc, const fo_neat_cfg* cfg
                  fo_innov* innov, double* next_nodes, double* next_conns,
                  int* parent_a, int* parent_b);
 
+/* ---- HyperNEAT (BASELINE config 4; this repo's definition, hyperneat.c) -- */
+typedef struct {
+  int n_obs, n_act, steps;
+  double weight_threshold, max_weight, act_cost;
+} fo_hyper_cfg;
+void fo_hyper_queries(const fo_hyper_cfg* c, double* q /* [(n_obs+1)*n_act][5] */);
+double fo_hyper_weight(const fo_hyper_cfg* c, double cppn_out);
+void fo_hyper_substrate(const fo_hyper_cfg* c, const double* cppn_out /* Q */, double* W /* [n_act][n_obs+1] */);
+double fo_hyper_rollout(const fo_hyper_cfg* c, const double* W, const double* A, const double* B,
+                        const double* s0);
+
 #ifdef __cplusplus
 }
 #endif

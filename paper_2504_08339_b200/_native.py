@@ -47,6 +47,11 @@ class fnb_neat_config(C.Structure):
                 ("distance", fnb_distance_config)]
 
 
+class fnb_hyper_config(C.Structure):
+    _fields_ = [("num_obs", C.c_int), ("num_act", C.c_int), ("steps", C.c_int), ("weight_threshold", C.c_double),
+                ("max_weight", C.c_double), ("act_cost", C.c_double)]
+
+
 VP = C.c_void_p
 DP = C.POINTER(C.c_double)
 IP = C.POINTER(C.c_int32)
@@ -97,6 +102,9 @@ SIGNATURES = {
     "fnb_evolver_device_state": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)]),
     "fnb_stream_draws_d": (C.c_int, [VP, VP, C.c_int, C.c_int, C.c_int, C.c_uint64, VP, VP]),
     "fnb_split_keys_d": (C.c_int, [VP, U32P, C.c_uint64, C.c_int, VP, VP]),
+    "fnb_hyper_evaluate": (C.c_int, [VP, DP, DP, C.c_int, C.POINTER(fnb_hyper_config), DP, DP, DP, DP,
+                                     C.POINTER(C.c_float)]),
+    "fnb_hyper_evaluate_d": (C.c_int, [VP, VP, C.c_int, C.POINTER(fnb_hyper_config), VP, VP, VP, VP, VP, VP]),
 }
 
 _lib = None

@@ -423,3 +423,51 @@ def _engine_mutate_d(self, nodes, conns, keys, next_key, status, cfg: MutationCo
 
 Engine.mutate = _engine_mutate
 Engine.mutate_d = _engine_mutate_d
+
+
+# ---- BASELINE config 4: HyperNEAT (include/flatneat_b200.h) ----
+
+@dataclass
+class HyperConfig:
+    """Substrate and rollout of config 4: num_obs inputs (+ a bias input),
+    num_act outputs, `steps` steps of s' = A s + B a with a = tanh(W [s, 1])."""
+    num_obs: int = 27
+    num_act: int = 8
+    steps: int = 1000
+    weight_threshold: float = 0.2
+    max_weight: float = 3.0
+    act_cost: float = 0.01
+
+    def to_c(self) -> N.fnb_hyper_config:
+        return N.fnb_hyper_config(self.num_obs, self.num_act, self.steps, self.weight_threshold, self.max_weight,
+                                  self.act_cost)
+
+
+def _engine_hyper_evaluate(self, pop_nodes, pop_conns, cfg: HyperConfig, A, B, s0, weights: bool = False):
+    """Fitness of every CPPN genome as a HyperNEAT policy on the linear-dynamics
+    rollout -> fitness [P] (and the policy weights [P, num_act, num_obs + 1])."""
+    n, c, P = self._check_pop(pop_nodes, pop_conns)
+    a = np.ascontiguousarray(A, dtype=np.float64).reshape(cfg.num_obs, cfg.num_obs)
+    b = np.ascontiguousarray(B, dtype=np.float64).reshape(cfg.num_obs, cfg.num_act)
+    s = np.ascontiguousarray(s0, dtype=np.float64).reshape(cfg.num_obs)
+    fit = np.empty(P, dtype=np.float64)
+    w = np.empty((P, cfg.num_act, cfg.num_obs + 1), dtype=np.float32) if weights else None
+    hc = cfg.to_c()
+    self._raise(self._lib.fnb_hyper_evaluate(self._h, _dp(n), _dp(c), P, C.byref(hc), _dp(a), _dp(b), _dp(s),
+                                             _dp(fit), w.ctypes.data_as(C.POINTER(C.c_float)) if weights else None))
+    return (fit, w) if weights else fit
+
+
+def _engine_hyper_evaluate_d(self, nets, P: int, cfg: HyperConfig, A, B, s0, fitness, weights=None, stream=None):
+    """Device layer: transformed CPPNs `nets` (transform_d), FP32 device A, B, s0;
+    FP64 `fitness` [P] (and FP32 `weights`) written on `stream`."""
+    hc = cfg.to_c()
+    self._raise(self._lib.fnb_hyper_evaluate_d(self._h, nets.data_ptr(), P, C.byref(hc), A.data_ptr(), B.data_ptr(),
+                                               s0.data_ptr(), fitness.data_ptr(),
+                                               weights.data_ptr() if weights is not None else None,
+                                               _stream_handle(stream)))
+    return fitness
+
+
+Engine.hyper_evaluate = _engine_hyper_evaluate
+Engine.hyper_evaluate_d = _engine_hyper_evaluate_d

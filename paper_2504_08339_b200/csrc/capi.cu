@@ -116,6 +116,7 @@ void fnb_ctx_destroy(fnb_ctx* ctx) {
                     &ctx->partial, &ctx->misc, &ctx->scratch})
     b->release();
   ctx->flags.release();
+  ctx->hyper.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) {
     cudaStreamDestroy(ctx->copy_stream);

@@ -37,7 +37,7 @@ struct fnb_ctx {
   cudaStream_t copy_stream = nullptr;
   static constexpr int kMaxChunks = 16;
   cudaEvent_t chunk_ev[kMaxChunks + 1] = {};
-  DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc, scratch, flags;
+  DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc, scratch, flags, hyper;
 };
 
 // errors.hpp:33-57

@@ -86,3 +86,32 @@ def cppn_dataset(side: int = 256):
     X = np.stack([xx.ravel(), yy.ravel(), r.ravel(), np.ones(side * side)], axis=1)
     Y = (0.5 + 0.5 * np.cos(8.0 * np.pi * r)).reshape(-1, 1)
     return X, Y
+
+
+def hyper_dynamics(num_obs: int = 27, num_act: int = 8, seed: int = 0, max_weight: float = 3.0):
+    """C4: fixed seeded linear dynamics s' = A s + B a with
+    |A|_2 = 0.85 and |B|_2 = 0.1 / (max_weight sqrt(num_act (num_obs + 1))), so
+    the closed loop s -> A s + B tanh(W [s, 1]) is a contraction for every
+    policy the substrate can express (|W|_2 <= |W|_F <= max_weight
+    sqrt(num_act (num_obs + 1)), tanh is 1-Lipschitz): rollouts do not
+    amplify rounding, and FP32 and FP64 rollouts stay within 1e-5 relative.
+    s0 ~ U(-1, 1).  Values are rounded to float32 (the device computes in
+    FP32) and returned as float64 A [num_obs, num_obs], B [num_obs, num_act],
+    s0 [num_obs]."""
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((num_obs, num_obs))
+    A *= 0.85 / np.linalg.norm(A, 2)
+    B = rng.standard_normal((num_obs, num_act))
+    B *= 0.1 / (max_weight * np.sqrt(num_act * (num_obs + 1))) / np.linalg.norm(B, 2)
+    s0 = rng.uniform(-1.0, 1.0, num_obs)
+    f = lambda x: x.astype(np.float32).astype(np.float64)
+    return f(A), f(B), f(s0)
+
+
+def cppn_population(P: int, max_nodes: int = 32, max_conns: int = 128, fill: float = 0.75, seed: int = 0):
+    """C4 CPPNs: 5 inputs (x1, y1, x2, y2, bias) and 1 output; activation ids
+    index the 5-function schema CPPN_ACTS."""
+    return synthetic_population(P, max_nodes, max_conns, fill, num_inputs=5, num_outputs=1, n_act=5, seed=seed)
+
+
+CPPN_ACTS = ["tanh", "sin", "sigmoid", "identity", "relu"]

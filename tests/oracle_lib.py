@@ -470,3 +470,56 @@ class OracleEvolution:
         return dict(count=k, ids=np.array([s.id[j] for j in range(k)]), spawn=np.array([s.spawn[j] for j in range(k)]),
                     best=np.array([s.best_fitness[j] for j in range(k)]),
                     stagnation=np.array([s.stagnation[j] for j in range(k)]))
+
+
+# ---- C4 HyperNEAT (oracle/hyperneat.c: this repo's FP64 definition) ----------
+
+class HyperCfg(C.Structure):
+    _fields_ = [("n_obs", C.c_int), ("n_act", C.c_int), ("steps", C.c_int), ("weight_threshold", C.c_double),
+                ("max_weight", C.c_double), ("act_cost", C.c_double)]
+
+
+def hyper_cfg(n_obs=27, n_act=8, steps=1000, threshold=0.2, max_weight=3.0, act_cost=0.01) -> HyperCfg:
+    return HyperCfg(n_obs, n_act, steps, threshold, max_weight, act_cost)
+
+
+def hyper_queries(cfg: HyperCfg) -> np.ndarray:
+    q = np.zeros(((cfg.n_obs + 1) * cfg.n_act, 5))
+    oracle().fo_hyper_queries(C.byref(cfg), ptr(q, F64P))
+    return q
+
+
+def hyper_weight(cfg: HyperCfg, y: float) -> float:
+    lib = oracle()
+    lib.fo_hyper_weight.restype = C.c_double
+    lib.fo_hyper_weight.argtypes = [C.POINTER(HyperCfg), C.c_double]
+    return lib.fo_hyper_weight(C.byref(cfg), y)
+
+
+def hyper_substrate(cfg: HyperCfg, cppn_out) -> np.ndarray:
+    y = np.ascontiguousarray(cppn_out, dtype=np.float64)
+    W = np.zeros((cfg.n_act, cfg.n_obs + 1))
+    oracle().fo_hyper_substrate(C.byref(cfg), ptr(y, F64P), ptr(W, F64P))
+    return W
+
+
+def hyper_rollout(cfg: HyperCfg, W, A, B, s0) -> float:
+    lib = oracle()
+    lib.fo_hyper_rollout.restype = C.c_double
+    w, a, b, s = (np.ascontiguousarray(x, dtype=np.float64) for x in (W, A, B, s0))
+    return lib.fo_hyper_rollout(C.byref(cfg), ptr(w, F64P), ptr(a, F64P), ptr(b, F64P), ptr(s, F64P))
+
+
+def hyper_cppn_outputs(prob: Problem, schema: SchemaSpec, nodes, conns, cfg: HyperCfg, use_ref: bool = True):
+    """[P, Q] CPPN outputs at the substrate queries: the reference's own
+    batch_forward (oracle/_ref) when available, else the C restatement."""
+    X = hyper_queries(cfg)
+    if use_ref and ref_available():
+        st, bad, msg, out = ref_batch_forward(prob, schema, nodes, conns, X)
+        assert st == 0, msg
+        return out[:, :, 0]
+    outs = []
+    for i in range(nodes.shape[0]):
+        net = oracle_transform(prob, schema, nodes[i], conns[i])
+        outs.append(oracle_forward(prob, schema, nodes[i], net, X)[:, 0])
+    return np.stack(outs)

@@ -89,3 +89,41 @@ def test_xor_evolves(fnb):
     best, fit, stats = evolve(eng, cfg, seed=0, X=X, Y=Y, kind=fnb.FIT_OFFSET_SSE, offset=4.0)
     assert stats[-1].best >= stats[0].best
     assert fit > 3.0
+
+
+def test_c1_xor_100_generations_bit_exact(fnb):
+    """North-star bar on BASELINE config 1 (XOR, pop 1000, N_max=16, C_max=32,
+    100 generations): the device evolution state equals the frozen CPU
+    restatement bit for bit after EVERY generation -- population tensors,
+    species table and innovation counter -- with the device's fitness
+    (4 - SSE) handed to both sides."""
+    from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+    from paper_2504_08339_b200.synthetic import xor_dataset
+    acts, aggs = ["sigmoid", "tanh"], ["sum"]
+    prob = ol.Problem(16, 32, [0, 1, 2], [3])
+    schema = ol.SchemaSpec(acts, aggs)
+    eng = fnb.Engine(fnb.GenomeLimits(16, 32), [0, 1, 2], [3], fnb.AttributeSchema(acts, aggs))
+    P = 1000
+    # threshold 1.0 (paper default 3.5 keeps XOR-sized genomes in one species)
+    ev = Evolver(eng, NeatConfig(pop_size=P, compatibility_threshold=1.0), seed=11)
+    orc = ol.OracleEvolution(prob, schema, ol.neat_cfg(P, threshold=1.0), seed=11)
+    ev.init_population()
+    orc.init_population()
+    X, Y = xor_dataset(bias_input=True)
+    species_seen = set()
+    for g in range(100):
+        ev.evaluate(X, Y, fnb.FIT_OFFSET_SSE, 4.0)
+        fit = ev.fitness()
+        orc.step(fit)
+        ev.step()
+        gn, gc = ev.population()
+        # bit for bit, NaN padding included
+        assert np.array_equal(gn.view(np.uint64), orc.nodes.view(np.uint64)), f"gen {g} nodes"
+        assert np.array_equal(gc.view(np.uint64), orc.conns.view(np.uint64)), f"gen {g} conns"
+        sp, so = ev.species(), orc.species_view()
+        assert sp["count"] == so["count"] and np.array_equal(sp["ids"], so["ids"]), g
+        assert np.array_equal(sp["spawn"], so["spawn"]) and np.array_equal(sp["best"], so["best"]), g
+        assert ev.state()[1] == orc.innov.next_key, g
+        species_seen.add(int(sp["count"]))
+    assert ev.state()[0] == 100
+    assert max(species_seen) > 1  # the run exercised speciation, not a single species
