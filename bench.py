@@ -245,6 +245,96 @@ def c4_hyperneat(dev, stream, flush, reps: int = 3):
             "generations_equiv_per_s": 1.0 / t}
 
 
+def c5_generation(dev, flush, gens: int = 4, warm: int = 2):
+    """BASELINE config 5 on one GPU: the full device generation loop (K1+K2
+    evaluation, then speciate / stagnation / spawn / reproduce with K3, K5,
+    K6, K7) at pop 100k, N128/C1024.  The population starts as 2,000
+    distinct synthetic genomes tiled to 100k on the device."""
+    import torch
+    import paper_2504_08339_b200 as fnb
+    from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
+    P5, N5, C5, uniq = 100_000, 128, 1024, 2_000
+    n_h, c_h = synthetic_population(uniq, N5, C5, FILL, NI, NO, seed=5)
+    eng5 = fnb.Engine(fnb.GenomeLimits(N5, C5), list(range(NI)), list(range(NI, NI + NO)), fnb.AttributeSchema(),
+                      device=dev.index)
+    ev = Evolver(eng5, NeatConfig(pop_size=P5), seed=5)
+    nodes = torch.from_numpy(n_h).to(dev).repeat(P5 // uniq, 1, 1)
+    conns = torch.from_numpy(c_h).to(dev).repeat(P5 // uniq, 1, 1)
+    ev.set_population_d(nodes, conns)
+    del nodes, conns
+    X_h, Y_h = regression_dataset(BATCH, NI, NO, seed=0)
+    X = torch.from_numpy(X_h.astype(np.float32)).to(dev)
+    Y = torch.from_numpy(Y_h.astype(np.float32)).to(dev)
+    es = torch.cuda.ExternalStream(ev.stream_handle())
+    gms, ems = [], []
+    for it in range(warm + gens):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(es)
+        ev.evaluate_d(X, Y)
+        e1.record(es)
+        ev.step()
+        e2.record(es)
+        es.synchronize()
+        if it >= warm:
+            gms.append(e0.elapsed_time(e2))
+            ems.append(e0.elapsed_time(e1))
+    sp = ev.species()
+    ev.close()
+    g_ms, e_ms = float(np.mean(gms)), float(np.mean(ems))
+    return {"workload": "C5 generation loop: pop 100k, N128/C1024, B=1024 func-fit, 1 GPU (2k distinct genomes tiled)",
+            "ms_per_generation": g_ms, "generations_per_s": 1e3 / g_ms, "evaluate_ms": e_ms, "evolve_step_ms": g_ms - e_ms,
+            "evals_per_s": P5 * BATCH / (e_ms / 1e3), "species": int(sp["count"]), "generations_timed": gens}
+
+
+def evolved_population(eng, dev, stream, flush, X, Y, gens: int = 100):
+    """K1+K2 on an EVOLVED pop-10k population (100 generations
+    of the device loop from minimal genomes on the C2 func-fit data) -- the
+    topologies a NEAT run actually evaluates, next to the synthetic fill-0.75
+    headline."""
+    import torch
+    import paper_2504_08339_b200 as fnb
+    from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+    ev = Evolver(eng, NeatConfig(pop_size=P_SHARD), seed=7)
+    ev.init_population()
+    es = torch.cuda.ExternalStream(ev.stream_handle())
+    t0 = time.perf_counter()
+    for _ in range(gens):
+        ev.evaluate_d(X, Y)
+        ev.step()
+    es.synchronize()
+    loop_s = time.perf_counter() - t0
+    n_ptr, c_ptr, _, _ = ev.device_state()
+    nh, ch = ev.population()
+    ev.close()
+    nodes, conns = torch.from_numpy(nh).to(dev), torch.from_numpy(ch).to(dev)
+    nets = eng.alloc_nets(P_SHARD)
+    fit = torch.empty(P_SHARD, dtype=torch.float64, device=dev)
+
+    def run():
+        eng.transform_d(nodes, conns, nets, stream)
+        eng.forward_d(nets, P_SHARD, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=stream)
+
+    run()
+    ms = []
+    for _ in range(5):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        run()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = float(np.median(ms)) / 1e3
+    n_nodes = float(np.mean(np.sum(~np.isnan(nh[:, :, 0]), axis=1)))
+    n_en = float(np.mean(np.sum(ch[:, :, 2] == 1.0, axis=1)))
+    return {"workload": f"pop 10k after {gens} device generations from minimal genomes (C2 data, N64/C256)",
+            "mean_nodes": n_nodes, "mean_enabled_conns": n_en, "transform_plus_forward_ms": t * 1e3,
+            "evals_per_s": P_SHARD * BATCH / t, "wall_s_100_generations": loop_s}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -423,6 +513,8 @@ def main():
 
     c3 = c3_cppn(eng, nets, dev, stream, flush) if not args.no_c5 else None
     c4 = c4_hyperneat(dev, stream, flush) if not args.no_c5 else None
+    evo = evolved_population(eng, dev, stream, flush, X, Y) if not args.no_generations else None
+    c5g = c5_generation(dev, flush) if not args.no_c5 and world == 1 else None
     c5 = None
     if not args.no_c5:
         c5 = c5_distance(dev, stream, flush)
@@ -477,6 +569,10 @@ def main():
             line["c3_cppn"] = c3
         if c4 is not None:
             line["c4_hyperneat"] = c4
+        if evo is not None:
+            line["evolved"] = evo
+        if c5g is not None:
+            line["c5_generation"] = c5g
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

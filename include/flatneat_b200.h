@@ -244,6 +244,7 @@ int fnb_hyper_evaluate_d(fnb_ctx* ctx, const void* d_nets, int P, const fnb_hype
 int fnb_evolver_create(fnb_ctx* ctx, const fnb_neat_config* cfg, uint64_t seed, fnb_evolver** out);
 void fnb_evolver_destroy(fnb_evolver* ev);
 int fnb_evolver_init_population(fnb_evolver* ev);  /* initialize_population */
+/* set / get accept host or device pointers (unified addressing) */
 int fnb_evolver_set_population(fnb_evolver* ev, const double* pop_nodes, const double* pop_conns);
 int fnb_evolver_get_population(fnb_evolver* ev, double* pop_nodes, double* pop_conns);
 int fnb_evolver_set_fitness(fnb_evolver* ev, const double* fitness);  /* inject (parity tests) */

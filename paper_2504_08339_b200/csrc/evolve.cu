@@ -891,8 +891,9 @@ int fnb_evolver_init_population(fnb_evolver* ev) {
 int fnb_evolver_set_population(fnb_evolver* ev, const double* nodes, const double* conns) {
   fnb::Evolver& v = ev->ev;
   cudaSetDevice(ev->ctx->device);
-  EV_CK(cudaMemcpyAsync(v.pn[v.cur], nodes, sizeof(double) * v.gn() * v.P, cudaMemcpyHostToDevice, v.st));
-  EV_CK(cudaMemcpyAsync(v.pc[v.cur], conns, sizeof(double) * v.gc() * v.P, cudaMemcpyHostToDevice, v.st));
+  // cudaMemcpyDefault: host or device (UVA) source
+  EV_CK(cudaMemcpyAsync(v.pn[v.cur], nodes, sizeof(double) * v.gn() * v.P, cudaMemcpyDefault, v.st));
+  EV_CK(cudaMemcpyAsync(v.pc[v.cur], conns, sizeof(double) * v.gc() * v.P, cudaMemcpyDefault, v.st));
   EV_CK(cudaStreamSynchronize(v.st));
   return 0;
 }
@@ -900,8 +901,8 @@ int fnb_evolver_set_population(fnb_evolver* ev, const double* nodes, const doubl
 int fnb_evolver_get_population(fnb_evolver* ev, double* nodes, double* conns) {
   fnb::Evolver& v = ev->ev;
   cudaSetDevice(ev->ctx->device);
-  if (nodes) EV_CK(cudaMemcpyAsync(nodes, v.pn[v.cur], sizeof(double) * v.gn() * v.P, cudaMemcpyDeviceToHost, v.st));
-  if (conns) EV_CK(cudaMemcpyAsync(conns, v.pc[v.cur], sizeof(double) * v.gc() * v.P, cudaMemcpyDeviceToHost, v.st));
+  if (nodes) EV_CK(cudaMemcpyAsync(nodes, v.pn[v.cur], sizeof(double) * v.gn() * v.P, cudaMemcpyDefault, v.st));
+  if (conns) EV_CK(cudaMemcpyAsync(conns, v.pc[v.cur], sizeof(double) * v.gc() * v.P, cudaMemcpyDefault, v.st));
   EV_CK(cudaStreamSynchronize(v.st));
   return 0;
 }

@@ -5,12 +5,7 @@
 // synthetic linear-dynamics rollout, one warp per policy.  Semantics:
 // DESIGN.md section 9 (restated in FP64 by oracle/hyperneat.c).
 //
-// The rollout is latency-bound, not bandwidth-bound: a warp keeps the state
-// s and the action a in shared memory (broadcast reads), lane j < n_act
-// holds policy row j in registers, lane i < n_obs holds dynamics row A[i] in
-// registers and reads B[i] from a padded (conflict-free) shared copy.  Each
-// step is two short FMA chains split over two accumulators; the reward
-// reduction is one shfl_xor tree and accumulates in FP64.
+// The rollout is latency-bound, not bandwidth-bound: see k_hyper_rollout.
 #include <algorithm>
 
 #include "fnb_common.cuh"
@@ -49,78 +44,99 @@ __device__ __forceinline__ float hyper_weight(double y, double thr, double wmax)
   return float(v < 0.0 ? -w : w);
 }
 
-__global__ void __launch_bounds__(kHyperWarps * 32)
+// One warp per policy.  Policy: lane l computes part (l % G) of output
+// j = l / G (G lanes per output, a chunk of CH = 32 / G inputs each, weights in
+// registers) and a shfl_xor tree over the G lanes finishes the dot product.
+// Dynamics: lane i < n_obs holds A[i] and B[i] in registers.  s (with the
+// constant bias input s[n_obs] = 1) and a live in per-warp shared memory
+// and are read with broadcast LDS.128.  Each lane sums its reward terms over
+// the steps in FP64; one shfl_xor tree combines them at the end.
+template <int G>
+__global__ void __launch_bounds__(kHyperWarps * 32, G == 4 ? 6 : 3)
 k_hyper_rollout(const double* __restrict__ cppn_out, int P, HyperParams hp, const float* __restrict__ A,
                 const float* __restrict__ B, const float* __restrict__ s0, double* __restrict__ fitness,
                 float* __restrict__ w_out) {
-  __shared__ float sB[kHyperMax * (kHyperMax + 1)];  // B[i][j], row stride n_act | 1
-  __shared__ float sS[kHyperWarps][kHyperMax];
-  __shared__ float sA[kHyperWarps][kHyperMax];
+  constexpr int CH = 32 / G;          // inputs per lane of the policy dot product
+  constexpr int NA = 32 / G;          // max outputs
+  __shared__ __align__(16) float sS[kHyperWarps][kHyperMax];
+  __shared__ __align__(16) float sA[kHyperWarps][kHyperMax];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int no = hp.n_obs, na = hp.n_act, ni = no + 1, Q = ni * na;
-  const int bs = na | 1;
-  for (int t = threadIdx.x; t < no * na; t += blockDim.x) sB[(t / na) * bs + t % na] = B[t];
-  __syncthreads();
   const int g = blockIdx.x * kHyperWarps + warp;
   if (g >= P) return;
-  // policy row `lane` (lanes < n_act) and dynamics row A[lane] (lanes < n_obs)
-  float wr[kHyperMax], ar[kHyperMax];
   const double* y = cppn_out + size_t(g) * Q;
+  // policy weights: output j = lane / G, inputs [part * CH, part * CH + CH)
+  const int j = lane / G, part = lane % G, i0 = part * CH;
+  float wp[CH];
 #pragma unroll
-  for (int i = 0; i < kHyperMax; ++i) {
+  for (int k = 0; k < CH; ++k) {
+    const int i = i0 + k;
     float w = 0.0f;
-    if (lane < na && i < no) w = hyper_weight(y[lane * ni + i], hp.thr, hp.wmax);
-    wr[i] = w;
-    if (w_out && lane < na && i < no) w_out[size_t(g) * Q + lane * ni + i] = w;
+    if (j < na && i < ni) {
+      w = hyper_weight(y[j * ni + i], hp.thr, hp.wmax);
+      if (w_out) w_out[size_t(g) * Q + j * ni + i] = w;
+    }
+    wp[k] = w;
   }
-  const float wbias = lane < na ? hyper_weight(y[lane * ni + no], hp.thr, hp.wmax) : 0.0f;  // the bias input
-  if (w_out && lane < na) w_out[size_t(g) * Q + lane * ni + no] = wbias;
+  // dynamics rows
+  float ar[kHyperMax], br[NA];
 #pragma unroll
   for (int k = 0; k < kHyperMax; ++k) ar[k] = (lane < no && k < no) ? A[lane * no + k] : 0.0f;
+#pragma unroll
+  for (int k = 0; k < NA; ++k) br[k] = (lane < no && k < na) ? B[lane * na + k] : 0.0f;
   float* s = sS[warp];
   float* a = sA[warp];
-  s[lane] = lane < no ? s0[lane] : 0.0f;
+  s[lane] = lane < no ? s0[lane] : (lane == no ? 1.0f : 0.0f);  // s[n_obs] = the bias input
   a[lane] = 0.0f;
   const float inv_obs = 1.0f / float(no), cost = hp.act_cost / float(na);
-  double total = 0.0;
+  const bool owner = part == 0 && j < na;  // the lane that publishes a_j
+  double acc = 0.0;  // this lane's reward terms over the steps
   __syncwarp();
   for (int t = 0; t < hp.steps; ++t) {
     // policy: a_j = tanh(W[j] . [s, 1])
-    float aj = 0.0f;
-    if (lane < na) {
-      float z0 = wbias, z1 = 0.0f;
+    float z0 = 0.0f, z1 = 0.0f;
 #pragma unroll
-      for (int i = 0; i < kHyperMax; i += 2) {
-        z0 = fmaf(wr[i], s[i], z0);  // wr[i >= n_obs] = 0
-        z1 = fmaf(wr[i + 1], s[i + 1], z1);
-      }
-      aj = tanhf(z0 + z1);
-      a[lane] = aj;
+    for (int k = 0; k < CH; k += 4) {
+      const float4 sv = *reinterpret_cast<const float4*>(s + i0 + k);
+      z0 = fmaf(wp[k], sv.x, z0);
+      z1 = fmaf(wp[k + 1], sv.y, z1);
+      z0 = fmaf(wp[k + 2], sv.z, z0);
+      z1 = fmaf(wp[k + 3], sv.w, z1);
     }
+    float z = z0 + z1;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    const float aj = tanhf(z);
+    if (owner) a[j] = aj;
     __syncwarp();
     // dynamics: s'_i = A[i] . s + B[i] . a
-    float v = 0.0f;
-    if (lane < no) {
-      float v0 = 0.0f, v1 = 0.0f;
+    float v0 = 0.0f, v1 = 0.0f, v2 = 0.0f, v3 = 0.0f;
 #pragma unroll
-      for (int k = 0; k < kHyperMax; k += 2) {
-        v0 = fmaf(ar[k], s[k], v0);
-        v1 = fmaf(ar[k + 1], s[k + 1], v1);
-      }
-      const float* br = sB + lane * bs;
-      for (int j = 0; j < na; ++j) v0 = fmaf(br[j], a[j], v0);
-      v = v0 + v1;
+    for (int k = 0; k < kHyperMax; k += 4) {
+      const float4 sv = *reinterpret_cast<const float4*>(s + k);
+      v0 = fmaf(ar[k], sv.x, v0);  // ar[k >= n_obs] = 0 (s[n_obs] is the bias 1)
+      v1 = fmaf(ar[k + 1], sv.y, v1);
+      v2 = fmaf(ar[k + 2], sv.z, v2);
+      v3 = fmaf(ar[k + 3], sv.w, v3);
     }
+#pragma unroll
+    for (int k = 0; k < NA; k += 4) {
+      const float4 av = *reinterpret_cast<const float4*>(a + k);
+      v0 = fmaf(br[k], av.x, v0);
+      v1 = fmaf(br[k + 1], av.y, v1);
+      v2 = fmaf(br[k + 2], av.z, v2);
+      v3 = fmaf(br[k + 3], av.w, v3);
+    }
+    const float v = (v0 + v1) + (v2 + v3);
     __syncwarp();
     if (lane < no) s[lane] = v;
-    // reward: -(sum s'^2)/n_obs - act_cost (sum a^2)/n_act
-    float r = v * v * inv_obs + aj * aj * cost;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    total -= double(r);
+    // reward terms: -(sum s'^2)/n_obs - act_cost (sum a^2)/n_act
+    acc -= double((lane < no ? v * v * inv_obs : 0.0f) + (owner ? aj * aj * cost : 0.0f));
     __syncwarp();
   }
-  if (lane == 0) fitness[g] = total / hp.steps;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) fitness[g] = acc / hp.steps;
 }
 
 cudaError_t launch_hyper_queries(const HyperParams& hp, float* X, cudaStream_t st) {
@@ -131,8 +147,13 @@ cudaError_t launch_hyper_queries(const HyperParams& hp, float* X, cudaStream_t s
 
 cudaError_t launch_hyper_rollout(const double* cppn_out, int P, const HyperParams& hp, const float* A,
                                  const float* B, const float* s0, double* fitness, float* w_out, cudaStream_t st) {
-  k_hyper_rollout<<<(P + kHyperWarps - 1) / kHyperWarps, kHyperWarps * 32, 0, st>>>(cppn_out, P, hp, A, B, s0,
-                                                                                    fitness, w_out);
+  const int grid = (P + kHyperWarps - 1) / kHyperWarps, block = kHyperWarps * 32;
+  if (hp.n_act <= 8)
+    k_hyper_rollout<4><<<grid, block, 0, st>>>(cppn_out, P, hp, A, B, s0, fitness, w_out);
+  else if (hp.n_act <= 16)
+    k_hyper_rollout<2><<<grid, block, 0, st>>>(cppn_out, P, hp, A, B, s0, fitness, w_out);
+  else
+    k_hyper_rollout<1><<<grid, block, 0, st>>>(cppn_out, P, hp, A, B, s0, fitness, w_out);
   return cudaGetLastError();
 }
 

@@ -105,6 +105,22 @@ class Evolver:
         top = int(np.nanmax(keys)) + 1 if np.any(~np.isnan(keys)) else 0
         self._raise(self._lib.fnb_evolver_set_next_key(self._h, max(top, self.state()[1])))
 
+    def set_population_d(self, nodes, conns):
+        """Load a device-resident population (torch float64 tensors on this
+        evolver's GPU, pop_size x limits); the innovation counter moves above
+        its largest key."""
+        import torch
+        P, L = self.cfg.pop_size, self.engine.limits
+        if tuple(nodes.shape) != (P, L.max_nodes, 5) or tuple(conns.shape) != (P, L.max_conns, 4) \
+                or nodes.dtype != torch.float64 or conns.dtype != torch.float64:
+            raise ValueError("population must be float64 tensors [pop_size, max_nodes, 5] / [pop_size, max_conns, 4]")
+        n, c = nodes.contiguous(), conns.contiguous()
+        self._raise(self._lib.fnb_evolver_set_population(self._h, C.cast(n.data_ptr(), N.DP), C.cast(c.data_ptr(), N.DP)))
+        keys = n[:, :, 0]
+        finite = keys[~torch.isnan(keys)]
+        top = int(finite.max().item()) + 1 if finite.numel() else 0
+        self._raise(self._lib.fnb_evolver_set_next_key(self._h, max(top, self.state()[1])))
+
     # -- fitness ----------------------------------------------------------------
     def evaluate(self, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0):
         x = np.ascontiguousarray(X, dtype=np.float64)

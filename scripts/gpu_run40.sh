@@ -1,0 +1,5 @@
+python -c "import paper_2504_08339_b200" 2>/dev/null || { echo "library stale: rebuilding"; python -c "import __graft_entry__ as g; g.build()"; }
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_hyper_rollout -c 1 -f -o gpurun_out/prof41_c4 python -c "
+import json,torch,bench
+dev=torch.device('cuda',0); fl=torch.empty(256<<20,dtype=torch.uint8,device=dev)
+print(json.dumps(bench.c4_hyperneat(dev, torch.cuda.current_stream(), fl, reps=1)))" > /dev/null 2>&1; echo ncu=$?

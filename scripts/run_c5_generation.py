@@ -1,0 +1,15 @@
+"""Run only the C5 generation-loop measurement of bench.py (profiling driver)."""
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+dev = torch.device("cuda", 0)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+g = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+print(json.dumps(bench.c5_generation(dev, flush, gens=g, warm=1)))
