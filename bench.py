@@ -245,13 +245,18 @@ def c4_hyperneat(dev, stream, flush, reps: int = 3):
             "generations_equiv_per_s": 1.0 / t}
 
 
-def c5_generation(dev, flush, gens: int = 4, warm: int = 2):
-    """BASELINE config 5 on one GPU: the full device generation loop (K1+K2
-    evaluation, then speciate / stagnation / spawn / reproduce with K3, K5,
-    K6, K7) at pop 100k, N128/C1024.  The population starts as 2,000
+def c5_generation(dev, flush, world: int = 1, gens: int = 4, warm: int = 2):
+    """BASELINE config 5: the full device generation loop (K1+K2 evaluation,
+    then speciate / stagnation / spawn / reproduce with K3, K5, K6, K7) at
+    pop 100k, N128/C1024, sharded over the job's GPUs: evaluation by genome
+    blocks with the fitness all-gather, and at N > 1 the reproduction too
+    (distributed.py shard_step: children [lo, hi) per rank, then an
+    all-gather of the next population).  The population starts as 2,000
     distinct synthetic genomes tiled to 100k on the device."""
     import torch
+    import torch.distributed as dist
     import paper_2504_08339_b200 as fnb
+    from paper_2504_08339_b200.distributed import DeviceShardBackend, ShardedGeneration
     from paper_2504_08339_b200.evolve import Evolver, NeatConfig
     from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
     P5, N5, C5, uniq = 100_000, 128, 1024, 2_000
@@ -266,27 +271,41 @@ def c5_generation(dev, flush, gens: int = 4, warm: int = 2):
     X_h, Y_h = regression_dataset(BATCH, NI, NO, seed=0)
     X = torch.from_numpy(X_h.astype(np.float32)).to(dev)
     Y = torch.from_numpy(Y_h.astype(np.float32)).to(dev)
-    es = torch.cuda.ExternalStream(ev.stream_handle())
+    sg = ShardedGeneration(DeviceShardBackend(ev, X, Y), shard_step=True)
+    es = sg.backend.stream
     gms, ems = [], []
     for it in range(warm + gens):
         flush.zero_()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(es)
-        ev.evaluate_d(X, Y)
+        sg.evaluate()
         e1.record(es)
-        ev.step()
+        if world > 1:
+            sg.reproduce_sharded()
+        else:
+            ev.step()
         e2.record(es)
-        es.synchronize()
+        torch.cuda.synchronize()
         if it >= warm:
             gms.append(e0.elapsed_time(e2))
             ems.append(e0.elapsed_time(e1))
+    g_ms, e_ms = float(np.mean(gms)), float(np.mean(ems))
+    if world > 1:
+        t = torch.tensor([g_ms, e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        g_ms, e_ms = (float(x) for x in t.tolist())
+    agree = sg.replicas_agree()
     sp = ev.species()
     ev.close()
-    g_ms, e_ms = float(np.mean(gms)), float(np.mean(ems))
-    return {"workload": "C5 generation loop: pop 100k, N128/C1024, B=1024 func-fit, 1 GPU (2k distinct genomes tiled)",
+    return {"workload": f"C5 generation loop: pop 100k, N128/C1024, B=1024 func-fit, {world} GPU(s) "
+                        "(2k distinct genomes tiled)",
             "ms_per_generation": g_ms, "generations_per_s": 1e3 / g_ms, "evaluate_ms": e_ms, "evolve_step_ms": g_ms - e_ms,
-            "evals_per_s": P5 * BATCH / (e_ms / 1e3), "species": int(sp["count"]), "generations_timed": gens}
+            "evals_per_s": P5 * BATCH / (e_ms / 1e3), "species": int(sp["count"]), "generations_timed": gens,
+            "sharding": "evaluation + reproduction by genome blocks" if world > 1 else "single GPU",
+            "replicas_agree": bool(agree), "scaling": "strong", "timing": "max over ranks"}
 
 
 def evolved_population(eng, dev, stream, flush, X, Y, gens: int = 100):
@@ -514,7 +533,7 @@ def main():
     c3 = c3_cppn(eng, nets, dev, stream, flush) if not args.no_c5 else None
     c4 = c4_hyperneat(dev, stream, flush) if not args.no_c5 else None
     evo = evolved_population(eng, dev, stream, flush, X, Y) if not args.no_generations else None
-    c5g = c5_generation(dev, flush) if not args.no_c5 and world == 1 else None
+    c5g = c5_generation(dev, flush, world) if not args.no_c5 else None
     c5 = None
     if not args.no_c5:
         c5 = c5_distance(dev, stream, flush)

@@ -263,6 +263,17 @@ int fnb_evolver_set_fitness_d(fnb_evolver* ev, const double* d_fitness);
    xor next_key << 32, xor generation): replicas of one run agree bit for bit */
 int fnb_evolver_checksum(fnb_evolver* ev, uint64_t* out);
 int fnb_evolver_step(fnb_evolver* ev);
+/* The same step split for sharded reproduction (one process per GPU, the
+ * population replicated): every rank runs step_front (speciate, stagnation,
+ * spawn, parent selection, node-split plans and innovation keys for ALL
+ * slots), then step_back for its slot range [lo, hi) (crossover + mutation
+ * into the next population buffer), the ranks all-gather the next buffer
+ * (fnb_evolver_next_population), and every rank calls step_commit.  Slots
+ * are independent, so the result equals fnb_evolver_step bit for bit. */
+int fnb_evolver_step_front(fnb_evolver* ev);
+int fnb_evolver_step_back(fnb_evolver* ev, int lo, int hi);
+int fnb_evolver_step_commit(fnb_evolver* ev);
+int fnb_evolver_next_population(fnb_evolver* ev, double** d_nodes, double** d_conns);
 /* species arrays have room for 32 entries; species_of[pop_size] may be NULL */
 int fnb_evolver_species(fnb_evolver* ev, int* count, int* ids, int* sizes, int* spawn, double* best,
                         int* stagnation, int* species_of);

@@ -93,6 +93,10 @@ SIGNATURES = {
     "fnb_evolver_evaluate": (C.c_int, [VP, DP, DP, C.c_int, C.c_int, C.c_double]),
     "fnb_evolver_evaluate_d": (C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_double]),
     "fnb_evolver_step": (C.c_int, [VP]),
+    "fnb_evolver_step_front": (C.c_int, [VP]),
+    "fnb_evolver_step_back": (C.c_int, [VP, C.c_int, C.c_int]),
+    "fnb_evolver_step_commit": (C.c_int, [VP]),
+    "fnb_evolver_next_population": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP)]),
     "fnb_evolver_evaluate_range_d": (C.c_int, [VP, C.c_int, C.c_int, VP, VP, C.c_int, C.c_int, C.c_double, VP]),
     "fnb_evolver_set_fitness_d": (C.c_int, [VP, VP]),
     "fnb_evolver_checksum": (C.c_int, [VP, C.POINTER(C.c_uint64)]),

@@ -465,9 +465,9 @@ __global__ void k_species_keys(const int* sorted_idx, int P, const int* species_
 
 __global__ void k_gen_advance(SpeciesDev* sd) { ++sd->generation; }
 
-__global__ void k_first_bad(const int* status, int P, SpeciesDev* sd) {
+__global__ void k_first_bad(const int* status, int n, SpeciesDev* sd, int base) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P && status[i]) atomicMin(&sd->first_bad, i);
+  if (i < n && status[i]) atomicMin(&sd->first_bad, base + i);
 }
 
 __global__ void k_reproduce_plan(const SpeciesDev* sd, const int* members, const double* fitness, int P, Key4 root1,
@@ -514,10 +514,14 @@ size_t distance_scratch_bytes(int S, int N, int C);
 cudaError_t launch_crossover(const double* nodes, const double* conns, const int32_t* fit, const int32_t* oth,
                              const uint32_t* keys, int n, int N, int C, double* cn, double* cc, cudaStream_t st);
 size_t mutate_scratch_bytes(int n);
-cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, int n, const uint8_t* active,
-                          const fnb_mutation_config* m, const DevShape& sh, int* d_next_key, int* d_status,
-                          void* scratch, size_t scratch_bytes, int* d_new_key_out, cudaStream_t st,
-                          long long* launches);
+cudaError_t launch_mutate_plan(const double* nodes, const double* conns, const int32_t* src, const uint32_t* keys,
+                               int n, const uint8_t* active, const fnb_mutation_config* m, const DevShape& sh,
+                               int* d_next_key, void* scratch, size_t scratch_bytes, int* d_new_key_out,
+                               cudaStream_t st, long long* launches);
+cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* keys, int n, int lo, int hi,
+                                const uint8_t* active, const fnb_mutation_config* m, const DevShape& sh,
+                                int* d_status, void* scratch, size_t scratch_bytes, const int* d_new_key,
+                                cudaStream_t st, long long* launches);
 
 struct Evolver {
   NeatCfg cfg;
@@ -704,6 +708,12 @@ struct Evolver {
       e = enqueue_step();
       if (e != cudaSuccess) return e;
     }
+    return read_status_and_swap(host_error);
+  }
+
+  // 12-byte status read after a step; the next buffer becomes current
+  cudaError_t read_status_and_swap(int* host_error) {
+    cudaError_t e;
     int stat[3] = {0, 0, INT_MAX};  // error, count, first_bad
     e = cudaMemcpyAsync(&stat[0], &sd->error, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&stat[1], &sd->count, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -726,8 +736,9 @@ struct Evolver {
         }
   }
 
-  // speciate -> update_stagnation -> compute_spawn_counts -> reproduce
-  cudaError_t enqueue_step() {
+  // speciate -> update_stagnation -> compute_spawn_counts -> parent
+  // selection -> mutation plans + innovation keys (all slots)
+  cudaError_t enqueue_front() {
     const int T = 256, B = (P + T - 1) / T;
     const double th = cfg.threshold;
     const double* n = pn[cur];
@@ -783,16 +794,72 @@ struct Evolver {
     k_reproduce_plan<<<B, T, 0, st>>>(sd, idx_sorted, fitness, P, root1, cfg.genome_elitism, cfg.survival, fit_idx,
                                       oth_idx, xkeys, mkeys, active);
     *launches += 22 + kDistanceLaunches;
-    e = launch_crossover(n, c, fit_idx, oth_idx, xkeys, P, N, C, pn[cur ^ 1], pc[cur ^ 1], st);
+    // mutate phase 1 over all slots (replicated on every rank of a sharded
+    // run): node-split plans read from the fit parents, K7 innovation keys
+    e = launch_mutate_plan(n, c, fit_idx, mkeys, P, active, &mut, sh, next_key, scratch, scratch_bytes, nullptr, st,
+                           launches);
+    return e;
+  }
+
+  // Children [lo, hi) into the next buffer: crossover (K5), then structural
+  // and attribute mutation (K6) with the keys planned by enqueue_front.
+  cudaError_t enqueue_back(int lo, int hi) {
+    if (hi <= lo) return cudaSuccess;
+    const double* n = pn[cur];
+    const double* c = pc[cur];
+    cudaError_t e = launch_crossover(n, c, fit_idx + lo, oth_idx + lo, xkeys + 4 * size_t(lo), hi - lo, N, C,
+                                     pn[cur ^ 1] + size_t(lo) * gn(), pc[cur ^ 1] + size_t(lo) * gc(), st);
     if (e != cudaSuccess) return e;
     ++*launches;
-    e = launch_mutate(pn[cur ^ 1], pc[cur ^ 1], mkeys, P, active, &mut, sh, next_key, status, scratch, scratch_bytes,
-                      nullptr, st, launches);
-    if (e != cudaSuccess) return e;
-    k_first_bad<<<B, T, 0, st>>>(status, P, sd);
-    k_gen_advance<<<1, 1, 0, st>>>(sd);
-    *launches += 2;
+    int* newk = mutate_new_keys();
+    return launch_mutate_apply(pn[cur ^ 1], pc[cur ^ 1], mkeys, P, lo, hi, active, &mut, sh, status, scratch,
+                               scratch_bytes, newk, st, launches);
+  }
+
+  // the K7 key array inside the mutate scratch (layout of mutate.cu mut_scratch)
+  int* mutate_new_keys() const {
+    const size_t H = size_t(table_capacity(P));
+    return reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) + size_t(P) * 8 + H * 8 + size_t(P) * 8);
+  }
+
+  // lowest failing slot among the slots this process produced
+  cudaError_t enqueue_first_bad(int lo, int hi) {
+    const int T = 256;
+    if (hi > lo) {
+      k_first_bad<<<(hi - lo + T - 1) / T, T, 0, st>>>(status + lo, hi - lo, sd, lo);
+      ++*launches;
+    }
     return cudaGetLastError();
+  }
+  // once per generation: the device generation counter the key tree reads
+  cudaError_t enqueue_advance() {
+    k_gen_advance<<<1, 1, 0, st>>>(sd);
+    ++*launches;
+    return cudaGetLastError();
+  }
+
+  // speciate -> update_stagnation -> compute_spawn_counts -> reproduce
+  cudaError_t enqueue_step() {
+    cudaError_t e = enqueue_front();
+    if (e == cudaSuccess) e = enqueue_back(0, P);
+    if (e == cudaSuccess) e = enqueue_first_bad(0, P);
+    if (e == cudaSuccess) e = enqueue_advance();
+    return e;
+  }
+
+  // Sharded reproduction (distributed.py): every rank runs the front on the
+  // replicated population, produces children [lo, hi) (any number of
+  // back calls over disjoint ranges) and the caller all-gathers the next
+  // buffer before commit().
+  cudaError_t front_eager() { return enqueue_front(); }
+  cudaError_t back_eager(int lo, int hi) {
+    cudaError_t e = enqueue_back(lo, hi);
+    if (e == cudaSuccess) e = enqueue_first_bad(lo, hi);
+    return e;
+  }
+  cudaError_t commit(int* host_error) {
+    cudaError_t e = enqueue_advance();
+    return e == cudaSuccess ? read_status_and_swap(host_error) : e;
   }
 };
 
@@ -969,6 +1036,35 @@ int fnb_evolver_step(fnb_evolver* ev) {
   EV_CK(ev->ev.step(&err));
   if (err == -2) return fnb_set_error(ev->ctx, FNB_E_EVAL_ERROR, "spawn counts do not sum to pop_size", -1);
   if (err >= 0) return fnb_set_error(ev->ctx, FNB_E_DUPLICATE_KEY, "mutation failed in child slot", err);
+  return 0;
+}
+
+int fnb_evolver_step_front(fnb_evolver* ev) {
+  cudaSetDevice(ev->ctx->device);
+  EV_CK(ev->ev.front_eager());
+  return 0;
+}
+
+int fnb_evolver_step_back(fnb_evolver* ev, int lo, int hi) {
+  if (lo < 0 || hi > ev->ev.P || lo > hi) return fnb_set_error(ev->ctx, FNB_E_CONFIG_ERROR, "slot range out of bounds", -1);
+  cudaSetDevice(ev->ctx->device);
+  EV_CK(ev->ev.back_eager(lo, hi));
+  return 0;
+}
+
+int fnb_evolver_step_commit(fnb_evolver* ev) {
+  cudaSetDevice(ev->ctx->device);
+  int err = -1;
+  EV_CK(ev->ev.commit(&err));
+  if (err == -2) return fnb_set_error(ev->ctx, FNB_E_EVAL_ERROR, "spawn counts do not sum to pop_size", -1);
+  if (err >= 0) return fnb_set_error(ev->ctx, FNB_E_DUPLICATE_KEY, "mutation failed in child slot", err);
+  return 0;
+}
+
+int fnb_evolver_next_population(fnb_evolver* ev, double** d_nodes, double** d_conns) {
+  fnb::Evolver& v = ev->ev;
+  if (d_nodes) *d_nodes = v.pn[v.cur ^ 1];
+  if (d_conns) *d_conns = v.pc[v.cur ^ 1];
   return 0;
 }
 

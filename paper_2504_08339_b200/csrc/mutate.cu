@@ -84,17 +84,21 @@ __device__ __forceinline__ int warp_kth(int n, int k, F pred) {
 // plan_node_split (ops.hpp:196-217)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128)
-k_mutate_plan(const double* __restrict__ nodes, const double* __restrict__ conns, const uint32_t* __restrict__ keys,
-              int n_children, const uint8_t* __restrict__ active, int N, int C, MutCfgDev cfg,
-              unsigned long long* __restrict__ plan_pair, int* __restrict__ plan_flag) {
+k_mutate_plan(const double* __restrict__ nodes, const double* __restrict__ conns, const int32_t* __restrict__ src,
+              const uint32_t* __restrict__ keys, int n_children, const uint8_t* __restrict__ active, int N, int C,
+              MutCfgDev cfg, unsigned long long* __restrict__ plan_pair, int* __restrict__ plan_flag) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= n_children) return;
   int split = 0;
   unsigned long long pair = 0;
   if ((!active || active[c]) && cfg.node_add > 0.0) {
-    const double* n = nodes + size_t(c) * N * kNodeCols;
-    const double* cc = conns + size_t(c) * C * kConnCols;
+    // the plan reads only structure (keys, endpoints, enabled flags, empty
+    // rows), which a crossover child inherits unchanged from its fit parent
+    // (ops.hpp:382-407): `src` lets the plan run on that parent instead
+    const size_t gsrc = size_t(src ? src[c] : c);
+    const double* n = nodes + gsrc * N * kNodeCols;
+    const double* cc = conns + gsrc * C * kConnCols;
     Stream s(key_split(load_key(keys, c), 0));
     int coin = 0;
     if (lane == 0) coin = s.coin(cfg.node_add);
@@ -758,55 +762,107 @@ size_t mutate_scratch_bytes(int n) {
   return size_t(n) * (8 + 4 + 4 + 4) + H * 12 + 64;
 }
 
-cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, int n, const uint8_t* active,
-                          const fnb_mutation_config* m, const DevShape& sh, int* d_next_key, int* d_status,
-                          void* scratch, size_t scratch_bytes, int* d_new_key_out, cudaStream_t st,
-                          long long* launches) {
-  if (n <= 0) return cudaSuccess;
-  const int N = sh.N, C = sh.C;
-  MutCfgDev cfg{m->node_add, m->node_delete, m->conn_add, m->conn_delete,
-                m->bias.init_mean, m->bias.init_std, m->bias.mutate_power, m->bias.mutate_rate, m->bias.replace_rate,
-                m->response.init_mean, m->response.init_std, m->response.mutate_power, m->response.mutate_rate,
-                m->response.replace_rate,
-                m->weight.init_mean, m->weight.init_std, m->weight.mutate_power, m->weight.mutate_rate,
-                m->weight.replace_rate,
-                m->activation_replace_rate, m->aggregation_replace_rate, sh.n_act, sh.n_agg, sh.default_act,
-                sh.default_agg};
-  const int H = table_capacity(n);
+static MutCfgDev mut_cfg_dev(const fnb_mutation_config* m, const DevShape& sh) {
+  return MutCfgDev{m->node_add, m->node_delete, m->conn_add, m->conn_delete,
+                   m->bias.init_mean, m->bias.init_std, m->bias.mutate_power, m->bias.mutate_rate, m->bias.replace_rate,
+                   m->response.init_mean, m->response.init_std, m->response.mutate_power, m->response.mutate_rate,
+                   m->response.replace_rate,
+                   m->weight.init_mean, m->weight.init_std, m->weight.mutate_power, m->weight.mutate_rate,
+                   m->weight.replace_rate,
+                   m->activation_replace_rate, m->aggregation_replace_rate, sh.n_act, sh.n_agg, sh.default_act,
+                   sh.default_agg};
+}
+
+struct MutScratch {
+  unsigned long long *pair, *tkeys;
+  int *flag, *rank, *newk, *tmin;
+  int H;
+};
+static bool mut_scratch(void* scratch, size_t scratch_bytes, int n, int* d_new_key_out, MutScratch* ms) {
+  ms->H = table_capacity(n);
   uint8_t* p = static_cast<uint8_t*>(scratch);
-  auto* pair = reinterpret_cast<unsigned long long*>(p); p += size_t(n) * 8;
-  auto* tkeys = reinterpret_cast<unsigned long long*>(p); p += size_t(H) * 8;
-  int* flag = reinterpret_cast<int*>(p); p += size_t(n) * 4;
-  int* rank = reinterpret_cast<int*>(p); p += size_t(n) * 4;
-  int* newk = d_new_key_out ? d_new_key_out : reinterpret_cast<int*>(p);
+  ms->pair = reinterpret_cast<unsigned long long*>(p); p += size_t(n) * 8;
+  ms->tkeys = reinterpret_cast<unsigned long long*>(p); p += size_t(ms->H) * 8;
+  ms->flag = reinterpret_cast<int*>(p); p += size_t(n) * 4;
+  ms->rank = reinterpret_cast<int*>(p); p += size_t(n) * 4;
+  ms->newk = d_new_key_out ? d_new_key_out : reinterpret_cast<int*>(p);
   p += size_t(n) * 4;
-  int* tmin = reinterpret_cast<int*>(p); p += size_t(H) * 4;
-  if (size_t(p - static_cast<uint8_t*>(scratch)) > scratch_bytes) return cudaErrorInvalidValue;
-  const int wpb = 4;
-  k_mutate_plan<<<(n + wpb - 1) / wpb, 32 * wpb, 0, st>>>(nodes, conns, keys, n, active, N, C, cfg, pair, flag);
-  k7_init<<<(H + 255) / 256, 256, 0, st>>>(tkeys, tmin, H);
-  k7_insert<<<(n + 255) / 256, 256, 0, st>>>(pair, flag, n, tkeys, tmin, H);
-  k7_rank<<<1, 1024, 0, st>>>(pair, flag, n, tkeys, tmin, H, rank, d_next_key);
-  k7_assign<<<(n + 255) / 256, 256, 0, st>>>(pair, flag, n, tkeys, tmin, H, rank, d_next_key, newk);
+  ms->tmin = reinterpret_cast<int*>(p); p += size_t(ms->H) * 4;
+  return size_t(p - static_cast<uint8_t*>(scratch)) <= scratch_bytes;
+}
+
+// Phase 1 of mutate for n slots: the node-split plan (stream split(0)) and the
+// K7 innovation keys, in slot order over ALL n slots.  `src` (may be null)
+// maps slot c to the genome its structure is read from (the fit parent).
+cudaError_t launch_mutate_plan(const double* nodes, const double* conns, const int32_t* src, const uint32_t* keys,
+                               int n, const uint8_t* active, const fnb_mutation_config* m, const DevShape& sh,
+                               int* d_next_key, void* scratch, size_t scratch_bytes, int* d_new_key_out,
+                               cudaStream_t st, long long* launches) {
+  if (n <= 0) return cudaSuccess;
+  const MutCfgDev cfg = mut_cfg_dev(m, sh);
+  MutScratch ms;
+  if (!mut_scratch(scratch, scratch_bytes, n, d_new_key_out, &ms)) return cudaErrorInvalidValue;
+  const int wpb = 4, H = ms.H;
+  k_mutate_plan<<<(n + wpb - 1) / wpb, 32 * wpb, 0, st>>>(nodes, conns, src, keys, n, active, sh.N, sh.C, cfg, ms.pair,
+                                                          ms.flag);
+  k7_init<<<(H + 255) / 256, 256, 0, st>>>(ms.tkeys, ms.tmin, H);
+  k7_insert<<<(n + 255) / 256, 256, 0, st>>>(ms.pair, ms.flag, n, ms.tkeys, ms.tmin, H);
+  k7_rank<<<1, 1024, 0, st>>>(ms.pair, ms.flag, n, ms.tkeys, ms.tmin, H, ms.rank, d_next_key);
+  k7_assign<<<(n + 255) / 256, 256, 0, st>>>(ms.pair, ms.flag, n, ms.tkeys, ms.tmin, H, ms.rank, d_next_key,
+                                              ms.newk);
   k7_advance<<<1, 1, 0, st>>>(d_next_key);
+  *launches += 6;
+  return cudaGetLastError();
+}
+
+// Phase 2 for slots [lo, hi) of the n planned ones: structural mutations
+// (node split with its K7 key, conn add, node / conn delete) and attributes.
+// Slots are independent, so any partition of [0, n) gives the same genomes.
+cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* keys, int n, int lo, int hi,
+                                const uint8_t* active, const fnb_mutation_config* m, const DevShape& sh,
+                                int* d_status, void* scratch, size_t scratch_bytes, const int* d_new_key,
+                                cudaStream_t st, long long* launches) {
+  if (hi <= lo) return cudaSuccess;
+  const int N = sh.N, C = sh.C, k = hi - lo;
+  const MutCfgDev cfg = mut_cfg_dev(m, sh);
+  MutScratch ms;
+  if (!mut_scratch(scratch, scratch_bytes, n, const_cast<int*>(d_new_key), &ms)) return cudaErrorInvalidValue;
+  double* nd = nodes + size_t(lo) * N * kNodeCols;
+  double* cd = conns + size_t(lo) * C * kConnCols;
+  const uint32_t* ky = keys + 4 * size_t(lo);
+  const uint8_t* ac = active ? active + lo : nullptr;
   const size_t per_warp = align16(mut_smem_bytes(N, C));
   int warps = 4;
   while (warps > 1 && per_warp * warps > 96 * 1024) warps >>= 1;
   cudaError_t e = cudaFuncSetAttribute(k_mutate_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(per_warp * warps));
   if (e != cudaSuccess) return e;
-  k_mutate_apply<<<(n + warps - 1) / warps, 32 * warps, per_warp * warps, st>>>(
-      nodes, conns, keys, n, active, N, C, cfg, sh, flag, pair, newk, d_status, per_warp);
+  k_mutate_apply<<<(k + warps - 1) / warps, 32 * warps, per_warp * warps, st>>>(
+      nd, cd, ky, k, ac, N, C, cfg, sh, ms.flag + lo, ms.pair + lo, ms.newk + lo, d_status + lo, per_warp);
   const int win = attr_window(N, C, attr_per_node(cfg));
   const size_t aw = attr_smem_bytes(N, C, win);
   int awarps = 8;
   while (awarps > 1 && aw * awarps > 96 * 1024) awarps >>= 1;
   e = cudaFuncSetAttribute(k_mutate_attrs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(aw * awarps));
   if (e != cudaSuccess) return e;
-  k_mutate_attrs<<<(n + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nodes, conns, keys, n, active, d_status,
-                                                                             N, C, cfg, sh, win, aw);
-  *launches += 8;
+  k_mutate_attrs<<<(k + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nd, cd, ky, k, ac, d_status + lo, N, C,
+                                                                             cfg, sh, win, aw);
+  *launches += 2;
   return cudaGetLastError();
+}
+
+// plan -> K7 -> apply over all n slots, on `st`
+cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, int n, const uint8_t* active,
+                          const fnb_mutation_config* m, const DevShape& sh, int* d_next_key, int* d_status,
+                          void* scratch, size_t scratch_bytes, int* d_new_key_out, cudaStream_t st,
+                          long long* launches) {
+  cudaError_t e = launch_mutate_plan(nodes, conns, nullptr, keys, n, active, m, sh, d_next_key, scratch,
+                                     scratch_bytes, d_new_key_out, st, launches);
+  if (e != cudaSuccess) return e;
+  MutScratch ms;
+  if (!mut_scratch(scratch, scratch_bytes, n, d_new_key_out, &ms)) return cudaErrorInvalidValue;
+  return launch_mutate_apply(nodes, conns, keys, n, 0, n, active, m, sh, d_status, scratch, scratch_bytes, ms.newk,
+                             st, launches);
 }
 
 }  // namespace fnb

@@ -14,6 +14,15 @@ RngKey) -- every random decision is a Philox draw keyed by (generation, slot)
   all-gathered (`all_gather_into_tensor`, padded to the largest shard) and
   injected device-to-device before the step.
 
+With `shard_step=True` the reproduction is sharded too (config 5 scale,
+where crossover + mutation dominate the step): every rank runs the step's
+front -- speciation, stagnation, spawn, parent selection, node-split plans
+and innovation keys for ALL slots (cheap, replicated) -- then produces only
+its own children [lo, hi) (K5 + K6), and the next population is all-gathered
+(`all_gather_into_tensor` of the node and connection rows) before every rank
+commits it.  Children are independent given the plans, so the population
+stays bit-identical to the replicated step.
+
 Fitness is partition-invariant on the device (forward.cu sums fixed
 32-sample units in order), so an N-rank run reproduces the 1-GPU run bit for
 bit.  The orchestration here is backend-neutral: `DeviceShardBackend` drives
@@ -47,11 +56,14 @@ class ShardedGeneration:
     device), evaluate_range(lo, hi, out), set_fitness(full), step(),
     checksum() -> int, and the stream hooks before_collective() /
     after_collective() that order the backend's work against the
-    collective's stream."""
+    collective's stream; for `shard_step` also step_front(),
+    step_back(lo, hi), next_population() -> (nodes, conns) tensors that alias
+    the next population, and step_commit()."""
 
-    def __init__(self, backend, group: Optional[dist.ProcessGroup] = None):
+    def __init__(self, backend, group: Optional[dist.ProcessGroup] = None, shard_step: bool = False):
         self.backend = backend
         self.group = group
+        self.shard_step = shard_step
         if dist.is_available() and dist.is_initialized():
             self.world = dist.get_world_size(group)
             self.rank = dist.get_rank(group)
@@ -89,8 +101,45 @@ class ShardedGeneration:
 
     def generation(self) -> torch.Tensor:
         fit = self.evaluate()
-        self.backend.step()
+        if self.world == 1 or not self.shard_step:
+            self.backend.step()
+        else:
+            self.reproduce_sharded()
         return fit
+
+    def _gather_rows(self, t: torch.Tensor):
+        """All-gather t's row blocks [lo, hi) of every rank into t itself."""
+        lo, hi = self.bounds[self.rank]
+        row = t[0].numel()
+        local = self._scratch(self.shard * row, t)
+        local[:(hi - lo) * row].copy_(t[lo:hi].reshape(-1))
+        flat = t.view(-1)
+        if self.shard * self.world == t.shape[0]:  # equal shards: gather straight into place
+            dist.all_gather_into_tensor(flat, local, group=self.group)
+        else:  # padded blocks, then back into population order
+            padded = self._scratch(self.shard * self.world * row, t, slot=1)
+            dist.all_gather_into_tensor(padded, local, group=self.group)
+            for r, (a, b) in enumerate(self.bounds):
+                flat[a * row:b * row].copy_(padded[r * self.shard * row:(r * self.shard + b - a) * row])
+
+    def _scratch(self, n: int, like: torch.Tensor, slot: int = 0) -> torch.Tensor:
+        key = (slot, n, like.dtype, like.device)
+        bufs = self.__dict__.setdefault("_bufs", {})
+        if key not in bufs:
+            bufs[key] = torch.empty(n, dtype=like.dtype, device=like.device)
+        return bufs[key]
+
+    def reproduce_sharded(self):
+        """The step with this rank producing only children [lo, hi)."""
+        lo, hi = self.bounds[self.rank]
+        self.backend.step_front()
+        self.backend.step_back(lo, hi)
+        nodes, conns = self.backend.next_population()
+        self.backend.before_collective()
+        self._gather_rows(nodes)
+        self._gather_rows(conns)
+        self.backend.after_collective()
+        self.backend.step_commit()
 
     def replicas_agree(self) -> bool:
         """True when every rank holds the same population (checksum gather)."""
@@ -135,6 +184,18 @@ class DeviceShardBackend:
 
     def step(self):
         self.ev.step()
+
+    def step_front(self):
+        self.ev.step_front()
+
+    def step_back(self, lo: int, hi: int):
+        self.ev.step_back(lo, hi)
+
+    def next_population(self):
+        return self.ev.next_population_d()
+
+    def step_commit(self):
+        self.ev.step_commit()
 
     def checksum(self) -> int:
         return self.ev.checksum()

@@ -168,6 +168,31 @@ class Evolver:
     def step(self):
         self._raise(self._lib.fnb_evolver_step(self._h))
 
+    # -- the step split for sharded reproduction (distributed.py) -------------------
+    def step_front(self):
+        """Speciate, stagnation, spawn, parent selection, split plans and
+        innovation keys for all slots (fnb_evolver_step_front)."""
+        self._raise(self._lib.fnb_evolver_step_front(self._h))
+
+    def step_back(self, lo: int, hi: int):
+        """Children [lo, hi) into the next population buffer."""
+        self._raise(self._lib.fnb_evolver_step_back(self._h, lo, hi))
+
+    def step_commit(self):
+        """The next buffer becomes the population (after the all-gather)."""
+        self._raise(self._lib.fnb_evolver_step_commit(self._h))
+
+    def next_population_d(self):
+        """Zero-copy torch views (float64) of the next population buffer:
+        nodes [pop_size, max_nodes, 5], conns [pop_size, max_conns, 4]."""
+        import torch
+        n, c = C.c_void_p(), C.c_void_p()
+        self._raise(self._lib.fnb_evolver_next_population(self._h, C.byref(n), C.byref(c)))
+        P, L = self.cfg.pop_size, self.engine.limits
+        dev = torch.device("cuda", self.engine.device)
+        return (torch.as_tensor(_DeviceArray(n.value, (P, L.max_nodes, 5)), device=dev),
+                torch.as_tensor(_DeviceArray(c.value, (P, L.max_conns, 4)), device=dev))
+
     def species(self):
         cnt = C.c_int(0)
         ids = np.zeros(32, dtype=np.int32)
@@ -192,6 +217,14 @@ class Evolver:
         n, c, f, s = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         self._raise(self._lib.fnb_evolver_device_state(self._h, C.byref(n), C.byref(c), C.byref(f), C.byref(s)))
         return n.value, c.value, f.value, s.value
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ for a float64 device buffer owned by the library."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
 
 
 def torch_float64():

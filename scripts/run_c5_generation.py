@@ -12,4 +12,4 @@ import bench  # noqa: E402
 dev = torch.device("cuda", 0)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 g = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-print(json.dumps(bench.c5_generation(dev, flush, gens=g, warm=1)))
+print(json.dumps(bench.c5_generation(dev, flush, 1, gens=g, warm=1)))

@@ -72,28 +72,50 @@ class OracleShardBackend:
     def step(self):
         self.orc.step(self.fitness)
 
+    # sharded reproduction: the oracle computes every child; step_back copies
+    # only this rank's slots into the next buffers (the rest stay NaN until
+    # the all-gather fills them)
+    def step_front(self):
+        self.orc.step(self.fitness)
+        self.staged = (self.orc.nodes.copy(), self.orc.conns.copy())
+        self.next = (torch.full(self.staged[0].shape, float("nan"), dtype=torch.float64),
+                     torch.full(self.staged[1].shape, float("nan"), dtype=torch.float64))
+
+    def step_back(self, lo, hi):
+        self.next[0][lo:hi] = torch.from_numpy(self.staged[0][lo:hi])
+        self.next[1][lo:hi] = torch.from_numpy(self.staged[1][lo:hi])
+        self.produced = getattr(self, "produced", []) + [(lo, hi)]
+
+    def next_population(self):
+        return self.next
+
+    def step_commit(self):
+        self.orc.nodes = self.next[0].numpy().copy()
+        self.orc.conns = self.next[1].numpy().copy()
+
     def checksum(self):
         return host_checksum(self.orc.nodes, self.orc.conns)
 
 
-def _run(world, rank, P, G, port, outdir):
+def _run(world, rank, P, G, port, outdir, shard_step=False):
     if world > 1:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
     be = OracleShardBackend(P)
-    sg = ShardedGeneration(be)
+    sg = ShardedGeneration(be, shard_step=shard_step)
     fits = []
     for _ in range(G):
         fits.append(sg.generation()[:P].numpy().copy())
     agree = sg.replicas_agree()
     np.savez(os.path.join(outdir, f"w{world}_r{rank}.npz"), fits=np.array(fits), nodes=be.orc.nodes,
-             conns=be.orc.conns, evaluated=np.array(be.evaluated), agree=agree, next_key=be.orc.innov.next_key)
+             conns=be.orc.conns, evaluated=np.array(be.evaluated), agree=agree, next_key=be.orc.innov.next_key,
+             produced=np.array(getattr(be, "produced", [])))
     if world > 1:
         dist.destroy_process_group()
 
 
-def _worker(rank, world, P, G, port, outdir):
-    _run(world, rank, P, G, port, outdir)
+def _worker(rank, world, P, G, port, outdir, shard_step=False):
+    _run(world, rank, P, G, port, outdir, shard_step)
 
 
 def _free_port():
@@ -117,11 +139,12 @@ def test_shard_bounds_rejects_bad_rank():
         shard_bounds(10, 2, 2)
 
 
-@pytest.mark.parametrize("P", [24, 25])  # even split, and the padded gather
-def test_sharded_generations_match_single_process(tmp_path, P):
+@pytest.mark.parametrize("P,shard_step", [(24, False), (25, False), (24, True), (25, True)])
+def test_sharded_generations_match_single_process(tmp_path, P, shard_step):
+    """Even split and the padded gather; replicated step and sharded reproduction."""
     G = 3
     _run(1, 0, P, G, 0, str(tmp_path))
-    mp.spawn(_worker, args=(2, P, G, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, P, G, _free_port(), str(tmp_path), shard_step), nprocs=2, join=True)
     one = np.load(tmp_path / "w1_r0.npz")
     for r in range(2):
         d = np.load(tmp_path / f"w2_r{r}.npz")
@@ -133,6 +156,8 @@ def test_sharded_generations_match_single_process(tmp_path, P):
         np.testing.assert_array_equal(d["conns"], one["conns"])
         assert int(d["next_key"]) == int(one["next_key"])
         assert bool(d["agree"])
+        if shard_step:  # each rank produced only its own children, every generation
+            assert [tuple(x) for x in d["produced"]] == [(lo, hi)] * G
 
 
 def test_host_checksum_sensitive():

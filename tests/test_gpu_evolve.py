@@ -127,3 +127,41 @@ def test_c1_xor_100_generations_bit_exact(fnb):
         species_seen.add(int(sp["count"]))
     assert ev.state()[0] == 100
     assert max(species_seen) > 1  # the run exercised speciation, not a single species
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3])
+def test_split_step_equals_step(fnb, parts):
+    """fnb_evolver_step_front / step_back(lo, hi) / step_commit -- the sharded
+    reproduction of distributed.py -- over `parts` slot ranges on one GPU give
+    the population, species table and innovation counter of fnb_evolver_step
+    bit for bit, generation after generation."""
+    from paper_2504_08339_b200.distributed import shard_bounds
+    from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+    from paper_2504_08339_b200.synthetic import regression_dataset
+    acts = ["tanh", "sigmoid", "identity"]
+    eng = fnb.Engine(fnb.GenomeLimits(24, 80), [0, 1, 2], [3], fnb.AttributeSchema(acts, ["sum", "product"]))
+    m = fnb.MutationConfig()
+    m.node_add, m.conn_add, m.node_delete = 0.5, 0.6, 0.1
+    cfg = NeatConfig(pop_size=301, compatibility_threshold=0.8, max_species=8, mutation=m)
+    a, b = Evolver(eng, cfg, seed=99), Evolver(eng, cfg, seed=99)
+    a.init_population()
+    b.init_population()
+    X, Y = regression_dataset(64, 3, 1, seed=4)
+    for g in range(8):
+        a.evaluate(X, Y)
+        b.set_fitness(a.fitness())
+        a.step()
+        b.step_front()
+        for r in range(parts):
+            b.step_back(*shard_bounds(301, parts, r))
+        b.step_commit()
+        an, ac = a.population()
+        bn, bc = b.population()
+        assert np.array_equal(an.view(np.uint64), bn.view(np.uint64)), g
+        assert np.array_equal(ac.view(np.uint64), bc.view(np.uint64)), g
+        sa, sb = a.species(), b.species()
+        assert sa["count"] == sb["count"] and np.array_equal(sa["spawn"], sb["spawn"]), g
+        assert a.state() == b.state(), g
+    # the next-population views alias the library's buffer
+    n_view, c_view = b.next_population_d()
+    assert tuple(n_view.shape) == (301, 24, 5) and tuple(c_view.shape) == (301, 80, 4)
