@@ -11,7 +11,8 @@
 //   k_mutate_apply  one warp per child: split(1) new node + two connections,
 //                   split(2) connection add (16 probes, then the sorted
 //                   fallback scan, with creates_cycle answered from a
-//                   reachability closure bitset), split(3) node delete,
+//                   successor bitsets + per-probe BFS; the closure only for
+//                   the exhaustive fallback), split(3) node delete,
 //                   split(4) connection delete, split(5) attribute pass.
 // Row scans (first empty row, k-th enabled row, cascades) are warp ballots;
 // every RngStream is owned by lane 0 so its draws are consumed in exactly
@@ -204,6 +205,8 @@ struct MutSmem {
   int* list_b;                // [N]
   uint8_t* nflag;             // [N] bit0 non-empty, bit1 input, bit2 output
   uint8_t* cflag;             // [C] bit0 non-empty, bit1 enabled
+  int* probe;                 // [32] the 16 candidate (from, to) pairs of pick_new_conn
+  uint32_t* bfs;              // [3W] visited / frontier / next row bitsets
 };
 
 __host__ __device__ inline size_t mut_smem_bytes(int N, int C) {
@@ -212,6 +215,7 @@ __host__ __device__ inline size_t mut_smem_bytes(int N, int C) {
   b += size_t(N) * W * 4 + size_t(2 * N) * 4;      // reach, sbuf
   b += size_t(N) * 4 * 3 + size_t(C) * 4 * 2;      // nkey, list_a, list_b, cin, cout
   b += size_t(N) + size_t(C) + 64;                 // flags, slack
+  b += 32 * 4 + size_t(3 * W) * 4 + 16;            // probes, BFS bitsets
   return align16(b);
 }
 
@@ -230,8 +234,49 @@ __device__ inline MutSmem mut_carve(uint8_t* p, int N, int C) {
   s.cin = reinterpret_cast<int*>(p); p += size_t(C) * 4;
   s.cout = reinterpret_cast<int*>(p); p += size_t(C) * 4;
   s.nflag = p; p += N;
-  s.cflag = p;
+  s.cflag = p; p += C;
+  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  s.probe = reinterpret_cast<int*>(p); p += 32 * 4;
+  s.bfs = reinterpret_cast<uint32_t*>(p);
   return s;
+}
+
+// Warp-collective: is row `dst` reachable from row `src` along the successor
+// bitsets succ[N][W] (one enabled edge at least)?  Level-synchronous BFS; it
+// touches only the part of the graph below `src`, where the all-pairs closure
+// costs N^3/32 bit operations per child.
+__device__ inline bool warp_reaches(const uint32_t* succ, int src, int dst, int N, int W, uint32_t* bfs) {
+  const int lane = threadIdx.x & 31;
+  uint32_t* vis = bfs;
+  uint32_t* fr = bfs + W;
+  uint32_t* nx = bfs + 2 * W;
+  for (int w = lane; w < W; w += 32) {
+    const uint32_t b = (src >> 5) == w ? 1u << (src & 31) : 0u;
+    vis[w] = 0u;  // src itself counts only if a path returns to it
+    fr[w] = b;
+    nx[w] = 0u;
+  }
+  __syncwarp();
+  for (;;) {
+    for (int q = lane; q < N; q += 32)
+      if ((fr[q >> 5] >> (q & 31)) & 1u)
+        for (int w = 0; w < W; ++w) {
+          const uint32_t v = succ[q * W + w];
+          if (v) atomicOr(&nx[w], v);
+        }
+    __syncwarp();
+    bool grew = false;
+    for (int w = lane; w < W; w += 32) {
+      const uint32_t n = nx[w] & ~vis[w];
+      fr[w] = n;
+      vis[w] |= n;
+      nx[w] = 0u;
+      grew = grew || n != 0u;
+    }
+    __syncwarp();
+    if ((vis[dst >> 5] >> (dst & 31)) & 1u) return true;
+    if (!__any_sync(kFullMask, grew)) return false;
+  }
 }
 
 __device__ __forceinline__ bool is_key_in(int key, const int* ks, int n) {
@@ -481,19 +526,21 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
             table_insert(sm.ckeys, sm.crows, Hc - 1,
                          (static_cast<unsigned long long>(uint32_t(sm.cin[q])) << 32) | uint32_t(sm.cout[q]), q);
         __syncwarp();
-        for (int q = lane; q < C; q += 32) {
-          if (sm.cflag[q] != 3) continue;  // enabled edges only (ops.hpp:106)
+        for (int q = lane; q < C; q += 32) {  // successor bitsets over enabled edges (ops.hpp:106)
+          if (sm.cflag[q] != 3) continue;
           const int a = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(sm.cin[q]));
           const int b = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(sm.cout[q]));
           if (a >= 0 && b >= 0) atomicOr(&sm.reach[a * W + (b >> 5)], 1u << (b & 31));
         }
+        // the 16 probes of pick_new_conn (ops.hpp:256-266): their draws do not
+        // depend on the legality of earlier probes, so lane 0 draws them all
+        if (lane == 0)
+          for (int p = 0; p < 16; ++p) {
+            sm.probe[2 * p] = sm.list_a[s.index(nk)];
+            sm.probe[2 * p + 1] = sm.list_b[s.index(nt)];
+          }
         __syncwarp();
-        for (int k = 0; k < N; ++k) {  // Warshall on bitsets
-          for (int i = lane; i < N; i += 32)
-            if ((sm.reach[i * W + (k >> 5)] >> (k & 31)) & 1u)
-              for (int w = 0; w < W; ++w) sm.reach[i * W + w] |= sm.reach[k * W + w];
-          __syncwarp();
-        }
+        // sm.reach holds successor bitsets; the fallback below closes it in place
         // legal(from, to): pair absent and !creates_cycle (ops.hpp:93-111, 261-263)
         auto legal = [&](int from, int to) {
           const unsigned long long pk = (static_cast<unsigned long long>(uint32_t(from)) << 32) | uint32_t(to);
@@ -504,15 +551,39 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
           if (rt < 0 || rf < 0) return true;
           return !((sm.reach[rt * W + (rf >> 5)] >> (rf & 31)) & 1u);
         };
-        int found = 0, pf = 0, pt = 0;
-        if (lane == 0) {
-          for (int probe = 0; probe < 16 && !found; ++probe) {
-            const int from = sm.list_a[s.index(nk)];
-            const int to = sm.list_b[s.index(nt)];
-            if (legal(from, to)) { found = 1; pf = from; pt = to; }
+        int found = 0, pf = 0, pt = 0, pidx = -1;
+        for (int p = 0; p < 16 && !found; ++p) {  // warp-uniform
+          const int from = sm.probe[2 * p], to = sm.probe[2 * p + 1];
+          const unsigned long long pk = (static_cast<unsigned long long>(uint32_t(from)) << 32) | uint32_t(to);
+          bool ok = false;
+          if (table_find(sm.ckeys, sm.crows, Hc - 1, pk) < 0 && from != to) {
+            const int rt = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(to));
+            const int rf = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(from));
+            ok = rt < 0 || rf < 0 || !warp_reaches(sm.reach, rt, rf, N, W, sm.bfs);
+          }
+          if (ok) {
+            found = 1;
+            pf = from;
+            pt = to;
+            pidx = p;
           }
         }
-        found = __shfl_sync(kFullMask, found, 0);
+        if (found && lane == 0) {  // the stream right after the accepted probe
+          s = Stream(key_split(key, 2));
+          s.coin(cfg.conn_add);
+          for (int p = 0; p <= pidx; ++p) {
+            s.index(nk);
+            s.index(nt);
+          }
+        }
+        if (!found) {  // all-pairs closure for the fallback enumeration (Warshall on bitsets)
+          for (int k = 0; k < N; ++k) {
+            for (int i = lane; i < N; i += 32)
+              if ((sm.reach[i * W + (k >> 5)] >> (k & 31)) & 1u)
+                for (int w = 0; w < W; ++w) sm.reach[i * W + w] |= sm.reach[k * W + w];
+            __syncwarp();
+          }
+        }
         if (!found) {
           // deterministic fallback: sorted keys x sorted targets, from-major
           // (ops.hpp:271-278); sorted position = rank of (key, list index)
