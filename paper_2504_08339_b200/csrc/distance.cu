@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(1024) k_ub_cuckoo(UnionView u) {
 
 // ---- distance kernel ------------------------------------------------------------
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kDistWarps = 16;  // one 512-thread CTA per SM
+constexpr int kDistWarps = 20;  // one 640-thread CTA per SM
 constexpr int kTileStride = 34;  // doubles per tile row (16-byte rows, conflict-light LDS.128)
 
 struct ClassTab {
