@@ -28,10 +28,18 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 
          "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "nsecond": 1e-9}
 
 
-def summarise(path):
+def summarise_all(path):
+    """One summary per kernel launch captured in the report."""
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    return [summarise_row(rows[0], rows[1], vals) for vals in rows[2:]]
+
+
+def summarise(path):
+    return summarise_all(path)[0]
+
+
+def summarise_row(hdr, units, vals):
     d = {"kernel": vals[hdr.index("Kernel Name")].split("(")[0]}
     for m, name in METRICS.items():
         if m in hdr:
@@ -51,7 +59,11 @@ def main():
     res = {}
     for arg in sys.argv[2:]:
         name, path = arg.split("=", 1)
-        res[name] = summarise(path)
+        if name.endswith("*"):  # every launch in the report: name + kernel
+            for d in summarise_all(path):
+                res[name[:-1] + d["kernel"].split("<")[0].split("::")[-1].replace("void ", "").strip()] = d
+        else:
+            res[name] = summarise(path)
     json.dump(res, open(dst, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
