@@ -1,4 +1,4 @@
-# round-1 refresh: full bench line, launch list, ncu summaries; compute-sanitizer memcheck + racecheck of key tests
+# A round's GPU evidence: full bench line, launch list, ncu summaries; compute-sanitizer memcheck + racecheck of key tests
 python -c "import paper_2504_08339_b200" 2>/dev/null || { echo "library stale: rebuilding"; python -c "import __graft_entry__ as g; g.build()"; }
 timeout 900 python bench.py > gpurun_out/bench51.json 2>gpurun_out/bench51.err; echo bench=$?; tail -2 gpurun_out/bench51.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches51.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo ncu_l=$?
