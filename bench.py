@@ -530,13 +530,18 @@ def main():
                        "max over ranks"}
         ev.close()
 
-    c3 = c3_cppn(eng, nets, dev, stream, flush) if not args.no_c5 else None
-    c4 = c4_hyperneat(dev, stream, flush) if not args.no_c5 else None
-    evo = evolved_population(eng, dev, stream, flush, X, Y) if not args.no_generations else None
-    c5g = c5_generation(dev, flush, world) if not args.no_c5 else None
-    c5 = None
-    if not args.no_c5:
-        c5 = c5_distance(dev, stream, flush)
+    def section(fn, *a):
+        """A secondary measurement; its failure is reported, never fatal to the headline line."""
+        try:
+            return fn(*a)
+        except Exception as e:  # noqa: BLE001
+            return {"error": repr(e)[:300]}
+
+    c3 = section(c3_cppn, eng, nets, dev, stream, flush) if not args.no_c5 else None
+    c4 = section(c4_hyperneat, dev, stream, flush) if not args.no_c5 else None
+    evo = section(evolved_population, eng, dev, stream, flush, X, Y) if not args.no_generations else None
+    c5g = section(c5_generation, dev, flush, world) if not args.no_c5 else None
+    c5 = section(c5_distance, dev, stream, flush) if not args.no_c5 else None
 
     # ---- roofline for the dominant kernel (K2 forward) ----
     k2_traffic, k2_traffic_src = ncu_traffic("k2_forward_main_pass")
