@@ -67,9 +67,12 @@ __device__ __forceinline__ uint32_t key_mix(unsigned long long k, uint32_t seed)
 }
 // the two candidate buckets: high bits of the mix, and of a bijective remix of it
 __device__ __forceinline__ uint32_t bucket_a(uint32_t h, uint32_t nb) { return __umulhi(h, nb); }
+// (never bucket_a: a key always has two distinct buckets)
 __device__ __forceinline__ uint32_t bucket_b(uint32_t h, uint32_t nb) {
   const uint32_t g = h * 0xC2B2AE3Du + 0x27D4EB2Fu;
-  return __umulhi(g ^ (g >> 15), nb);
+  const uint32_t a = __umulhi(h, nb);
+  const uint32_t b = __umulhi(g ^ (g >> 15), nb - 1);  // nb >= 16
+  return b >= a ? b + 1 : b;
 }
 __device__ __forceinline__ uint32_t bucket1(unsigned long long k, uint32_t seed, uint32_t nb) {
   return bucket_a(key_mix(k, seed), nb);
@@ -294,7 +297,8 @@ __device__ bool cuckoo_place(uint32_t* ids, const unsigned long long* keys, int 
     uint32_t cur = uint32_t(i);
     uint32_t b = bucket1(keys[cur], seed, nb);
     bool placed = false;
-    for (int it = 0; it < 1024 && !placed; ++it) {
+    const int max_it = min(1024, 16 * U + 64);  // a placeable key rarely needs more evictions
+    for (int it = 0; it < max_it && !placed; ++it) {
       for (int j = 0; j < 2 && !placed; ++j) placed = atomicCAS(&ids[2 * b + j], kNoId, cur) == kNoId;
       if (!placed && it == 0) {  // a fresh key also tries its second bucket before evicting
         const uint32_t b2 = bucket2(keys[cur], seed, nb);
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(1024) k_ub_cuckoo(UnionView u) {
   const uint32_t* lm = conn ? u.lm_c : u.lm_n;
   const uint32_t* lb = conn ? u.lb_c : u.lb_n;
   const uint32_t key_bytes = align16u(uint32_t(U) * 8u);
-  uint32_t nb = max(4u, uint32_t((U * 10 + 13) / 14));  // load <= 0.7
+  uint32_t nb = max(16u, uint32_t((U * 10 + 13) / 14));  // load <= 0.7
   // keys in shared memory if they leave room for twice the first table
   const bool keys_sm = key_bytes + 16u * nb <= u.smem_cuckoo;
   const uint32_t room = u.smem_cuckoo - (keys_sm ? key_bytes : 0u);
