@@ -3,6 +3,7 @@
 // asynchronous device layer.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -323,10 +324,18 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
     CK(ctx->fit.ensure(sizeof(double) * size_t(P)));
     d_fit = static_cast<double*>(ctx->fit.p);
   }
-  // ~8 MB chunks (enough to keep the copy engine streaming), at most kMaxChunks
+  // chunks of ~chunk_mb MB, at most kMaxChunks.  8 MB measured best at C2
+  // (scripts/sweep_h2d.py): smaller chunks leave K1/K2 too little work per
+  // launch, larger ones lengthen the pipeline fill; a second copy stream
+  // only contends for the link.  FNB_H2D_CHUNK_MB overrides (tuning).
+  static const int chunk_mb = [] {
+    const char* e = std::getenv("FNB_H2D_CHUNK_MB");
+    const int v = e ? std::atoi(e) : 8;
+    return v >= 1 && v <= 256 ? v : 8;
+  }();
   const size_t total = (nrow + crow) * size_t(P);
   const int chunks = int(std::max<size_t>(
-      1, std::min<size_t>(std::min<size_t>(fnb_ctx::kMaxChunks, size_t(P)), total / (size_t(8) << 20))));
+      1, std::min<size_t>(std::min<size_t>(fnb_ctx::kMaxChunks, size_t(P)), total / (size_t(chunk_mb) << 20))));
   auto lo_of = [&](int k) { return int((long long)P * k / chunks); };
   // the copies must not overwrite buffers still read by earlier work on the compute stream
   CK(cudaEventRecord(ctx->chunk_ev[fnb_ctx::kMaxChunks], ctx->stream));
@@ -335,11 +344,12 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
   uint8_t* dc = static_cast<uint8_t*>(ctx->conns.p);
   for (int k = 0; k < chunks; ++k) {
     const size_t lo = size_t(lo_of(k)), n = size_t(lo_of(k + 1)) - lo;
+    cudaStream_t cs = ctx->copy_stream;
     CK(cudaMemcpyAsync(dn + lo * nrow, reinterpret_cast<const uint8_t*>(pop_nodes) + lo * nrow, n * nrow,
-                       cudaMemcpyHostToDevice, ctx->copy_stream));
+                       cudaMemcpyHostToDevice, cs));
     CK(cudaMemcpyAsync(dc + lo * crow, reinterpret_cast<const uint8_t*>(pop_conns) + lo * crow, n * crow,
-                       cudaMemcpyHostToDevice, ctx->copy_stream));
-    CK(cudaEventRecord(ctx->chunk_ev[k], ctx->copy_stream));
+                       cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(ctx->chunk_ev[k], cs));
   }
   uint8_t* nets = static_cast<uint8_t*>(ctx->nets.p);
   for (int k = 0; k < chunks; ++k) {

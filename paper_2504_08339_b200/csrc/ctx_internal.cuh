@@ -35,7 +35,7 @@ struct fnb_ctx {
   // host-layer pipeline: population chunks go up on copy_stream while the
   // previous chunk is transformed and evaluated on `stream`
   cudaStream_t copy_stream = nullptr;
-  static constexpr int kMaxChunks = 16;
+  static constexpr int kMaxChunks = 32;
   cudaEvent_t chunk_ev[kMaxChunks + 1] = {};
   DevBuf nodes, conns, nets, X, Y, fit, out, partial, misc, scratch, flags, hyper;
 };
