@@ -211,6 +211,20 @@ int fnb_forward_d(fnb_ctx* ctx, const void* d_nets, int P, const float* d_X, con
                   int batch, int fitness_kind, double fitness_offset, double* d_fitness,
                   double* d_out, void* stream);
 
+/* ---- explain_invalid (genome.hpp:364-417) over a population ----------------
+ * codes[p] = 0 for a valid genome, else the first failing check in the
+ * reference's order (1-4 node row: partially NaN / non-integral key / bad
+ * aggregation id / bad activation id, 5 duplicate node key, 6 input key
+ * missing, 7 output key missing, 8-11 conn row: partially NaN / non-boolean
+ * enabled flag / non-integral endpoint / missing node, 12 duplicate pair);
+ * details[p] the row or key the message names.  fnb_explain_message formats
+ * the reference's string ("" for 0) and returns its length. */
+int fnb_explain_invalid(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P, int32_t* codes,
+                        int32_t* details);
+int fnb_explain_invalid_d(fnb_ctx* ctx, const double* d_nodes, const double* d_conns, int P, int32_t* d_codes,
+                          int32_t* d_details, void* stream);
+int fnb_explain_message(int code, int detail, char* buf, size_t n);
+
 /* ---- BASELINE config 4: HyperNEAT ---------------------
  * The context's genomes are CPPNs with 5 inputs (x1, y1, x2, y2, bias) and 1
  * output.  Each CPPN is queried at the (num_obs + 1) x num_act substrate
@@ -270,6 +284,10 @@ int fnb_evolver_step(fnb_evolver* ev);
  * into the next population buffer), the ranks all-gather the next buffer
  * (fnb_evolver_next_population), and every rank calls step_commit.  Slots
  * are independent, so the result equals fnb_evolver_step bit for bit. */
+/* explain_invalid over the current population: first_invalid = lowest invalid
+ * genome or -1; an invalid one also returns 1 + FNB_E_CORRUPT_ROW with the
+ * reference's explanation in fnb_last_error */
+int fnb_evolver_validate(fnb_evolver* ev, int* first_invalid);
 int fnb_evolver_step_front(fnb_evolver* ev);
 int fnb_evolver_step_back(fnb_evolver* ev, int lo, int hi);
 int fnb_evolver_step_commit(fnb_evolver* ev);

@@ -93,6 +93,7 @@ SIGNATURES = {
     "fnb_evolver_evaluate": (C.c_int, [VP, DP, DP, C.c_int, C.c_int, C.c_double]),
     "fnb_evolver_evaluate_d": (C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_double]),
     "fnb_evolver_step": (C.c_int, [VP]),
+    "fnb_evolver_validate": (C.c_int, [VP, C.POINTER(C.c_int)]),
     "fnb_evolver_step_front": (C.c_int, [VP]),
     "fnb_evolver_step_back": (C.c_int, [VP, C.c_int, C.c_int]),
     "fnb_evolver_step_commit": (C.c_int, [VP]),
@@ -106,6 +107,9 @@ SIGNATURES = {
     "fnb_evolver_device_state": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)]),
     "fnb_stream_draws_d": (C.c_int, [VP, VP, C.c_int, C.c_int, C.c_int, C.c_uint64, VP, VP]),
     "fnb_split_keys_d": (C.c_int, [VP, U32P, C.c_uint64, C.c_int, VP, VP]),
+    "fnb_explain_invalid": (C.c_int, [VP, DP, DP, C.c_int, IP, IP]),
+    "fnb_explain_invalid_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, VP]),
+    "fnb_explain_message": (C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     "fnb_hyper_evaluate": (C.c_int, [VP, DP, DP, C.c_int, C.POINTER(fnb_hyper_config), DP, DP, DP, DP,
                                      C.POINTER(C.c_float)]),
     "fnb_hyper_evaluate_d": (C.c_int, [VP, VP, C.c_int, C.POINTER(fnb_hyper_config), VP, VP, VP, VP, VP, VP]),

@@ -471,3 +471,32 @@ def _engine_hyper_evaluate_d(self, nets, P: int, cfg: HyperConfig, A, B, s0, fit
 
 Engine.hyper_evaluate = _engine_hyper_evaluate
 Engine.hyper_evaluate_d = _engine_hyper_evaluate_d
+
+
+# ---- explain_invalid (genome.hpp:364-417) ------------------------------------------
+
+def explain_message(code: int, detail: int) -> str:
+    """The reference's explain_invalid string for a device check code."""
+    buf = C.create_string_buffer(128)
+    N.lib().fnb_explain_message(int(code), int(detail), buf, 128)
+    return buf.value.decode()
+
+
+def _engine_explain_invalid(self, pop_nodes, pop_conns):
+    """explain_invalid of every genome -> list of strings ('' = valid)."""
+    n, c, P = self._check_pop(pop_nodes, pop_conns)
+    codes = np.empty(P, dtype=np.int32)
+    details = np.empty(P, dtype=np.int32)
+    self._raise(self._lib.fnb_explain_invalid(self._h, _dp(n), _dp(c), P, codes.ctypes.data_as(N.IP),
+                                              details.ctypes.data_as(N.IP)))
+    return [explain_message(k, d) if k else "" for k, d in zip(codes, details)]
+
+
+def _engine_explain_invalid_d(self, nodes, conns, codes, details, stream=None):
+    """Device layer: int32 `codes` / `details` [P] for device populations."""
+    self._raise(self._lib.fnb_explain_invalid_d(self._h, nodes.data_ptr(), conns.data_ptr(), nodes.shape[0],
+                                                codes.data_ptr(), details.data_ptr(), _stream_handle(stream)))
+
+
+Engine.explain_invalid = _engine_explain_invalid
+Engine.explain_invalid_d = _engine_explain_invalid_d

@@ -885,6 +885,12 @@ cudaError_t launch_transform(const double* n, const double* c, int P, uint8_t* n
                              const DevShape& sh, cudaStream_t st);
 }  // namespace fnb
 
+namespace fnb {
+cudaError_t launch_validate(const double* nodes, const double* conns, int P, const DevShape& sh, int32_t* codes,
+                            int32_t* details, cudaStream_t st);
+std::string validate_message(int code, int detail);
+}  // namespace fnb
+
 #define EV_CK(expr)                                                         \
   do {                                                                      \
     cudaError_t e_ = (expr);                                                \
@@ -1036,6 +1042,25 @@ int fnb_evolver_step(fnb_evolver* ev) {
   EV_CK(ev->ev.step(&err));
   if (err == -2) return fnb_set_error(ev->ctx, FNB_E_EVAL_ERROR, "spawn counts do not sum to pop_size", -1);
   if (err >= 0) return fnb_set_error(ev->ctx, FNB_E_DUPLICATE_KEY, "mutation failed in child slot", err);
+  return 0;
+}
+
+int fnb_evolver_validate(fnb_evolver* ev, int* first_invalid) {
+  fnb::Evolver& v = ev->ev;
+  cudaSetDevice(ev->ctx->device);
+  fnb_ctx* ctx = ev->ctx;
+  EV_CK(ctx->misc.ensure(sizeof(int32_t) * 2 * size_t(v.P)));
+  int32_t* codes = static_cast<int32_t*>(ctx->misc.p);
+  EV_CK(fnb::launch_validate(v.pn[v.cur], v.pc[v.cur], v.P, v.sh, codes, codes + v.P, v.st));
+  ++ctx->launches;
+  std::vector<int32_t> h(2 * size_t(v.P));
+  EV_CK(cudaMemcpyAsync(h.data(), codes, sizeof(int32_t) * 2 * size_t(v.P), cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  int bad = -1;
+  for (int p = 0; p < v.P && bad < 0; ++p)
+    if (h[p]) bad = p;
+  if (first_invalid) *first_invalid = bad;
+  if (bad >= 0) return fnb_set_error(ctx, FNB_E_CORRUPT_ROW, fnb::validate_message(h[bad], h[v.P + bad]), bad);
   return 0;
 }
 

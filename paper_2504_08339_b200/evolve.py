@@ -168,6 +168,14 @@ class Evolver:
     def step(self):
         self._raise(self._lib.fnb_evolver_step(self._h))
 
+    def validate(self) -> int:
+        """explain_invalid over the current population on the device: -1 when
+        every genome is valid; else raises FlatneatError (corrupt_row) whose
+        message is the reference's explanation and .index the genome."""
+        bad = C.c_int(-1)
+        self._raise(self._lib.fnb_evolver_validate(self._h, C.byref(bad)))
+        return bad.value
+
     # -- the step split for sharded reproduction (distributed.py) -------------------
     def step_front(self):
         """Speciate, stagnation, spawn, parent selection, split plans and

@@ -523,3 +523,15 @@ def hyper_cppn_outputs(prob: Problem, schema: SchemaSpec, nodes, conns, cfg: Hyp
         net = oracle_transform(prob, schema, nodes[i], conns[i])
         outs.append(oracle_forward(prob, schema, nodes[i], net, X)[:, 0])
     return np.stack(outs)
+
+
+def explain_invalid(prob: Problem, schema: SchemaSpec, nodes, conns, use_ref: bool = True) -> str:
+    """explain_invalid (genome.hpp:364-417): the reference's string, '' if valid."""
+    buf = C.create_string_buffer(512)
+    sh, sc = prob.c(), schema.c()
+    n = np.ascontiguousarray(nodes, dtype=np.float64)
+    c = np.ascontiguousarray(conns, dtype=np.float64)
+    lib = ref() if use_ref and ref_available() else oracle()
+    fn = lib.fr_explain_invalid if lib is not oracle() else lib.fo_explain_invalid
+    fn(C.byref(sh), C.byref(sc), ptr(n, F64P), ptr(c, F64P), buf, C.c_size_t(512))
+    return buf.value.decode()
