@@ -132,24 +132,32 @@ def cpu_reference(P_sample: int, seed: int = 0, target_s: float = 8.0):
             "sample": f"{P} genomes x {BATCH} samples of the C2 workload, transform+forward+MSE, {dt:.2f} s"}
 
 
-def c5_distance(dev, stream, flush, reps: int = 5):
+def c5_distance(dev, stream, flush, reps: int = 5, population: str = "random"):
     """K3 at C5 shapes: pop 100k, N128/C1024, S = 10
     representatives; HBM-bound, so reported against the measured HBM peak.
-    The population is 2,000 distinct synthetic genomes tiled to 100k on the
-    device (K3's cost depends on row counts, not on the values)."""
+    population "random": 2,000 distinct synthetic genomes (random topologies:
+    ~17% of a row's markers in any one representative) tiled to 100k on the
+    device, representatives drawn from them; "lineage": 2,000 mutated copies
+    of 10 ancestors (the representatives), the overlap a NEAT run's species
+    have.  K3's cost depends on row counts and marker overlap, not values."""
     import torch
     import paper_2504_08339_b200 as fnb
-    from paper_2504_08339_b200.synthetic import synthetic_population
+    from paper_2504_08339_b200.synthetic import lineage_population, synthetic_population
     P5, N5, C5, S5, uniq = 100_000, 128, 1024, 10, 2_000
-    n_h, c_h = synthetic_population(uniq, N5, C5, FILL, NI, NO, seed=5)
+    if population == "lineage":
+        n_h, c_h, rn_h, rc_h = lineage_population(uniq, N5, C5, ancestors=S5, fill=FILL, num_inputs=NI,
+                                                  num_outputs=NO, seed=5)
+    else:
+        n_h, c_h = synthetic_population(uniq, N5, C5, FILL, NI, NO, seed=5)
+        rn_h, rc_h = n_h[1::200][:S5], c_h[1::200][:S5]
     eng5 = fnb.Engine(fnb.GenomeLimits(N5, C5), list(range(NI)), list(range(NI, NI + NO)), fnb.AttributeSchema(),
                       device=dev.index)
     base_n, base_c = torch.from_numpy(n_h).to(dev), torch.from_numpy(c_h).to(dev)
     nodes5 = base_n.repeat(P5 // uniq, 1, 1).contiguous()
     conns5 = base_c.repeat(P5 // uniq, 1, 1).contiguous()
     del base_n, base_c
-    rn = torch.from_numpy(np.ascontiguousarray(n_h[1::200][:S5])).to(dev)
-    rc = torch.from_numpy(np.ascontiguousarray(c_h[1::200][:S5])).to(dev)
+    rn = torch.from_numpy(np.ascontiguousarray(rn_h)).to(dev)
+    rc = torch.from_numpy(np.ascontiguousarray(rc_h)).to(dev)
     out = torch.empty((P5, S5), dtype=torch.float64, device=dev)
     for _ in range(2):
         eng5.distance_d(nodes5, conns5, rn, rc, out, stream=stream)
@@ -168,7 +176,8 @@ def c5_distance(dev, stream, flush, reps: int = 5):
     achieved = alg / t / 1e9
     c5_traffic, c5_src = ncu_traffic("k3_distance_c5")
     del nodes5, conns5
-    return {"workload": "C5 K3 distance: pop 100k, N128/C1024, S=10 reps, fill 0.75 (2k distinct genomes tiled)",
+    return {"workload": f"C5 K3 distance: pop 100k, N128/C1024, S=10 reps, fill 0.75, {population} population "
+                        "(2k distinct genomes tiled)",
             "ms": t * 1e3, "genomes_per_s": P5 / t,
             "roofline": {"kernel": "K3 union-table build (6 kernels) + k_distance", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -542,6 +551,7 @@ def main():
     evo = section(evolved_population, eng, dev, stream, flush, X, Y) if not args.no_generations else None
     c5g = section(c5_generation, dev, flush, world) if not args.no_c5 else None
     c5 = section(c5_distance, dev, stream, flush) if not args.no_c5 else None
+    c5l = section(c5_distance, dev, stream, flush, 5, "lineage") if not args.no_c5 else None
 
     # ---- roofline for the dominant kernel (K2 forward) ----
     k2_traffic, k2_traffic_src = ncu_traffic("k2_forward_main_pass")
@@ -589,6 +599,8 @@ def main():
             line["generations"] = gen
         if c5 is not None:
             line["c5_distance"] = c5
+        if c5l is not None:
+            line["c5_distance_lineage"] = c5l
         if c3 is not None:
             line["c3_cppn"] = c3
         if c4 is not None:

@@ -56,6 +56,30 @@ def synthetic_population(P: int, max_nodes: int, max_conns: int, fill: float = 0
     return nodes, conns
 
 
+def lineage_population(P: int, max_nodes: int, max_conns: int, ancestors: int = 10, fill: float = 0.75,
+                       num_inputs: int = 4, num_outputs: int = 1, seed: int = 0):
+    """A population descended from `ancestors` synthetic genomes, as a NEAT
+    run's species are: genome i copies ancestor i % ancestors with mutation-like
+    noise -- 80% of the connection weights and biases moved by N(0, 0.5^2),
+    5% of the enabled connections disabled.  Markers (keys, endpoints) are
+    the ancestor's, so a genome matches its own representative densely and
+    the others as the ancestors overlap.  Returns (nodes, conns, anc_nodes,
+    anc_conns)."""
+    an, ac = synthetic_population(ancestors, max_nodes, max_conns, fill, num_inputs, num_outputs, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    idx = np.arange(P) % ancestors
+    nodes, conns = an[idx].copy(), ac[idx].copy()
+    live_c = ~np.isnan(conns[:, :, 0])
+    live_n = ~np.isnan(nodes[:, :, 0])
+    mw = live_c & (rng.random(live_c.shape) < 0.8)
+    conns[:, :, 3] += np.where(mw, rng.normal(0.0, 0.5, live_c.shape), 0.0)
+    off = live_c & (conns[:, :, 2] == 1.0) & (rng.random(live_c.shape) < 0.05)
+    conns[:, :, 2] = np.where(off, 0.0, conns[:, :, 2])
+    mb = live_n & (rng.random(live_n.shape) < 0.8)
+    nodes[:, :, 1] += np.where(mb, rng.normal(0.0, 0.5, live_n.shape), 0.0)
+    return nodes, conns, an, ac
+
+
 def regression_dataset(batch: int, num_inputs: int = 4, num_outputs: int = 1, seed: int = 0):
     """X ~ U(-2, 2) sample-major [B, I]; y = a smooth fixed target [B, O]."""
     rng = np.random.default_rng(seed)

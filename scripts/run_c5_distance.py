@@ -11,4 +11,5 @@ import bench  # noqa: E402
 
 dev = torch.device("cuda", 0)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-print(json.dumps(bench.c5_distance(dev, torch.cuda.current_stream(), flush, reps=int(sys.argv[1]) if len(sys.argv) > 1 else 3)))
+print(json.dumps(bench.c5_distance(dev, torch.cuda.current_stream(), flush, reps=int(sys.argv[1]) if len(sys.argv) > 1 else 3,
+                                   population=sys.argv[2] if len(sys.argv) > 2 else "random")))
