@@ -505,6 +505,75 @@ __global__ void k_reproduce_plan(const SpeciesDev* sd, const int* members, const
   active[c] = 1;
 }
 
+// Populations up to kCountRankMax: the two stable sorts of the step (fitness
+// ranks, then members by species) are a counting rank -- the position of
+// item i is #(k_j < k_i) + #(k_j == k_i, j < i), exactly the stable sort's --
+// spread over the whole GPU (O(P^2) compares, ~1e8 at pop 10k, a few
+// microseconds) and a scatter, instead of a chain of radix-sort kernels.
+// Grid: x = blocks of 256 items, y = tiles of 256 keys staged in shared
+// memory; a tile wholly before / after a block compares with <= / <, only
+// the tile holding the block breaks ties by index.  Partial counts are
+// summed with integer atomics (order-independent).
+constexpr int kCountRankMax = 16384;
+constexpr int kRankItems = 256, kRankTile = 256;
+
+template <typename K>
+__global__ void __launch_bounds__(128) k_count_rank(const K* __restrict__ keys, int n, int* __restrict__ rank) {
+  __shared__ K sk[kRankTile];
+  const int ib = blockIdx.x * kRankItems, j0 = blockIdx.y * kRankTile;
+  const int jn = min(kRankTile, n - j0);
+  for (int t = threadIdx.x; t < jn; t += blockDim.x) sk[t] = keys[j0 + t];
+  __syncthreads();
+  const int i0 = ib + threadIdx.x, i1 = i0 + 128;
+  const K k0 = i0 < n ? keys[i0] : K(0), k1 = i1 < n ? keys[i1] : K(0);
+  int c0 = 0, c1 = 0;
+  if (j0 + jn <= ib) {
+#pragma unroll 8
+    for (int j = 0; j < jn; ++j) {
+      const K kj = sk[j];
+      c0 += kj <= k0;
+      c1 += kj <= k1;
+    }
+  } else if (j0 >= ib + kRankItems) {
+#pragma unroll 8
+    for (int j = 0; j < jn; ++j) {
+      const K kj = sk[j];
+      c0 += kj < k0;
+      c1 += kj < k1;
+    }
+  } else {
+    for (int j = 0; j < jn; ++j) {
+      const K kj = sk[j];
+      const int jj = j0 + j;
+      c0 += (kj < k0) | ((kj == k0) & (jj < i0));
+      c1 += (kj < k1) | ((kj == k1) & (jj < i1));
+    }
+  }
+  if (i0 < n && c0) atomicAdd(&rank[i0], c0);
+  if (i1 < n && c1) atomicAdd(&rank[i1], c1);
+}
+
+// out position rank[i] receives item i: its key (when kout) and vals[i] (i when vals is null)
+template <typename K>
+__global__ void k_rank_scatter(const K* __restrict__ keys, const int* __restrict__ vals, const int* __restrict__ rank,
+                               int n, K* __restrict__ kout, int* __restrict__ vout) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = rank[i];
+  if (kout) kout[r] = keys[i];
+  vout[r] = vals ? vals[i] : i;
+}
+
+template <typename K>
+cudaError_t launch_count_sort(const K* keys, const int* vals, int n, int* rank, K* kout, int* vout, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(rank, 0, sizeof(int) * size_t(n), st);
+  if (e != cudaSuccess) return e;
+  const dim3 grid((n + kRankItems - 1) / kRankItems, (n + kRankTile - 1) / kRankTile);
+  k_count_rank<K><<<grid, 128, 0, st>>>(keys, n, rank);
+  k_rank_scatter<K><<<(n + 255) / 256, 256, 0, st>>>(keys, vals, rank, n, kout, vout);
+  return cudaGetLastError();
+}
+
 // ---- host-side launchers used by capi.cu ------------------------------------------------------
 cudaError_t launch_distance_masked(const double* nodes, const double* conns, int P, const double* rn,
                                    const double* rc, int S, int N, int C, double cd, double ch, double* out,
@@ -780,7 +849,9 @@ struct Evolver {
     k_remap_or_drop<<<B, T, 0, st>>>(species_of, P, sd);
     // ---- compute_spawn_counts: ranks by a stable ascending radix sort
     k_fit_keys<<<B, T, 0, st>>>(fitness, P, kasc, kdesc, idx);
-    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
+    e = P <= kCountRankMax
+            ? launch_count_sort<unsigned long long>(kasc, nullptr, P, skey_tmp, ktmp, idx_sorted, st)
+            : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
     if (e != cudaSuccess) return e;
     k_spawn_begin<<<1, 1, 0, st>>>(sd);
     k_rank_sums<<<B, T, 0, st>>>(idx_sorted, P, species_of, sd);
@@ -788,7 +859,9 @@ struct Evolver {
     // ---- reproduce: members by (fitness desc, index asc), then by species
     k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp);
     k_species_keys<<<B, T, 0, st>>>(idx_tmp, P, species_of, skey);
-    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, skey, skey_tmp, idx_tmp, idx_sorted, P, 0, 6, st);
+    e = P <= kCountRankMax
+            ? launch_count_sort<int>(skey, idx_tmp, P, skey_tmp, nullptr, idx_sorted, st)
+            : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, skey, skey_tmp, idx_tmp, idx_sorted, P, 0, 6, st);
     if (e != cudaSuccess) return e;
     const Key4 root1 = key_split(key_from_seed(seed), 1);
     k_reproduce_plan<<<B, T, 0, st>>>(sd, idx_sorted, fitness, P, root1, cfg.genome_elitism, cfg.survival, fit_idx,
