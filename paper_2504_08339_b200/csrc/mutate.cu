@@ -302,13 +302,52 @@ __device__ __forceinline__ void stage_conn(MutSmem& sm, const double* c, int r) 
 
 // attribute action code: bit0-1 kind (0 none, 1 add normal(0,power), 2 replace
 // normal(init)), bits 2.. = stream position of the normal's first draw
-__device__ __noinline__ double apply_scalar(double v, uint32_t a, const Key4& k, double power, double mean,
+__device__ __forceinline__ double apply_scalar(double v, uint32_t a, const Key4& k, double power, double mean,
                                                double sd) {
   if ((a & 3u) == 0) return v;
   const uint64_t pos = a >> 2;
-  const double u0 = u64_to_uniform(stream_u64_at(k, pos)), u1 = u64_to_uniform(stream_u64_at(k, pos + 1));
+  uint32_t b[4];
+  stream_block(k, pos >> 1, b);
+  uint64_t x0, x1;
+  if (pos & 1) {  // draws 2q+1 and 2q+2 straddle two blocks
+    x0 = (uint64_t(b[1]) << 32) | b[0];
+    stream_block(k, (pos >> 1) + 1, b);
+    x1 = (uint64_t(b[3]) << 32) | b[2];
+  } else {
+    x0 = (uint64_t(b[3]) << 32) | b[2];
+    x1 = (uint64_t(b[1]) << 32) | b[0];
+  }
+  const double u0 = u64_to_uniform(x0), u1 = u64_to_uniform(x1);
   if ((a & 3u) == 1) return __dadd_rn(v, glibc::normal_from_uniforms(u0, u1, 0.0, power));
   return glibc::normal_from_uniforms(u0, u1, mean, sd);
+}
+
+// Triggered normals of the attribute pass are not evaluated where the walk
+// finds them (a few lanes at a time) but appended to a per-warp list and
+// evaluated afterwards with all 32 lanes busy.  Entry: target word
+// (bits 30-31 attribute: 0 bias, 1 response, 2 weight; bits 0-29 the double
+// offset in the child's node / connection rows) and the action code.
+struct NormalList {
+  uint32_t* tgt;
+  uint32_t* act;
+  int* count;
+  __device__ __forceinline__ void push(uint32_t attr, uint32_t off, uint32_t a) const {
+    const int i = atomicAdd(count, 1);
+    tgt[i] = (attr << 30) | off;
+    act[i] = a;
+  }
+};
+
+__device__ __forceinline__ void apply_normals(const NormalList& nl, int total, double* n, double* cc, const Key4& k5,
+                                              const MutCfgDev& cfg) {
+  for (int t = threadIdx.x & 31; t < total; t += 32) {
+    const uint32_t g = nl.tgt[t], a = nl.act[t], attr = g >> 30, off = g & 0x3fffffffu;
+    const double power = attr == 0 ? cfg.b_power : attr == 1 ? cfg.r_power : cfg.w_power;
+    const double mean = attr == 0 ? cfg.b_mean : attr == 1 ? cfg.r_mean : cfg.w_mean;
+    const double sd = attr == 0 ? cfg.b_std : attr == 1 ? cfg.r_std : cfg.w_std;
+    double* v = (attr == 2 ? cc : n) + off;
+    *v = apply_scalar(*v, a, k5, power, mean, sd);
+  }
 }
 
 // Every decision the split(5) attribute walk can take at one stream position,
@@ -363,12 +402,12 @@ __device__ __noinline__ uint32_t slow_word(const Key4& k5, uint32_t q, const Att
 // every lane folds its chunk of [p0, p0 + 3m) into a 3-entry state map, a warp
 // scan of map compositions gives each chunk's incoming state, a scan of visit
 // counts gives each visit's connection index k, and the lane that finds
-// visit k applies its normal to the k-th live row.  Returns false (nothing
-// written) when the walk could leave the decision window.
+// visit k lists its normal for the k-th live row.  Returns false (nothing
+// listed) when the walk could leave the decision window.
 __device__ __forceinline__ uint32_t map_at(uint32_t m, uint32_t s) { return (m >> (2 * s)) & 3u; }
 
 __device__ bool conn_walk(const uint16_t* dw, uint32_t need, uint32_t p0, int m, const int16_t* live_row,
-                          double* cc, const Key4& k5, const MutCfgDev& cfg) {
+                          const NormalList& nl) {
   const int lane = threadIdx.x & 31;
   const uint32_t span = 3u * uint32_t(m);
   if (p0 + span > need) return false;
@@ -406,16 +445,13 @@ __device__ bool conn_walk(const uint16_t* dw, uint32_t need, uint32_t p0, int m,
     const int v = __shfl_up_sync(kFullMask, incl, d);
     if (lane >= d) incl += v;
   }
-  // pass 3: apply the triggered normals of this chunk's visits
+  // pass 3: list the triggered normals of this chunk's visits
   int k = incl - cnt;
   s = s_in;
   for (uint32_t p = lo; p < hi; ++p) {
     if (s == 0) {
       const uint32_t b = bits(p);
-      if (b && k < m) {
-        double* w = cc + size_t(live_row[k]) * kConnCols + kW;
-        *w = apply_scalar(*w, ((p + 1) << 2) | ((b & 1u) ? 1u : 2u), k5, cfg.w_power, cfg.w_mean, cfg.w_std);
-      }
+      if (b && k < m) nl.push(2u, uint32_t(live_row[k]) * kConnCols + kW, ((p + 1) << 2) | ((b & 1u) ? 1u : 2u));
       ++k;
       s = b ? 2u : 0u;
     } else {
@@ -715,8 +751,8 @@ __host__ __device__ inline int attr_per_node(const MutCfgDev& cfg) {
 }
 __host__ __device__ inline int attr_window(int N, int C, int per_node) { return (per_node * N + 3 * C + 1) & ~1; }
 __host__ __device__ inline size_t attr_smem_bytes(int N, int C, int win) {
-  return align16(size_t(win) * 2) + align16(size_t(C) * 2) + align16(size_t(2 * N) * 4) + align16(size_t(2 * N)) +
-         align16(size_t(N));
+  return align16(size_t(win) * 2) + align16(size_t(C) * 2) + 2 * align16(size_t(2 * N + C) * 4) +
+         align16(size_t(2 * N)) + align16(size_t(N)) + 16;
 }
 
 __global__ void __launch_bounds__(256)
@@ -731,9 +767,12 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   uint8_t* p8 = smem_raw + size_t(warp) * smem_per_warp;
   uint16_t* dw = reinterpret_cast<uint16_t*>(p8); p8 += align16(size_t(win) * 2);
   int16_t* live_row = reinterpret_cast<int16_t*>(p8); p8 += align16(size_t(C) * 2);
-  uint32_t* act_n = reinterpret_cast<uint32_t*>(p8); p8 += align16(size_t(2 * N) * 4);
+  NormalList nl;
+  nl.tgt = reinterpret_cast<uint32_t*>(p8); p8 += align16(size_t(2 * N + C) * 4);
+  nl.act = reinterpret_cast<uint32_t*>(p8); p8 += align16(size_t(2 * N + C) * 4);
   int8_t* new_id = reinterpret_cast<int8_t*>(p8); p8 += align16(size_t(2 * N));  // [q] agg, [N + q] act
-  uint8_t* hid = p8;                                                              // [N] mutable node row
+  uint8_t* hid = p8; p8 += align16(size_t(N));                                    // [N] mutable node row
+  nl.count = reinterpret_cast<int*>(p8);
   double* n = nodes + size_t(c) * N * kNodeCols;
   double* cc = conns + size_t(c) * C * kConnCols;
   const Key4 k5 = key_split(load_key(keys, c), 5);
@@ -783,43 +822,48 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
         if ((f >> acc_bit) & 1u) return int((f >> val_shift) & 7u);
       }
     };
+    int listed = 0;
     for (int q = 0; q < N; ++q) {
-      uint32_t ab = 0u, ar = 0u;
       int ag = -1, ac = -1;
       if (hid[q]) {
-        ab = scalar(AttrDecider::kBias);
-        ar = scalar(AttrDecider::kResp);
+        const uint32_t ab = scalar(AttrDecider::kBias);
+        if (ab) {
+          nl.tgt[listed] = uint32_t(q * kNodeCols + kBias);
+          nl.act[listed++] = ab;
+        }
+        const uint32_t ar = scalar(AttrDecider::kResp);
+        if (ar) {
+          nl.tgt[listed] = (1u << 30) | uint32_t(q * kNodeCols + kResp);
+          nl.act[listed++] = ar;
+        }
         if (cfg.agg_rate > 0.0 && ((word(p++) >> AttrDecider::kAggCoin) & 1u))
           ag = index(AttrDecider::kAggAcc, AttrDecider::kAggVal);
         if (cfg.act_rate > 0.0 && ((word(p++) >> AttrDecider::kActCoin) & 1u))
           ac = index(AttrDecider::kActAcc, AttrDecider::kActVal);
       }
-      act_n[2 * q] = ab;
-      act_n[2 * q + 1] = ar;
       new_id[q] = int8_t(ag);
       new_id[N + q] = int8_t(ac);
     }
     p_nodes_end = p;
+    *nl.count = listed;
   }
+  __syncwarp();
   // connection weights from p0 (warp-parallel; lane-0 chase if the window is short)
   const uint32_t p0 = __shfl_sync(kFullMask, p_nodes_end, 0);
-  if (!conn_walk(dw, uint32_t(need), p0, nc, live_row, cc, k5, cfg) && lane == 0) {
+  if (!conn_walk(dw, uint32_t(need), p0, nc, live_row, nl) && lane == 0) {
     uint32_t p = p0;
     for (int k = 0; k < nc; ++k) {
       const uint32_t f = ((p < uint32_t(need) ? uint32_t(dw[p]) : slow_word(k5, p, dec)) >> AttrDecider::kWeight) & 3u;
       ++p;
       if (f) {
-        double* w = cc + size_t(live_row[k]) * kConnCols + kW;
-        *w = apply_scalar(*w, (p << 2) | ((f & 1u) ? 1u : 2u), k5, cfg.w_power, cfg.w_mean, cfg.w_std);
+        nl.push(2u, uint32_t(live_row[k]) * kConnCols + kW, (p << 2) | ((f & 1u) ? 1u : 2u));
         p += 2;
       }
     }
   }
   __syncwarp();
+  apply_normals(nl, *nl.count, n, cc, k5, cfg);
   for (int q = lane; q < N; q += 32) {
-    const uint32_t ab = act_n[2 * q], ar = act_n[2 * q + 1];
-    if (ab) n[q * kNodeCols + kBias] = apply_scalar(n[q * kNodeCols + kBias], ab, k5, cfg.b_power, cfg.b_mean, cfg.b_std);
-    if (ar) n[q * kNodeCols + kResp] = apply_scalar(n[q * kNodeCols + kResp], ar, k5, cfg.r_power, cfg.r_mean, cfg.r_std);
     if (new_id[q] >= 0) n[q * kNodeCols + kAgg] = double(new_id[q]);
     if (new_id[N + q] >= 0) n[q * kNodeCols + kAct] = double(new_id[N + q]);
   }
