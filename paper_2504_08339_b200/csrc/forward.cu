@@ -118,6 +118,23 @@ __device__ __forceinline__ void sts(uint32_t addr, const float (&x)[SPT]) {
   }
 }
 
+// Packed FP32 pair FMA (FFMA2 on sm_100a): each half is one fma.rn.f32, so
+// results are bit-identical to scalar fmaf; the weight is a scalar operand
+// broadcast to both halves (no pair construction in SASS).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpk2(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long ffma2(float w, unsigned long long x, unsigned long long a) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(w, w)), "l"(x), "l"(a));
+  return d;
+}
+
 struct FwdParams {
   const uint8_t* nets;
   NetLayout L;
@@ -241,14 +258,23 @@ k_forward(FwdParams p) {
       lds_pred<SPT>(cnt > 3, vb + __byte_perm(srcs, 0u, 0x4443) * row_bytes, x3);
       if (agg == FNB_AGG_SUM || agg == FNB_AGG_MEAN) {
         // pad slots contribute 0 * 0: branch-free, ascending source row
+if constexpr (SPT == 1) {
+          float a = first ? 0.0f : acc[0];
+          a = fmaf(cur.w.x, x0[0], a);
+          a = fmaf(cur.w.y, x1[0], a);
+          a = fmaf(cur.w.z, x2[0], a);
+          a = fmaf(cur.w.w, x3[0], a);
+          acc[0] = a;
+        } else {
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-          float a = first ? 0.0f : acc[k];
-          a = fmaf(cur.w.x, x0[k], a);
-          a = fmaf(cur.w.y, x1[k], a);
-          a = fmaf(cur.w.z, x2[k], a);
-          a = fmaf(cur.w.w, x3[k], a);
-          acc[k] = a;
+          for (int k = 0; k < SPT; k += 2) {
+            unsigned long long a = first ? 0ull : pk2(acc[k], acc[k + 1]);
+            a = ffma2(cur.w.x, pk2(x0[k], x0[k + 1]), a);
+            a = ffma2(cur.w.y, pk2(x1[k], x1[k + 1]), a);
+            a = ffma2(cur.w.z, pk2(x2[k], x2[k + 1]), a);
+            a = ffma2(cur.w.w, pk2(x3[k], x3[k + 1]), a);
+            unpk2(a, acc[k], acc[k + 1]);
+          }
         }
       } else {
         const float w[4] = {cur.w.x, cur.w.y, cur.w.z, cur.w.w};
