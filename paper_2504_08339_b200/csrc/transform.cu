@@ -18,29 +18,46 @@
 namespace fnb {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned long long kHtEmpty = ~0ull;
+constexpr int kLastForever = 0x7fffffff;  // last_use of an output row
 
+// Per-warp shared memory.  Arrays that die after a step are reused by a later
+// one (noted at the reuse).
 struct TfSmem {
-  long long* kr;        // [N] (key << 8 | row) or INT64_MAX for empty rows
-  int* sorted_key;      // [N]
-  int* R;               // [N] enabled rows per destination
-  uint32_t* pred;       // [N * W]
-  uint32_t* die;        // [N * W] rows whose last consumer is op k (by op index)
+  long long* kr;        // [N, padded even] (key << 8 | row) or INT64_MAX for empty rows
+  unsigned long long* ht;  // [HT] key -> lowest row (key << 32 | row), open addressing
+  int* sorted_key;      // [N] key of rank k
+  int* R;               // [N] enabled rows per destination row
+  uint32_t* pred;       // [N * W] predecessor rows of each row (row bits)
+  uint32_t* predr;      // [N * W] predecessor ranks of each rank (rank bits); free_at after Kahn
   uint16_t* row_of_rank;// [N]
   uint16_t* rank;       // [N]
   uint16_t* order;      // [N]
-  uint16_t* ebeg;       // [N] edge begin of the op writing row r
+  uint16_t* ebeg;       // [N] record begin of the op writing row r (in ht's space after step 4)
+  uint16_t* op_row;     // [N] row of op k (in ht's space after step 4)
+  uint16_t* ncode;      // [N] act code | agg code << 8
+  float* nbias;         // [N]
+  float* nresp;         // [N]
   uint8_t* flags;       // [N] bit0 non-empty, bit1 input
   int16_t* csrc;        // [C]
   int16_t* cdst;        // [C] destination row of an enabled finite edge, else -1
+  uint32_t ht_mask, ht_shift;
 };
+
+__host__ __device__ inline int tf_ht_size(int N) {
+  int h = 32;
+  while (h < 2 * N) h <<= 1;
+  return h;
+}
 
 __host__ __device__ inline size_t tf_smem_bytes(int N, int C, int W) {
   size_t b = 0;
-  b += align16(size_t(N) * 8);           // kr
-  b += align16(size_t(N) * 4);           // sorted_key
-  b += align16(size_t(N) * 4);           // R
-  b += align16(size_t(N) * W * 4) * 2;   // pred, die
-  b += align16(size_t(N) * 2) * 4;       // row_of_rank, rank, order, ebeg
+  b += align16(size_t(N + 1) * 8);       // kr
+  b += align16(size_t(tf_ht_size(N)) * 8);  // ht
+  b += align16(size_t(N) * 4) * 2;       // sorted_key, R
+  b += align16(size_t(N) * W * 4) * 2;   // pred, predr
+  b += align16(size_t(N) * 2) * 4;       // row_of_rank, rank, order, ncode
+  b += align16(size_t(N) * 4) * 2;       // nbias, nresp
   b += align16(size_t(N));               // flags
   b += align16(size_t(C) * 2) * 2;       // csrc, cdst
   return b;
@@ -48,30 +65,58 @@ __host__ __device__ inline size_t tf_smem_bytes(int N, int C, int W) {
 
 __device__ inline TfSmem tf_carve(uint8_t* p, int N, int C, int W) {
   TfSmem s;
-  s.kr = reinterpret_cast<long long*>(p); p += align16(size_t(N) * 8);
+  s.kr = reinterpret_cast<long long*>(p); p += align16(size_t(N + 1) * 8);
+  const int ht = tf_ht_size(N);
+  s.ht = reinterpret_cast<unsigned long long*>(p); p += align16(size_t(ht) * 8);
+  s.ht_mask = uint32_t(ht - 1);
+  s.ht_shift = uint32_t(32 - __ffs(ht) + 1);
   s.sorted_key = reinterpret_cast<int*>(p); p += align16(size_t(N) * 4);
   s.R = reinterpret_cast<int*>(p); p += align16(size_t(N) * 4);
   s.pred = reinterpret_cast<uint32_t*>(p); p += align16(size_t(N) * W * 4);
-  s.die = reinterpret_cast<uint32_t*>(p); p += align16(size_t(N) * W * 4);
+  s.predr = reinterpret_cast<uint32_t*>(p); p += align16(size_t(N) * W * 4);
   s.row_of_rank = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
   s.rank = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
   s.order = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
-  s.ebeg = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
+  s.ebeg = reinterpret_cast<uint16_t*>(s.ht);  // ht (>= 16N bytes) is dead after step 4
+  s.op_row = s.ebeg + N;
+  s.ncode = reinterpret_cast<uint16_t*>(p); p += align16(size_t(N) * 2);
+  s.nbias = reinterpret_cast<float*>(p); p += align16(size_t(N) * 4);
+  s.nresp = reinterpret_cast<float*>(p); p += align16(size_t(N) * 4);
   s.flags = p; p += align16(size_t(N));
   s.csrc = reinterpret_cast<int16_t*>(p); p += align16(size_t(C) * 2);
   s.cdst = reinterpret_cast<int16_t*>(p);
   return s;
 }
 
-// lower_bound over the sorted keys; row of the first (key,row) or -1
-// (TransformedNetwork::row_of_key, network.hpp:57-63).
-__device__ inline int tf_lookup(const TfSmem& s, int n, int key) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (s.sorted_key[mid] < key) lo = mid + 1; else hi = mid;
+__device__ __forceinline__ uint32_t tf_hash(const TfSmem& s, int key) {
+  return (uint32_t(key) * 0x9E3779B1u) >> s.ht_shift;
+}
+
+// key -> lowest row holding it: the row of the first (key,row) in sorted order,
+// i.e. TransformedNetwork::row_of_key's lower_bound (network.hpp:57-63)
+__device__ inline void tf_insert(const TfSmem& s, int key, int row) {
+  const unsigned long long v = (static_cast<unsigned long long>(uint32_t(key)) << 32) | uint32_t(row);
+  uint32_t h = tf_hash(s, key);
+  for (;;) {
+    const unsigned long long prev = atomicCAS(&s.ht[h], kHtEmpty, v);
+    if (prev == kHtEmpty) return;
+    if (uint32_t(prev >> 32) == uint32_t(key)) {
+      atomicMin(&s.ht[h], v);
+      return;
+    }
+    h = (h + 1) & s.ht_mask;
   }
-  return (lo < n && s.sorted_key[lo] == key) ? int(s.row_of_rank[lo]) : -1;
+}
+
+// row of `key`, or -1
+__device__ inline int tf_lookup(const TfSmem& s, int key) {
+  uint32_t h = tf_hash(s, key);
+  for (;;) {
+    const unsigned long long v = s.ht[h];
+    if (v == kHtEmpty) return -1;
+    if (uint32_t(v >> 32) == uint32_t(key)) return int(uint32_t(v));
+    h = (h + 1) & s.ht_mask;
+  }
 }
 
 __device__ inline void tf_fail(uint8_t* net, int status, int kind, int a, int b,
@@ -101,29 +146,42 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   const double* crow = conns + size_t(g) * C * kConnCols;
   uint8_t* net = nets + size_t(g) * L.bytes;
 
-  // ---- 1. node rows: keys, activation/aggregation ids (network.hpp:139-152)
+  // ---- 1. node rows: keys, activation/aggregation ids (network.hpp:139-152);
+  //         the op attributes are kept in shared memory for step 6d
+  for (int i = lane; i <= int(s.ht_mask); i += 32) s.ht[i] = kHtEmpty;
+  if (lane == 0) s.kr[N] = 0x7fffffffffffffffll;  // pad for the paired rank loads
   int populated = 0;
+  bool narrow = true;  // every key in [-2^23, 2^23 - 1): (key << 8 | row) fits an int32 below INT32_MAX
   for (int r0 = 0; r0 < N; r0 += 32) {
     const int r = r0 + lane;
     int bad = kErrNone, badid = 0;
     bool ne = false;
     if (r < N) {
-      const double k = nrow[r * kNodeCols + kKey];
+      const double* row = nrow + r * kNodeCols;
+      const double k = row[kKey];
       ne = !isnan(k);
       long long kr = 0x7fffffffffffffffll;
       if (ne) {
         const int key = int(k);
         kr = (static_cast<long long>(key) << 8) | r;
-        const int act = int(nrow[r * kNodeCols + kAct]);
-        const int agg = int(nrow[r * kNodeCols + kAgg]);
+        narrow = narrow && key >= -(1 << 23) && key < (1 << 23) - 1;  // INT32_MAX stays the empty mark
+        const int act = int(row[kAct]);
+        const int agg = int(row[kAgg]);
         if (act < 0 || act >= sh.n_act) { bad = kErrActId; badid = act; }
         else if (agg < 0 || agg >= sh.n_agg) { bad = kErrAggId; badid = agg; }
+        else {
+          s.ncode[r] = uint16_t(sh.act[act] | (sh.agg[agg] << 8));
+          s.nbias[r] = float(row[kBias]);
+          s.nresp[r] = float(row[kResp]);
+        }
       }
       s.kr[r] = kr;
       s.flags[r] = ne ? 1 : 0;
       s.R[r] = 0;
 #pragma unroll
       for (int w = 0; w < W; ++w) s.pred[r * W + w] = 0u;
+#pragma unroll
+      for (int w = 0; w < W; ++w) s.predr[r * W + w] = 0u;
     }
     const unsigned m = __ballot_sync(kFull, bad != kErrNone);
     if (m) {
@@ -135,17 +193,56 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     }
     populated += __popc(__ballot_sync(kFull, ne));
   }
+  narrow = __all_sync(kFull, narrow);
   __syncwarp();
+  if (narrow) {  // repack in place as int32 (INT32_MAX for empty rows), padded to a multiple of 4
+    int* k32 = reinterpret_cast<int*>(s.kr);
+    int v[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const int r = lane + 32 * j;
+      v[j] = 0x7fffffff;
+      if (r < N) {
+        const long long x = s.kr[r];
+        if (x != 0x7fffffffffffffffll) v[j] = int(x);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const int r = lane + 32 * j;
+      if (r < ((N + 3) & ~3)) k32[r] = v[j];
+    }
+    __syncwarp();
+  }
 
-  // ---- 2. ranks of (key,row): the Kahn priority and the key_to_row sort
+  // ---- 2. ranks of (key,row): the Kahn priority and the key_to_row sort;
+  //         the key -> lowest-row hash table
   for (int r = lane; r < N; r += 32) {
-    const long long mine = s.kr[r];
-    if (mine == 0x7fffffffffffffffll) continue;
-    int rk = 0;
-    for (int q = 0; q < N; ++q) rk += (s.kr[q] < mine) ? 1 : 0;
+    int rk = 0, key;
+    if (narrow) {
+      const int mine = reinterpret_cast<const int*>(s.kr)[r];
+      if (mine == 0x7fffffff) continue;
+      const int4* k4 = reinterpret_cast<const int4*>(s.kr);
+      for (int q = 0; q < (N + 3) / 4; ++q) {
+        const int4 v = k4[q];
+        rk += (v.x < mine ? 1 : 0) + (v.y < mine ? 1 : 0) + (v.z < mine ? 1 : 0) + (v.w < mine ? 1 : 0);
+      }
+      key = mine >> 8;  // arithmetic shift: (key << 8 | row) >> 8 == key
+    } else {
+      const long long mine = s.kr[r];
+      if (mine == 0x7fffffffffffffffll) continue;
+      const longlong2* kr2 = reinterpret_cast<const longlong2*>(s.kr);
+      for (int q = 0; q < (N + 1) / 2; ++q) {
+        const longlong2 v = kr2[q];
+        rk += (v.x < mine ? 1 : 0) + (v.y < mine ? 1 : 0);
+      }
+      key = int(mine >> 8);
+    }
     s.rank[r] = uint16_t(rk);
     s.row_of_rank[rk] = uint16_t(r);
-    s.sorted_key[rk] = int(mine >> 8);
+    s.sorted_key[rk] = key;
+    tf_insert(s, key, r);
   }
   __syncwarp();
 
@@ -159,7 +256,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
       int row = 0, key = 0;
       if (i < n) {
         key = pass == 0 ? sh.input_keys[i] : sh.output_keys[i];
-        row = tf_lookup(s, populated, key);
+        row = tf_lookup(s, key);
       }
       const unsigned m = __ballot_sync(kFull, i < n && row < 0);
       if (m) {
@@ -177,8 +274,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   }
   __syncwarp();
 
-  // ---- 4. connection rows: dangling check, in-degree, predecessor bits
-  //         (network.hpp:167-183)
+  // ---- 4. connection rows: dangling check, in-degree, predecessor bits in
+  //         row and rank space (network.hpp:167-183)
   for (int r0 = 0; r0 < C; r0 += 32) {
     const int r = r0 + lane;
     double cin = __longlong_as_double(0x7ff8000000000000ll), cout = 0, en = 0, w = 0;
@@ -190,8 +287,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     const bool ne = !isnan(cin);
     int src = -1, dst = -1;
     if (ne) {
-      src = tf_lookup(s, populated, int(cin));
-      dst = tf_lookup(s, populated, int(cout));
+      src = tf_lookup(s, int(cin));
+      dst = tf_lookup(s, int(cout));
     }
     const bool bad = ne && (src < 0 || dst < 0);
     const unsigned m = __ballot_sync(kFull, bad);
@@ -209,6 +306,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
         atomicAdd(&s.R[dst], 1);
         if (!isnan(w)) {
           atomicOr(&s.pred[dst * W + (src >> 5)], 1u << (src & 31));
+          const int rs = s.rank[src], rd = s.rank[dst];
+          atomicOr(&s.predr[rd * W + (rs >> 5)], 1u << (rs & 31));
           d = int16_t(dst);
         }
       }
@@ -218,51 +317,80 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   }
   __syncwarp();
 
-  // ---- 5. Kahn with min-(key,row) pop (network.hpp:192-214)
-  constexpr int NJ = W;  // rows per lane (N <= 32*W)
+  // ---- 5. Kahn with min-(key,row) pop (network.hpp:192-214), in rank space:
+  //         lane l owns ranks l + 32j.  A rank is ready when every predecessor
+  //         has been emitted; the pop is the lowest ready rank (first set bit
+  //         of the ready ballots).  Predecessor bits stay in registers for
+  //         W <= 4; wider genomes count down with shared-memory bit tests.
+  constexpr int NJ = W;  // ranks per lane (N <= 32*W)
+  constexpr bool kRegBits = W <= 4;
+  uint32_t pr[kRegBits ? NJ : 1][kRegBits ? W : 1];
   int cnt[NJ];
-  unsigned rk[NJ];
   unsigned live = 0;     // bit j: eligible and not yet emitted
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
-    const int r = lane + 32 * j;
+    const int rk = lane + 32 * j;
+    int pc = 0;
     cnt[j] = 0;
-    rk[j] = 0xffffffffu;
-    if (r < N && (s.flags[r] & 1)) {
-      int pc = 0;
+    if (kRegBits) {
 #pragma unroll
-      for (int w = 0; w < W; ++w) pc += __popc(s.pred[r * W + w]);
-      const int R = s.R[r];
-      const int key = int(s.kr[r] >> 8);
-      if (R == pc && (key >= 0 || R > 0)) live |= 1u << j;
+      for (int w = 0; w < W; ++w) pr[kRegBits ? j : 0][kRegBits ? w : 0] = 0u;
+    }
+    if (rk < populated) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint32_t b = s.predr[rk * W + w];
+        pc += __popc(b);
+        if (kRegBits) pr[kRegBits ? j : 0][kRegBits ? w : 0] = b;
+      }
+      const int R = s.R[s.row_of_rank[rk]];
+      if (R == pc && (s.sorted_key[rk] >= 0 || R > 0)) live |= 1u << j;
       cnt[j] = pc;
-      rk[j] = s.rank[r];
     }
   }
+  uint32_t em[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) em[w] = 0u;
   int count = 0;
   for (;;) {
-    unsigned best = 0xffffffffu;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-      if (((live >> j) & 1u) && cnt[j] == 0) best = min(best, rk[j]);
-    best = __reduce_min_sync(kFull, best);
-    if (best == 0xffffffffu) break;
-    const int u = s.row_of_rank[best];
-    if (lane == 0) s.order[count] = uint16_t(u);
-    ++count;
-    const int uw = u >> 5;
-    const uint32_t ub = 1u << (u & 31);
+    int best = -1;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
-      if (!((live >> j) & 1u)) continue;
-      if (rk[j] == best) { live &= ~(1u << j); continue; }
-      const int r = lane + 32 * j;
-      if (s.pred[r * W + uw] & ub) --cnt[j];
+      bool rdy;
+      if (kRegBits) {
+        uint32_t pend = 0u;
+#pragma unroll
+        for (int w = 0; w < W; ++w) pend |= pr[kRegBits ? j : 0][kRegBits ? w : 0] & ~em[w];
+        rdy = ((live >> j) & 1u) && pend == 0u;
+      } else {
+        rdy = ((live >> j) & 1u) && cnt[j] == 0;
+      }
+      const unsigned b = __ballot_sync(kFull, rdy);
+      if (best < 0 && b) best = 32 * j + __ffs(b) - 1;
+    }
+    if (best < 0) break;
+    if (lane == 0) s.order[count] = uint16_t(best);  // a rank; rows below
+    ++count;
+    const int bw = best >> 5;
+    const uint32_t bb = 1u << (best & 31);
+    if ((best & 31) == lane) live &= ~(1u << bw);
+    if (kRegBits) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) em[w] |= (w == bw) ? bb : 0u;
+    } else {
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (((live >> j) & 1u) && (s.predr[(lane + 32 * j) * W + bw] & bb)) --cnt[j];
     }
   }
   __syncwarp();
   uint16_t* gorder = reinterpret_cast<uint16_t*>(net + L.order_off);
-  for (int p = lane; p < count; p += 32) gorder[p] = s.order[p];
+  for (int p = lane; p < count; p += 32) {
+    const uint16_t row = s.row_of_rank[s.order[p]];
+    s.order[p] = row;
+    gorder[p] = row;
+  }
+  __syncwarp();
   if (count != populated) {  // network.hpp:216-218; path rebuilt by k_describe
     if (lane == 0) tf_fail(net, 1 + FNB_E_CYCLE_DETECTED, kErrCycle, 0, 0, count);
     return;
@@ -270,12 +398,13 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
 
   // ---- 6a. ops in topological order, skipping input rows (network.hpp:252-254):
   //          op index and record base per row; each op = max(1, ceil(fanin/4))
-  //          records.  (rank / row_of_rank / R / sorted_key are free after
-  //          Kahn and reused as opos / slot_of / last_use / fanin.)
+  //          records.  (rank / row_of_rank / R / sorted_key / predr are free
+  //          after Kahn and reused as opos / slot_of / last_use / fanin / free_at.)
   uint16_t* opos = s.rank;
   uint16_t* slot_of = s.row_of_rank;
   int* last_use = s.R;
   int* fanin = s.sorted_key;
+  uint32_t* free_at = s.predr;  // [op][W]: slots whose value's last reader is the op
   int op_base = 0, rec_base = 0, edge_total = 0;
   for (int p0 = 0; p0 < count; p0 += 32) {
     const int p = p0 + lane;
@@ -299,7 +428,9 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
       if (lane >= d) { incl += t; incl_e += te; }
     }
     if (is_op) {
-      opos[row] = uint16_t(op_base + __popc(m & ((1u << lane) - 1u)));
+      const int k = op_base + __popc(m & ((1u << lane) - 1u));
+      opos[row] = uint16_t(k);
+      s.op_row[k] = uint16_t(row);
       s.ebeg[row] = uint16_t(rec_base + incl - nrec);
       fanin[row] = ne;
     }
@@ -312,10 +443,10 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     last_use[r] = -1;
     slot_of[r] = 0xffff;
 #pragma unroll
-    for (int w = 0; w < W; ++w) s.die[r * W + w] = 0u;
+    for (int w = 0; w < W; ++w) free_at[r * W + w] = 0u;
   }
   __syncwarp();
-  for (int i = lane; i < sh.O; i += 32) last_use[out_rows[i]] = 0x7fffffff;
+  for (int i = lane; i < sh.O; i += 32) last_use[out_rows[i]] = kLastForever;
   __syncwarp();
   for (int r = lane; r < C; r += 32) {
     const int dst = s.cdst[r];
@@ -323,82 +454,79 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     atomicMax(&last_use[s.csrc[r]], int(opos[dst]));
   }
   __syncwarp();
-  // values dying at each op, as row bitmasks indexed by op
-  for (int r = lane; r < N; r += 32) {
-    const int k = last_use[r];
-    if (k >= 0 && k < 0x7fffffff) atomicOr(&s.die[k * W + (r >> 5)], 1u << (r & 31));
-  }
-  __syncwarp();
   // ---- 6c. value slots: linear scan over the op order, lowest free slot
-  //          (slots = max live values); lane 0 touches each value once.  The
-  //          free mask is a W-word register array indexed only by unrolled
-  //          compile-time loops (no local memory).
+  //          (slots = max live values).  A value's slot is queued on the op
+  //          that reads it last (free_at), so each op costs W mask words, one
+  //          find-first-zero and one queue update.  The used mask is a W-word
+  //          register array indexed only by unrolled loops.
   int n_slots = 0;
   if (lane == 0) {
     uint32_t used[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) used[w] = 0u;
-    auto alloc = [&]() {
-      int sl = -1;
+    auto alloc = [&]() {  // lowest free slot (select chain, no branches)
+      int sl = 0;
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        if (sl < 0 && used[w] != 0xffffffffu) {
-          const int b = __ffs(~used[w]) - 1;
-          used[w] |= 1u << b;
-          sl = w * 32 + b;
-        }
+      for (int w = W - 1; w >= 0; --w) {
+        const uint32_t f = ~used[w];
+        sl = f ? w * 32 + __ffs(f) - 1 : sl;
       }
+      const int sw = sl >> 5;
+      const uint32_t bit = 1u << (sl & 31);
+#pragma unroll
+      for (int w = 0; w < W; ++w) used[w] |= (w == sw) ? bit : 0u;
       n_slots = max(n_slots, sl + 1);
       return sl;
     };
-    auto release = [&](int sl) {
+    auto retire = [&](int sl, int lu) {  // queue the slot on its last reader, or free it now
+      const int sw = sl >> 5;
+      const uint32_t bit = 1u << (sl & 31);
+      if (lu < 0) {
 #pragma unroll
-      for (int w = 0; w < W; ++w)
-        if (w == (sl >> 5)) used[w] &= ~(1u << (sl & 31));
+        for (int w = 0; w < W; ++w) used[w] &= (w == sw) ? ~bit : 0xffffffffu;
+      } else if (lu != kLastForever) {
+        free_at[lu * W + sw] |= bit;
+      }
     };
     for (int i = 0; i < sh.I; ++i) {
       const int r = in_rows[i];
-      if (slot_of[r] == 0xffff) slot_of[r] = uint16_t(alloc());
-    }
-    int k = 0;
-    for (int p = 0; p < count; ++p) {
-      const int row = s.order[p];
-      if (s.flags[row] & 2) continue;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        uint32_t bits = s.die[k * W + w];
-        while (bits) {
-          release(slot_of[w * 32 + __ffs(bits) - 1]);
-          bits &= bits - 1;
-        }
+      if (slot_of[r] == 0xffff) {
+        const int sl = alloc();
+        slot_of[r] = uint16_t(sl);
+        const int lu = last_use[r];
+        if (lu >= 0) retire(sl, lu);  // an unread input keeps its slot (as before)
       }
+    }
+    for (int k = 0; k < op_base; ++k) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) used[w] &= ~free_at[k * W + w];
+      const int row = s.op_row[k];
       const int sl = alloc();
       slot_of[row] = uint16_t(sl);
-      if (last_use[row] < 0) release(sl);  // written, never read
-      ++k;
+      retire(sl, last_use[row]);
     }
   }
   n_slots = __shfl_sync(kFull, n_slots, 0);
   __syncwarp();
   // ---- 6d. record headers; pad slots read the zero slot n_slots
   Rec* grec = reinterpret_cast<Rec*>(net + L.ops_off);
-  for (int p = lane; p < count; p += 32) {
-    const int row = s.order[p];
-    if (s.flags[row] & 2) continue;
+  for (int k = lane; k < op_base; k += 32) {
+    const int row = s.op_row[k];
     const int ne = fanin[row];
     const int nrec = ne == 0 ? 1 : (ne + kRecSlots - 1) / kRecSlots;
     const int rb = s.ebeg[row];
+    const uint16_t code = s.ncode[row];
     RecHeader h;
-    h.bias = float(nrow[row * kNodeCols + kBias]);
-    h.resp = float(nrow[row * kNodeCols + kResp]);
+    h.bias = s.nbias[row];
+    h.resp = s.nresp[row];
     h.dst = slot_of[row];
-    h.act = sh.act[int(nrow[row * kNodeCols + kAct])];
-    h.agg = sh.agg[int(nrow[row * kNodeCols + kAgg])];
+    h.act = uint8_t(code & 0xff);
+    h.agg = uint8_t(code >> 8);
     h.fanin = uint16_t(ne);
-    for (int k = 0; k < nrec; ++k) {
-      h.cnt = uint8_t(min(kRecSlots, ne - k * kRecSlots > 0 ? ne - k * kRecSlots : 0));
-      h.flags = uint8_t((k == 0 ? kRecFirst : 0) | (k == nrec - 1 ? kRecLast : 0));
-      grec[rb + k].h = h;
+    for (int q = 0; q < nrec; ++q) {
+      h.cnt = uint8_t(min(kRecSlots, ne - q * kRecSlots > 0 ? ne - q * kRecSlots : 0));
+      h.flags = uint8_t((q == 0 ? kRecFirst : 0) | (q == nrec - 1 ? kRecLast : 0));
+      grec[rb + q].h = h;
     }
     Edge z;  // pad slots of the last record: zero weight, the zero slot
     z.w = 0.0f;
@@ -410,6 +538,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   // ---- 7. edges: the i-th predecessor (ascending source row) of an op goes
   //         to slot i%4 of its record i/4, reading the source's value slot
   for (int r = lane; r < C; r += 32) {
+    const double w = crow[r * kConnCols + kW];
     const int dst = s.cdst[r];
     if (dst < 0 || (s.flags[dst] & 2)) continue;
     const int src = s.csrc[r];
@@ -422,7 +551,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
       else if (w == sw) below += __popc(bits & ((1u << (src & 31)) - 1u));
     }
     Edge e;
-    e.w = float(crow[r * kConnCols + kW]);
+    e.w = float(w);
     e.src = slot_of[src];
     e.conn_row = uint16_t(r);
     grec[s.ebeg[dst] + below / kRecSlots].slot[below % kRecSlots] = e;
@@ -432,8 +561,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   for (int i = lane; i < sh.I; i += 32) in_rows[i] = slot_of[in_rows[i]];
   for (int i = lane; i < sh.O; i += 32) out_rows[i] = slot_of[out_rows[i]];
   if (lane == 0) {
-    reinterpret_cast<NetHeader*>(net)->n_slots = n_slots;
     NetHeader* h = reinterpret_cast<NetHeader*>(net);
+    h->n_slots = n_slots;
     h->status = 0;
     h->err_kind = kErrNone;
     h->err_a = 0;
