@@ -194,8 +194,7 @@ __global__ void k7_advance(int* next_key) { next_key[0] += next_key[1]; }
 struct MutSmem {
   unsigned long long* nkeys;  // marker table: node key -> first row
   int* nrows;
-  unsigned long long* ckeys;  // marker table: conn pair -> first row
-  int* crows;
+  uint32_t* pairs;             // [N][W]: live connection (from row, to row) present (find_conn, ops.hpp:261)
   uint32_t* reach;            // [N][W]: rows reachable (>= 1 enabled edge) from row
   int* sbuf;                  // [2N] S2 fallback: sorted keys / targets
   int* nkey;                  // [N] node key (rows)
@@ -211,8 +210,8 @@ struct MutSmem {
 
 __host__ __device__ inline size_t mut_smem_bytes(int N, int C) {
   const int W = (N + 31) / 32;
-  size_t b = size_t(table_capacity(N)) * 12 + size_t(table_capacity(C)) * 12;
-  b += size_t(N) * W * 4 + size_t(2 * N) * 4;      // reach, sbuf
+  size_t b = size_t(table_capacity(N)) * 12;
+  b += size_t(N) * W * 4 * 2 + size_t(2 * N) * 4;  // reach, pairs, sbuf
   b += size_t(N) * 4 * 3 + size_t(C) * 4 * 2;      // nkey, list_a, list_b, cin, cout
   b += size_t(N) + size_t(C) + 64;                 // flags, slack
   b += 32 * 4 + size_t(3 * W) * 4 + 16;            // probes, BFS bitsets
@@ -221,12 +220,11 @@ __host__ __device__ inline size_t mut_smem_bytes(int N, int C) {
 
 __device__ inline MutSmem mut_carve(uint8_t* p, int N, int C) {
   MutSmem s;
-  const int Hn = table_capacity(N), Hc = table_capacity(C), W = (N + 31) / 32;
+  const int Hn = table_capacity(N), W = (N + 31) / 32;
   s.nkeys = reinterpret_cast<unsigned long long*>(p); p += size_t(Hn) * 8;
-  s.ckeys = reinterpret_cast<unsigned long long*>(p); p += size_t(Hc) * 8;
   s.nrows = reinterpret_cast<int*>(p); p += size_t(Hn) * 4;
-  s.crows = reinterpret_cast<int*>(p); p += size_t(Hc) * 4;
   s.reach = reinterpret_cast<uint32_t*>(p); p += size_t(N) * W * 4;
+  s.pairs = reinterpret_cast<uint32_t*>(p); p += size_t(N) * W * 4;
   s.sbuf = reinterpret_cast<int*>(p); p += size_t(2 * N) * 4;
   s.nkey = reinterpret_cast<int*>(p); p += size_t(N) * 4;
   s.list_a = reinterpret_cast<int*>(p); p += size_t(N) * 4;
@@ -461,7 +459,9 @@ __device__ bool conn_walk(const uint16_t* dw, uint32_t need, uint32_t p0, int m,
   return true;
 }
 
-__global__ void __launch_bounds__(128)
+// 8 CTAs (32 warps) per SM: the kernel is latency-bound (lane-0 streams, warp
+// scans), so occupancy is worth a few spilled registers
+__global__ void __launch_bounds__(128, 8)
 k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
                int n_children, const uint8_t* __restrict__ active, int N, int C, MutCfgDev cfg, DevShape sh,
                const int* __restrict__ plan_flag, const unsigned long long* __restrict__ plan_pair,
@@ -478,7 +478,7 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
   double* n = nodes + size_t(c) * N * kNodeCols;
   double* cc = conns + size_t(c) * C * kConnCols;
   const Key4 key = load_key(keys, c);
-  const int Hn = table_capacity(N), Hc = table_capacity(C), W = (N + 31) / 32;
+  const int Hn = table_capacity(N), W = (N + 31) / 32;
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
   int st = 0;
   for (int r = lane; r < N; r += 32) stage_node(sm, n, r, sh);
@@ -552,21 +552,23 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
       }
       if (nk > 0 && nt > 0) {
         for (int i = lane; i < Hn; i += 32) { sm.nkeys[i] = kEmptyKey; sm.nrows[i] = INT_MAX; }
-        for (int i = lane; i < Hc; i += 32) { sm.ckeys[i] = kEmptyKey; sm.crows[i] = INT_MAX; }
-        for (int i = lane; i < N * W; i += 32) sm.reach[i] = 0u;
+        for (int i = lane; i < N * W; i += 32) { sm.reach[i] = 0u; sm.pairs[i] = 0u; }
         __syncwarp();
         for (int q = lane; q < N; q += 32)
           if (n_live(q)) table_insert(sm.nkeys, sm.nrows, Hn - 1, uint32_t(sm.nkey[q]), q);
-        for (int q = lane; q < C; q += 32)
-          if (c_live(q))
-            table_insert(sm.ckeys, sm.crows, Hc - 1,
-                         (static_cast<unsigned long long>(uint32_t(sm.cin[q])) << 32) | uint32_t(sm.cout[q]), q);
         __syncwarp();
-        for (int q = lane; q < C; q += 32) {  // successor bitsets over enabled edges (ops.hpp:106)
-          if (sm.cflag[q] != 3) continue;
+        // present pairs over live rows (find_conn) and successor bitsets over
+        // enabled edges (ops.hpp:106), both by node row (a key's first row).
+        // Probe endpoints are node keys, so a pair whose endpoint has no node
+        // row can never match a probe.
+        for (int q = lane; q < C; q += 32) {
+          if (!c_live(q)) continue;
           const int a = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(sm.cin[q]));
           const int b = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(sm.cout[q]));
-          if (a >= 0 && b >= 0) atomicOr(&sm.reach[a * W + (b >> 5)], 1u << (b & 31));
+          if (a >= 0 && b >= 0) {
+            atomicOr(&sm.pairs[a * W + (b >> 5)], 1u << (b & 31));
+            if (sm.cflag[q] == 3) atomicOr(&sm.reach[a * W + (b >> 5)], 1u << (b & 31));
+          }
         }
         // the 16 probes of pick_new_conn (ops.hpp:256-266): their draws do not
         // depend on the legality of earlier probes, so lane 0 draws them all
@@ -578,25 +580,25 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
         __syncwarp();
         // sm.reach holds successor bitsets; the fallback below closes it in place
         // legal(from, to): pair absent and !creates_cycle (ops.hpp:93-111, 261-263)
+        auto present = [&](int rf, int rt) {  // find_conn(from, to) >= 0
+          return rf >= 0 && rt >= 0 && ((sm.pairs[rf * W + (rt >> 5)] >> (rt & 31)) & 1u);
+        };
         auto legal = [&](int from, int to) {
-          const unsigned long long pk = (static_cast<unsigned long long>(uint32_t(from)) << 32) | uint32_t(to);
-          if (table_find(sm.ckeys, sm.crows, Hc - 1, pk) >= 0) return false;
-          if (from == to) return false;
           const int rt = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(to));
           const int rf = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(from));
+          if (present(rf, rt)) return false;
+          if (from == to) return false;
           if (rt < 0 || rf < 0) return true;
           return !((sm.reach[rt * W + (rf >> 5)] >> (rf & 31)) & 1u);
         };
         int found = 0, pf = 0, pt = 0, pidx = -1;
         for (int p = 0; p < 16 && !found; ++p) {  // warp-uniform
           const int from = sm.probe[2 * p], to = sm.probe[2 * p + 1];
-          const unsigned long long pk = (static_cast<unsigned long long>(uint32_t(from)) << 32) | uint32_t(to);
+          const int rt = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(to));
+          const int rf = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(from));
           bool ok = false;
-          if (table_find(sm.ckeys, sm.crows, Hc - 1, pk) < 0 && from != to) {
-            const int rt = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(to));
-            const int rf = table_find(sm.nkeys, sm.nrows, Hn - 1, uint32_t(from));
+          if (!present(rf, rt) && from != to)
             ok = rt < 0 || rf < 0 || !warp_reaches(sm.reach, rt, rf, N, W, sm.bfs);
-          }
           if (ok) {
             found = 1;
             pf = from;
