@@ -485,7 +485,8 @@ struct NodeRow {
 // conn (or node) steps of successive genomes, skipping masked genomes, so
 // the prefetch runs across genome boundaries.
 struct Cursor {
-  int g, j;  // genome (>= P: exhausted), step inside it
+  int g, j;         // genome (>= P: exhausted), step inside it
+  const double* p;  // this lane's row of step j of genome g
 };
 
 __device__ __forceinline__ bool skip_genome(const DistArgs& a, int g) {
@@ -495,39 +496,44 @@ __device__ __forceinline__ bool skip_genome(const DistArgs& a, int g) {
   if (a.after_founder && (a.after_founder[0] < 0 || g <= a.after_founder[0])) return true;
   return false;
 }
+template <bool kMasked>
 __device__ __forceinline__ int valid_from(const DistArgs& a, int g, int stride) {
-  while (g < a.P && skip_genome(a, g)) g += stride;
+  if (kMasked)
+    while (g < a.P && skip_genome(a, g)) g += stride;
   return g;
 }
-__device__ __forceinline__ void advance(const DistArgs& a, Cursor& c, int steps, int stride) {
-  if (++c.j == steps) {
-    c.j = 0;
-    c.g = valid_from(a, c.g + stride, stride);
-  }
+// Cursor over one gene class: `rows` rows of `cols` doubles per genome; the
+// lane's row pointer moves by one 32-row step, or to the next genome
+__device__ __forceinline__ Cursor cursor_at(int g, const double* base, int rows, int cols, int lane) {
+  return Cursor{g, 0, base + (size_t(g) * rows + lane) * cols};
+}
+template <bool kMasked>
+__device__ __forceinline__ void advance(const DistArgs& a, Cursor& c, int steps, int stride, const double* base,
+                                        int rows, int cols, int lane) {
+  if (++c.j == steps)
+    c = cursor_at(valid_from<kMasked>(a, c.g + stride, stride), base, rows, cols, lane);
+  else
+    c.p += 32 * cols;
 }
 
 __device__ __forceinline__ ConnRow load_conn(const DistArgs& a, const Cursor& c, int lane) {
   ConnRow x;
   x.io = make_double2(__longlong_as_double(0x7ff8000000000000ll), 0.0);
   x.w = 0.0;
-  const int r = c.j * 32 + lane;
-  if (c.g < a.P && r < a.C) {
-    const double* p = a.conns + (size_t(c.g) * a.C + r) * kConnCols;
-    x.io = __ldg(reinterpret_cast<const double2*>(p));
-    x.w = __ldg(p + kW);
+  if (c.g < a.P && c.j * 32 + lane < a.C) {
+    x.io = __ldg(reinterpret_cast<const double2*>(c.p));
+    x.w = __ldg(c.p + kW);
   }
   return x;
 }
 __device__ __forceinline__ NodeRow load_node(const DistArgs& a, const Cursor& c, int lane) {
   NodeRow x{__longlong_as_double(0x7ff8000000000000ll), 0.0, 0.0, 0.0, 0.0};
-  const int r = c.j * 32 + lane;
-  if (c.g < a.P && r < a.N) {
-    const double* p = a.nodes + (size_t(c.g) * a.N + r) * kNodeCols;
-    x.k = __ldg(p + kKey);
-    x.b = __ldg(p + kBias);
-    x.r = __ldg(p + kResp);
-    x.ag = __ldg(p + kAgg);
-    x.ac = __ldg(p + kAct);
+  if (c.g < a.P && c.j * 32 + lane < a.N) {
+    x.k = __ldg(c.p + kKey);
+    x.b = __ldg(c.p + kBias);
+    x.r = __ldg(c.p + kResp);
+    x.ag = __ldg(c.p + kAgg);
+    x.ac = __ldg(c.p + kAct);
   }
   return x;
 }
@@ -573,7 +579,7 @@ __device__ __forceinline__ void step_terms(uint32_t msk, uint32_t e, int lane, i
 // image in the caller's branch, so the compiler emits shared-space loads there.
 // A genome's node steps are spread between its connection steps, so the
 // one-step node prefetch gets several connection steps of lead time.
-template <bool kCompact>
+template <bool kCompact, bool kMasked>
 __device__ __forceinline__ void distance_genomes(const DistArgs& a, const ClassTab& tc, const ClassTab& tn, int n2,
                                                  int c2, double* tile) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -582,18 +588,21 @@ __device__ __forceinline__ void distance_genomes(const DistArgs& a, const ClassT
   const int stride = gridDim.x * kDistWarps;
   const double* cw = static_cast<const double*>(tc.ent);
   const NodeEnt* ne = static_cast<const NodeEnt*>(tn.ent);
-  const int g0 = valid_from(a, blockIdx.x * kDistWarps + warp, stride);
+  const int g0 = valid_from<kMasked>(a, blockIdx.x * kDistWarps + warp, stride);
   // prefetch: node rows one node step ahead, connection rows three steps ahead
-  Cursor nc{g0, 0}, cc{g0, 0};
+  Cursor nc = cursor_at(g0, a.nodes, a.N, kNodeCols, lane);
+  Cursor cc = cursor_at(g0, a.conns, a.C, kConnCols, lane);
+  auto next_n = [&]() { advance<kMasked>(a, nc, NS, stride, a.nodes, a.N, kNodeCols, lane); };
+  auto next_c = [&]() { advance<kMasked>(a, cc, CS, stride, a.conns, a.C, kConnCols, lane); };
   NodeRow nq = load_node(a, nc, lane);
-  advance(a, nc, NS, stride);
+  next_n();
   ConnRow q0 = load_conn(a, cc, lane);
-  advance(a, cc, CS, stride);
+  next_c();
   ConnRow q1 = load_conn(a, cc, lane);
-  advance(a, cc, CS, stride);
+  next_c();
   ConnRow q2 = load_conn(a, cc, lane);
-  advance(a, cc, CS, stride);
-  for (int g = g0; g < a.P; g = valid_from(a, g + stride, stride)) {
+  next_c();
+  for (int g = g0; g < a.P; g = valid_from<kMasked>(a, g + stride, stride)) {
     int n1 = 0, c1 = 0, mn = 0, mc = 0;
     double sum_n = 0.0, sum_c = 0.0;
     int ni = 0;  // next node step
@@ -604,7 +613,7 @@ __device__ __forceinline__ void distance_genomes(const DistArgs& a, const ClassT
         q0 = q1;
         q1 = q2;
         q2 = load_conn(a, cc, lane);
-        advance(a, cc, CS, stride);
+        next_c();
         const bool nonempty = !isnan(x.io.x);
         c1 += __popc(__ballot_sync(kFull, nonempty));
         uint32_t msk = 0u, e = 0u;
@@ -612,12 +621,13 @@ __device__ __forceinline__ void distance_genomes(const DistArgs& a, const ClassT
         step_terms(msk, e, lane, S, tile, mc, sum_c,
                    [&](int, uint32_t i) { return fabs(__dsub_rn(x.w, cw[i])); });  // |dw| / 1.0 == |dw|
       }
-      // ---- node genes: (|db| + |dr| + [agg!=] + [act!=]) / 4 (ops.hpp:428-441)
-      while (ni < NS && ni * CS <= j * NS) {
+      // ---- node genes: (|db| + |dr| + [agg!=] + [act!=]) / 4 (ops.hpp:428-441);
+      //      spread between the connection steps, the last one takes any left (N > C)
+      while (ni < NS && (ni * CS <= j * NS || j == CS - 1)) {
         ++ni;
         const NodeRow x = nq;
         nq = load_node(a, nc, lane);
-        advance(a, nc, NS, stride);
+        next_n();
         const bool nonempty = !isnan(x.k);
         n1 += __popc(__ballot_sync(kFull, nonempty));
         uint32_t msk = 0u, e = 0u;
@@ -666,7 +676,7 @@ __device__ __forceinline__ ClassTab node_tab(const uint8_t* img, const UnionHdr*
                   img + h->off_nent, reinterpret_cast<const uint32_t*>(img + h->off_ncode), h->nb_n, h->seed_n};
 }
 
-template <bool kCompact>
+template <bool kCompact, bool kMasked>
 __device__ __forceinline__ void distance_placed(const DistArgs& a, const UnionView& u, uint32_t smem_img_cap,
                                                 double* tile, uint8_t* simg, int n2, int c2) {
   const UnionHdr* h = u.hdr;
@@ -678,13 +688,13 @@ __device__ __forceinline__ void distance_placed(const DistArgs& a, const UnionVi
     copy16(simg, u.img, cb);
     copy16(simg + cb, gnode, align16u(nbytes));
     __syncthreads();
-    distance_genomes<kCompact>(a, conn_tab(simg, h), node_tab(simg + cb, h), n2, c2, tile);
+    distance_genomes<kCompact, kMasked>(a, conn_tab(simg, h), node_tab(simg + cb, h), n2, c2, tile);
   } else if (cb <= smem_img_cap) {
     copy16(simg, u.img, cb);
     __syncthreads();
-    distance_genomes<kCompact>(a, conn_tab(simg, h), node_tab(gnode, h), n2, c2, tile);
+    distance_genomes<kCompact, kMasked>(a, conn_tab(simg, h), node_tab(gnode, h), n2, c2, tile);
   } else {
-    distance_genomes<kCompact>(a, conn_tab(u.img, h), node_tab(gnode, h), n2, c2, tile);
+    distance_genomes<kCompact, kMasked>(a, conn_tab(u.img, h), node_tab(gnode, h), n2, c2, tile);
   }
 }
 
@@ -697,10 +707,14 @@ k_distance(DistArgs a, UnionView u, uint32_t smem_img_cap) {
   uint8_t* simg = smem_raw + size_t(kDistWarps) * a.S * kTileStride * sizeof(double);
   const UnionHdr* h = u.hdr;
   const int n2 = lane < a.S ? h->counts[2 * lane] : 0, c2 = lane < a.S ? h->counts[2 * lane + 1] : 0;
-  if (h->compact)
-    distance_placed<true>(a, u, smem_img_cap, tile, simg, n2, c2);
-  else
-    distance_placed<false>(a, u, smem_img_cap, tile, simg, n2, c2);
+  const bool masked = a.only_unassigned != nullptr || a.after_founder != nullptr;
+  if (h->compact) {
+    if (masked) distance_placed<true, true>(a, u, smem_img_cap, tile, simg, n2, c2);
+    else distance_placed<true, false>(a, u, smem_img_cap, tile, simg, n2, c2);
+  } else {
+    if (masked) distance_placed<false, true>(a, u, smem_img_cap, tile, simg, n2, c2);
+    else distance_placed<false, false>(a, u, smem_img_cap, tile, simg, n2, c2);
+  }
 }
 
 // ---- host launcher -----------------------------------------------------------

@@ -75,6 +75,24 @@ def test_distance_bit_exact(fnb, seed, limits):
             assert got[p, s] == want, (p, s, got[p, s], want)
 
 
+def test_distance_more_node_steps_than_conn_steps(fnb):
+    """N_max = 100, C_max = 40: four 32-row node steps against two connection
+    steps, node rows scattered so the last node step holds genes."""
+    schema = ol.SchemaSpec(["tanh", "identity"], ["sum"])
+    prob = ol.Problem(100, 40, [0, 1, 2], [3])
+    nodes, conns = ol.random_genomes(404, schema, 60, 100, 40)
+    rng = np.random.default_rng(404)
+    for i in range(nodes.shape[0]):
+        nodes[i] = nodes[i][rng.permutation(100)]
+    reps_n, reps_c = nodes[:4].copy(), conns[:4].copy()
+    got = _engine(fnb, prob, schema).distance(nodes, conns, reps_n, reps_c)
+    use_ref = ol.ref_available()
+    for p in range(nodes.shape[0]):
+        for s in range(reps_n.shape[0]):
+            want = ol.distance(prob, nodes[p], conns[p], reps_n[s], reps_c[s], use_ref=use_ref)
+            assert got[p, s] == want, (p, s, got[p, s], want)
+
+
 def test_distance_known_answer(fnb):
     """test_ops.cpp:244-255: identical genomes -> 0, one extra node -> 1/5."""
     schema = ol.SchemaSpec(["tanh", "identity"], ["sum"])
