@@ -280,9 +280,18 @@ __global__ void k_rep_copy(const SpeciesDev* sd, const double* pn, const double*
     rep_c[size_t(j) * C * kConnCols + i] = pc[size_t(m) * C * kConnCols + i];
 }
 
+// Per-species integer reductions are aggregated per CTA in shared memory
+// first (a few species, thousands of genomes: global same-address atomics
+// serialise); integer adds and max are order-independent, so no bit moves.
 __global__ void k_sizes(const int* species_of, int P, SpeciesDev* sd) {
+  __shared__ int s_n[kMaxSpecies];
+  for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x) s_n[t] = 0;
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P && species_of[i] >= 0) atomicAdd(&sd->size[species_of[i]], 1);
+  if (i < P && species_of[i] >= 0) atomicAdd(&s_n[species_of[i]], 1);
+  __syncthreads();
+  for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x)
+    if (s_n[t]) atomicAdd(&sd->size[t], s_n[t]);
 }
 
 __global__ void k_mark_nonempty(SpeciesDev* sd) {
@@ -333,8 +342,14 @@ __global__ void k_stag_begin(SpeciesDev* sd) {
   for (int j = 0; j < kMaxSpecies; ++j) sd->mxbits[j] = 0ull;
 }
 __global__ void k_species_max(const double* fitness, const int* species_of, int P, SpeciesDev* sd) {
+  __shared__ unsigned long long s_mx[kMaxSpecies];
+  for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x) s_mx[t] = 0ull;
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P && species_of[i] >= 0) atomicMax(&sd->mxbits[species_of[i]], ordered_bits(fitness[i]));
+  if (i < P && species_of[i] >= 0) atomicMax(&s_mx[species_of[i]], ordered_bits(fitness[i]));
+  __syncthreads();
+  for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x)
+    if (s_mx[t]) atomicMax(&sd->mxbits[t], s_mx[t]);
 }
 __global__ void k_stagnation(SpeciesDev* sd, int species_elitism, int max_stagnation) {
   const int S = sd->count;
@@ -377,13 +392,27 @@ __global__ void k_fit_keys(const double* fitness, int P, unsigned long long* asc
   idx[i] = i;
 }
 __global__ void k_rank_sums(const int* sorted_idx, int P, const int* species_of, SpeciesDev* sd) {
+  __shared__ unsigned long long s_sum[kMaxSpecies];
+  __shared__ int s_cnt[kMaxSpecies];
+  for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x) {
+    s_sum[t] = 0ull;
+    s_cnt[t] = 0;
+  }
+  __syncthreads();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P) return;
-  const int i = sorted_idx[r];
-  const int j = species_of[i];
-  if (j < 0) return;
-  atomicAdd(reinterpret_cast<unsigned long long*>(&sd->rsum[j]), (unsigned long long)r);
-  atomicAdd(&sd->cnt[j], 1);
+  if (r < P) {
+    const int j = species_of[sorted_idx[r]];
+    if (j >= 0) {
+      atomicAdd(&s_sum[j], (unsigned long long)r);
+      atomicAdd(&s_cnt[j], 1);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x)
+    if (s_cnt[t]) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sd->rsum[t]), s_sum[t]);
+      atomicAdd(&sd->cnt[t], s_cnt[t]);
+    }
 }
 __global__ void k_spawn_begin(SpeciesDev* sd) {
   for (int j = 0; j < kMaxSpecies; ++j) { sd->rsum[j] = 0; sd->cnt[j] = 0; }

@@ -137,17 +137,21 @@ __global__ void k7_insert(const unsigned long long* __restrict__ pair, const int
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < n && flag[c]) table_insert(tkeys, tmin, H - 1, pair[c], c);
 }
-// single-CTA scan of first-occurrence flags in slot order -> rank[c]
+// first occurrence of each slot's pair (grid-wide; the lookups stay out of the scan)
+__global__ void k7_first(const unsigned long long* __restrict__ pair, const int* __restrict__ flag, int n,
+                         const unsigned long long* tkeys, const int* tmin, int H, int* __restrict__ rank) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) rank[c] = flag[c] && table_find(tkeys, tmin, H - 1, pair[c]) == c ? 1 : 0;
+}
+// single-CTA scan of the first-occurrence flags in slot order -> rank[c] (-1: not first)
 __global__ void __launch_bounds__(1024)
-k7_rank(const unsigned long long* __restrict__ pair, const int* __restrict__ flag, int n,
-        const unsigned long long* tkeys, const int* tmin, int H, int* __restrict__ rank, int* __restrict__ next_key) {
+k7_rank(int n, int* __restrict__ rank, int* __restrict__ next_key) {
   __shared__ int warp_sums[32];
   const int t = threadIdx.x, nt = blockDim.x;
   const int per = (n + nt - 1) / nt;
   const int lo = min(n, t * per), hi = min(n, lo + per);
   int cnt = 0;
-  for (int c = lo; c < hi; ++c)
-    if (flag[c] && table_find(tkeys, tmin, H - 1, pair[c]) == c) ++cnt;
+  for (int c = lo; c < hi; ++c) cnt += rank[c];
   // block exclusive scan of cnt
   const int lane = t & 31, w = t >> 5;
   int incl = cnt;
@@ -167,10 +171,7 @@ k7_rank(const unsigned long long* __restrict__ pair, const int* __restrict__ fla
   }
   __syncthreads();
   int base = (w > 0 ? warp_sums[w - 1] : 0) + incl - cnt;
-  for (int c = lo; c < hi; ++c) {
-    rank[c] = -1;
-    if (flag[c] && table_find(tkeys, tmin, H - 1, pair[c]) == c) rank[c] = base++;
-  }
+  for (int c = lo; c < hi; ++c) rank[c] = rank[c] ? base++ : -1;
   if (t == nt - 1) next_key[1] = warp_sums[(nt >> 5) - 1];  // distinct new pairs
 }
 __global__ void k7_assign(const unsigned long long* __restrict__ pair, const int* __restrict__ flag, int n,
@@ -924,11 +925,12 @@ cudaError_t launch_mutate_plan(const double* nodes, const double* conns, const i
                                                           ms.flag);
   k7_init<<<(H + 255) / 256, 256, 0, st>>>(ms.tkeys, ms.tmin, H);
   k7_insert<<<(n + 255) / 256, 256, 0, st>>>(ms.pair, ms.flag, n, ms.tkeys, ms.tmin, H);
-  k7_rank<<<1, 1024, 0, st>>>(ms.pair, ms.flag, n, ms.tkeys, ms.tmin, H, ms.rank, d_next_key);
+  k7_first<<<(n + 255) / 256, 256, 0, st>>>(ms.pair, ms.flag, n, ms.tkeys, ms.tmin, H, ms.rank);
+  k7_rank<<<1, 1024, 0, st>>>(n, ms.rank, d_next_key);
   k7_assign<<<(n + 255) / 256, 256, 0, st>>>(ms.pair, ms.flag, n, ms.tkeys, ms.tmin, H, ms.rank, d_next_key,
                                               ms.newk);
   k7_advance<<<1, 1, 0, st>>>(d_next_key);
-  *launches += 6;
+  *launches += 7;
   return cudaGetLastError();
 }
 
