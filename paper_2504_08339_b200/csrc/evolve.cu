@@ -524,8 +524,9 @@ __global__ void k_reproduce_plan(const SpeciesDev* sd, const int* members, const
   if (pool > m) pool = m;
   const Key4 ck = key_split(key_split(root1, uint64_t(sd->generation)), uint64_t(c));
   Stream sel(key_split(ck, 0));
-  const int a = mem[int(sel.below(uint64_t(pool)))];
-  const int b = mem[int(sel.below(uint64_t(pool)))];
+  const uint64_t lim = Stream::below_limit(uint64_t(pool));
+  const int a = mem[sel.index_lim(pool, lim)];
+  const int b = mem[sel.index_lim(pool, lim)];
   const bool a_fit = fitness[a] > fitness[b] || (fitness[a] == fitness[b] && a <= b);
   fit_idx[c] = a_fit ? a : b;
   oth_idx[c] = a_fit ? b : a;

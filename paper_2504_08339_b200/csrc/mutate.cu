@@ -573,11 +573,13 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
         }
         // the 16 probes of pick_new_conn (ops.hpp:256-266): their draws do not
         // depend on the legality of earlier probes, so lane 0 draws them all
-        if (lane == 0)
+        if (lane == 0) {
+          const uint64_t lim_k = Stream::below_limit(uint64_t(nk)), lim_t = Stream::below_limit(uint64_t(nt));
           for (int p = 0; p < 16; ++p) {
-            sm.probe[2 * p] = sm.list_a[s.index(nk)];
-            sm.probe[2 * p + 1] = sm.list_b[s.index(nt)];
+            sm.probe[2 * p] = sm.list_a[s.index_lim(nk, lim_k)];
+            sm.probe[2 * p + 1] = sm.list_b[s.index_lim(nt, lim_t)];
           }
+        }
         __syncwarp();
         // sm.reach holds successor bitsets; the fallback below closes it in place
         // legal(from, to): pair absent and !creates_cycle (ops.hpp:93-111, 261-263)
@@ -610,9 +612,10 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
         if (found && lane == 0) {  // the stream right after the accepted probe
           s = Stream(key_split(key, 2));
           s.coin(cfg.conn_add);
+          const uint64_t lim_k = Stream::below_limit(uint64_t(nk)), lim_t = Stream::below_limit(uint64_t(nt));
           for (int p = 0; p <= pidx; ++p) {
-            s.index(nk);
-            s.index(nt);
+            s.index_lim(nk, lim_k);
+            s.index_lim(nt, lim_t);
           }
         }
         if (!found) {  // all-pairs closure for the fallback enumeration (Warshall on bitsets)

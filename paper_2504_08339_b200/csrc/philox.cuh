@@ -100,6 +100,17 @@ struct Stream {
     return x % n;
   }
   __host__ __device__ __forceinline__ int index(int n) { return int(below(uint64_t(n))); }
+  // below(n) with the rejection limit computed once by the caller (the same n
+  // drawn repeatedly: the 64-bit remainders of the limit are most of the cost)
+  __host__ __device__ __forceinline__ static uint64_t below_limit(uint64_t n) {
+    const uint64_t mx = ~uint64_t(0);
+    return mx - ((mx % n) + 1) % n;
+  }
+  __host__ __device__ __forceinline__ int index_lim(int n, uint64_t limit) {
+    uint64_t x = next_u64();
+    while (x > limit) x = next_u64();
+    return int(x % uint64_t(n));
+  }
   // draws consumed so far
   __host__ __device__ __forceinline__ uint64_t position() const { return block * 2 - uint64_t(avail / 2); }
 };
