@@ -415,10 +415,18 @@ def main():
 
     if args.spt:
         fnb._native.lib().fnb_set_forward_spt(args.spt)
+    # FNB_BENCH_ONE_GPU=1 (test hook): every rank on cuda:0 over gloo, to run the
+    # N>1 orchestration on a one-GPU box; numbers from it are not bench values
+    one_gpu = os.environ.get("FNB_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     nodes_h, conns_h = synthetic_population(P_SHARD, N_MAX, C_MAX, FILL, NI, NO, seed=1000 + rank)
     X_h, Y_h = regression_dataset(BATCH, NI, NO, seed=0)
