@@ -326,21 +326,50 @@ __device__ __forceinline__ double apply_scalar(double v, uint32_t a, const Key4&
 // evaluated afterwards with all 32 lanes busy.  Entry: target word
 // (bits 30-31 attribute: 0 bias, 1 response, 2 weight; bits 0-29 the double
 // offset in the child's node / connection rows) and the action code.
+//
+// Packed form (one word per entry, when C_max < 2^13 and the window < 2^15):
+// bit 31 connection weight, bit 30 replace (else add), bits 15-29 the stream
+// position, bits 0-14 the double offset; a node entry's attribute is its
+// column (bias / response).  It halves the list, the largest per-warp array.
+// (stream positions run past the window only through below() rejections, each
+// with probability < 2^-61: the margin to 2^15 is never reached)
+__host__ __device__ inline bool normals_packed(int C, int win) { return C < 8192 && win < 30000; }
+
 struct NormalList {
   uint32_t* tgt;
-  uint32_t* act;
+  uint32_t* act;  // unpacked form only
   int* count;
+  bool packed;
+  __device__ __forceinline__ void put(int i, uint32_t attr, uint32_t off, uint32_t a) const {
+    if (packed) {
+      tgt[i] = (attr == 2u ? 0x80000000u : 0u) | ((a & 3u) == 2u ? 0x40000000u : 0u) | ((a >> 2) << 15) | off;
+    } else {
+      tgt[i] = (attr << 30) | off;
+      act[i] = a;
+    }
+  }
   __device__ __forceinline__ void push(uint32_t attr, uint32_t off, uint32_t a) const {
-    const int i = atomicAdd(count, 1);
-    tgt[i] = (attr << 30) | off;
-    act[i] = a;
+    put(atomicAdd(count, 1), attr, off, a);
+  }
+  __device__ __forceinline__ void get(int i, uint32_t& attr, uint32_t& off, uint32_t& a) const {
+    const uint32_t g = tgt[i];
+    if (packed) {
+      off = g & 0x7fffu;
+      a = (((g >> 15) & 0x7fffu) << 2) | ((g >> 30) & 1u ? 2u : 1u);
+      attr = (g >> 31) ? 2u : (off % kNodeCols == kBias ? 0u : 1u);
+    } else {
+      attr = g >> 30;
+      off = g & 0x3fffffffu;
+      a = act[i];
+    }
   }
 };
 
 __device__ __forceinline__ void apply_normals(const NormalList& nl, int total, double* n, double* cc, const Key4& k5,
                                               const MutCfgDev& cfg) {
   for (int t = threadIdx.x & 31; t < total; t += 32) {
-    const uint32_t g = nl.tgt[t], a = nl.act[t], attr = g >> 30, off = g & 0x3fffffffu;
+    uint32_t attr, off, a;
+    nl.get(t, attr, off, a);
     const double power = attr == 0 ? cfg.b_power : attr == 1 ? cfg.r_power : cfg.w_power;
     const double mean = attr == 0 ? cfg.b_mean : attr == 1 ? cfg.r_mean : cfg.w_mean;
     const double sd = attr == 0 ? cfg.b_std : attr == 1 ? cfg.r_std : cfg.w_std;
@@ -757,8 +786,9 @@ __host__ __device__ inline int attr_per_node(const MutCfgDev& cfg) {
 }
 __host__ __device__ inline int attr_window(int N, int C, int per_node) { return (per_node * N + 3 * C + 1) & ~1; }
 __host__ __device__ inline size_t attr_smem_bytes(int N, int C, int win) {
-  return align16(size_t(win) * 2) + align16(size_t(C) * 2) + 2 * align16(size_t(2 * N + C) * 4) +
-         align16(size_t(2 * N)) + align16(size_t(N)) + 16;
+  return align16(size_t(win) * 2) + align16(size_t(C) * 2) +
+         (normals_packed(C, win) ? 1 : 2) * align16(size_t(2 * N + C) * 4) + align16(size_t(2 * N)) +
+         align16(size_t(N)) + 16;
 }
 
 __global__ void __launch_bounds__(256)
@@ -774,8 +804,13 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   uint16_t* dw = reinterpret_cast<uint16_t*>(p8); p8 += align16(size_t(win) * 2);
   int16_t* live_row = reinterpret_cast<int16_t*>(p8); p8 += align16(size_t(C) * 2);
   NormalList nl;
+  nl.packed = normals_packed(C, win);
   nl.tgt = reinterpret_cast<uint32_t*>(p8); p8 += align16(size_t(2 * N + C) * 4);
-  nl.act = reinterpret_cast<uint32_t*>(p8); p8 += align16(size_t(2 * N + C) * 4);
+  nl.act = nullptr;
+  if (!nl.packed) {
+    nl.act = reinterpret_cast<uint32_t*>(p8);
+    p8 += align16(size_t(2 * N + C) * 4);
+  }
   int8_t* new_id = reinterpret_cast<int8_t*>(p8); p8 += align16(size_t(2 * N));  // [q] agg, [N + q] act
   uint8_t* hid = p8; p8 += align16(size_t(N));                                    // [N] mutable node row
   nl.count = reinterpret_cast<int*>(p8);
@@ -834,13 +869,11 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
       if (hid[q]) {
         const uint32_t ab = scalar(AttrDecider::kBias);
         if (ab) {
-          nl.tgt[listed] = uint32_t(q * kNodeCols + kBias);
-          nl.act[listed++] = ab;
+          nl.put(listed++, 0u, uint32_t(q * kNodeCols + kBias), ab);
         }
         const uint32_t ar = scalar(AttrDecider::kResp);
         if (ar) {
-          nl.tgt[listed] = (1u << 30) | uint32_t(q * kNodeCols + kResp);
-          nl.act[listed++] = ar;
+          nl.put(listed++, 1u, uint32_t(q * kNodeCols + kResp), ar);
         }
         if (cfg.agg_rate > 0.0 && ((word(p++) >> AttrDecider::kAggCoin) & 1u))
           ag = index(AttrDecider::kAggAcc, AttrDecider::kAggVal);
@@ -963,8 +996,9 @@ cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* ke
       nd, cd, ky, k, ac, N, C, cfg, sh, ms.flag + lo, ms.pair + lo, ms.newk + lo, d_status + lo, per_warp);
   const int win = attr_window(N, C, attr_per_node(cfg));
   const size_t aw = attr_smem_bytes(N, C, win);
+  // small CTAs when the per-warp footprint is large: more warps fit an SM
   int awarps = 8;
-  while (awarps > 1 && aw * awarps > 96 * 1024) awarps >>= 1;
+  while (awarps > 1 && aw * awarps > 48 * 1024) awarps >>= 1;
   e = cudaFuncSetAttribute(k_mutate_attrs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(aw * awarps));
   if (e != cudaSuccess) return e;
   k_mutate_attrs<<<(k + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nd, cd, ky, k, ac, d_status + lo, N, C,

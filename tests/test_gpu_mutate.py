@@ -42,7 +42,8 @@ CONFIGS = [
 
 
 @pytest.mark.parametrize("cfgkw", CONFIGS)
-@pytest.mark.parametrize("limits,seed", [((18, 60), 404), ((64, 256), 7)])
+# (20, 8200): C_max past 2^13, so K6 attrs keeps its normal list unpacked
+@pytest.mark.parametrize("limits,seed", [((18, 60), 404), ((64, 256), 7), ((20, 8200), 3)])
 def test_mutate_population_bit_exact(fnb, cfgkw, limits, seed):
     schema = ol.SchemaSpec(["tanh", "sigmoid", "identity"], ["sum", "product"])
     prob = ol.Problem(limits[0], limits[1], [0, 1, 2], [3])
