@@ -111,6 +111,29 @@ struct DevShape {
   int output_keys[32];
 };
 
+// Warps per CTA (a power of two <= max_warps) that lets the most warps of a
+// warp-per-item kernel reside on an SM when shared memory is what limits it
+// (1 KB per CTA is reserved by the hardware).  Ties keep the larger CTA.
+inline int warps_per_cta_for_smem(size_t per_warp, int max_warps) {
+  static int smem_sm = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    return v > 0 ? v : 233472;
+  }();
+  int best_w = 1;
+  long best = -1;
+  for (int w = max_warps; w >= 1; w >>= 1) {
+    long ctas = long(smem_sm) / long(size_t(w) * per_warp + 1024);
+    if (ctas > 32) ctas = 32;
+    if (ctas * w > best) {
+      best = ctas * w;
+      best_w = w;
+    }
+  }
+  return best_w;
+}
+
 }  // namespace fnb
 
 #define FNB_CUDA_OK(expr)                                   \

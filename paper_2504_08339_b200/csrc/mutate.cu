@@ -987,8 +987,7 @@ cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* ke
   const uint32_t* ky = keys + 4 * size_t(lo);
   const uint8_t* ac = active ? active + lo : nullptr;
   const size_t per_warp = align16(mut_smem_bytes(N, C));
-  int warps = 4;
-  while (warps > 1 && per_warp * warps > 96 * 1024) warps >>= 1;
+  const int warps = warps_per_cta_for_smem(per_warp, 4);
   cudaError_t e = cudaFuncSetAttribute(k_mutate_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(per_warp * warps));
   if (e != cudaSuccess) return e;
@@ -996,9 +995,7 @@ cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* ke
       nd, cd, ky, k, ac, N, C, cfg, sh, ms.flag + lo, ms.pair + lo, ms.newk + lo, d_status + lo, per_warp);
   const int win = attr_window(N, C, attr_per_node(cfg));
   const size_t aw = attr_smem_bytes(N, C, win);
-  // small CTAs when the per-warp footprint is large: more warps fit an SM
-  int awarps = 8;
-  while (awarps > 1 && aw * awarps > 48 * 1024) awarps >>= 1;
+  const int awarps = warps_per_cta_for_smem(aw, 8);
   e = cudaFuncSetAttribute(k_mutate_attrs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(aw * awarps));
   if (e != cudaSuccess) return e;
   k_mutate_attrs<<<(k + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nd, cd, ky, k, ac, d_status + lo, N, C,

@@ -647,7 +647,7 @@ template <int W>
 static cudaError_t launch_transform_w(const double* n, const double* c, int P, uint8_t* nets,
                                       const NetLayout& L, const DevShape& sh, cudaStream_t st) {
   const size_t per_warp = tf_smem_bytes(sh.N, sh.C, W);
-  const int warps = 4;
+  const int warps = warps_per_cta_for_smem(per_warp, 4);
   const size_t smem = per_warp * warps;
   cudaError_t e = cudaFuncSetAttribute(k_transform<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
