@@ -23,6 +23,8 @@ from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_popula
 
 def main():
     P, N, C, B, NI, NO = 10_000, 64, 256, 1024, 4, 1
+    if os.environ.get("FNB_SWEEP_SHAPE") == "c5":  # C5 genome shapes, 20k genomes (K2 is linear in P)
+        P, N, C = 20_000, 128, 1024
     dev = torch.device("cuda", 0)
     nodes_h, conns_h = synthetic_population(P, N, C, 0.75, NI, NO, seed=1000)
     X_h, Y_h = regression_dataset(B, NI, NO, seed=0)
@@ -54,7 +56,10 @@ def main():
     base_ms = run()
     base_fit = fit.clone()
     res = []
-    for spt, cols, pct, kb in itertools.product((1, 2, 4), (64, 128, 256, 512), (45, 55, 62, 75, 100), (48, 72, 96)):
+    grid = ((1, 2, 4), (64, 128, 256, 512), (45, 55, 62, 75, 100), (48, 72, 96))
+    if os.environ.get("FNB_SWEEP_SHAPE") == "c5":
+        grid = ((2, 4), (64, 128, 256), (30, 40, 50, 62, 75), (48, 72, 96, 144, 200))
+    for spt, cols, pct, kb in itertools.product(*grid):
         lib.fnb_set_forward_tuning(spt, cols, pct, kb)
         try:
             ms = run()
