@@ -434,7 +434,8 @@ __device__ __noinline__ uint32_t slow_word(const Key4& k5, uint32_t q, const Att
 // listed) when the walk could leave the decision window.
 __device__ __forceinline__ uint32_t map_at(uint32_t m, uint32_t s) { return (m >> (2 * s)) & 3u; }
 
-__device__ bool conn_walk(const uint16_t* dw, uint32_t need, uint32_t p0, int m, const int16_t* live_row,
+template <typename DW>
+__device__ bool conn_walk(const DW* dw, uint32_t need, uint32_t p0, int m, const int16_t* live_row,
                           const NormalList& nl) {
   const int lane = threadIdx.x & 31;
   const uint32_t span = 3u * uint32_t(m);
@@ -785,12 +786,18 @@ __host__ __device__ inline int attr_per_node(const MutCfgDev& cfg) {
   return 6 + (cfg.agg_rate > 0.0 ? 2 : 0) + (cfg.act_rate > 0.0 ? 2 : 0);
 }
 __host__ __device__ inline int attr_window(int N, int C, int per_node) { return (per_node * N + 3 * C + 1) & ~1; }
-__host__ __device__ inline size_t attr_smem_bytes(int N, int C, int win) {
-  return align16(size_t(win) * 2) + align16(size_t(C) * 2) +
+// Decision words are one byte when neither activation nor aggregation is ever
+// replaced (bits 6-15 of AttrDecider are then never read).
+__host__ __device__ inline bool attr_words_narrow(const MutCfgDev& cfg) {
+  return !(cfg.agg_rate > 0.0) && !(cfg.act_rate > 0.0);
+}
+__host__ __device__ inline size_t attr_smem_bytes(int N, int C, int win, bool narrow) {
+  return align16(size_t(win) * (narrow ? 1 : 2)) + align16(size_t(C) * 2) +
          (normals_packed(C, win) ? 1 : 2) * align16(size_t(2 * N + C) * 4) + align16(size_t(2 * N)) +
          align16(size_t(N)) + 16;
 }
 
+template <typename DW>
 __global__ void __launch_bounds__(256)
 k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
                int n_children, const uint8_t* __restrict__ active, const int* __restrict__ status, int N, int C,
@@ -801,7 +808,7 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   if (c >= n_children) return;
   if ((active && !active[c]) || status[c]) return;
   uint8_t* p8 = smem_raw + size_t(warp) * smem_per_warp;
-  uint16_t* dw = reinterpret_cast<uint16_t*>(p8); p8 += align16(size_t(win) * 2);
+  DW* dw = reinterpret_cast<DW*>(p8); p8 += align16(size_t(win) * sizeof(DW));
   int16_t* live_row = reinterpret_cast<int16_t*>(p8); p8 += align16(size_t(C) * 2);
   NormalList nl;
   nl.packed = normals_packed(C, win);
@@ -842,8 +849,8 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   for (int b = lane; 2 * b < need; b += 32) {
     uint32_t w[4];
     stream_block(k5, uint64_t(b), w);
-    dw[2 * b] = dec((uint64_t(w[3]) << 32) | w[2]);
-    dw[2 * b + 1] = dec((uint64_t(w[1]) << 32) | w[0]);
+    dw[2 * b] = DW(dec((uint64_t(w[3]) << 32) | w[2]));
+    dw[2 * b + 1] = DW(dec((uint64_t(w[1]) << 32) | w[0]));
   }
   __syncwarp();
   uint32_t p_nodes_end = 0;
@@ -994,12 +1001,14 @@ cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* ke
   k_mutate_apply<<<(k + warps - 1) / warps, 32 * warps, per_warp * warps, st>>>(
       nd, cd, ky, k, ac, N, C, cfg, sh, ms.flag + lo, ms.pair + lo, ms.newk + lo, d_status + lo, per_warp);
   const int win = attr_window(N, C, attr_per_node(cfg));
-  const size_t aw = attr_smem_bytes(N, C, win);
+  const bool narrow = attr_words_narrow(cfg);
+  const size_t aw = attr_smem_bytes(N, C, win, narrow);
   const int awarps = warps_per_cta_for_smem(aw, 8);
-  e = cudaFuncSetAttribute(k_mutate_attrs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(aw * awarps));
+  auto kern = narrow ? k_mutate_attrs<uint8_t> : k_mutate_attrs<uint16_t>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(aw * awarps));
   if (e != cudaSuccess) return e;
-  k_mutate_attrs<<<(k + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nd, cd, ky, k, ac, d_status + lo, N, C,
-                                                                             cfg, sh, win, aw);
+  kern<<<(k + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nd, cd, ky, k, ac, d_status + lo, N, C, cfg, sh,
+                                                                    win, aw);
   *launches += 2;
   return cudaGetLastError();
 }
