@@ -59,6 +59,37 @@ def test_transform_order_matches_reference(fnb):
         np.testing.assert_array_equal(order[i], r["order"])
 
 
+@pytest.mark.parametrize("variant", ["wide_keys", "duplicate_rows"])
+def test_transform_key_paths_match_reference(fnb, variant):
+    """K1's rank keys are packed into 32 bits unless a key leaves [-2^23,
+    2^23 - 1) (wide path), and its key -> row hash keeps the LOWEST row of a
+    duplicated key (network.hpp:57-63): order and outputs against the reference."""
+    prob = ol.Problem(16, 60, [0, 1, 2], [3])
+    schema = ol.RICH
+    nodes, conns = ol.random_genomes(2718, schema, 120, 16, 60)
+    rng = np.random.default_rng(5)
+    if variant == "wide_keys":
+        for a in (nodes[..., 0], conns[..., 0], conns[..., 1]):
+            a[a >= 4] += float(1 << 24)
+    else:
+        for i in range(nodes.shape[0]):
+            live = np.where(~np.isnan(nodes[i, :, 0]))[0]
+            empty = np.where(np.isnan(nodes[i, :, 0]))[0]
+            if len(empty) and len(live) > 4:
+                nodes[i, empty[rng.integers(len(empty))]] = nodes[i, live[4 + rng.integers(len(live) - 4)]]
+    eng = _engine(fnb, prob, schema)
+    order, cnt = eng.transform(nodes, conns)
+    X = rng.uniform(-2, 2, size=(8, 3))
+    want = _ref_forward(prob, schema, nodes, conns, X)
+    got = eng.batch_forward(nodes, conns, X).values
+    for i in range(nodes.shape[0]):
+        r = _ref_transform(prob, schema, nodes[i], conns[i])
+        assert r["status"] == 0
+        assert cnt[i] == r["order_count"]
+        np.testing.assert_array_equal(order[i], r["order"])
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
 @pytest.mark.parametrize("kind", ["cycle", "selfloop", "dangling", "bad_act", "bad_agg", "missing_output",
                                   "dup_pair"])
 def test_transform_errors_match_reference(fnb, kind):
