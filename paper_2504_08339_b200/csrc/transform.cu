@@ -20,6 +20,7 @@ namespace fnb {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned long long kHtEmpty = ~0ull;
 constexpr int kLastForever = 0x7fffffff;  // last_use of an output row
+constexpr uint8_t kNoRow = 0xff;          // (node rows are < FNB_MAX_NODES_LIMIT = 255)
 
 // Per-warp shared memory.  Arrays that die after a step are reused by a later
 // one (noted at the reuse).
@@ -39,8 +40,8 @@ struct TfSmem {
   float* nbias;         // [N]
   float* nresp;         // [N]
   uint8_t* flags;       // [N] bit0 non-empty, bit1 input
-  int16_t* csrc;        // [C]
-  int16_t* cdst;        // [C] destination row of an enabled finite edge, else -1
+  uint8_t* csrc;        // [C] source row (rows fit a byte: N_max <= 255)
+  uint8_t* cdst;        // [C] destination row of an enabled finite edge, else kNoRow
   uint32_t ht_mask, ht_shift;
 };
 
@@ -59,7 +60,7 @@ __host__ __device__ inline size_t tf_smem_bytes(int N, int C, int W) {
   b += align16(size_t(N) * 2) * 4;       // row_of_rank, rank, order, ncode
   b += align16(size_t(N) * 4) * 2;       // nbias, nresp
   b += align16(size_t(N));               // flags
-  b += align16(size_t(C) * 2) * 2;       // csrc, cdst
+  b += align16(size_t(C)) * 2;           // csrc, cdst
   return b;
 }
 
@@ -83,8 +84,8 @@ __device__ inline TfSmem tf_carve(uint8_t* p, int N, int C, int W) {
   s.nbias = reinterpret_cast<float*>(p); p += align16(size_t(N) * 4);
   s.nresp = reinterpret_cast<float*>(p); p += align16(size_t(N) * 4);
   s.flags = p; p += align16(size_t(N));
-  s.csrc = reinterpret_cast<int16_t*>(p); p += align16(size_t(C) * 2);
-  s.cdst = reinterpret_cast<int16_t*>(p);
+  s.csrc = p; p += align16(size_t(C));
+  s.cdst = p;
   return s;
 }
 
@@ -301,17 +302,17 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     }
     if (r < C) {
       const bool edge = ne && en == 1.0;
-      int16_t d = -1;
+      uint8_t d = kNoRow;
       if (edge) {
         atomicAdd(&s.R[dst], 1);
         if (!isnan(w)) {
           atomicOr(&s.pred[dst * W + (src >> 5)], 1u << (src & 31));
           const int rs = s.rank[src], rd = s.rank[dst];
           atomicOr(&s.predr[rd * W + (rs >> 5)], 1u << (rs & 31));
-          d = int16_t(dst);
+          d = uint8_t(dst);
         }
       }
-      s.csrc[r] = int16_t(src);
+      s.csrc[r] = uint8_t(src);
       s.cdst[r] = d;
     }
   }
@@ -450,7 +451,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   __syncwarp();
   for (int r = lane; r < C; r += 32) {
     const int dst = s.cdst[r];
-    if (dst < 0 || (s.flags[dst] & 2)) continue;
+    if (dst == kNoRow || (s.flags[dst] & 2)) continue;
     atomicMax(&last_use[s.csrc[r]], int(opos[dst]));
   }
   __syncwarp();
@@ -540,7 +541,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   for (int r = lane; r < C; r += 32) {
     const double w = crow[r * kConnCols + kW];
     const int dst = s.cdst[r];
-    if (dst < 0 || (s.flags[dst] & 2)) continue;
+    if (dst == kNoRow || (s.flags[dst] & 2)) continue;
     const int src = s.csrc[r];
     int below = 0;
     const int sw = src >> 5;
