@@ -52,7 +52,7 @@ __device__ __forceinline__ float hyper_weight(double y, double thr, double wmax)
 // and are read with broadcast LDS.128.  Each lane sums its reward terms over
 // the steps in FP64; one shfl_xor tree combines them at the end.
 template <int G>
-__global__ void __launch_bounds__(kHyperWarps * 32, G == 4 ? 6 : 3)
+__global__ void __launch_bounds__(kHyperWarps * 32, G == 4 ? 7 : 3)
 k_hyper_rollout(const double* __restrict__ cppn_out, int P, HyperParams hp, const float* __restrict__ A,
                 const float* __restrict__ B, const float* __restrict__ s0, double* __restrict__ fitness,
                 float* __restrict__ w_out) {
