@@ -472,9 +472,30 @@ static cudaError_t launch_pass(const FwdConfig& c, FwdParams p, int rows_lo, int
   }
 }
 
+// Side stream + fork/join events of the overflow pass, per host thread and
+// device (a context is used from one host thread; graph capture follows the
+// fork into the side stream and back).
+struct FwdAux {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static FwdAux& fwd_aux() {
+  static thread_local FwdAux aux[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  FwdAux& x = aux[dev & 63];
+  if (!x.side) {
+    if (cudaStreamCreateWithFlags(&x.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess)
+      x.side = nullptr;
+  }
+  return x;
+}
+
 // Two passes: genomes whose live values fit the main slot capacity (almost
-// all), then -- over the same grid, exiting immediately for the rest -- the
-// few that need up to max_nodes + 1 rows.
+// all) and -- over the same grid, exiting immediately for the rest, on a side
+// stream concurrently -- the few that need up to max_nodes + 1 rows.
 // uniform_agg / uniform_act: the single registry entry, or -1 for mixed schemas
 int launch_forward(const void* nets, NetLayout L, int P, const float* X, const float* Y, int B, int fit_kind,
                    double offset, double* fitness, double* out, double* partial_buf, size_t partial_cap,
@@ -496,11 +517,21 @@ int launch_forward(const void* nets, NetLayout L, int P, const float* X, const f
   p.units = fitness_units(B);
   const bool fit = fit_kind != FNB_FIT_NONE;
   if (fit && sizeof(double) * size_t(P) * p.units > partial_cap) return 1;
-  if (launch_pass(c, p, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
-  ++*launches;
   if (rows_main < L.N + 1) {
+    // The overflow pass (a few genomes, long per-CTA latency) runs on a side
+    // stream next to the main pass instead of as a tail after it; both write
+    // disjoint genomes' units, so no bit depends on the overlap.
+    FwdAux& x = fwd_aux();
+    if (!x.side) return 1;
     const FwdConfig co = fwd_config(L, P, B, L.N + 1, true);
-    if (launch_pass(co, p, rows_main, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
+    if (cudaEventRecord(x.fork, st) != cudaSuccess || cudaStreamWaitEvent(x.side, x.fork, 0) != cudaSuccess) return 1;
+    if (launch_pass(co, p, rows_main, uniform_agg, uniform_act, x.side) != cudaSuccess) return 1;
+    if (cudaEventRecord(x.join, x.side) != cudaSuccess) return 1;
+    if (launch_pass(c, p, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
+    if (cudaStreamWaitEvent(st, x.join, 0) != cudaSuccess) return 1;
+    *launches += 2;
+  } else {
+    if (launch_pass(c, p, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
     ++*launches;
   }
   if (fit) {
