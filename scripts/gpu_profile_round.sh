@@ -2,7 +2,7 @@
 python -c "import paper_2504_08339_b200" 2>/dev/null || { echo "library stale: rebuilding"; python -c "import __graft_entry__ as g; g.build()"; }
 timeout 900 python bench.py > gpurun_out/bench${TAG:-r01d}.json 2>gpurun_out/bench${TAG:-r01d}.err; echo bench=$?; tail -2 gpurun_out/bench${TAG:-r01d}.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches${TAG:-r01d}.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo ncu_l=$?
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_forward --launch-skip 4 -c 1 -f -o gpurun_out/prof${TAG:-r01d}_k2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-c5 --no-generations > /dev/null 2>&1; echo ncu_k2=$?
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_forward --launch-skip 5 -c 1 -f -o gpurun_out/prof${TAG:-r01d}_k2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-c5 --no-generations > /dev/null 2>&1; echo ncu_k2=$?
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_distance --launch-skip 2 -c 1 -f -o gpurun_out/prof${TAG:-r01d}_k3_c5 python scripts/run_c5_distance.py 1 > /dev/null 2>&1; echo ncu_k3=$?
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_hyper_rollout -c 1 -f -o gpurun_out/prof${TAG:-r01d}_c4 python -c "
 import torch,bench
