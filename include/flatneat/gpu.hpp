@@ -78,6 +78,7 @@ class Context {
 
   // transform() of every genome (network.hpp:122): int32 orders, -1 padded
   std::vector<std::int32_t> transform_orders(const PopulationTensors& pop) {
+    check_pop(pop);
     std::vector<std::int32_t> order(std::size_t(pop.pop_size) * std::size_t(limits_.max_nodes));
     check(fnb_transform(ctx_, pop.pop_nodes.data(), pop.pop_conns.data(), pop.pop_size, order.data(), nullptr));
     return order;
@@ -85,6 +86,7 @@ class Context {
 
   // transform + batch_forward (network.hpp:294-330); FP32 on the device
   BatchResult batch_forward(const PopulationTensors& pop, std::span<const double> inputs, int batch) {
+    check_pop(pop);
     if (int(inputs.size()) != batch * int(in_.size()))
       raise(Errc::shape_mismatch, "input matrix is not batch x num_inputs");
     BatchResult r;
@@ -102,6 +104,7 @@ class Context {
   std::vector<double> evaluate(const PopulationTensors& pop, std::span<const double> inputs,
                                std::span<const double> targets, int batch, int fitness_kind = FNB_FIT_NEG_MSE,
                                double offset = 0.0) {
+    check_pop(pop);
     if (int(inputs.size()) != batch * int(in_.size()) || int(targets.size()) != batch * int(out_.size()))
       raise(Errc::shape_mismatch, "input / target matrix is not batch x num_inputs / num_outputs");
     std::vector<double> fit(std::size_t(pop.pop_size));
@@ -113,6 +116,8 @@ class Context {
   // distance(genome_p, rep_s) (ops.hpp:415) for a population x representatives
   std::vector<double> distance(const PopulationTensors& pop, const PopulationTensors& reps,
                                const DistanceConfig& cfg = {}) {
+    check_pop(pop);
+    check_pop(reps);
     std::vector<double> out(std::size_t(pop.pop_size) * std::size_t(reps.pop_size));
     const fnb_distance_config dc{cfg.compatibility_disjoint, cfg.compatibility_homologous};
     check(fnb_distance(ctx_, pop.pop_nodes.data(), pop.pop_conns.data(), pop.pop_size, reps.pop_nodes.data(),
@@ -123,6 +128,10 @@ class Context {
   // crossover(fit[i], other[i], keys[i]) (ops.hpp:382) pairwise
   PopulationTensors crossover(const PopulationTensors& fit, const PopulationTensors& other,
                               std::span<const RngKey> keys) {
+    check_pop(fit);
+    check_pop(other);
+    if (other.pop_size != fit.pop_size || int(keys.size()) != fit.pop_size)
+      raise(Errc::shape_mismatch, "crossover needs one other parent and one key per fit parent");
     std::vector<std::uint32_t> k(keys.size() * 4);
     for (std::size_t i = 0; i < keys.size(); ++i) detail::copy_key(keys[i], k.data() + 4 * i);
     PopulationTensors child = fit;
@@ -133,24 +142,39 @@ class Context {
   }
 
   // mutate(genome_p, keys[p], cfg, schema, table) for p in slot order with
-  // one InnovationTable (ops.hpp:169-175, 363); `table` advances as the
-  // sequential loop would leave it.
+  // the caller's InnovationTable (ops.hpp:169-175, 363): the table's
+  // get_or_assign is called once per splitting slot, in slot order, so its
+  // memo and counter end exactly as the sequential loop leaves them --
+  // including entries it already held from earlier calls this generation.
+  // On error, genomes before the failing slot are mutated and the rest untouched.
   void mutate(PopulationTensors& pop, std::span<const RngKey> keys, const MutationConfig& cfg,
               InnovationTable& table) {
+    check_pop(pop);
+    if (int(keys.size()) != pop.pop_size) raise(Errc::shape_mismatch, "mutate needs one key per genome");
     std::vector<std::uint32_t> k(keys.size() * 4);
     for (std::size_t i = 0; i < keys.size(); ++i) detail::copy_key(keys[i], k.data() + 4 * i);
     const fnb_mutation_config mc{cfg.node_add, cfg.node_delete, cfg.conn_add, cfg.conn_delete,
                                  detail::attr(cfg.bias), detail::attr(cfg.response), detail::attr(cfg.weight),
                                  cfg.activation_replace_rate, cfg.aggregation_replace_rate};
-    int next = table.next_key();
-    const int st = fnb_mutate(ctx_, pop.pop_nodes.data(), pop.pop_conns.data(), pop.pop_size, k.data(), &mc, &next);
-    table.reserve_up_to(next);
-    check(st);
+    auto thunk = [](void* user, int in_key, int out_key) -> int {
+      return static_cast<InnovationTable*>(user)->get_or_assign(in_key, out_key);
+    };
+    check(fnb_mutate_table(ctx_, pop.pop_nodes.data(), pop.pop_conns.data(), pop.pop_size, k.data(), &mc, thunk,
+                           &table, nullptr));
   }
 
   fnb_ctx* handle() { return ctx_; }
 
  private:
+  // the flat arrays must hold pop_size genomes of this context's limits
+  // (PopulationTensors layout, genome.hpp:315-338)
+  void check_pop(const PopulationTensors& p) const {
+    if (p.limits.max_nodes != limits_.max_nodes || p.limits.max_conns != limits_.max_conns || p.pop_size < 0 ||
+        p.pop_nodes.size() != std::size_t(p.pop_size) * std::size_t(limits_.max_nodes) * kNodeCols ||
+        p.pop_conns.size() != std::size_t(p.pop_size) * std::size_t(limits_.max_conns) * kConnCols)
+      raise(Errc::shape_mismatch, "population tensors do not match the context's limits");
+  }
+
   void check(int st) {
     if (!st) return;
     const std::string what = fnb_last_error(ctx_);

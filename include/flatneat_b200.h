@@ -165,6 +165,19 @@ int fnb_crossover(fnb_ctx* ctx, const double* fit_nodes, const double* fit_conns
 int fnb_mutate(fnb_ctx* ctx, double* pop_nodes, double* pop_conns, int P, const uint32_t* keys,
                const fnb_mutation_config* cfg, int* next_key);
 
+/* InnovationTable::get_or_assign of the caller's table (ops.hpp:149-156). */
+typedef int (*fnb_innovation_fn)(void* user, int in_key, int out_key);
+/* mutate() of P genomes in slot order against the caller's own table
+ * (ops.hpp:169-175): `assign` is called once per splitting slot, in slot
+ * order, exactly as the sequential loop calls get_or_assign, and the keys it
+ * returns go into the genomes.  splits[P][3] (may be NULL) receives
+ * (in_key, out_key, new_key) per slot, -1 for a slot that did not split.  A
+ * duplicate_key failure at slot b (the key already names a node of genome b,
+ * ops.hpp:19-23) leaves genomes [0, b) mutated, b.. untouched, and the table
+ * with the calls up to and including b's. */
+int fnb_mutate_table(fnb_ctx* ctx, double* pop_nodes, double* pop_conns, int P, const uint32_t* keys,
+                     const fnb_mutation_config* cfg, fnb_innovation_fn assign, void* user, int32_t* splits);
+
 /* RngKey(seed) and RngKey::split (rng.hpp:48-66), host side. */
 void fnb_key_seed(uint64_t seed, uint32_t out[4]);
 void fnb_key_split(const uint32_t key[4], uint64_t index, uint32_t out[4]);
@@ -256,7 +269,7 @@ int fnb_hyper_evaluate_d(fnb_ctx* ctx, const void* d_nets, int P, const fnb_hype
  * E1-E5 in DESIGN.md): evaluate -> step (speciate, update_stagnation,
  * compute_spawn_counts, reproduce) -> next generation. */
 int fnb_evolver_create(fnb_ctx* ctx, const fnb_neat_config* cfg, uint64_t seed, fnb_evolver** out);
-void fnb_evolver_destroy(fnb_evolver* ev);
+void fnb_evolver_destroy(fnb_evolver* ev);  /* before fnb_ctx_destroy of its context */
 int fnb_evolver_init_population(fnb_evolver* ev);  /* initialize_population */
 /* set / get accept host or device pointers (unified addressing) */
 int fnb_evolver_set_population(fnb_evolver* ev, const double* pop_nodes, const double* pop_conns);
@@ -268,6 +281,13 @@ int fnb_evolver_evaluate(fnb_evolver* ev, const double* inputs, const double* ta
                          int fitness_kind, double fitness_offset);
 int fnb_evolver_evaluate_d(fnb_evolver* ev, const float* d_X, const float* d_Y, int batch, int fitness_kind,
                            double fitness_offset);
+/* The *_d evaluations are asynchronous: fnb_evolver_eval_check synchronises
+ * the evolver stream and returns the last evaluation's error in the
+ * reference's order -- the lowest genome whose transform failed (its
+ * reference message, fnb_last_error_index = genome), else
+ * non_finite_input (network.hpp:245-246).  batch <= 0 is empty_dataset
+ * (SPEC.md:457).  The host variant fnb_evolver_evaluate checks itself. */
+int fnb_evolver_eval_check(fnb_evolver* ev);
 /* a rank's shard [lo, hi): fitness of those genomes into d_fitness_out[hi-lo] */
 int fnb_evolver_evaluate_range_d(fnb_evolver* ev, int lo, int hi, const float* d_X, const float* d_Y, int batch,
                                  int fitness_kind, double fitness_offset, double* d_fitness_out);

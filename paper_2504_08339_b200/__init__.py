@@ -7,10 +7,10 @@ reference flatneat API.  Importing it without the built library fails loudly.
 from . import _native
 from .api import (ACTIVATIONS, AGGREGATIONS, ERRC, FIT_NEG_MSE, FIT_NONE, FIT_OFFSET_SSE, AttrMutation,
                   AttributeSchema, BatchResult, DistanceConfig, Engine, FlatneatError, GenomeLimits,
-                  HyperConfig, MutationConfig, PopulationTensors)
+                  HyperConfig, InnovationTable, MutationConfig, PopulationTensors)
 
 _native.lib()  # fail at import time if the CUDA library is absent
 
 __all__ = ["ACTIVATIONS", "AGGREGATIONS", "ERRC", "FIT_NEG_MSE", "FIT_NONE", "FIT_OFFSET_SSE", "AttrMutation",
            "AttributeSchema", "BatchResult", "DistanceConfig", "Engine", "FlatneatError", "GenomeLimits",
-           "HyperConfig", "MutationConfig", "PopulationTensors"]
+           "HyperConfig", "InnovationTable", "MutationConfig", "PopulationTensors"]

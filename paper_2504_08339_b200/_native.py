@@ -82,6 +82,8 @@ SIGNATURES = {
     "fnb_distance_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.c_int, C.POINTER(fnb_distance_config), VP, VP]),
     "fnb_crossover_d": (C.c_int, [VP, VP, VP, VP, VP, VP, C.c_int, VP, VP, VP]),
     "fnb_mutate": (C.c_int, [VP, DP, DP, C.c_int, U32P, C.POINTER(fnb_mutation_config), C.POINTER(C.c_int)]),
+    "fnb_mutate_table": (C.c_int, [VP, DP, DP, C.c_int, U32P, C.POINTER(fnb_mutation_config), VP, VP, IP]),
+    "fnb_evolver_eval_check": (C.c_int, [VP]),
     "fnb_mutate_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.POINTER(fnb_mutation_config), VP, VP, VP, VP]),
     "fnb_evolver_create": (C.c_int, [VP, C.POINTER(fnb_neat_config), C.c_uint64, C.POINTER(VP)]),
     "fnb_evolver_destroy": (None, [VP]),
@@ -114,6 +116,9 @@ SIGNATURES = {
                                      C.POINTER(C.c_float)]),
     "fnb_hyper_evaluate_d": (C.c_int, [VP, VP, C.c_int, C.POINTER(fnb_hyper_config), VP, VP, VP, VP, VP, VP]),
 }
+
+# typedef int (*fnb_innovation_fn)(void* user, int in_key, int out_key)
+INNOVATION_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int)
 
 _lib = None
 

@@ -15,6 +15,7 @@ Two call styles:
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -192,9 +193,12 @@ class Engine:
         if st:
             raise FlatneatError(st, f"{ERRC[st - 1]}: fnb_ctx_create failed")
         self._h = h
+        self._dependents = weakref.WeakSet()  # evolvers on this context: closed first
 
     def close(self):
         if getattr(self, "_h", None):
+            for d in list(getattr(self, "_dependents", ())):
+                d.close()
             self._lib.fnb_ctx_destroy(self._h)
             self._h = None
 
@@ -392,17 +396,61 @@ Engine.stream_draws_d = _engine_stream_draws_d
 Engine.split_keys_d = _engine_split_keys_d
 
 
-def _engine_mutate(self, pop_nodes, pop_conns, keys, cfg: MutationConfig = MutationConfig(), next_key: int = 0):
-    """mutate() of every genome in slot order with one InnovationTable(next_key)
-    (ops.hpp:363-374, 169-175) -> (nodes, conns, next_key).  Raises
-    FlatneatError at the lowest failing genome (its .index)."""
+class InnovationTable:
+    """The reference's InnovationTable (ops.hpp:145-167): (in, out) -> key memo
+    for one generation and a counter that never runs backwards."""
+
+    def __init__(self, first_key: int = 0):
+        self._next = int(first_key)
+        self._assignments = {}
+
+    def get_or_assign(self, in_key: int, out_key: int) -> int:
+        pair = (int(in_key), int(out_key))
+        k = self._assignments.get(pair)
+        if k is None:
+            k = self._next
+            self._next += 1
+            self._assignments[pair] = k
+        return k
+
+    def next_generation(self):
+        self._assignments.clear()
+
+    def next_key(self) -> int:
+        return self._next
+
+    def reserve_up_to(self, key: int):
+        self._next = max(self._next, int(key))
+
+
+def _engine_mutate(self, pop_nodes, pop_conns, keys, cfg: MutationConfig = MutationConfig(), next_key: int = 0,
+                   table: Optional[InnovationTable] = None):
+    """mutate() of every genome in slot order (ops.hpp:363-374, 169-175) ->
+    (nodes, conns, next_key).  With `table` (an InnovationTable), its
+    get_or_assign is called once per splitting slot in slot order, as the
+    sequential loop calls it (fnb_mutate_table); without it a fresh
+    InnovationTable(next_key) is used on the device.  Raises FlatneatError at
+    the lowest failing genome (its .index)."""
     n = np.array(pop_nodes, dtype=np.float64, copy=True, order="C")
     c = np.array(pop_conns, dtype=np.float64, copy=True, order="C")
     P = n.shape[0]
     self._check_pop(n, c)
-    k = np.ascontiguousarray(keys, dtype=np.uint32).reshape(P, 4)
-    nk = C.c_int(next_key)
+    k = np.ascontiguousarray(keys, dtype=np.uint32)
+    if k.size != 4 * P:
+        raise FlatneatError(9, "shape_mismatch: mutate needs one key per genome")
+    k = k.reshape(P, 4)
     mc = cfg.to_c()
+    if table is not None:
+        cb = N.INNOVATION_FN(lambda _u, a, b: table.get_or_assign(a, b))
+        st = self._lib.fnb_mutate_table(self._h, _dp(n), _dp(c), P, k.ctypes.data_as(N.U32P), C.byref(mc), cb,
+                                        None, None)
+        if st:
+            err = FlatneatError(st, self._lib.fnb_last_error(self._h).decode(),
+                                int(self._lib.fnb_last_error_index(self._h)))
+            err.partial = (n, c, table.next_key())
+            raise err
+        return n, c, table.next_key()
+    nk = C.c_int(next_key)
     st = self._lib.fnb_mutate(self._h, _dp(n), _dp(c), P, k.ctypes.data_as(N.U32P), C.byref(mc), C.byref(nk))
     if st:
         err = FlatneatError(st, self._lib.fnb_last_error(self._h).decode(), int(self._lib.fnb_last_error_index(self._h)))

@@ -1,3 +1,4 @@
+#include <cmath>
 // capi.cu -- extern "C" boundary (include/flatneat_b200.h): contexts, the
 // synchronous host layer mirroring the reference free functions, and the
 // asynchronous device layer.
@@ -389,6 +390,8 @@ int fnb_batch_forward(fnb_ctx* ctx, const double* pop_nodes, const double* pop_c
 int fnb_evaluate(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P, const double* inputs,
                  const double* targets, int batch, int fitness_kind, double fitness_offset, double* fitness_out) {
   if (fitness_kind == FNB_FIT_NONE) return set_err(ctx, FNB_E_CONFIG_ERROR, "fitness kind required", -1);
+  // SPEC.md:458 (func_fit / xor): an empty dataset has no fitness
+  if (batch <= 0) return set_err(ctx, FNB_E_EMPTY_DATASET, "dataset is empty", -1);
   return evaluate_impl(ctx, pop_nodes, pop_conns, P, inputs, targets, batch, fitness_kind, fitness_offset,
                        fitness_out, nullptr);
 }
@@ -531,6 +534,15 @@ cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, in
                           const fnb_mutation_config* m, const DevShape& sh, int* d_next_key, int* d_status,
                           void* scratch, size_t scratch_bytes, int* d_new_key_out, cudaStream_t st,
                           long long* launches);
+cudaError_t launch_mutate_plan(const double* nodes, const double* conns, const int32_t* src, const uint32_t* keys,
+                               int n, const uint8_t* active, const fnb_mutation_config* m, const DevShape& sh,
+                               int* d_next_key, void* scratch, size_t scratch_bytes, int* d_new_key_out,
+                               cudaStream_t st, long long* launches);
+cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* keys, int n, int lo, int hi,
+                                const uint8_t* active, const fnb_mutation_config* m, const DevShape& sh,
+                                int* d_status, void* scratch, size_t scratch_bytes, const int* d_new_key,
+                                cudaStream_t st, long long* launches);
+void mutate_scratch_views(void* scratch, int n, unsigned long long** pair, int** flag, int** newk);
 }  // namespace fnb
 
 extern "C" {
@@ -591,10 +603,91 @@ int fnb_mutate(fnb_ctx* ctx, double* pop_nodes, double* pop_conns, int P, const 
   *next_key = nk;
   if (bad >= 0) {
     const int code = status[size_t(bad)] - 1;
-    return set_err(ctx, code, code == FNB_E_DUPLICATE_KEY ? "node key collides with the innovation counter"
-                                                           : "mutation failed",
+    return set_err(ctx, code, code == FNB_E_DUPLICATE_KEY ? "node key " + std::to_string(newk[size_t(bad)])
+                                                           : std::string("no free node row"),
                    bad);
   }
+  return 0;
+}
+
+// mutate() of P genomes in slot order against the CALLER's InnovationTable
+// (ops.hpp:145-175, 363-374): the node-split plans (split(0), a pure function
+// of each genome) run on the device, the table's get_or_assign is replayed on
+// the host in slot order through `assign`, and the keys it hands out drive the
+// device apply.  add_node's duplicate-key check (ops.hpp:19-23) is the only
+// way a slot can fail; it is tested on the host right after the slot's
+// get_or_assign, so the table sees exactly the calls the sequential loop makes
+// before it throws.
+int fnb_mutate_table(fnb_ctx* ctx, double* pop_nodes, double* pop_conns, int P, const uint32_t* keys,
+                     const fnb_mutation_config* cfg, fnb_innovation_fn assign, void* user, int32_t* splits) {
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (P <= 0) return 0;
+  if (!assign) return set_err(ctx, FNB_E_CONFIG_ERROR, "no innovation callback", -1);
+  CK(cudaSetDevice(ctx->device));
+  const int N = ctx->L.N;
+  const size_t nrow = size_t(N) * kNodeCols, crow = size_t(ctx->L.C) * kConnCols;
+  const size_t nb = sizeof(double) * nrow * size_t(P), cb = sizeof(double) * crow * size_t(P);
+  CK(ctx->nodes.ensure(nb));
+  CK(ctx->conns.ensure(cb));
+  CK(ctx->scratch.ensure(mutate_scratch_bytes(P)));
+  CK(ctx->misc.ensure(sizeof(uint32_t) * 4 * size_t(P) + sizeof(int) * (size_t(P) + 2) + 64));
+  uint32_t* d_keys = static_cast<uint32_t*>(ctx->misc.p);
+  int* d_status = reinterpret_cast<int*>(d_keys + 4 * size_t(P));
+  int* d_nk = d_status + P;
+  const int nk2[2] = {0, 0};
+  cudaStream_t st = ctx->stream;
+  CK(cudaMemcpyAsync(ctx->nodes.p, pop_nodes, nb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->conns.p, pop_conns, cb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_keys, keys, sizeof(uint32_t) * 4 * size_t(P), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_nk, nk2, sizeof(nk2), cudaMemcpyHostToDevice, st));
+  double* dn = static_cast<double*>(ctx->nodes.p);
+  double* dc = static_cast<double*>(ctx->conns.p);
+  CK(launch_mutate_plan(dn, dc, nullptr, d_keys, P, nullptr, cfg, ctx->sh, d_nk, ctx->scratch.p, ctx->scratch.cap,
+                        nullptr, st, &ctx->launches));
+  unsigned long long* d_pair;
+  int *d_flag, *d_newk;
+  mutate_scratch_views(ctx->scratch.p, P, &d_pair, &d_flag, &d_newk);
+  std::vector<unsigned long long> pair(static_cast<size_t>(P));
+  std::vector<int> flag(static_cast<size_t>(P)), newk(static_cast<size_t>(P), -1);
+  CK(cudaMemcpyAsync(pair.data(), d_pair, sizeof(unsigned long long) * P, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(flag.data(), d_flag, sizeof(int) * P, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int bad = -1;
+  for (int c = 0; c < P && bad < 0; ++c) {
+    int in_key = 0, out_key = 0;
+    if (flag[size_t(c)]) {
+      in_key = int(uint32_t(pair[size_t(c)] >> 32));
+      out_key = int(uint32_t(pair[size_t(c)]));
+      const int k = assign(user, in_key, out_key);
+      newk[size_t(c)] = k;
+      const double* g = pop_nodes + size_t(c) * nrow;
+      for (int r = 0; r < N; ++r)
+        if (!std::isnan(g[size_t(r) * kNodeCols]) && int(g[size_t(r) * kNodeCols]) == k) { bad = c; break; }
+    }
+    if (splits) {
+      splits[3 * size_t(c)] = flag[size_t(c)] ? in_key : -1;
+      splits[3 * size_t(c) + 1] = flag[size_t(c)] ? out_key : -1;
+      splits[3 * size_t(c) + 2] = newk[size_t(c)];
+    }
+  }
+  if (splits)
+    for (int c = bad < 0 ? P : bad + 1; c < P; ++c)
+      splits[3 * size_t(c)] = splits[3 * size_t(c) + 1] = splits[3 * size_t(c) + 2] = -1;
+  const int done = bad < 0 ? P : bad;  // genomes [0, done) are mutated, the rest untouched
+  if (done > 0) {
+    CK(cudaMemcpyAsync(d_newk, newk.data(), sizeof(int) * size_t(done), cudaMemcpyHostToDevice, st));
+    CK(launch_mutate_apply(dn, dc, d_keys, P, 0, done, nullptr, cfg, ctx->sh, d_status, ctx->scratch.p,
+                           ctx->scratch.cap, d_newk, st, &ctx->launches));
+    std::vector<int> status(static_cast<size_t>(done));
+    CK(cudaMemcpyAsync(status.data(), d_status, sizeof(int) * size_t(done), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pop_nodes, dn, sizeof(double) * nrow * size_t(done), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pop_conns, dc, sizeof(double) * crow * size_t(done), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int c = 0; c < done; ++c)  // the plan guarantees the rows add_node / add_conn need
+      if (status[size_t(c)]) return set_err(ctx, status[size_t(c)] - 1, "mutation failed", c);
+  }
+  if (bad >= 0) return set_err(ctx, FNB_E_DUPLICATE_KEY, "node key " + std::to_string(newk[size_t(bad)]), bad);
   return 0;
 }
 

@@ -23,6 +23,7 @@
 //              K5 crossover (elites are self-crossovers = exact copies), K6/K7
 //              mutation with one slot-ordered innovation table.
 #include <algorithm>
+#include <cmath>
 #include <climits>
 #include <cstdlib>
 #include <cstdio>
@@ -977,6 +978,10 @@ struct fnb_evolver {
   fnb_ctx* ctx = nullptr;
   fnb::Evolver ev;
   DevBuf nets, X, Y;
+  // evaluation status (written on the evolver stream, read by eval_check):
+  // [0] lowest genome whose transform failed (INT_MAX none), [1] non-finite X
+  DevBuf eflags;
+  int eval_lo = 0, eval_n = 0;
 };
 
 namespace fnb {
@@ -989,6 +994,18 @@ cudaError_t launch_transform(const double* n, const double* c, int P, uint8_t* n
 }  // namespace fnb
 
 namespace fnb {
+cudaError_t launch_first_error(const uint8_t* nets, size_t stride, int P, int* out, cudaStream_t st);
+
+__global__ void k_eval_flags_init(int* f) {
+  f[0] = INT_MAX;
+  f[1] = 0;
+}
+// network.hpp:245-246: every input must be finite
+__global__ void k_nonfinite_f32(const float* __restrict__ x, size_t n, int* bad) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    if (!isfinite(x[i])) atomicOr(bad, 1);
+}
+
 cudaError_t launch_validate(const double* nodes, const double* conns, int P, const DevShape& sh, int32_t* codes,
                             int32_t* details, cudaStream_t st);
 std::string validate_message(int code, int detail);
@@ -1054,7 +1071,9 @@ void fnb_evolver_destroy(fnb_evolver* ev) {
   ev->nets.release();
   ev->X.release();
   ev->Y.release();
+  ev->eflags.release();
   delete ev;
+  cudaGetLastError();  // leave no error behind for the context's next call
 }
 
 int fnb_evolver_init_population(fnb_evolver* ev) {
@@ -1099,22 +1118,68 @@ int fnb_evolver_get_fitness(fnb_evolver* ev, double* fitness) {
   return 0;
 }
 
-// transform + forward + fused fitness of the current population (device data)
-int fnb_evolver_evaluate_d(fnb_evolver* ev, const float* d_X, const float* d_Y, int batch, int fitness_kind,
-                           double fitness_offset) {
+// transform + forward + fused fitness of genomes [lo, lo+n) of the current
+// population into d_fit, plus the evaluation status words (eflags) that
+// fnb_evolver_eval_check reads: everything is enqueued on the evolver stream
+// with no host synchronisation (capture-safe).
+static int evolver_eval_enqueue(fnb_evolver* ev, int lo, int n, const float* d_X, const float* d_Y, int batch,
+                                int fitness_kind, double fitness_offset, double* d_fit) {
   fnb::Evolver& v = ev->ev;
   fnb_ctx* ctx = ev->ctx;
   cudaSetDevice(ctx->device);
-  EV_CK(ev->nets.ensure(ctx->L.bytes * size_t(v.P)));
-  EV_CK(fnb::launch_transform(v.pn[v.cur], v.pc[v.cur], v.P, static_cast<uint8_t*>(ev->nets.p), ctx->L, ctx->sh,
-                              v.st));
+  if (batch <= 0) return fnb_set_error(ctx, FNB_E_EMPTY_DATASET, "batch is empty", -1);
+  EV_CK(ev->nets.ensure(ctx->L.bytes * size_t(std::max(n, 1))));
+  EV_CK(ev->eflags.ensure(4 * sizeof(int)));
+  int* fl = static_cast<int*>(ev->eflags.p);
+  ev->eval_lo = lo;
+  ev->eval_n = n;
+  fnb::k_eval_flags_init<<<1, 1, 0, v.st>>>(fl);
+  const size_t nx = size_t(batch) * ctx->sh.I;
+  fnb::k_nonfinite_f32<<<int(std::min<size_t>((nx + 255) / 256, 148)), 256, 0, v.st>>>(d_X, nx, fl + 1);
+  ctx->launches += 2;
+  if (n == 0) return 0;
+  EV_CK(fnb::launch_transform(v.pn[v.cur] + size_t(lo) * v.gn(), v.pc[v.cur] + size_t(lo) * v.gc(), n,
+                              static_cast<uint8_t*>(ev->nets.p), ctx->L, ctx->sh, v.st));
   ctx->launches++;
-  EV_CK(ctx->partial.ensure(fnb::forward_partial_needed(ctx->L, v.P, batch)));
-  if (fnb::launch_forward(ev->nets.p, ctx->L, v.P, d_X, d_Y, batch, fitness_kind, fitness_offset, v.fitness, nullptr,
+  EV_CK(ctx->partial.ensure(fnb::forward_partial_needed(ctx->L, n, batch)));
+  // genomes that failed K1 are skipped by K2 (their fitness is not written)
+  if (fnb::launch_forward(ev->nets.p, ctx->L, n, d_X, d_Y, batch, fitness_kind, fitness_offset, d_fit, nullptr,
                           static_cast<double*>(ctx->partial.p), ctx->partial.cap,
                           ctx->sh.n_agg == 1 ? int(ctx->sh.agg[0]) : -1, ctx->sh.n_act == 1 ? int(ctx->sh.act[0]) : -1,
                           v.st, &ctx->launches))
     return fnb_cuda_error(ctx, cudaGetLastError(), "forward launch");
+  EV_CK(fnb::launch_first_error(static_cast<const uint8_t*>(ev->nets.p), ctx->L.bytes, n, fl, v.st));
+  ctx->launches++;
+  return 0;
+}
+
+int fnb_evolver_evaluate_d(fnb_evolver* ev, const float* d_X, const float* d_Y, int batch, int fitness_kind,
+                           double fitness_offset) {
+  return evolver_eval_enqueue(ev, 0, ev->ev.P, d_X, d_Y, batch, fitness_kind, fitness_offset, ev->ev.fitness);
+}
+
+// Synchronises the evolver stream and reports the last evaluation's errors in
+// the reference's order (forward_into, network.hpp:238-268 via transform,
+// network.hpp:122-220): the lowest genome whose transform failed, with the
+// reference's message, else a non-finite input.
+int fnb_evolver_eval_check(fnb_evolver* ev) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (!ev->eflags.p) return 0;
+  int fl[2] = {INT_MAX, 0};
+  EV_CK(cudaMemcpyAsync(fl, ev->eflags.p, sizeof(fl), cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  if (fl[0] != INT_MAX) {
+    const int lo = ev->eval_lo;
+    const int st = fnb_check_nets_d(ctx, v.pn[v.cur] + size_t(lo) * v.gn(), v.pc[v.cur] + size_t(lo) * v.gc(),
+                                    ev->nets.p, ev->eval_n, v.st);
+    if (st && ctx->err_index >= 0) ctx->err_index += lo;
+    if (st) return st;
+  }
+  if (fl[1]) return fnb_set_error(ctx, FNB_E_NON_FINITE_INPUT, "input not finite", 0);
   return 0;
 }
 
@@ -1125,8 +1190,12 @@ int fnb_evolver_evaluate(fnb_evolver* ev, const double* X, const double* Y, int 
   fnb_ctx* ctx = ev->ctx;
   cudaSetDevice(ctx->device);
   const size_t nx = size_t(batch) * ctx->sh.I, ny = size_t(batch) * ctx->sh.O;
+  if (batch <= 0) return fnb_set_error(ctx, FNB_E_EMPTY_DATASET, "batch is empty", -1);
   std::vector<float> xf(nx), yf(ny);
-  for (size_t i = 0; i < nx; ++i) xf[i] = float(X[i]);
+  for (size_t i = 0; i < nx; ++i) {
+    if (!std::isfinite(X[i])) return fnb_set_error(ctx, FNB_E_NON_FINITE_INPUT, "input not finite", 0);
+    xf[i] = float(X[i]);
+  }
   for (size_t i = 0; i < ny; ++i) yf[i] = float(Y[i]);
   EV_CK(ev->X.ensure(sizeof(float) * nx + 16));
   EV_CK(ev->Y.ensure(sizeof(float) * ny + 16));
@@ -1135,8 +1204,7 @@ int fnb_evolver_evaluate(fnb_evolver* ev, const double* X, const double* Y, int 
   int st = fnb_evolver_evaluate_d(ev, static_cast<float*>(ev->X.p), static_cast<float*>(ev->Y.p), batch,
                                   fitness_kind, fitness_offset);
   if (st) return st;
-  EV_CK(cudaStreamSynchronize(v.st));
-  return 0;
+  return fnb_evolver_eval_check(ev);
 }
 
 int fnb_evolver_step(fnb_evolver* ev) {
@@ -1230,23 +1298,8 @@ int fnb_evolver_state(fnb_evolver* ev, int* generation, int* next_key) {
 // shard of the population in the multi-GPU loop)
 int fnb_evolver_evaluate_range_d(fnb_evolver* ev, int lo, int hi, const float* d_X, const float* d_Y, int batch,
                                  int fitness_kind, double fitness_offset, double* d_fitness_out) {
-  fnb::Evolver& v = ev->ev;
-  fnb_ctx* ctx = ev->ctx;
-  if (lo < 0 || hi > v.P || lo > hi) return fnb_set_error(ctx, FNB_E_SHAPE_MISMATCH, "bad genome range", -1);
-  const int n = hi - lo;
-  if (n == 0) return 0;
-  cudaSetDevice(ctx->device);
-  EV_CK(ev->nets.ensure(ctx->L.bytes * size_t(n)));
-  EV_CK(fnb::launch_transform(v.pn[v.cur] + size_t(lo) * v.gn(), v.pc[v.cur] + size_t(lo) * v.gc(), n,
-                              static_cast<uint8_t*>(ev->nets.p), ctx->L, ctx->sh, v.st));
-  ctx->launches++;
-  EV_CK(ctx->partial.ensure(fnb::forward_partial_needed(ctx->L, n, batch)));
-  if (fnb::launch_forward(ev->nets.p, ctx->L, n, d_X, d_Y, batch, fitness_kind, fitness_offset, d_fitness_out,
-                          nullptr, static_cast<double*>(ctx->partial.p), ctx->partial.cap,
-                          ctx->sh.n_agg == 1 ? int(ctx->sh.agg[0]) : -1, ctx->sh.n_act == 1 ? int(ctx->sh.act[0]) : -1,
-                          v.st, &ctx->launches))
-    return fnb_cuda_error(ctx, cudaGetLastError(), "forward launch");
-  return 0;
+  if (lo < 0 || hi > ev->ev.P || lo > hi) return fnb_set_error(ev->ctx, FNB_E_SHAPE_MISMATCH, "bad genome range", -1);
+  return evolver_eval_enqueue(ev, lo, hi - lo, d_X, d_Y, batch, fitness_kind, fitness_offset, d_fitness_out);
 }
 
 // population checksum: sum over 64-bit words w_i * (2i + 1) mod 2^64 (order

@@ -952,6 +952,15 @@ static bool mut_scratch(void* scratch, size_t scratch_bytes, int n, int* d_new_k
   return size_t(p - static_cast<uint8_t*>(scratch)) <= scratch_bytes;
 }
 
+// the plan arrays inside the scratch (host-layer replay of a caller's InnovationTable)
+void mutate_scratch_views(void* scratch, int n, unsigned long long** pair, int** flag, int** newk) {
+  MutScratch ms;
+  mut_scratch(scratch, size_t(-1), n, nullptr, &ms);
+  *pair = ms.pair;
+  *flag = ms.flag;
+  *newk = ms.newk;
+}
+
 // Phase 1 of mutate for n slots: the node-split plan (stream split(0)) and the
 // K7 innovation keys, in slot order over ALL n slots.  `src` (may be null)
 // maps slot c to the genome its structure is read from (the fit parent).

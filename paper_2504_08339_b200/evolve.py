@@ -68,11 +68,13 @@ class Evolver:
         if st:
             raise FlatneatError(st, self._lib.fnb_last_error(engine._h).decode())
         self._h = h
+        engine._dependents.add(self)
 
     def close(self):
-        if getattr(self, "_h", None):
+        # an evolver lives on its engine's context: never destroy it after the context
+        if getattr(self, "_h", None) and getattr(self.engine, "_h", None):
             self._lib.fnb_evolver_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -129,6 +131,12 @@ class Evolver:
 
     def evaluate_d(self, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0):
         self._raise(self._lib.fnb_evolver_evaluate_d(self._h, X.data_ptr(), Y.data_ptr(), X.shape[0], kind, offset))
+
+    def eval_check(self):
+        """Synchronise and raise the last (device-input) evaluation's error:
+        the lowest failing genome's transform error, else non_finite_input
+        (fnb_evolver_eval_check)."""
+        self._raise(self._lib.fnb_evolver_eval_check(self._h))
 
     def evaluate_range_d(self, lo: int, hi: int, X, Y, out, kind: int = FIT_NEG_MSE, offset: float = 0.0):
         """Fitness of genomes [lo, hi) into the device FP64 tensor `out` (hi-lo),

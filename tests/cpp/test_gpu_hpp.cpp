@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "flatneat/genome.hpp"
@@ -81,6 +82,101 @@ int main() {
     if (!(mp.slice(i) == m)) ++fails;
   }
   if (tref.next_key() != tgpu.next_key()) ++fails;
+
+  // a pre-seeded table, and reference / GPU mutate calls mixed within one
+  // generation: the memo must carry across them (ops.hpp:145-175)
+  {
+    InnovationTable ra(2000), ga(2000);
+    for (int i = 0; i < pop.pop_size; i += 3) {  // seed the splits some slots will plan
+      const NodeSplitPlan pl = plan_node_split(gs[std::size_t(i)], keys[std::size_t(i)], mc);
+      if (pl.split) { ra.get_or_assign(pl.in_key, pl.out_key); ga.get_or_assign(pl.in_key, pl.out_key); }
+    }
+    const int half = pop.pop_size / 2;
+    std::vector<GenomeTensors> want_m;
+    for (int i = 0; i < pop.pop_size; ++i) want_m.push_back(mutate(gs[std::size_t(i)], keys[std::size_t(i)], mc, s, ra));
+    // slots [0, half) on the reference, [half, P) on the GPU, one table
+    std::vector<GenomeTensors> first;
+    for (int i = 0; i < half; ++i) first.push_back(mutate(gs[std::size_t(i)], keys[std::size_t(i)], mc, s, ga));
+    std::vector<GenomeTensors> second(gs.begin() + half, gs.end());
+    PopulationTensors sp = concat_population(second);
+    ctx.mutate(sp, std::span<const RngKey>(keys).subspan(std::size_t(half)), mc, ga);
+    for (int i = 0; i < half; ++i)
+      if (!(first[std::size_t(i)] == want_m[std::size_t(i)])) ++fails;
+    for (int i = half; i < pop.pop_size; ++i)
+      if (!(sp.slice(i - half) == want_m[std::size_t(i)])) { std::printf("mixed slot %d differs\n", i); ++fails; }
+    // the memo: every pair the reference table knows maps to the same key
+    for (int i = 0; i < pop.pop_size; ++i) {
+      const NodeSplitPlan pl = plan_node_split(gs[std::size_t(i)], keys[std::size_t(i)], mc);
+      if (pl.split && ra.get_or_assign(pl.in_key, pl.out_key) != ga.get_or_assign(pl.in_key, pl.out_key)) ++fails;
+    }
+    if (ra.next_key() != ga.next_key()) ++fails;
+  }
+
+  // duplicate_key: a table whose counter runs into existing node keys throws
+  // at the first colliding slot; earlier genomes are mutated, later ones not
+  {
+    MutationConfig m2;
+    m2.node_add = 1.0;
+    InnovationTable ra(0), ga(0);
+    int ref_bad = -1;
+    std::string ref_what;
+    std::vector<GenomeTensors> want_m;
+    for (int i = 0; i < pop.pop_size; ++i) {
+      try {
+        want_m.push_back(mutate(gs[std::size_t(i)], keys[std::size_t(i)], m2, s, ra));
+      } catch (const Error& e) {
+        ref_bad = i;
+        ref_what = e.what();
+        break;
+      }
+    }
+    PopulationTensors dp = pop;
+    int gpu_bad = -1;
+    std::string gpu_what;
+    try {
+      ctx.mutate(dp, keys, m2, ga);
+    } catch (const Error& e) {
+      gpu_bad = fnb_last_error_index(ctx.handle());
+      gpu_what = e.what();
+    }
+    if (ref_bad < 0 || gpu_bad != ref_bad || gpu_what != ref_what || ra.next_key() != ga.next_key()) {
+      std::printf("duplicate_key: ref slot %d '%s' next %d, gpu slot %d '%s' next %d\n", ref_bad, ref_what.c_str(),
+                  ra.next_key(), gpu_bad, gpu_what.c_str(), ga.next_key());
+      ++fails;
+    }
+    for (int i = 0; i < pop.pop_size; ++i) {
+      const bool ok = i < ref_bad ? dp.slice(i) == want_m[std::size_t(i)] : dp.slice(i) == gs[std::size_t(i)];
+      if (!ok) { std::printf("duplicate_key: genome %d\n", i); ++fails; break; }
+    }
+  }
+
+  // span sizes and the empty dataset
+  {
+    bool threw = false;
+    try {
+      PopulationTensors q = pop;
+      ctx.mutate(q, std::span<const RngKey>(keys).first(3), mc, tgpu);
+    } catch (const Error& e) {
+      threw = e.code() == Errc::shape_mismatch;
+    }
+    if (!threw) { std::printf("short key span accepted\n"); ++fails; }
+    threw = false;
+    try {
+      PopulationTensors q = opop;
+      q.pop_size = pop.pop_size + 1;
+      (void)ctx.crossover(pop, q, keys);
+    } catch (const Error& e) {
+      threw = e.code() == Errc::shape_mismatch;
+    }
+    if (!threw) { std::printf("short other population accepted\n"); ++fails; }
+    threw = false;
+    try {
+      (void)ctx.evaluate(pop, std::span<const double>(), std::span<const double>(), 0);
+    } catch (const Error& e) {
+      threw = e.code() == Errc::empty_dataset;
+    }
+    if (!threw) { std::printf("empty dataset accepted\n"); ++fails; }
+  }
 
   std::printf(fails ? "gpu.hpp parity FAILED (%d)\n" : "gpu.hpp parity ok\n", fails);
   return fails ? 1 : 0;
