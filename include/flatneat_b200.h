@@ -201,7 +201,8 @@ int fnb_mutate_d(fnb_ctx* ctx, double* d_nodes, double* d_conns, int P, const ui
                  const uint8_t* d_active, const fnb_mutation_config* cfg, int* d_next_key, int* d_status,
                  int* d_new_key, void* stream);
 /* Sequential RngStream draws per key (parity tooling): kind 0 next_u64,
- * 1 uniform() bits, 2 below(n).  d_out[n_keys][n_draws]. */
+ * 1 uniform() bits, 2 below(n), 3 normal(0, 1) bits (rng.hpp:111-116, glibc
+ * log / cos restated on the device).  d_out[n_keys][n_draws]. */
 int fnb_stream_draws_d(fnb_ctx* ctx, const uint32_t* d_keys, int n_keys, int n_draws, int kind,
                        uint64_t n, uint64_t* d_out, void* stream);
 /* d_out[i] = key.split(base + i), i < n (RngKey tree on the device). */

@@ -22,8 +22,9 @@
  *     +1; counter > max_stagnation removes the species unless it is among
  *     the species_elitism best (max fitness desc, ties lower id); at least
  *     one species always survives.
- *  E4 spawn: rank r_i of (fitness asc, index asc) normalised r/(P-1);
- *     species mean = exact integer rank sum / ((P-1) n_j); target = P * af/sum(af); clamp to
+ *  E4 spawn: mid-rank r_i of fitness (ties share their mean position)
+ *     normalised r/(P-1); species mean = exact integer sum of 2 r_i /
+ *     (2 (P-1) n_j); target = P * af/sum(af); clamp to
  *     old +- round(rate*old); rescale to P; largest remainder (ties lower
  *     id); raise to genome_elitism, taking surplus from the largest
  *     allocation (ties highest id).
@@ -271,14 +272,23 @@ void fo_compute_spawn(const fo_neat_cfg* cfg, const double* fitness,
                       const int* species_of, fo_species* s) {
   const int P = cfg->pop_size;
   const int S = s->count;
-  /* rank r_i of (fitness asc, index asc); the species mean of r_i/(P-1) is
-   * formed from the EXACT integer rank sum, so the value does not depend on
-   * summation order: af_j = double(sum r_i) / (double(P-1) * double(n_j)). */
+  /* mid-rank of fitness (ties share the mean of their positions, SPEC.md:
+   * 374-382 "population ranks mapped to [0,1]"; the symmetric tie rule keeps
+   * the SPEC example "identical fitness distributions -> equal split"):
+   * 2 r_i = lo + hi - 1 for the tie group [lo, hi) of the ascending order.
+   * The species mean of r_i/(P-1) is formed from the EXACT integer sum of
+   * 2 r_i, so it does not depend on summation order:
+   * af_j = double(sum 2 r_i) / ((2 (P-1)) * n_j). */
   fi_t* ord = (fi_t*)malloc(sizeof(fi_t) * (size_t)P);
   long long* rk = (long long*)malloc(sizeof(long long) * (size_t)P);
   for (int i = 0; i < P; ++i) { ord[i].f = fitness[i]; ord[i].i = i; }
   qsort(ord, (size_t)P, sizeof(fi_t), fi_asc);
-  for (int r = 0; r < P; ++r) rk[ord[r].i] = r;
+  for (int lo = 0; lo < P;) {
+    int hi = lo + 1;
+    while (hi < P && ord[hi].f == ord[lo].f) ++hi;
+    for (int r = lo; r < hi; ++r) rk[ord[r].i] = (long long)lo + (long long)hi - 1;
+    lo = hi;
+  }
   long long* rsum = (long long*)calloc((size_t)S, sizeof(long long));
   double* af = (double*)calloc((size_t)S, sizeof(double));
   int* cnt = (int*)calloc((size_t)S, sizeof(int));
@@ -290,7 +300,7 @@ void fo_compute_spawn(const fo_neat_cfg* cfg, const double* fitness,
   }
   double total = 0.0;
   for (int j = 0; j < S; ++j) {
-    af[j] = (double)rsum[j] / ((double)(P - 1) * (double)cnt[j]);
+    af[j] = (double)rsum[j] / ((2.0 * (double)(P - 1)) * (double)cnt[j]);
     total += af[j];
   }
   double* nw = (double*)malloc(sizeof(double) * (size_t)S);

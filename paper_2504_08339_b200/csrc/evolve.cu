@@ -15,8 +15,8 @@
 //              atomicMin on (distance bits, index)); empty species dropped.
 //   stagnate   per-species max fitness (atomicMax on order-preserving bits),
 //              counter update, species_elitism protection, compaction.
-//   spawn      fitness ranks by a stable radix sort (CUB), exact integer
-//              rank sums per species, then the clamp / rescale / largest-
+//   spawn      fitness mid-ranks from a stable radix sort (CUB), exact
+//              integer sums of 2*rank per species, then the clamp / rescale / largest-
 //              remainder / elitism arithmetic on one thread.
 //   reproduce  members ordered (fitness desc, index asc) from the ranking
 //              sort (equal-key groups reversed) and a 6-bit species sort, per-slot parent selection from the split(0) stream,
@@ -392,7 +392,10 @@ __global__ void k_fit_keys(const double* fitness, int P, unsigned long long* asc
   desc[i] = ~o;
   idx[i] = i;
 }
-__global__ void k_rank_sums(const int* sorted_idx, int P, const int* species_of, SpeciesDev* sd) {
+// mid-ranks (oracle E4): position r of the ascending sort lies in the tie
+// group [lo, hi) of its key; 2 * rank = lo + hi - 1, an exact integer
+__global__ void k_rank_sums(const unsigned long long* __restrict__ sorted_keys, const int* sorted_idx, int P,
+                            const int* species_of, SpeciesDev* sd) {
   __shared__ unsigned long long s_sum[kMaxSpecies];
   __shared__ int s_cnt[kMaxSpecies];
   for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x) {
@@ -404,7 +407,22 @@ __global__ void k_rank_sums(const int* sorted_idx, int P, const int* species_of,
   if (r < P) {
     const int j = species_of[sorted_idx[r]];
     if (j >= 0) {
-      atomicAdd(&s_sum[j], (unsigned long long)r);
+      const unsigned long long k = sorted_keys[r];
+      int a = 0, b = r;  // lo = first position with key >= k
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (sorted_keys[m] < k) a = m + 1;
+        else b = m;
+      }
+      const int lo = a;
+      a = r + 1;
+      b = P;  // hi = first position with key > k
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (sorted_keys[m] <= k) a = m + 1;
+        else b = m;
+      }
+      atomicAdd(&s_sum[j], (unsigned long long)(lo + a - 1));
       atomicAdd(&s_cnt[j], 1);
     }
   }
@@ -423,7 +441,7 @@ __global__ void k_spawn(SpeciesDev* sd, int P, double rate, int genome_elitism) 
   double af[kMaxSpecies], nw[kMaxSpecies], frac[kMaxSpecies];
   double total = 0.0;
   for (int j = 0; j < S; ++j) {
-    af[j] = __ddiv_rn(double(sd->rsum[j]), __dmul_rn(double(P - 1), double(sd->cnt[j])));
+    af[j] = __ddiv_rn(double(sd->rsum[j]), __dmul_rn(__dmul_rn(2.0, double(P - 1)), double(sd->cnt[j])));
     total = __dadd_rn(total, af[j]);
   }
   double sum_new = 0.0;
@@ -885,7 +903,7 @@ struct Evolver {
             : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
     if (e != cudaSuccess) return e;
     k_spawn_begin<<<1, 1, 0, st>>>(sd);
-    k_rank_sums<<<B, T, 0, st>>>(idx_sorted, P, species_of, sd);
+    k_rank_sums<<<B, T, 0, st>>>(ktmp, idx_sorted, P, species_of, sd);
     k_spawn<<<1, 1, 0, st>>>(sd, P, cfg.spawn_rate, cfg.genome_elitism);
     // ---- reproduce: members by (fitness desc, index asc), then by species
     k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp);

@@ -3,10 +3,12 @@
 // batched key derivation (the RngKey tree, rng.hpp:58-66).
 #include "fnb_common.cuh"
 #include "philox.cuh"
+#include "glibc_math.cuh"
 
 namespace fnb {
 
-// kind 0: next_u64, 1: uniform (as bits), 2: below(n)
+// kind 0: next_u64, 1: uniform (as bits), 2: below(n), 3: normal(0, 1) (as
+// bits; rng.hpp:111-116 with the glibc-exact log / cos of glibc_math.cuh)
 __global__ void k_stream_draws(const uint32_t* __restrict__ keys, int n_keys, int n_draws, int kind, uint64_t n,
                                uint64_t* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -16,7 +18,12 @@ __global__ void k_stream_draws(const uint32_t* __restrict__ keys, int n_keys, in
     uint64_t v;
     if (kind == 0) v = s.next_u64();
     else if (kind == 1) v = uint64_t(__double_as_longlong(s.uniform()));
-    else v = s.below(n);
+    else if (kind == 2) v = s.below(n);
+    else {
+      const double a0 = s.uniform();
+      const double a1 = s.uniform();
+      v = uint64_t(__double_as_longlong(glibc::normal_from_uniforms(a0, a1, 0.0, 1.0)));
+    }
     out[size_t(i) * n_draws + d] = v;
   }
 }

@@ -462,7 +462,18 @@ class OracleEvolution:
                               ptr(nn, F64P), ptr(nc, F64P), ptr(pa, I32P), ptr(pb, I32P))
         assert st == 0, st
         self.nodes, self.conns = nn, nc
+        self.last_parents = (pa, pb)
         self.generation += 1
+
+    def set_population(self, nodes, conns):
+        """Load a population; the innovation counter moves above its largest
+        key (InnovationTable::reserve_up_to), as fnb_evolver_set_population
+        + fnb_evolver_set_next_key do."""
+        self.nodes = np.array(nodes, dtype=np.float64, copy=True, order="C")
+        self.conns = np.array(conns, dtype=np.float64, copy=True, order="C")
+        keys = self.nodes[:, :, 0]
+        if np.any(~np.isnan(keys)):
+            self.innov.next_key = max(self.innov.next_key, int(np.nanmax(keys)) + 1)
 
     def species_view(self):
         s = self.species

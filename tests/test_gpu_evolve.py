@@ -165,3 +165,48 @@ def test_split_step_equals_step(fnb, parts):
     # the next-population views alias the library's buffer
     n_view, c_view = b.next_population_d()
     assert tuple(n_view.shape) == (301, 24, 5) and tuple(c_view.shape) == (301, 80, 4)
+
+
+@pytest.mark.parametrize("name,P,limits,inputs,th,G", [
+    # P > 16,384: both stable sorts of the step take the CUB radix path (evolve.cu kCountRankMax)
+    ("cub-sorts-P20000", 20000, (16, 32), 3, 0.6, 6),
+    # BASELINE config 2 genome shape (N_max=64, C_max=256, 4 inputs)
+    ("c2-shape-P2000", 2000, (64, 256), 4, 1.0, 10),
+])
+def test_generation_loop_bit_exact_large(fnb, name, P, limits, inputs, th, G):
+    """The device loop against oracle/evolution.c at the populations and
+    genome shapes the benchmarks run: whole population bit for bit (NaN
+    padding included), species table and innovation counter, every generation."""
+    from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+    from paper_2504_08339_b200.synthetic import regression_dataset
+    acts, aggs = ["tanh", "sigmoid", "identity"], ["sum", "product"]
+    ik = list(range(inputs))
+    prob = ol.Problem(limits[0], limits[1], ik, [inputs])
+    schema = ol.SchemaSpec(acts, aggs)
+    eng = fnb.Engine(fnb.GenomeLimits(*limits), ik, [inputs], fnb.AttributeSchema(acts, aggs))
+    mkw = dict(node_add=0.5, conn_add=0.6, node_delete=0.05, conn_delete=0.05)
+    cfg = NeatConfig(pop_size=P, max_species=10, compatibility_threshold=th, mutation=_mut(fnb, mkw),
+                     output_activation=1)
+    ev = Evolver(eng, cfg, seed=77)
+    orc = ol.OracleEvolution(prob, schema, ol.neat_cfg(P, max_species=10, threshold=th, output_activation=1,
+                                                       mutation=ol.mut_cfg(**mkw)), seed=77)
+    ev.init_population()
+    orc.init_population()
+    X, Y = regression_dataset(128, inputs, 1, seed=6)
+    counts = set()
+    for g in range(G):
+        ev.evaluate(X, Y)
+        fit = ev.fitness()
+        orc.step(fit)
+        ev.step()
+        gn, gc = ev.population()
+        assert np.array_equal(gn.view(np.uint64), orc.nodes.view(np.uint64)), f"{name} gen {g} nodes"
+        assert np.array_equal(gc.view(np.uint64), orc.conns.view(np.uint64)), f"{name} gen {g} conns"
+        sp, so = ev.species(), orc.species_view()
+        assert sp["count"] == so["count"] and np.array_equal(sp["ids"], so["ids"]), (name, g)
+        np.testing.assert_array_equal(sp["spawn"], so["spawn"])
+        np.testing.assert_array_equal(sp["best"], so["best"])
+        np.testing.assert_array_equal(sp["stagnation"], so["stagnation"])
+        assert ev.state()[1] == orc.innov.next_key, (name, g)
+        counts.add(int(sp["count"]))
+    assert max(counts) > 1, f"{name}: the run never left one species"

@@ -6,6 +6,8 @@ other by tests/test_oracle_vs_ref.py.  Bars (north star): topological order,
 error codes and messages bit-exact; outputs within rtol 1e-5 + atol 1e-5 of
 the FP64 reference; fitness within rtol 1e-5.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -231,3 +233,80 @@ def test_pipelined_host_path_chunks(fnb):
     assert ei.value.index == 2900 and ei.value.code == "dangling_endpoint"
     # the context recovers: the next call is clean and identical
     assert np.array_equal(eng.evaluate(nodes, conns, X, Y, fnb.FIT_NEG_MSE), fit)
+
+
+# ---- BASELINE config 5 shapes (N_max=128, C_max=1024): K1 runs k_transform<4>,
+# K2 the N=128 tile geometry --------------------------------
+
+@pytest.mark.parametrize("schema_name", ["tanh", "rich"])
+def test_transform_and_forward_c5_shape(fnb, schema_name):
+    """C5 shape (pop 100k config: N128/C1024, fill 0.75) on a 96-genome slice:
+    K1 order (k_transform<4>) bit-exact, K2 outputs within 1e-5, fitness."""
+    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
+    rich = schema_name == "rich"
+    # {sum, max, mean}: a product over ~8 FP64 terms of N(0,1) weights stays far from FP32 overflow,
+    # but not over the C5 fan-ins, where FP32 and FP64 saturate differently
+    schema = ol.SchemaSpec(["tanh", "sigmoid", "identity", "relu", "sin"], ["sum", "max", "mean"]) if rich \
+        else ol.SchemaSpec()
+    nodes, conns = synthetic_population(96, 128, 1024, fill=0.75, n_act=5 if rich else 1, n_agg=3 if rich else 1,
+                                        seed=55 if rich else 56)
+    prob = ol.Problem(128, 1024, [0, 1, 2, 3], [4])
+    eng = _engine(fnb, prob, schema)
+    order, cnt = eng.transform(nodes, conns)
+    for i in range(nodes.shape[0]):
+        r = _ref_transform(prob, schema, nodes[i], conns[i])
+        assert r["status"] == 0
+        assert cnt[i] == r["order_count"]
+        np.testing.assert_array_equal(order[i], r["order"])
+    X, Y = regression_dataset(96, seed=5)
+    want = _ref_forward(prob, schema, nodes, conns, X)
+    got = eng.batch_forward(nodes, conns, X).values
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    fit = eng.evaluate(nodes, conns, X, Y, fnb.FIT_NEG_MSE)
+    np.testing.assert_allclose(fit, -np.mean((Y[None] - want) ** 2, axis=(1, 2)), rtol=RTOL)
+
+
+@pytest.mark.parametrize("kind", ["cycle", "selfloop", "dangling", "bad_act", "dup_pair"])
+def test_transform_errors_c5_shape(fnb, kind):
+    """k_transform<4> error paths, messages (the cycle path string) and the
+    lowest failing genome at N128/C1024."""
+    from test_oracle_vs_ref import _corrupt
+    from paper_2504_08339_b200.synthetic import synthetic_population
+    schema = ol.RICH
+    prob = ol.Problem(128, 1024, [0, 1, 2, 3], [4])
+    nodes, conns = synthetic_population(12, 128, 1024, fill=0.75, n_act=5, n_agg=4, seed=9)
+    rng = np.random.default_rng(13)
+    eng = _engine(fnb, prob, schema)
+    for i in range(0, 12, 3):
+        n, c = _corrupt(nodes[i], conns[i], rng, kind)
+        r = _ref_transform(prob, schema, n, c)
+        pn = np.stack([nodes[i + 1], nodes[i + 2], n, nodes[i]])
+        pc = np.stack([conns[i + 1], conns[i + 2], c, conns[i]])
+        if r["status"] == 0:
+            eng.transform(pn, pc)
+            continue
+        with pytest.raises(fnb.FlatneatError) as ei:
+            eng.transform(pn, pc)
+        assert ei.value.status == r["status"] and ei.value.index == 2
+        assert str(ei.value) == r["msg"], (kind, str(ei.value), r["msg"])
+
+
+def test_c3_cppn_fitness_full_grid(fnb):
+    """BASELINE config 3 at its real batch: 32 C2 networks queried at the full
+    256 x 256 grid (B = 65,536 samples each), outputs and image-MSE fitness
+    against the reference's batch_forward."""
+    from paper_2504_08339_b200.synthetic import cppn_dataset, synthetic_population
+    if not ol.ref_available():
+        pytest.skip("needs oracle/_ref")
+    nodes, conns = synthetic_population(32, 64, 256, fill=0.75, seed=33)
+    X, Y = cppn_dataset(256)
+    assert X.shape[0] == 65536
+    schema = ol.SchemaSpec()
+    prob = ol.Problem(64, 256, [0, 1, 2, 3], [4])
+    st, bad, msg, want = ol.ref_batch_forward(prob, schema, nodes, conns, X, nthreads=os.cpu_count() or 4)
+    assert st == 0, msg
+    eng = _engine(fnb, prob, schema)
+    got = eng.batch_forward(nodes, conns, X).values
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    fit = eng.evaluate(nodes, conns, X, Y, fnb.FIT_NEG_MSE)
+    np.testing.assert_allclose(fit, -np.mean((Y[None] - want) ** 2, axis=(1, 2)), rtol=RTOL)

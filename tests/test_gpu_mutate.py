@@ -103,3 +103,30 @@ def test_mutation_known_answers(fnb):
     rows = {(int(r[0]), int(r[1])): (r[2], r[3]) for r in gc[0] if not np.isnan(r[0])}
     assert rows == {(0, 1): (0.0, 0.7), (0, 2): (1.0, 1.0), (2, 1): (1.0, 0.7)}
     assert gn[0, 2, 0] == 2 and gn[0, 2, 1] == 0.0 and gn[0, 2, 2] == 1.0
+
+
+@pytest.mark.parametrize("cfgkw", CONFIGS)
+def test_mutate_c5_shape_bit_exact(fnb, cfgkw):
+    """K6 + K7 at BASELINE config 5 shapes (N128/C1024, fill 0.75; K6 runs
+    1-2-warp CTAs there): 3 slot-order steps x 4 mutation configs against
+    the reference's mutate with one InnovationTable, every normal included."""
+    from paper_2504_08339_b200.synthetic import synthetic_population
+    schema = ol.SchemaSpec(["tanh", "sigmoid", "identity"], ["sum", "product"])
+    prob = ol.Problem(128, 1024, [0, 1, 2, 3], [4])
+    nodes, conns = synthetic_population(64, 128, 1024, fill=0.75, n_act=3, n_agg=2, seed=71)
+    eng = _engine(fnb, prob, schema)
+    cfg_o = ol.mut_cfg(**cfgkw)
+    cfg_g = _cfg(fnb, cfgkw)
+    root = ol.key_seed(72)
+    next_key = 1000
+    use_ref = ol.ref_available()
+    for step in range(3):
+        keys = np.stack([ol.key_words(ol.key_split(ol.key_split(root, step), p)) for p in range(64)])
+        st, bad, nk_ref, wn, wc = ol.mutate_population(prob, schema, nodes, conns, keys, cfg_o, next_key,
+                                                       use_ref=use_ref)
+        assert st == 0
+        gn, gc, nk = eng.mutate(nodes, conns, keys, cfg_g, next_key)
+        assert nk == nk_ref
+        np.testing.assert_array_equal(gn, wn)
+        np.testing.assert_array_equal(gc, wc)
+        nodes, conns, next_key = gn, gc, nk

@@ -2,6 +2,8 @@
 
 All three are bit-exact against the reference (oracle/_ref when present,
 else the pinned C restatement)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -53,6 +55,51 @@ def test_device_streams_match_reference(fnb):
         assert [ol.oracle().fo_below(ol.C.byref(s), 3 * 2**61) for _ in range(33)] == [int(x) for x in b[i]]
         s = ol.stream(ol.key_from_words(keys[i]))
         assert [ol.oracle().fo_uniform(ol.C.byref(s)) for _ in range(33)] == list(f[i])
+
+
+def _ref_normals(keys, n_draws):
+    """RngStream::normal(0, 1) (rng.hpp:111-116) of the REFERENCE with this
+    host's glibc, n_draws per key, threaded over keys (ctypes drops the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    lib = ol.ref() if ol.ref_available() else None
+    out = np.empty((keys.shape[0], n_draws))
+
+    def one(i):
+        k = np.ascontiguousarray(keys[i], dtype=np.uint32)
+        row = out[i]
+        if lib is not None:
+            lib.fr_stream_draws(k.ctypes.data_as(ol.C.POINTER(ol.C.c_uint32)), 2, n_draws, ol.C.c_double(0.0),
+                                ol.C.c_double(1.0), None, row.ctypes.data_as(ol.C.POINTER(ol.C.c_double)))
+        else:
+            s = ol.stream(ol.key_from_words(keys[i]))
+            for d in range(n_draws):
+                row[d] = ol.oracle().fo_normal(ol.C.byref(s), 0.0, 1.0)
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        list(ex.map(one, range(keys.shape[0])))
+    return out
+
+
+def test_device_normals_match_reference_1e8(fnb):
+    """H1 on the device: 1.0e8 RngStream::normal draws (4 chunks of 1024 keys
+    x 24,415 draws) are bit-identical to the reference's host normals, whose
+    log / cos come from this box's glibc."""
+    import torch
+    if not ol.ref_available():
+        pytest.skip("needs oracle/_ref (the reference's own RngStream::normal)")
+    prob = ol.Problem(8, 8, [0], [1])
+    eng = _engine(fnb, prob, ol.SchemaSpec())
+    n_draws, total = 24415, 0
+    for chunk in range(4):
+        root = ol.key_split(ol.key_seed(2025), chunk)
+        keys = np.stack([ol.key_words(ol.key_split(root, i)) for i in range(1024)])
+        dk = torch.from_numpy(keys.view(np.int32)).cuda()
+        got = eng.stream_draws_d(dk, n_draws, kind=3).cpu().numpy().view(np.float64)
+        want = _ref_normals(keys, n_draws)
+        bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+        assert bad.size == 0, f"chunk {chunk}: {bad.size} mismatches, first at {bad[:4]}"
+        total += got.size
+    assert total >= 10**8
 
 
 @pytest.mark.parametrize("seed,limits", [(31, (20, 80)), (2024, (64, 256))])
@@ -212,3 +259,27 @@ def test_distance_image_formats(fnb, variant):
         for s in range(S):
             want = ol.distance(prob, gn[p], gc[p], reps_n[s], reps_c[s], use_ref=use_ref)
             assert got[p, s] == want, (variant, p, s, got[p, s], want)
+
+
+def test_crossover_c5_shape_bit_exact(fnb):
+    """K5 at BASELINE config 5 shapes (N128/C1024, fill 0.75): 96 children of
+    related parents (the reference's mutate of each parent) against the
+    reference's crossover, bit for bit."""
+    from paper_2504_08339_b200.synthetic import synthetic_population
+    schema = ol.SchemaSpec()
+    prob = ol.Problem(128, 1024, [0, 1, 2, 3], [4])
+    nodes, conns = synthetic_population(96, 128, 1024, fill=0.75, seed=61)
+    keys = np.stack([ol.key_words(ol.key_split(ol.key_seed(62), i)) for i in range(96)])
+    use_ref = ol.ref_available()
+    st, _, _, mn, mc = ol.mutate_population(prob, schema, nodes, conns, keys,
+                                            ol.mut_cfg(node_add=0.5, conn_add=0.5, node_delete=0.1), 500,
+                                            use_ref=use_ref)
+    assert st == 0
+    ck = np.stack([ol.key_words(ol.key_split(ol.key_seed(63), t)) for t in range(96)])
+    # both argument orders: the child takes the FIT parent's structure
+    for a_n, a_c, b_n, b_c in ((nodes, conns, mn, mc), (mn, mc, nodes, conns)):
+        cn, cc = _engine(fnb, prob, schema).crossover(a_n, a_c, b_n, b_c, ck)
+        for t in range(96):
+            wn, wc = ol.crossover(prob, a_n[t], a_c[t], b_n[t], b_c[t], ol.key_from_words(ck[t]), use_ref=use_ref)
+            np.testing.assert_array_equal(cn[t], wn)
+            np.testing.assert_array_equal(cc[t], wc)
