@@ -319,6 +319,55 @@ int fnb_evolver_species(fnb_evolver* ev, int* count, int* ids, int* sizes, int* 
 int fnb_evolver_state(fnb_evolver* ev, int* generation, int* next_key);
 /* InnovationTable::reserve_up_to for a population loaded with set_population */
 int fnb_evolver_set_next_key(fnb_evolver* ev, int next_key);
+/* ---- checkpoint / resume ---------------------------------------------------
+ * Everything a generation step reads besides the population (SPEC.md:337-340
+ * SpeciesState; the key tree root of oracle E1): after set_population with
+ * the saved population and set_state with the saved record and
+ * representatives, the run continues bit for bit. */
+typedef struct fnb_run_state {
+  uint64_t seed;                /* RngKey(seed) root of the key tree          */
+  int generation;               /* generations stepped so far                 */
+  int next_key;                 /* InnovationTable counter (ops.hpp:145-167)  */
+  int species_count;
+  int next_species_id;
+  int species_id[32];           /* ascending                                   */
+  double species_best[32];      /* best-ever fitness                           */
+  int species_stagnation[32];
+  int species_size[32];         /* members at the last speciation              */
+  int species_spawn[32];
+} fnb_run_state;
+/* rep_nodes [species_count][max_nodes][5], rep_conns [species_count][max_conns][4]
+ * (either may be NULL on get) */
+int fnb_evolver_get_state(fnb_evolver* ev, fnb_run_state* state, double* rep_nodes, double* rep_conns);
+int fnb_evolver_set_state(fnb_evolver* ev, const fnb_run_state* state, const double* rep_nodes,
+                          const double* rep_conns);
+
+/* ---- SPEC evolve(problem, cfg, key) ------------------------
+ * RunStats: one record per completed generation. */
+typedef struct fnb_run_stats {
+  int generation;               /* the evolver's generation counter at evaluation */
+  double best, mean, std;       /* fitness over the population (population std) */
+  int best_index;               /* argmax, lowest index on ties                */
+  int species_count;            /* after this generation's speciation          */
+  int species_size[32];
+  double elapsed_ms;            /* wall clock of the generation                */
+} fnb_run_stats;
+/* called after every generation; a nonzero return stops the run */
+typedef int (*fnb_run_stats_fn)(void* user, const fnb_run_stats* stats);
+/* Loops evaluate -> (stop if best >= fitness_target) -> step for at most
+ * generation_limit generations on the func-fit / xor problem given by
+ * inputs[batch][I], targets[batch][O] and fitness_kind; each generation runs
+ * as one CUDA graph with the termination test on the device.  Returns
+ * pop[argmax(fit)] of the last evaluated generation (best_* may be NULL).
+ * Evaluation errors abort with "generation g, genome i: ..." context
+ * (SPEC.md:419). */
+int fnb_evolve(fnb_evolver* ev, const double* inputs, const double* targets, int batch, int fitness_kind,
+               double fitness_offset, double fitness_target, int generation_limit, fnb_run_stats_fn on_generation,
+               void* user, double* best_nodes, double* best_conns, double* best_fitness, int* generations_run);
+/* how the last fnb_evolve ran: 2 one graph per generation (conditional step
+ * node), 1 evaluate graph + host check + step graph, 0 eager; -1 never ran */
+int fnb_evolver_run_mode(fnb_evolver* ev);
+
 /* device pointers of the current population / fitness and the evolver's stream */
 int fnb_evolver_device_state(fnb_evolver* ev, double** d_nodes, double** d_conns, double** d_fitness,
                              void** stream);

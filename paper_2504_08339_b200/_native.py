@@ -52,6 +52,22 @@ class fnb_hyper_config(C.Structure):
                 ("max_weight", C.c_double), ("act_cost", C.c_double)]
 
 
+class fnb_run_state(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("generation", C.c_int), ("next_key", C.c_int), ("species_count", C.c_int),
+                ("next_species_id", C.c_int), ("species_id", C.c_int * 32), ("species_best", C.c_double * 32),
+                ("species_stagnation", C.c_int * 32), ("species_size", C.c_int * 32),
+                ("species_spawn", C.c_int * 32)]
+
+
+class fnb_run_stats(C.Structure):
+    _fields_ = [("generation", C.c_int), ("best", C.c_double), ("mean", C.c_double), ("std", C.c_double),
+                ("best_index", C.c_int), ("species_count", C.c_int), ("species_size", C.c_int * 32),
+                ("elapsed_ms", C.c_double)]
+
+
+# typedef int (*fnb_run_stats_fn)(void* user, const fnb_run_stats* stats)
+RUN_STATS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(fnb_run_stats))
+
 VP = C.c_void_p
 DP = C.POINTER(C.c_double)
 IP = C.POINTER(C.c_int32)
@@ -84,6 +100,11 @@ SIGNATURES = {
     "fnb_mutate": (C.c_int, [VP, DP, DP, C.c_int, U32P, C.POINTER(fnb_mutation_config), C.POINTER(C.c_int)]),
     "fnb_mutate_table": (C.c_int, [VP, DP, DP, C.c_int, U32P, C.POINTER(fnb_mutation_config), VP, VP, IP]),
     "fnb_evolver_eval_check": (C.c_int, [VP]),
+    "fnb_evolver_get_state": (C.c_int, [VP, C.POINTER(fnb_run_state), DP, DP]),
+    "fnb_evolver_set_state": (C.c_int, [VP, C.POINTER(fnb_run_state), DP, DP]),
+    "fnb_evolver_run_mode": (C.c_int, [VP]),
+    "fnb_evolve": (C.c_int, [VP, DP, DP, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, VP, VP, DP, DP, DP,
+                             C.POINTER(C.c_int)]),
     "fnb_mutate_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.POINTER(fnb_mutation_config), VP, VP, VP, VP]),
     "fnb_evolver_create": (C.c_int, [VP, C.POINTER(fnb_neat_config), C.c_uint64, C.POINTER(VP)]),
     "fnb_evolver_destroy": (None, [VP]),

@@ -23,6 +23,7 @@
 //              K5 crossover (elites are self-crossovers = exact copies), K6/K7
 //              mutation with one slot-ordered innovation table.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <climits>
 #include <cstdlib>
@@ -1000,6 +1001,7 @@ struct fnb_evolver {
   // [0] lowest genome whose transform failed (INT_MAX none), [1] non-finite X
   DevBuf eflags;
   int eval_lo = 0, eval_n = 0;
+  int run_mode = -1;  // fnb_evolve: 2 conditional generation graphs, 1 evaluate graph + step graph, 0 eager
 };
 
 namespace fnb {
@@ -1379,3 +1381,430 @@ int fnb_evolver_device_state(fnb_evolver* ev, double** d_nodes, double** d_conns
 }
 
 }  // extern "C"
+
+// =================================================================================
+// checkpoint / resume (SPEC.md:337-340 SpeciesState, :122 / :525-532 save-load):
+// everything a generation step reads besides the population -- the seed (the
+// key tree, oracle E1), the generation counter, the InnovationTable counter,
+// and the species table with its representatives.
+// =================================================================================
+extern "C" {
+
+int fnb_evolver_get_state(fnb_evolver* ev, fnb_run_state* s, double* rep_nodes, double* rep_conns) {
+  fnb::Evolver& v = ev->ev;
+  if (!s) return fnb_set_error(ev->ctx, FNB_E_CONFIG_ERROR, "no state buffer", -1);
+  cudaSetDevice(ev->ctx->device);
+  fnb::SpeciesDev h;
+  int nk[2] = {0, 0};
+  EV_CK(cudaMemcpyAsync(&h, v.sd, sizeof(h), cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaMemcpyAsync(nk, v.next_key, sizeof(nk), cudaMemcpyDeviceToHost, v.st));
+  if (rep_nodes && h.count > 0)
+    EV_CK(cudaMemcpyAsync(rep_nodes, v.rep_n, sizeof(double) * v.gn() * h.count, cudaMemcpyDeviceToHost, v.st));
+  if (rep_conns && h.count > 0)
+    EV_CK(cudaMemcpyAsync(rep_conns, v.rep_c, sizeof(double) * v.gc() * h.count, cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  *s = fnb_run_state{};
+  s->seed = v.seed;
+  s->generation = v.generation;
+  s->next_key = nk[0];
+  s->species_count = h.count;
+  s->next_species_id = h.next_id;
+  for (int j = 0; j < h.count; ++j) {
+    s->species_id[j] = h.id[j];
+    s->species_best[j] = h.best[j];
+    s->species_stagnation[j] = h.stag[j];
+    s->species_size[j] = h.size[j];
+    s->species_spawn[j] = h.spawn[j];
+  }
+  return 0;
+}
+
+int fnb_evolver_set_state(fnb_evolver* ev, const fnb_run_state* s, const double* rep_nodes, const double* rep_conns) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  if (!s || s->species_count < 0 || s->species_count > v.cfg.max_species || s->generation < 0 ||
+      (s->species_count > 0 && (!rep_nodes || !rep_conns)))
+    return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "invalid evolver state", -1);
+  for (int j = 0; j < s->species_count; ++j)
+    if (s->species_id[j] < 0 || s->species_id[j] >= s->next_species_id || (j && s->species_id[j] <= s->species_id[j - 1]))
+      return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "species ids must ascend below next_species_id", j);
+  cudaSetDevice(ctx->device);
+  fnb::SpeciesDev h{};
+  h.count = s->species_count;
+  h.next_id = s->next_species_id;
+  h.generation = s->generation;
+  h.first_bad = INT_MAX;
+  for (int j = 0; j < s->species_count; ++j) {
+    h.id[j] = s->species_id[j];
+    h.best[j] = s->species_best[j];
+    h.stag[j] = s->species_stagnation[j];
+    h.size[j] = s->species_size[j];
+    h.spawn[j] = s->species_spawn[j];
+  }
+  const int nk[2] = {s->next_key, 0};
+  EV_CK(cudaMemcpyAsync(v.sd, &h, sizeof(h), cudaMemcpyHostToDevice, v.st));
+  EV_CK(cudaMemcpyAsync(v.next_key, nk, sizeof(nk), cudaMemcpyHostToDevice, v.st));
+  if (s->species_count > 0) {
+    EV_CK(cudaMemcpyAsync(v.rep_n, rep_nodes, sizeof(double) * v.gn() * s->species_count, cudaMemcpyHostToDevice,
+                          v.st));
+    EV_CK(cudaMemcpyAsync(v.rep_c, rep_conns, sizeof(double) * v.gc() * s->species_count, cudaMemcpyHostToDevice,
+                          v.st));
+  }
+  EV_CK(cudaStreamSynchronize(v.st));
+  v.seed = s->seed;
+  v.generation = s->generation;
+  v.host_species = s->species_count;
+  return 0;
+}
+
+}  // extern "C"
+
+// =================================================================================
+// SPEC evolve(problem, cfg, key) (PAPER Algorithm 1) as one
+// device-resident loop.  Each generation is ONE CUDA graph:
+//     K1 + K2 (evaluate) -> k_gen_stats -> IF (no error and best < target) { step }
+// The conditional node (cudaGraphCondTypeIf, set from k_gen_stats) keeps the
+// termination check BEFORE reproduction without a host round
+// trip between evaluation and the step; the host reads one small GenStats
+// record per generation for RunStats.  Graphs are keyed like the step graphs
+// by (species count before the step, current buffer).  Without conditional
+// node support the same sequence runs as an evaluate graph, a host check and
+// the step graph.
+// =================================================================================
+namespace fnb {
+
+struct GenStats {
+  double best, mean, std;
+  int best_index;
+  int eval_first_bad;   // lowest genome whose transform failed (INT_MAX none)
+  int eval_nonfinite;
+  int stepped;          // the step body ran
+  int step_error, species_count, first_bad;
+  int species_size[kMaxSpecies];
+};
+
+// Fitness statistics in one CTA, in a fixed order (deterministic for a given
+// P): each thread reduces a contiguous run, then a fixed shared-memory tree.
+// best = max (lowest index on ties), mean = sum / P, std = population std.
+__global__ void __launch_bounds__(1024) k_gen_stats(const double* __restrict__ fit, int P, const int* eflags,
+                                                    double target, cudaGraphConditionalHandle h, int use_cond,
+                                                    GenStats* out) {
+  __shared__ double s_sum[1024];
+  __shared__ double s_max[1024];
+  __shared__ int s_arg[1024];
+  __shared__ double s_mean;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int per = (P + nt - 1) / nt, lo = min(P, t * per), hi = min(P, lo + per);
+  double sum = 0.0, mx = -INFINITY;
+  int arg = INT_MAX;
+  for (int i = lo; i < hi; ++i) {
+    const double f = fit[i];
+    sum = __dadd_rn(sum, f);
+    if (arg == INT_MAX || f > mx) { mx = f; arg = i; }
+  }
+  s_sum[t] = sum;
+  s_max[t] = mx;
+  s_arg[t] = arg;
+  __syncthreads();
+  for (int d = nt / 2; d > 0; d >>= 1) {
+    if (t < d) {
+      s_sum[t] = __dadd_rn(s_sum[t], s_sum[t + d]);
+      const bool take = s_arg[t + d] != INT_MAX &&
+                        (s_arg[t] == INT_MAX || s_max[t + d] > s_max[t] ||
+                         (s_max[t + d] == s_max[t] && s_arg[t + d] < s_arg[t]));
+      if (take) { s_max[t] = s_max[t + d]; s_arg[t] = s_arg[t + d]; }
+    }
+    __syncthreads();
+  }
+  if (t == 0) s_mean = __ddiv_rn(s_sum[0], double(P));
+  __syncthreads();
+  const double mean = s_mean;
+  double sq = 0.0;
+  for (int i = lo; i < hi; ++i) {
+    const double d = __dsub_rn(fit[i], mean);
+    sq = __dadd_rn(sq, __dmul_rn(d, d));
+  }
+  __syncthreads();
+  s_sum[t] = sq;
+  __syncthreads();
+  for (int d = nt / 2; d > 0; d >>= 1) {
+    if (t < d) s_sum[t] = __dadd_rn(s_sum[t], s_sum[t + d]);
+    __syncthreads();
+  }
+  if (t == 0) {
+    out->best = s_max[0];
+    out->best_index = s_arg[0];
+    out->mean = mean;
+    out->std = sqrt(__ddiv_rn(s_sum[0], double(P)));
+    out->eval_first_bad = eflags[0];
+    out->eval_nonfinite = eflags[1];
+    out->stepped = 0;
+    const bool ok = eflags[0] == INT_MAX && eflags[1] == 0;
+    const bool done = s_max[0] >= target;
+    if (use_cond) cudaGraphSetConditional(h, ok && !done ? 1u : 0u);
+  }
+}
+
+// the step's outcome for the host (tail of the conditional body)
+__global__ void k_gen_step_status(const SpeciesDev* sd, GenStats* out) {
+  const int t = threadIdx.x;
+  if (t < kMaxSpecies) out->species_size[t] = t < sd->count ? sd->size[t] : 0;
+  if (t == 0) {
+    out->stepped = 1;
+    out->step_error = sd->error;
+    out->species_count = sd->count;
+    out->first_bad = sd->first_bad;
+  }
+}
+
+}  // namespace fnb
+
+struct fnb_gen_graph {
+  cudaGraphExec_t exec = nullptr;
+  long long n_eval = 0, n_step = 0;
+};
+
+struct fnb_evolve_run {
+  fnb_gen_graph g[fnb::kMaxSpecies + 1][2];
+  bool use_cond = true;
+  fnb::GenStats* d_stats = nullptr;
+  fnb::GenStats* h_stats = nullptr;  // pinned
+  ~fnb_evolve_run() {
+    for (auto& row : g)
+      for (auto& x : row)
+        if (x.exec) cudaGraphExecDestroy(x.exec);
+    if (d_stats) cudaFree(d_stats);
+    if (h_stats) cudaFreeHost(h_stats);
+  }
+};
+
+static long long count_kernel_nodes(cudaGraph_t graph) {
+  size_t n = 0;
+  if (cudaGraphGetNodes(graph, nullptr, &n) != cudaSuccess || n == 0) return 0;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (cudaGraphGetNodes(graph, nodes.data(), &n) != cudaSuccess) return 0;
+  long long k = 0;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
+// evaluate + stats (+ the conditional step when `with_step`) for the current
+// (species count, buffer), captured on the evolver stream.
+static cudaError_t build_gen_graph(fnb_evolver* ev, fnb_evolve_run& run, const float* X, const float* Y, int batch,
+                                   int kind, double offset, double target, fnb_gen_graph* out) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  const long long before = ctx->launches;
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(v.st, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return e;
+  cudaGraphConditionalHandle h = 0;
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t cap = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  e = cudaStreamGetCaptureInfo(v.st, &cs, nullptr, &cap, nullptr, nullptr);
+  if (e == cudaSuccess && run.use_cond) e = cudaGraphConditionalHandleCreate(&h, cap, 0, cudaGraphCondAssignDefault);
+  int st = 0;
+  if (e == cudaSuccess) st = evolver_eval_enqueue(ev, 0, v.P, X, Y, batch, kind, offset, v.fitness);
+  if (e == cudaSuccess && !st) {
+    fnb::k_gen_stats<<<1, 1024, 0, v.st>>>(v.fitness, v.P, static_cast<const int*>(ev->eflags.p), target, h,
+                                            run.use_cond ? 1 : 0, run.d_stats);
+    e = cudaGetLastError();
+  }
+  cudaGraphNode_t cond = nullptr;
+  cudaGraph_t body = nullptr;
+  if (e == cudaSuccess && !st && run.use_cond) {
+    e = cudaStreamGetCaptureInfo(v.st, &cs, nullptr, &cap, &deps, &ndeps);
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&cond, cap, deps, ndeps, &p);
+    if (e == cudaSuccess) {
+      body = p.conditional.phGraph_out[0];
+      e = cudaStreamUpdateCaptureDependencies(v.st, &cond, 1, cudaStreamSetCaptureDependencies);
+    }
+  }
+  const cudaError_t ee = cudaStreamEndCapture(v.st, &graph);
+  if (e == cudaSuccess) e = ee;
+  if (st && e == cudaSuccess) e = cudaErrorInvalidValue;
+  const long long n_eval = ctx->launches - before + 1;
+  long long n_step = 0;
+  if (e == cudaSuccess && body) {  // the step, captured into the conditional body
+    const long long b2 = ctx->launches;
+    e = cudaStreamBeginCaptureToGraph(v.st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      cudaError_t es = v.enqueue_step();
+      if (es == cudaSuccess) {
+        fnb::k_gen_step_status<<<1, 32, 0, v.st>>>(v.sd, run.d_stats);
+        es = cudaGetLastError();
+      }
+      cudaGraph_t b_out = nullptr;
+      e = cudaStreamEndCapture(v.st, &b_out);
+      if (es != cudaSuccess) e = es;
+    }
+    n_step = ctx->launches - b2 + 1;
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&out->exec, graph, 0);
+  if (e == cudaSuccess) {
+    out->n_eval = run.use_cond ? n_eval : count_kernel_nodes(graph);
+    out->n_step = n_step;
+  }
+  if (graph) cudaGraphDestroy(graph);
+  ctx->launches = before;
+  return e;
+}
+
+extern "C" {
+
+int fnb_evolve(fnb_evolver* ev, const double* inputs, const double* targets, int batch, int fitness_kind,
+               double fitness_offset, double fitness_target, int generation_limit, fnb_run_stats_fn on_generation,
+               void* user, double* best_nodes, double* best_conns, double* best_fitness, int* generations_run) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  ctx->err_index = -1;
+  if (generations_run) *generations_run = 0;
+  if (batch <= 0) return fnb_set_error(ctx, FNB_E_EMPTY_DATASET, "batch is empty", -1);
+  if (generation_limit < 0 || fitness_kind == FNB_FIT_NONE)
+    return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "generation_limit >= 0 and a fitness kind are required", -1);
+  // the problem's data go up once, narrowed to FP32 (the forward's arithmetic)
+  const size_t nx = size_t(batch) * ctx->sh.I, ny = size_t(batch) * ctx->sh.O;
+  std::vector<float> xf(nx), yf(ny);
+  for (size_t i = 0; i < nx; ++i) {
+    if (!std::isfinite(inputs[i])) return fnb_set_error(ctx, FNB_E_NON_FINITE_INPUT, "input not finite", 0);
+    xf[i] = float(inputs[i]);
+  }
+  for (size_t i = 0; i < ny; ++i) yf[i] = float(targets[i]);
+  EV_CK(ev->X.ensure(sizeof(float) * nx + 16));
+  EV_CK(ev->Y.ensure(sizeof(float) * ny + 16));
+  EV_CK(cudaMemcpyAsync(ev->X.p, xf.data(), sizeof(float) * nx, cudaMemcpyHostToDevice, v.st));
+  EV_CK(cudaMemcpyAsync(ev->Y.p, yf.data(), sizeof(float) * ny, cudaMemcpyHostToDevice, v.st));
+  EV_CK(ev->nets.ensure(ctx->L.bytes * size_t(v.P)));
+  EV_CK(ev->eflags.ensure(4 * sizeof(int)));
+  EV_CK(ctx->partial.ensure(fnb::forward_partial_needed(ctx->L, v.P, batch)));
+  const float* X = static_cast<const float*>(ev->X.p);
+  const float* Y = static_cast<const float*>(ev->Y.p);
+  fnb_evolve_run run;
+  EV_CK(cudaMalloc(&run.d_stats, sizeof(fnb::GenStats)));
+  EV_CK(cudaMallocHost(&run.h_stats, sizeof(fnb::GenStats)));
+  EV_CK(cudaStreamSynchronize(v.st));
+  bool use_graphs = v.use_graphs;
+  if (const char* g = std::getenv("FNB_GEN_GRAPH")) run.use_cond = std::string(g) != "0";
+  int last_eval_buf = v.cur, last_best = 0;
+  double last_fit = -INFINITY;
+  int gens = 0;
+  for (int g = 0; g < generation_limit; ++g) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int eval_buf = v.cur, gen_no = v.generation;
+    bool stepped_in_graph = false;
+    fnb_gen_graph* gg = nullptr;
+    if (use_graphs) {
+      gg = &run.g[v.host_species][v.cur];
+      if (!gg->exec) {
+        cudaError_t e = build_gen_graph(ev, run, X, Y, batch, fitness_kind, fitness_offset, fitness_target, gg);
+        if (e != cudaSuccess && run.use_cond) {  // no conditional nodes here: evaluate graph + host check
+          cudaGetLastError();
+          run.use_cond = false;
+          for (auto& row : run.g)
+            for (auto& x : row)
+              if (x.exec) { cudaGraphExecDestroy(x.exec); x.exec = nullptr; }
+          e = build_gen_graph(ev, run, X, Y, batch, fitness_kind, fitness_offset, fitness_target, gg);
+        }
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          use_graphs = false;
+          gg = nullptr;
+        }
+      }
+    }
+    if (gg) {
+      EV_CK(cudaGraphLaunch(gg->exec, v.st));
+      ctx->launches += gg->n_eval;
+    } else {
+      if (int st = evolver_eval_enqueue(ev, 0, v.P, X, Y, batch, fitness_kind, fitness_offset, v.fitness)) return st;
+      fnb::k_gen_stats<<<1, 1024, 0, v.st>>>(v.fitness, v.P, static_cast<const int*>(ev->eflags.p), fitness_target,
+                                              0, 0, run.d_stats);
+      EV_CK(cudaGetLastError());
+      ++ctx->launches;
+    }
+    EV_CK(cudaMemcpyAsync(run.h_stats, run.d_stats, sizeof(fnb::GenStats), cudaMemcpyDeviceToHost, v.st));
+    EV_CK(cudaStreamSynchronize(v.st));
+    const fnb::GenStats s = *run.h_stats;
+    if (s.eval_first_bad != INT_MAX || s.eval_nonfinite) {  // abort with context
+      ev->eval_lo = 0;
+      ev->eval_n = v.P;
+      int st = 0;
+      if (s.eval_first_bad != INT_MAX)
+        st = fnb_check_nets_d(ctx, v.pn[eval_buf], v.pc[eval_buf], ev->nets.p, v.P, v.st);
+      if (!st) st = fnb_set_error(ctx, FNB_E_NON_FINITE_INPUT, "input not finite", 0);
+      ctx->err = ctx->err.substr(0, ctx->err.find(": ") + 2) + "generation " + std::to_string(gen_no) + ", genome " +
+                 std::to_string(ctx->err_index) + ": " + ctx->err.substr(ctx->err.find(": ") + 2);
+      return st;
+    }
+    const bool done = s.best >= fitness_target;
+    fnb_run_stats rs{};
+    rs.generation = gen_no;
+    rs.best = s.best;
+    rs.mean = s.mean;
+    rs.std = s.std;
+    rs.best_index = s.best_index;
+    if (gg && run.use_cond) {
+      stepped_in_graph = s.stepped != 0;
+      if (stepped_in_graph) {
+        ctx->launches += gg->n_step;
+        if (s.step_error) return fnb_set_error(ctx, FNB_E_EVAL_ERROR, "spawn counts do not sum to pop_size", -1);
+        if (s.first_bad != INT_MAX)
+          return fnb_set_error(ctx, FNB_E_DUPLICATE_KEY, "mutation failed in child slot", s.first_bad);
+        v.host_species = s.species_count;
+        v.cur ^= 1;
+        ++v.generation;
+      }
+    } else if (!done) {
+      int err = -1;
+      EV_CK(v.step(&err));
+      if (err == -2) return fnb_set_error(ctx, FNB_E_EVAL_ERROR, "spawn counts do not sum to pop_size", -1);
+      if (err >= 0) return fnb_set_error(ctx, FNB_E_DUPLICATE_KEY, "mutation failed in child slot", err);
+    }
+    // species after this generation's speciation (the previous table when it stopped first)
+    fnb::SpeciesDev h;
+    if (!stepped_in_graph) {
+      EV_CK(cudaMemcpyAsync(&h, v.sd, sizeof(h), cudaMemcpyDeviceToHost, v.st));
+      EV_CK(cudaStreamSynchronize(v.st));
+      rs.species_count = h.count;
+      for (int j = 0; j < h.count; ++j) rs.species_size[j] = h.size[j];
+    } else {
+      rs.species_count = s.species_count;
+      for (int j = 0; j < s.species_count; ++j) rs.species_size[j] = s.species_size[j];
+    }
+    rs.elapsed_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    last_eval_buf = eval_buf;
+    last_best = s.best_index;
+    last_fit = s.best;
+    ++gens;
+    const int stop = on_generation ? on_generation(user, &rs) : 0;
+    if (done || stop) break;
+  }
+  if (generations_run) *generations_run = gens;
+  if (best_fitness) *best_fitness = last_fit;
+  ev->run_mode = use_graphs ? (run.use_cond ? 2 : 1) : 0;
+  // pop[argmax(fit)] of the last evaluated generation: one genome leaves the device
+  if (gens > 0 && best_nodes)
+    EV_CK(cudaMemcpyAsync(best_nodes, v.pn[last_eval_buf] + size_t(last_best) * v.gn(), sizeof(double) * v.gn(),
+                          cudaMemcpyDeviceToHost, v.st));
+  if (gens > 0 && best_conns)
+    EV_CK(cudaMemcpyAsync(best_conns, v.pc[last_eval_buf] + size_t(last_best) * v.gc(), sizeof(double) * v.gc(),
+                          cudaMemcpyDeviceToHost, v.st));
+  EV_CK(cudaStreamSynchronize(v.st));
+  return 0;
+}
+
+}  // extern "C"
+
+extern "C" int fnb_evolver_run_mode(fnb_evolver* ev) { return ev ? ev->run_mode : -1; }

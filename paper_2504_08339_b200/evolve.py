@@ -54,6 +54,14 @@ class RunStats:
     std: float
     species_count: int
     elapsed_ms: float
+    best_index: int = -1
+    species_sizes: tuple = ()
+
+    @staticmethod
+    def from_c(rs) -> "RunStats":
+        k = rs.species_count
+        return RunStats(rs.generation, rs.best, rs.mean, rs.std, k, rs.elapsed_ms, rs.best_index,
+                        tuple(rs.species_size[j] for j in range(k)))
 
 
 class Evolver:
@@ -229,6 +237,94 @@ class Evolver:
         self._raise(self._lib.fnb_evolver_state(self._h, C.byref(g), C.byref(nk)))
         return g.value, nk.value
 
+    # -- checkpoint / resume (fnb_evolver_get_state / set_state) ------------------------
+    def get_state(self):
+        """(state dict, representative nodes [S,N,5], representative conns [S,C,4])."""
+        st = N.fnb_run_state()
+        L = self.engine.limits
+        rn = np.empty((32, L.max_nodes, 5))
+        rc = np.empty((32, L.max_conns, 4))
+        self._raise(self._lib.fnb_evolver_get_state(self._h, C.byref(st), _dp(rn), _dp(rc)))
+        k = st.species_count
+        d = dict(seed=int(st.seed), generation=st.generation, next_key=st.next_key, next_species_id=st.next_species_id,
+                 species_id=[st.species_id[j] for j in range(k)], species_best=[st.species_best[j] for j in range(k)],
+                 species_stagnation=[st.species_stagnation[j] for j in range(k)],
+                 species_size=[st.species_size[j] for j in range(k)],
+                 species_spawn=[st.species_spawn[j] for j in range(k)])
+        return d, rn[:k].copy(), rc[:k].copy()
+
+    def set_state(self, state: dict, rep_nodes, rep_conns):
+        st = N.fnb_run_state()
+        k = len(state["species_id"])
+        st.seed, st.generation, st.next_key = state["seed"], state["generation"], state["next_key"]
+        st.species_count, st.next_species_id = k, state["next_species_id"]
+        for j in range(k):
+            st.species_id[j] = state["species_id"][j]
+            st.species_best[j] = state["species_best"][j]
+            st.species_stagnation[j] = state["species_stagnation"][j]
+            st.species_size[j] = state["species_size"][j]
+            st.species_spawn[j] = state["species_spawn"][j]
+        rn = np.ascontiguousarray(rep_nodes, dtype=np.float64)
+        rc = np.ascontiguousarray(rep_conns, dtype=np.float64)
+        self._raise(self._lib.fnb_evolver_set_state(self._h, C.byref(st), _dp(rn), _dp(rc)))
+
+    def save_checkpoint(self) -> str:
+        """The whole run state as one wire document (wire.save_checkpoint)."""
+        from .wire import save_checkpoint
+        state, rn, rc = self.get_state()
+        n, c = self.population()
+        sch = self.engine.schema
+        return save_checkpoint(state, rn, rc, n, c, self.engine.input_keys, self.engine.output_keys,
+                               sch.activations, sch.aggregations)
+
+    def load_checkpoint(self, text: str):
+        """Restore population, species table, innovation counter, generation and
+        seed; the run then continues bit for bit."""
+        from .wire import load_checkpoint
+        state, rn, rc, n, c, meta = load_checkpoint(text)
+        L = self.engine.limits
+        if n.shape != (self.cfg.pop_size, L.max_nodes, 5) or c.shape != (self.cfg.pop_size, L.max_conns, 4):
+            raise FlatneatError(9, "shape_mismatch: checkpoint population does not match this evolver")
+        if meta["input_keys"] != list(self.engine.input_keys) or meta["output_keys"] != list(self.engine.output_keys):
+            raise FlatneatError(9, "shape_mismatch: checkpoint input/output keys differ")
+        pn = np.ascontiguousarray(n)
+        pc = np.ascontiguousarray(c)
+        self._raise(self._lib.fnb_evolver_set_population(self._h, _dp(pn), _dp(pc)))
+        self.set_state(state, rn, rc)
+
+    # -- SPEC evolve on the device (fnb_evolve) -----------------------------------------
+    def run(self, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0, fitness_target: float = float("inf"),
+            generation_limit: int = 100, on_generation: Optional[Callable[[RunStats], None]] = None):
+        """fnb_evolve: evaluate -> stop at the target -> step, one CUDA graph per
+        generation.  Returns (best (nodes, conns), best fitness, [RunStats])."""
+        x = np.ascontiguousarray(X, dtype=np.float64)
+        y = np.ascontiguousarray(Y, dtype=np.float64)
+        B = x.shape[0] if x.ndim > 1 else x.size // max(1, self.engine.num_inputs)
+        stats: List[RunStats] = []
+
+        def cb(_user, p):
+            rs = RunStats.from_c(p.contents)
+            stats.append(rs)
+            if on_generation:
+                return 1 if on_generation(rs) else 0
+            return 0
+
+        fn = N.RUN_STATS_FN(cb)
+        L = self.engine.limits
+        bn = np.full((L.max_nodes, 5), np.nan)
+        bc = np.full((L.max_conns, 4), np.nan)
+        bf = C.c_double(float("nan"))
+        gens = C.c_int(0)
+        self._raise(self._lib.fnb_evolve(self._h, _dp(x), _dp(y), B, kind, offset, fitness_target, generation_limit,
+                                         C.cast(fn, C.c_void_p), None, _dp(bn), _dp(bc), C.byref(bf),
+                                         C.byref(gens)))
+        return (bn, bc), bf.value, stats
+
+    def run_mode(self) -> int:
+        """2: the last run() used one CUDA graph per generation (conditional
+        step node); 1: evaluate graph + host check + step graph; 0: eager."""
+        return int(self._lib.fnb_evolver_run_mode(self._h))
+
     def device_state(self):
         n, c, f, s = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         self._raise(self._lib.fnb_evolver_device_state(self._h, C.byref(n), C.byref(c), C.byref(f), C.byref(s)))
@@ -248,30 +344,47 @@ def torch_float64():
     return torch.float64
 
 
-def evolve(engine: Engine, cfg: NeatConfig, seed: int, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0,
-           on_generation: Optional[Callable[[RunStats], None]] = None):
-    """evaluate -> check target -> speciate/stagnate/spawn/reproduce.
-    Returns (best genome (nodes, conns), best fitness, [RunStats])."""
-    ev = Evolver(engine, cfg, seed)
-    ev.init_population()
+def evolve(engine: Engine, cfg: NeatConfig, seed: int, X=None, Y=None, kind: int = FIT_NEG_MSE, offset: float = 0.0,
+           on_generation: Optional[Callable[[RunStats], None]] = None, fitness_fn=None,
+           evolver: Optional[Evolver] = None):
+    """SPEC.md:392-400 evolve(problem, cfg, key): evaluate -> stop when
+    max(fit) >= fitness_target (BEFORE reproducing) -> speciate / stagnate /
+    apportion / reproduce, for at most cfg.generation_limit generations.
+
+    The problem is the func-fit / xor dataset (X, Y, kind, offset), run on the
+    device by fnb_evolve (one CUDA graph per generation), or any host-side
+    `fitness_fn(nodes, conns) -> fitness[P]` (a user problem; its fitness is
+    injected each generation).  `evolver` continues an existing run (e.g. one
+    restored from a checkpoint) instead of a fresh initialize_population.
+    Returns (pop[argmax(fit)] of the last evaluated generation as (nodes,
+    conns), its fitness, [RunStats])."""
+    ev = evolver
+    if ev is None:
+        ev = Evolver(engine, cfg, seed)
+        ev.init_population()
+    if fitness_fn is None:
+        return ev.run(X, Y, kind, offset, cfg.fitness_target, cfg.generation_limit, on_generation)
     stats: List[RunStats] = []
-    best = (None, -np.inf)
-    for gen in range(cfg.generation_limit):
+    best = (None, float("nan"))
+    for _ in range(cfg.generation_limit):
         t0 = time.perf_counter()
-        ev.evaluate(X, Y, kind, offset)
-        fit = ev.fitness()
+        gen = ev.state()[0]
+        n, c = ev.population()
+        fit = np.ascontiguousarray(fitness_fn(n, c), dtype=np.float64)
+        if fit.shape != (cfg.pop_size,) or not np.all(np.isfinite(fit)):
+            raise FlatneatError(1 + 19, f"eval_error: generation {gen}: fitness_fn must return pop_size finite values")
+        ev.set_fitness(fit)
         i = int(np.argmax(fit))  # lowest index on ties
-        if fit[i] > best[1]:
-            n, c = ev.population()
-            best = ((n[i].copy(), c[i].copy()), float(fit[i]))
+        best = ((n[i].copy(), c[i].copy()), float(fit[i]))
         done = fit[i] >= cfg.fitness_target
         if not done:
             ev.step()
-        rs = RunStats(gen, float(fit[i]), float(fit.mean()), float(fit.std()), ev.species()["count"],
-                      (time.perf_counter() - t0) * 1e3)
+        sp = ev.species()
+        rs = RunStats(gen, float(fit[i]), float(fit.mean()), float(fit.std()), sp["count"],
+                      (time.perf_counter() - t0) * 1e3, i, tuple(int(x) for x in sp["sizes"]))
         stats.append(rs)
-        if on_generation:
-            on_generation(rs)
+        if on_generation and on_generation(rs):
+            break
         if done:
             break
     return best[0], best[1], stats

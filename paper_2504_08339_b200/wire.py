@@ -133,3 +133,122 @@ def load_population(docs: Sequence[str]) -> Tuple[np.ndarray, np.ndarray, dict]:
     if len(shapes) != 1:
         raise FlatneatError(1 + 8, "shape_mismatch: genomes of a population must share limits")
     return np.stack([n for n, _, _ in loaded]), np.stack([c for _, c, _ in loaded]), loaded[0][2]
+
+
+# ---- checkpoint / resume -------------------------------------
+CHECKPOINT_FORMAT = "flatneat-b200-checkpoint"
+
+
+def _fnum(x: float) -> str:
+    if math.isinf(x):
+        return '"inf"' if x > 0 else '"-inf"'
+    return _num(x)
+
+
+def save_checkpoint(state: dict, rep_nodes, rep_conns, pop_nodes, pop_conns, input_keys, output_keys,
+                    activations=("tanh",), aggregations=("sum",)) -> str:
+    """An evolver's run state (Evolver.get_state: seed, generation, innovation
+    counter, species table with representatives) and its population as one
+    document, in the genome format's conventions: sorted keys, 17 significant
+    digits, null for the NaN padding -- load(save(x)) restores every bit."""
+    rn = np.asarray(rep_nodes, dtype=np.float64)
+    rc = np.asarray(rep_conns, dtype=np.float64)
+    pn = np.asarray(pop_nodes, dtype=np.float64)
+    pc = np.asarray(pop_conns, dtype=np.float64)
+    k = len(state["species_id"])
+    species = []
+    for j in range(k):
+        species.append("{" + ",".join([
+            '"best":' + _fnum(float(state["species_best"][j])),
+            '"id":%d' % state["species_id"][j],
+            '"rep_conns":' + _rows(rc[j]),
+            '"rep_nodes":' + _rows(rn[j]),
+            '"size":%d' % state["species_size"][j],
+            '"spawn":%d' % state["species_spawn"][j],
+            '"stagnation":%d' % state["species_stagnation"][j],
+        ]) + "}")
+    parts = [
+        '"activations":' + json.dumps(list(activations)),
+        '"aggregations":' + json.dumps(list(aggregations)),
+        '"format":' + json.dumps(CHECKPOINT_FORMAT),
+        '"generation":%d' % state["generation"],
+        '"input_keys":' + json.dumps([int(x) for x in input_keys]),
+        '"limits":{"max_conns":%d,"max_nodes":%d}' % (pc.shape[1], pn.shape[1]),
+        '"next_key":%d' % state["next_key"],
+        '"next_species_id":%d' % state["next_species_id"],
+        '"output_keys":' + json.dumps([int(x) for x in output_keys]),
+        '"population":[' + ",".join('{"conns":%s,"nodes":%s}' % (_rows(pc[i]), _rows(pn[i]))
+                                    for i in range(pn.shape[0])) + "]",
+        '"seed":%d' % int(state["seed"]),
+        '"species":[' + ",".join(species) + "]",
+        '"version":%d' % VERSION,
+    ]
+    return "{" + ",".join(parts) + "}\n"
+
+
+def load_checkpoint(text: str):
+    """Document -> (state dict, rep_nodes [S,N,5], rep_conns [S,C,4],
+    pop_nodes [P,N,5], pop_conns [P,C,4], meta)."""
+    try:
+        doc = json.loads(text)
+    except json.JSONDecodeError as e:
+        _fail(e.msg, line=e.lineno)
+    if not isinstance(doc, dict) or doc.get("format") != CHECKPOINT_FORMAT:
+        _fail(f"format must be '{CHECKPOINT_FORMAT}'", "format")
+    version = doc.get("version")
+    if not isinstance(version, int) or isinstance(version, bool):
+        _fail("version must be an integer", "version")
+    if version != VERSION:
+        raise FlatneatError(_VERSION_UNSUPPORTED, f"version_unsupported: checkpoint document version {version}")
+
+    def _int(f):
+        v = doc.get(f)
+        if not isinstance(v, int) or isinstance(v, bool):
+            _fail("must be an integer", f)
+        return v
+
+    limits = doc.get("limits")
+    if not isinstance(limits, dict):
+        _fail("missing limits", "limits")
+    N, Cm = limits.get("max_nodes"), limits.get("max_conns")
+    if not all(isinstance(x, int) and not isinstance(x, bool) and x > 0 for x in (N, Cm)):
+        _fail("limits must be positive integers", "limits")
+    meta = {}
+    for f in ("input_keys", "output_keys", "activations", "aggregations"):
+        v = doc.get(f)
+        want = int if f.endswith("keys") else str
+        if not isinstance(v, list) or not all(isinstance(x, want) and not isinstance(x, bool) for x in v):
+            _fail(f"must be a list of {want.__name__}", f)
+        meta[f] = v
+    pop = doc.get("population")
+    if not isinstance(pop, list) or not pop:
+        _fail("must be a non-empty list", "population")
+    pn = np.stack([_rows_in(g, "nodes", 5, N) if isinstance(g, dict) else _fail("genome is not an object", "population")
+                   for g in pop])
+    pc = np.stack([_rows_in(g, "conns", 4, Cm) for g in pop])
+    sp = doc.get("species")
+    if not isinstance(sp, list) or len(sp) > 32:
+        _fail("must be a list of at most 32 species", "species")
+    state = dict(seed=_int("seed"), generation=_int("generation"), next_key=_int("next_key"),
+                 next_species_id=_int("next_species_id"), species_id=[], species_best=[], species_stagnation=[],
+                 species_size=[], species_spawn=[])
+    rn = np.empty((len(sp), N, 5))
+    rc = np.empty((len(sp), Cm, 4))
+    for j, e in enumerate(sp):
+        if not isinstance(e, dict):
+            _fail(f"species {j} is not an object", "species")
+        for f, key in (("id", "species_id"), ("stagnation", "species_stagnation"), ("size", "species_size"),
+                       ("spawn", "species_spawn")):
+            v = e.get(f)
+            if not isinstance(v, int) or isinstance(v, bool):
+                _fail(f"species {j} {f} must be an integer", "species")
+            state[key].append(v)
+        b = e.get("best")
+        if b in ("inf", "-inf"):
+            b = float(b)
+        elif not isinstance(b, (int, float)) or isinstance(b, bool):
+            _fail(f"species {j} best must be a number", "species")
+        state["species_best"].append(float(b))
+        rn[j] = _rows_in(e, "rep_nodes", 5, N)
+        rc[j] = _rows_in(e, "rep_conns", 4, Cm)
+    return state, rn, rc, pn, pc, meta

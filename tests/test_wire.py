@@ -98,3 +98,34 @@ def test_infinite_value_is_refused(pop):
     with pytest.raises(FlatneatError) as e:
         save_genome(n, pop[1][0], **KW)
     assert e.value.code == "non_finite_state"
+
+
+def test_checkpoint_document_round_trip():
+    """save_checkpoint / load_checkpoint restore every double bit for bit,
+    infinite best-ever values included, and reject other formats / versions."""
+    import pytest
+    from paper_2504_08339_b200.api import FlatneatError
+    from paper_2504_08339_b200.wire import load_checkpoint, save_checkpoint
+    rng = np.random.default_rng(0)
+    P, N, Cm = 6, 10, 20
+    pn = np.full((P, N, 5), np.nan)
+    pc = np.full((P, Cm, 4), np.nan)
+    pn[:, :4] = rng.normal(size=(P, 4, 5))
+    pc[:, :7] = rng.normal(size=(P, 7, 4))
+    rn, rc = pn[:2].copy(), pc[:2].copy()
+    state = dict(seed=2**63 + 5, generation=12, next_key=345, next_species_id=7, species_id=[3, 6],
+                 species_best=[float("-inf"), 0.1 + 0.2], species_stagnation=[4, 0], species_size=[4, 2],
+                 species_spawn=[3, 3])
+    text = save_checkpoint(state, rn, rc, pn, pc, [0, 1], [2], ["tanh"], ["sum"])
+    st, a, b, n, c, meta = load_checkpoint(text)
+    assert st == state
+    for x, y in ((a, rn), (b, rc), (n, pn), (c, pc)):
+        assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+    assert meta == dict(input_keys=[0, 1], output_keys=[2], activations=["tanh"], aggregations=["sum"])
+    assert save_checkpoint(st, a, b, n, c, [0, 1], [2], ["tanh"], ["sum"]) == text
+    with pytest.raises(FlatneatError) as ei:
+        load_checkpoint(text.replace('"version":1', '"version":2'))
+    assert ei.value.code == "version_unsupported"
+    with pytest.raises(FlatneatError) as ei:
+        load_checkpoint(text.replace("flatneat-b200-checkpoint", "other"))
+    assert ei.value.code == "parse_error"
