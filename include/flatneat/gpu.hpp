@@ -12,7 +12,10 @@
 // paper_2504_08339_b200/libflatneat_b200.so.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <functional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -164,6 +167,8 @@ class Context {
   }
 
   fnb_ctx* handle() { return ctx_; }
+  // a nonzero ABI status as flatneat::Error with the reference's Errc and text
+  void rethrow(int st) { check(st); }
 
  private:
   // the flat arrays must hold pop_size genomes of this context's limits
@@ -185,6 +190,131 @@ class Context {
   GenomeLimits limits_;
   std::vector<int> in_, out_;
   fnb_ctx* ctx_ = nullptr;
+};
+
+// SPEC's evolution module on the device: the population,
+// species table and innovation counter stay in HBM.  NeatConfig is SPEC-only
+// (the reference has no type for it), so the C struct is used as is.
+struct RunStats {
+  int generation = 0;
+  double best = 0, mean = 0, std = 0;
+  int best_index = -1;
+  std::vector<int> species_sizes;  // one entry per species
+  double elapsed_ms = 0;
+};
+
+struct EvolveResult {
+  GenomeTensors best;      // pop[argmax(fit)] of the last evaluated generation
+  double fitness = 0;
+  std::vector<RunStats> stats;
+};
+
+// Checkpoint of everything a generation step reads (fnb_evolver_get_state).
+struct EvolverState {
+  fnb_run_state state{};
+  PopulationTensors representatives;
+  PopulationTensors population;
+};
+
+class Evolver {
+ public:
+  Evolver(Context& ctx, const fnb_neat_config& cfg, std::uint64_t seed, GenomeLimits limits,
+          std::vector<int> input_keys, std::vector<int> output_keys)
+      : ctx_(ctx), cfg_(cfg), limits_(limits), in_(std::move(input_keys)), out_(std::move(output_keys)) {
+    if (const int st = fnb_evolver_create(ctx_.handle(), &cfg_, seed, &ev_)) ctx_.rethrow(st);
+  }
+  ~Evolver() { fnb_evolver_destroy(ev_); }
+  Evolver(const Evolver&) = delete;
+  Evolver& operator=(const Evolver&) = delete;
+
+  void init_population() { ctx_.rethrow(fnb_evolver_init_population(ev_)); }
+
+  PopulationTensors population() {
+    PopulationTensors p = empty(cfg_.pop_size);
+    ctx_.rethrow(fnb_evolver_get_population(ev_, p.pop_nodes.data(), p.pop_conns.data()));
+    return p;
+  }
+  // loads a population; the innovation counter moves above its largest key
+  void set_population(const PopulationTensors& p) {
+    if (p.pop_size != cfg_.pop_size || p.limits.max_nodes != limits_.max_nodes ||
+        p.limits.max_conns != limits_.max_conns)
+      raise(Errc::shape_mismatch, "population does not match the evolver");
+    ctx_.rethrow(fnb_evolver_set_population(ev_, p.pop_nodes.data(), p.pop_conns.data()));
+    int top = 0;
+    for (std::size_t i = 0; i < p.pop_nodes.size(); i += kNodeCols)
+      if (!std::isnan(p.pop_nodes[i])) top = std::max(top, int(p.pop_nodes[i]) + 1);
+    int gen = 0, nk = 0;
+    ctx_.rethrow(fnb_evolver_state(ev_, &gen, &nk));
+    ctx_.rethrow(fnb_evolver_set_next_key(ev_, std::max(top, nk)));
+  }
+
+  // evolve(problem, cfg, key) on a func-fit / xor dataset
+  EvolveResult evolve(std::span<const double> inputs, std::span<const double> targets, int batch,
+                      double fitness_target, int generation_limit, int fitness_kind = FNB_FIT_NEG_MSE,
+                      double offset = 0.0, const std::function<bool(const RunStats&)>& on_generation = {}) {
+    if (int(inputs.size()) != batch * int(in_.size()) || int(targets.size()) != batch * int(out_.size()))
+      raise(Errc::shape_mismatch, "input / target matrix is not batch x num_inputs / num_outputs");
+    struct Ctx {
+      std::vector<RunStats>* out;
+      const std::function<bool(const RunStats&)>* cb;
+    };
+    EvolveResult r{GenomeTensors(limits_, in_, out_), 0.0, {}};
+    Ctx c{&r.stats, &on_generation};
+    auto thunk = [](void* user, const fnb_run_stats* s) -> int {
+      auto* c = static_cast<Ctx*>(user);
+      RunStats rs;
+      rs.generation = s->generation;
+      rs.best = s->best;
+      rs.mean = s->mean;
+      rs.std = s->std;
+      rs.best_index = s->best_index;
+      rs.species_sizes.assign(s->species_size, s->species_size + s->species_count);
+      rs.elapsed_ms = s->elapsed_ms;
+      c->out->push_back(rs);
+      return (*c->cb && (*c->cb)(c->out->back())) ? 1 : 0;
+    };
+    int gens = 0;
+    ctx_.rethrow(fnb_evolve(ev_, inputs.data(), targets.data(), batch, fitness_kind, offset, fitness_target,
+                            generation_limit, thunk, &c, r.best.nodes.data(), r.best.conns.data(), &r.fitness, &gens));
+    return r;
+  }
+
+  EvolverState save() {
+    EvolverState s;
+    s.representatives = empty(32);
+    ctx_.rethrow(fnb_evolver_get_state(ev_, &s.state, s.representatives.pop_nodes.data(),
+                                       s.representatives.pop_conns.data()));
+    s.representatives.pop_size = s.state.species_count;
+    s.representatives.pop_nodes.resize(std::size_t(s.state.species_count) * limits_.max_nodes * kNodeCols);
+    s.representatives.pop_conns.resize(std::size_t(s.state.species_count) * limits_.max_conns * kConnCols);
+    s.population = population();
+    return s;
+  }
+  void restore(const EvolverState& s) {
+    ctx_.rethrow(fnb_evolver_set_population(ev_, s.population.pop_nodes.data(), s.population.pop_conns.data()));
+    ctx_.rethrow(fnb_evolver_set_state(ev_, &s.state, s.representatives.pop_nodes.data(),
+                                       s.representatives.pop_conns.data()));
+  }
+
+  fnb_evolver* handle() { return ev_; }
+
+ private:
+  PopulationTensors empty(int n) const {
+    PopulationTensors p;
+    p.pop_size = n;
+    p.limits = limits_;
+    p.input_keys = in_;
+    p.output_keys = out_;
+    p.pop_nodes.assign(std::size_t(n) * limits_.max_nodes * kNodeCols, kNaN);
+    p.pop_conns.assign(std::size_t(n) * limits_.max_conns * kConnCols, kNaN);
+    return p;
+  }
+
+  Context& ctx_;
+  fnb_neat_config cfg_;
+  GenomeLimits limits_;
+  std::vector<int> in_, out_;
+  fnb_evolver* ev_ = nullptr;
 };
 
 }  // namespace flatneat::gpu

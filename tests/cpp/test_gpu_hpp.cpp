@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -176,6 +177,52 @@ int main() {
       threw = e.code() == Errc::empty_dataset;
     }
     if (!threw) { std::printf("empty dataset accepted\n"); ++fails; }
+  }
+
+  // the evolver wrapper: evolve() with RunStats, save / restore continuing bit for bit
+  {
+    const GenomeLimits el{20, 60};
+    gpu::Context ectx(el, {0, 1, 2}, {3}, s);
+    fnb_neat_config nc{};
+    nc.pop_size = 200;
+    nc.max_species = 6;
+    nc.compatibility_threshold = 0.8;
+    nc.species_elitism = 2;
+    nc.max_stagnation = 15;
+    nc.genome_elitism = 2;
+    nc.survival_threshold = 0.2;
+    nc.spawn_number_change_rate = 0.5;
+    nc.output_activation = 0;
+    nc.mutation = fnb_mutation_config{0.3, 0.05, 0.5, 0.05, {0.0, 1.0, 0.5, 0.7, 0.1}, {1.0, 0.0, 0.0, 0.0, 0.0},
+                                      {0.0, 1.0, 0.5, 0.8, 0.1}, 0.0, 0.0};
+    nc.distance = fnb_distance_config{1.0, 0.5};
+    std::vector<double> ex, ey;
+    for (int b = 0; b < 32; ++b) {
+      double t = 0;
+      for (int i = 0; i < 3; ++i) { ex.push_back(stream.uniform(-1, 1)); t += ex.back(); }
+      ey.push_back(std::tanh(t));
+    }
+    gpu::Evolver full(ectx, nc, 77, el, {0, 1, 2}, {3});
+    full.init_population();
+    const auto all = full.evolve(ex, ey, 32, std::numeric_limits<double>::infinity(), 12);
+    gpu::Evolver part(ectx, nc, 77, el, {0, 1, 2}, {3});
+    part.init_population();
+    part.evolve(ex, ey, 32, std::numeric_limits<double>::infinity(), 6);
+    const gpu::EvolverState st = part.save();
+    gpu::Evolver resumed(ectx, nc, 1, el, {0, 1, 2}, {3});
+    resumed.restore(st);
+    const auto rest = resumed.evolve(ex, ey, 32, std::numeric_limits<double>::infinity(), 6);
+    if (all.stats.size() != 12 || rest.stats.size() != 6) ++fails;
+    for (std::size_t g = 0; g < rest.stats.size() && g + 6 < all.stats.size(); ++g) {
+      const auto &a = all.stats[g + 6], &b = rest.stats[g];
+      if (a.generation != b.generation || a.best != b.best || a.mean != b.mean || a.best_index != b.best_index ||
+          a.species_sizes != b.species_sizes) { std::printf("resumed generation %zu differs\n", g); ++fails; }
+    }
+    if (!(all.best == rest.best) || !same_bits(full.population().pop_nodes, resumed.population().pop_nodes) ||
+        !same_bits(full.population().pop_conns, resumed.population().pop_conns)) {
+      std::printf("resumed population differs\n");
+      ++fails;
+    }
   }
 
   std::printf(fails ? "gpu.hpp parity FAILED (%d)\n" : "gpu.hpp parity ok\n", fails);
