@@ -305,6 +305,65 @@ int fnb_evolver_step(fnb_evolver* ev);
  * into the next population buffer), the ranks all-gather the next buffer
  * (fnb_evolver_next_population), and every rank calls step_commit.  Slots
  * are independent, so the result equals fnb_evolver_step bit for bit. */
+/* ---- the step sharded over ranks (distributed.py) -------------
+ * Rank r of `world` owns genomes [bounds[r], bounds[r+1]) of the population
+ * (evaluation, speciation distances, its children); the population buffers
+ * keep global genome indices.  The caller runs the phases in order and, in
+ * between, the collectives on the buffers fnb_evolver_shard_buffers names
+ * (all exact: integer sums, MIN / MAX of integers or order-preserving bits,
+ * broadcasts and all-gathers of bits), on the evolver's stream:
+ *   all-gather fitness[lo,hi) -> fitness (each rank evaluates its shard)
+ *   BEGIN                       first match against the old representatives
+ *   repeat while species < max_species:
+ *     MIN_UNASSIGNED            -> all-reduce MIN min_unassigned; f = its value
+ *                                  (stop when INT_MAX); j = species count
+ *     FOUND(a = f, b = j)       the owner of f writes representative slot j
+ *                               -> broadcast rep slot j from f's owner
+ *     JOIN(b = j)               commit species j, join the shard's genomes
+ *   ASSIGN_REST                 nearest overflow -> all-reduce MIN rep_dmin
+ *   REP_ARGMIN                  -> all-reduce MIN rep_argmin
+ *   REP_STAGE                   -> all-reduce SUM rep_stage (u64 words)
+ *   REP_COMMIT                  -> all-reduce SUM species_size
+ *   COMPACT                     -> all-reduce MAX species_max
+ *   STAGNATION                  -> all-reduce SUM rank_sum, rank_count;
+ *                                  all-gather species_of[lo,hi) -> species_of
+ *   SELECT(out = counts[world]) parents each rank holds (synchronises);
+ *                               M = max(counts)
+ *   PACK(a = M)                 -> all-gather send_* (M genomes) -> pool_*
+ *   BACK(a = M)                 the shard's children -> all-reduce MIN first_bad
+ *   fnb_evolver_step_commit
+ * With world = 1 the sequence equals fnb_evolver_step bit for bit. */
+enum fnb_shard_phase {
+  FNB_SHARD_BEGIN = 0, FNB_SHARD_MIN_UNASSIGNED, FNB_SHARD_FOUND, FNB_SHARD_JOIN, FNB_SHARD_ASSIGN_REST,
+  FNB_SHARD_REP_ARGMIN, FNB_SHARD_REP_STAGE, FNB_SHARD_REP_COMMIT, FNB_SHARD_COMPACT, FNB_SHARD_STAGNATION,
+  FNB_SHARD_SELECT, FNB_SHARD_PACK, FNB_SHARD_BACK
+};
+typedef struct fnb_shard_buffers {
+  int* min_unassigned;              /* 1                     MIN  */
+  unsigned long long* rep_dmin;     /* 32                    MIN  */
+  int* rep_argmin;                  /* 32                    MIN  */
+  unsigned long long* rep_stage;    /* rep_stage_words       SUM  */
+  size_t rep_stage_words;
+  int* species_size;                /* 32                    SUM  */
+  unsigned long long* species_max;  /* 32                    MAX  */
+  long long* rank_sum;              /* 32                    SUM  */
+  int* rank_count;                  /* 32                    SUM  */
+  int* first_bad;                   /* 1                     MIN  */
+  double* fitness;                  /* pop_size              all-gather */
+  int* species_of;                  /* pop_size              all-gather */
+  double* rep_nodes;                /* 32 genomes            broadcast of one slot */
+  double* rep_conns;
+  double* send_nodes;               /* M genomes (after PACK) */
+  double* send_conns;
+  double* pool_nodes;               /* world x M genomes     all-gather of send_* */
+  double* pool_conns;
+} fnb_shard_buffers;
+int fnb_evolver_shard_init(fnb_evolver* ev, int world, const int* bounds);
+/* species count before the next step (host mirror; no synchronisation) */
+int fnb_evolver_host_species(fnb_evolver* ev);
+int fnb_evolver_shard_buffers(fnb_evolver* ev, fnb_shard_buffers* out);
+int fnb_evolver_shard_phase(fnb_evolver* ev, int phase, int rank, int a, int b, int* out);
+
 /* explain_invalid over the current population: first_invalid = lowest invalid
  * genome or -1; an invalid one also returns 1 + FNB_E_CORRUPT_ROW with the
  * reference's explanation in fnb_last_error */

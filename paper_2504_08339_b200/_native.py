@@ -65,6 +65,15 @@ class fnb_run_stats(C.Structure):
                 ("elapsed_ms", C.c_double)]
 
 
+class fnb_shard_buffers(C.Structure):
+    _fields_ = [("min_unassigned", C.c_void_p), ("rep_dmin", C.c_void_p), ("rep_argmin", C.c_void_p),
+                ("rep_stage", C.c_void_p), ("rep_stage_words", C.c_size_t), ("species_size", C.c_void_p),
+                ("species_max", C.c_void_p), ("rank_sum", C.c_void_p), ("rank_count", C.c_void_p),
+                ("first_bad", C.c_void_p), ("fitness", C.c_void_p), ("species_of", C.c_void_p),
+                ("rep_nodes", C.c_void_p), ("rep_conns", C.c_void_p), ("send_nodes", C.c_void_p),
+                ("send_conns", C.c_void_p), ("pool_nodes", C.c_void_p), ("pool_conns", C.c_void_p)]
+
+
 # typedef int (*fnb_run_stats_fn)(void* user, const fnb_run_stats* stats)
 RUN_STATS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(fnb_run_stats))
 
@@ -103,6 +112,10 @@ SIGNATURES = {
     "fnb_evolver_get_state": (C.c_int, [VP, C.POINTER(fnb_run_state), DP, DP]),
     "fnb_evolver_set_state": (C.c_int, [VP, C.POINTER(fnb_run_state), DP, DP]),
     "fnb_evolver_run_mode": (C.c_int, [VP]),
+    "fnb_evolver_host_species": (C.c_int, [VP]),
+    "fnb_evolver_shard_init": (C.c_int, [VP, C.c_int, IP]),
+    "fnb_evolver_shard_buffers": (C.c_int, [VP, C.POINTER(fnb_shard_buffers)]),
+    "fnb_evolver_shard_phase": (C.c_int, [VP, C.c_int, C.c_int, C.c_int, C.c_int, IP]),
     "fnb_evolve": (C.c_int, [VP, DP, DP, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, VP, VP, DP, DP, DP,
                              C.POINTER(C.c_int)]),
     "fnb_mutate_d": (C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.POINTER(fnb_mutation_config), VP, VP, VP, VP]),

@@ -141,15 +141,17 @@ __global__ void k_spec_begin(SpeciesDev* sd) {
   for (int j = 0; j <= kMaxSpecies; ++j) sd->rcand[j] = INT_MAX;
   sd->first_bad = INT_MAX;
   for (int j = 0; j < kMaxSpecies; ++j) {
-    sd->dmin[j] = ~0ull;
+    sd->dmin[j] = 0x7fffffffffffffffull;  // above every distance bits, and positive as int64 (sharded MIN)
     sd->argmin[j] = INT_MAX;
     sd->size[j] = 0;
   }
 }
 
-__global__ void k_assign_first(const double* __restrict__ d, int P, int S_old, double th, int* species_of) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
+// Per-genome kernels of the step take a genome range [lo, hi): the whole
+// population in one process, a rank's shard in the sharded step.
+__global__ void k_assign_first(const double* __restrict__ d, int lo, int hi, int S_old, double th, int* species_of) {
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi) return;
   int a = -1;
   for (int j = 0; j < S_old; ++j)
     if (d[size_t(i) * S_old + j] < th) { a = j; break; }
@@ -246,9 +248,10 @@ __global__ void k_desc_from_asc(const unsigned long long* __restrict__ keys, con
   out[(P - a) + (i - lo)] = idx[i];
 }
 
-__global__ void k_nearest(const double* __restrict__ d, int P, int stride, const SpeciesDev* sd, int* species_of) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P || species_of[i] >= 0) return;
+__global__ void k_nearest(const double* __restrict__ d, int lo, int hi, int stride, const SpeciesDev* sd,
+                          int* species_of) {
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi || species_of[i] >= 0) return;
   int best = 0;
   double bd = 0.0;
   for (int j = 0; j < sd->count; ++j) {
@@ -258,10 +261,10 @@ __global__ void k_nearest(const double* __restrict__ d, int P, int stride, const
   species_of[i] = best;
 }
 
-__global__ void k_rep_min(const double* __restrict__ d, int P, int S_old, const int* species_of, SpeciesDev* sd,
-                          int pass) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
+__global__ void k_rep_min(const double* __restrict__ d, int lo, int hi, int S_old, const int* species_of,
+                          SpeciesDev* sd, int pass) {
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi) return;
   const int j = species_of[i];
   if (j < 0 || j >= S_old) return;
   const unsigned long long b = (unsigned long long)__double_as_longlong(d[size_t(i) * S_old + j]);  // d >= 0
@@ -285,12 +288,12 @@ __global__ void k_rep_copy(const SpeciesDev* sd, const double* pn, const double*
 // Per-species integer reductions are aggregated per CTA in shared memory
 // first (a few species, thousands of genomes: global same-address atomics
 // serialise); integer adds and max are order-independent, so no bit moves.
-__global__ void k_sizes(const int* species_of, int P, SpeciesDev* sd) {
+__global__ void k_sizes(const int* species_of, int lo, int hi, SpeciesDev* sd) {
   __shared__ int s_n[kMaxSpecies];
   for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x) s_n[t] = 0;
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P && species_of[i] >= 0) atomicAdd(&s_n[species_of[i]], 1);
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < hi && species_of[i] >= 0) atomicAdd(&s_n[species_of[i]], 1);
   __syncthreads();
   for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x)
     if (s_n[t]) atomicAdd(&sd->size[t], s_n[t]);
@@ -334,21 +337,21 @@ __global__ void k_apply_compaction(SpeciesDev* sd, double* rep_n, double* rep_c,
   }
 }
 
-__global__ void k_remap(int* species_of, int P, const SpeciesDev* sd) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P && species_of[i] >= 0) species_of[i] = sd->remap[species_of[i]];
+__global__ void k_remap(int* species_of, int lo, int hi, const SpeciesDev* sd) {
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < hi && species_of[i] >= 0) species_of[i] = sd->remap[species_of[i]];
 }
 
 // ---- update_stagnation (oracle E3) --------------------------------------------------
 __global__ void k_stag_begin(SpeciesDev* sd) {
   for (int j = 0; j < kMaxSpecies; ++j) sd->mxbits[j] = 0ull;
 }
-__global__ void k_species_max(const double* fitness, const int* species_of, int P, SpeciesDev* sd) {
+__global__ void k_species_max(const double* fitness, const int* species_of, int lo, int hi, SpeciesDev* sd) {
   __shared__ unsigned long long s_mx[kMaxSpecies];
   for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x) s_mx[t] = 0ull;
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P && species_of[i] >= 0) atomicMax(&s_mx[species_of[i]], ordered_bits(fitness[i]));
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < hi && species_of[i] >= 0) atomicMax(&s_mx[species_of[i]], ordered_bits(fitness[i]));
   __syncthreads();
   for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x)
     if (s_mx[t]) atomicMax(&sd->mxbits[t], s_mx[t]);
@@ -379,9 +382,9 @@ __global__ void k_stagnation(SpeciesDev* sd, int species_elitism, int max_stagna
   }
   for (int j = 0; j < S; ++j) sd->remap[j] = (!prot[j] && sd->stag[j] > max_stagnation) ? -1 : 1;
 }
-__global__ void k_remap_or_drop(int* species_of, int P, const SpeciesDev* sd) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P && species_of[i] >= 0) species_of[i] = sd->remap[species_of[i]];
+__global__ void k_remap_or_drop(int* species_of, int lo, int hi, const SpeciesDev* sd) {
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < hi && species_of[i] >= 0) species_of[i] = sd->remap[species_of[i]];
 }
 
 // ---- compute_spawn_counts (oracle E4) ------------------------------------------------
@@ -396,7 +399,7 @@ __global__ void k_fit_keys(const double* fitness, int P, unsigned long long* asc
 // mid-ranks (oracle E4): position r of the ascending sort lies in the tie
 // group [lo, hi) of its key; 2 * rank = lo + hi - 1, an exact integer
 __global__ void k_rank_sums(const unsigned long long* __restrict__ sorted_keys, const int* sorted_idx, int P,
-                            const int* species_of, SpeciesDev* sd) {
+                            const int* species_of, int lo, int hi, SpeciesDev* sd) {
   __shared__ unsigned long long s_sum[kMaxSpecies];
   __shared__ int s_cnt[kMaxSpecies];
   for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x) {
@@ -405,8 +408,9 @@ __global__ void k_rank_sums(const unsigned long long* __restrict__ sorted_keys, 
   }
   __syncthreads();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < P) {
-    const int j = species_of[sorted_idx[r]];
+  const int gi = r < P ? sorted_idx[r] : -1;
+  if (r < P && gi >= lo && gi < hi) {  // this process's genomes; ranks are over the whole population
+    const int j = species_of[gi];
     if (j >= 0) {
       const unsigned long long k = sorted_keys[r];
       int a = 0, b = r;  // lo = first position with key >= k
@@ -642,6 +646,143 @@ cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* ke
                                 int* d_status, void* scratch, size_t scratch_bytes, const int* d_new_key,
                                 cudaStream_t st, long long* launches);
 
+
+// ---- the step sharded over ranks (distributed.py ShardedEvolution) ----------------
+// Rank r owns genomes [lo, hi) of full-size buffers (global genome indices
+// everywhere).  The kernels below are the rank-local parts of speciate /
+// stagnation / spawn / reproduce; the collectives between them (all-reduce
+// MIN / MAX / SUM of exact integers or order-preserving bits, broadcast of a
+// founder, all-gathers of fitness, species ids and parent genomes) run in the
+// caller, so the result is the one-process step bit for bit.
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
+__global__ void k_min_unassigned(const int* species_of, int lo, int hi, int* out) {
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool u = i < hi && species_of[i] < 0;
+  const unsigned b = __ballot_sync(0xffffffffu, u);
+  if (b && (threadIdx.x & 31) == __ffs(b) - 1) atomicMin(out, i);
+}
+
+// the founder's owner: representative slot j <- genome f, f joins species j
+__global__ void k_found_copy(const double* pn, const double* pc, int f, int j, double* rep_n, double* rep_c,
+                             int* species_of, int N, int C) {
+  const size_t gn = size_t(N) * kNodeCols, gc = size_t(C) * kConnCols;
+  for (size_t i = threadIdx.x; i < gn; i += blockDim.x) rep_n[size_t(j) * gn + i] = pn[size_t(f) * gn + i];
+  for (size_t i = threadIdx.x; i < gc; i += blockDim.x) rep_c[size_t(j) * gc + i] = pc[size_t(f) * gc + i];
+  if (threadIdx.x == 0) species_of[f] = j;
+}
+
+// every rank: species j exists (oracle E2 founding), as k_found_rounds commits it
+__global__ void k_found_commit(SpeciesDev* sd, int j) {
+  sd->count = j + 1;
+  sd->id[j] = sd->next_id++;
+  sd->best[j] = -INFINITY;
+  sd->stag[j] = 0;
+}
+
+__global__ void k_join(const double* __restrict__ d, int lo, int hi, double th, int j, int* species_of) {
+  const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < hi && species_of[i] < 0 && d[i] < th) species_of[i] = j;
+}
+
+// new representative candidates: slot j holds genome argmin[j]'s bits on
+// its owner and zeros elsewhere, so an integer SUM over ranks is a gather
+__global__ void k_rep_stage(const SpeciesDev* sd, const double* pn, const double* pc, int lo, int hi,
+                            unsigned long long* stage, int N, int C) {
+  const int j = blockIdx.x;
+  const size_t gn = size_t(N) * kNodeCols, gc = size_t(C) * kConnCols;
+  const int m = sd->argmin[j];
+  const bool mine = m != INT_MAX && m >= lo && m < hi;
+  unsigned long long* dst = stage + size_t(j) * (gn + gc);
+  const unsigned long long* a = reinterpret_cast<const unsigned long long*>(pn) + (mine ? size_t(m) * gn : 0);
+  const unsigned long long* b = reinterpret_cast<const unsigned long long*>(pc) + (mine ? size_t(m) * gc : 0);
+  for (size_t i = threadIdx.x; i < gn; i += blockDim.x) dst[i] = mine ? a[i] : 0ull;
+  for (size_t i = threadIdx.x; i < gc; i += blockDim.x) dst[gn + i] = mine ? b[i] : 0ull;
+}
+__global__ void k_rep_commit(const SpeciesDev* sd, const unsigned long long* stage, double* rep_n, double* rep_c,
+                             int N, int C) {
+  const int j = blockIdx.x;
+  if (j >= sd->old_count || sd->argmin[j] == INT_MAX) return;
+  const size_t gn = size_t(N) * kNodeCols, gc = size_t(C) * kConnCols;
+  const unsigned long long* src = stage + size_t(j) * (gn + gc);
+  unsigned long long* rn = reinterpret_cast<unsigned long long*>(rep_n) + size_t(j) * gn;
+  unsigned long long* rc = reinterpret_cast<unsigned long long*>(rep_c) + size_t(j) * gc;
+  for (size_t i = threadIdx.x; i < gn; i += blockDim.x) rn[i] = src[i];
+  for (size_t i = threadIdx.x; i < gc; i += blockDim.x) rc[i] = src[gn + i];
+}
+
+// parents: genomes some slot reads (elites are self-crossovers)
+__global__ void k_need(const int* fit_idx, const int* oth_idx, int P, int* need) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < P) {
+    need[fit_idx[c]] = 1;
+    need[oth_idx[c]] = 1;
+  }
+}
+// exclusive scan of need[P] into prefix[P + 1] (one CTA, contiguous runs per thread)
+__global__ void __launch_bounds__(1024) k_scan_need(const int* need, int P, int* prefix) {
+  __shared__ int warp_sums[32];
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int per = (P + nt - 1) / nt;
+  const int lo = min(P, t * per), hi = min(P, lo + per);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i) cnt += need[i];
+  const int lane = t & 31, w = t >> 5;
+  int incl = cnt;
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) warp_sums[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < (nt >> 5) ? warp_sums[lane] : 0;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += u;
+    }
+    warp_sums[lane] = v;
+  }
+  __syncthreads();
+  int run = (w > 0 ? warp_sums[w - 1] : 0) + incl - cnt;
+  for (int i = lo; i < hi; ++i) {
+    prefix[i] = run;
+    run += need[i];
+  }
+  if (t == nt - 1) prefix[P] = run;
+}
+__global__ void k_need_counts(const int* prefix, const int* bounds, int G, int* counts) {
+  const int r = threadIdx.x;
+  if (r < G) counts[r] = prefix[bounds[r + 1]] - prefix[bounds[r]];
+}
+// this rank's needed genomes, in index order, into the send buffers
+__global__ void k_pack(const int* need, const int* prefix, int lo, int hi, const double* pn, const double* pc,
+                       double* send_n, double* send_c, int N, int C) {
+  const int i = lo + blockIdx.x;
+  if (i >= hi || !need[i]) return;
+  const size_t gn = size_t(N) * kNodeCols, gc = size_t(C) * kConnCols;
+  const size_t d = size_t(prefix[i] - prefix[lo]);
+  const double2* a = reinterpret_cast<const double2*>(pn + size_t(i) * gn);
+  const double2* b = reinterpret_cast<const double2*>(pc + size_t(i) * gc);
+  double2* x = reinterpret_cast<double2*>(send_n + d * gn);
+  double2* y = reinterpret_cast<double2*>(send_c + d * gc);
+  for (size_t k = threadIdx.x; k < gn / 2; k += blockDim.x) x[k] = a[k];
+  for (size_t k = threadIdx.x; k < gc / 2; k += blockDim.x) y[k] = b[k];
+}
+// parent indices -> positions in the gathered pool [G][M] genomes
+__global__ void k_remap_parents(const int* fit_idx, const int* oth_idx, int P, const int* prefix, const int* bounds,
+                                int G, int M, int* fitp, int* othp) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P) return;
+  auto pos = [&](int g) {
+    int r = 0;
+    while (r + 1 < G && bounds[r + 1] <= g) ++r;
+    return r * M + (prefix[g] - prefix[bounds[r]]);
+  };
+  fitp[c] = pos(fit_idx[c]);
+  othp[c] = pos(oth_idx[c]);
+}
+
 struct Evolver {
   NeatCfg cfg;
   fnb_mutation_config mut;
@@ -725,6 +866,7 @@ struct Evolver {
 
   void release() {
     release_graphs();
+    shard_release();
     void* ps[] = {pn[0], pn[1], pc[0], pc[1], fitness, rep_n, rep_c, dmat, species_of, sd,
                   kasc, kdesc, ktmp, idx, idx_sorted, idx_tmp, skey, skey_tmp, fit_idx, oth_idx, status, next_key,
                   xkeys, mkeys, active, cub_tmp, scratch};
@@ -871,7 +1013,7 @@ struct Evolver {
                                  dist.compatibility_homologous, dmat, scratch, scratch_bytes, nullptr, nullptr, st);
       if (e != cudaSuccess) return e;
     }
-    k_assign_first<<<B, T, 0, st>>>(dmat, P, S_old, th, species_of);
+    k_assign_first<<<B, T, 0, st>>>(dmat, 0, P, S_old, th, species_of);
     *launches += 2 + (S_old > 0 ? kDistanceLaunches : 0);
     if (S_old < cfg.max_species) {
       e = launch_found_rounds(S_old, n, c);
@@ -881,22 +1023,22 @@ struct Evolver {
                                dist.compatibility_homologous, dmat + size_t(P) * S_old, scratch, scratch_bytes,
                                species_of, nullptr, st);
     if (e != cudaSuccess) return e;
-    k_nearest<<<B, T, 0, st>>>(dmat + size_t(P) * S_old, P, cfg.max_species, sd, species_of);
+    k_nearest<<<B, T, 0, st>>>(dmat + size_t(P) * S_old, 0, P, cfg.max_species, sd, species_of);
     if (S_old > 0) {
-      k_rep_min<<<B, T, 0, st>>>(dmat, P, S_old, species_of, sd, 0);
-      k_rep_min<<<B, T, 0, st>>>(dmat, P, S_old, species_of, sd, 1);
+      k_rep_min<<<B, T, 0, st>>>(dmat, 0, P, S_old, species_of, sd, 0);
+      k_rep_min<<<B, T, 0, st>>>(dmat, 0, P, S_old, species_of, sd, 1);
       k_rep_copy<<<S_old, 256, 0, st>>>(sd, n, c, rep_n, rep_c, N, C);
     }
-    k_sizes<<<B, T, 0, st>>>(species_of, P, sd);
+    k_sizes<<<B, T, 0, st>>>(species_of, 0, P, sd);
     k_mark_nonempty<<<1, 1, 0, st>>>(sd);
     k_apply_compaction<<<1, 256, 0, st>>>(sd, rep_n, rep_c, N, C);
-    k_remap<<<B, T, 0, st>>>(species_of, P, sd);
+    k_remap<<<B, T, 0, st>>>(species_of, 0, P, sd);
     // ---- update_stagnation
     k_stag_begin<<<1, 1, 0, st>>>(sd);
-    k_species_max<<<B, T, 0, st>>>(fitness, species_of, P, sd);
+    k_species_max<<<B, T, 0, st>>>(fitness, species_of, 0, P, sd);
     k_stagnation<<<1, 1, 0, st>>>(sd, cfg.species_elitism, cfg.max_stagnation);
     k_apply_compaction<<<1, 256, 0, st>>>(sd, rep_n, rep_c, N, C);
-    k_remap_or_drop<<<B, T, 0, st>>>(species_of, P, sd);
+    k_remap_or_drop<<<B, T, 0, st>>>(species_of, 0, P, sd);
     // ---- compute_spawn_counts: ranks by a stable ascending radix sort
     k_fit_keys<<<B, T, 0, st>>>(fitness, P, kasc, kdesc, idx);
     e = P <= kCountRankMax
@@ -904,7 +1046,7 @@ struct Evolver {
             : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
     if (e != cudaSuccess) return e;
     k_spawn_begin<<<1, 1, 0, st>>>(sd);
-    k_rank_sums<<<B, T, 0, st>>>(ktmp, idx_sorted, P, species_of, sd);
+    k_rank_sums<<<B, T, 0, st>>>(ktmp, idx_sorted, P, species_of, 0, P, sd);
     k_spawn<<<1, 1, 0, st>>>(sd, P, cfg.spawn_rate, cfg.genome_elitism);
     // ---- reproduce: members by (fitness desc, index asc), then by species
     k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp);
@@ -983,6 +1125,244 @@ struct Evolver {
   cudaError_t commit(int* host_error) {
     cudaError_t e = enqueue_advance();
     return e == cudaSuccess ? read_status_and_swap(host_error) : e;
+  }
+
+  // ---- the sharded step: buffers and phases (fnb_evolver_shard_phase) ----------------
+  int sh_world = 0;
+  std::vector<int> sh_bounds;                   // host copy, world + 1
+  int* d_bounds = nullptr;                      // device copy
+  int *need = nullptr, *prefix = nullptr, *counts = nullptr, *fitp = nullptr, *othp = nullptr, *min_u = nullptr;
+  double* dfound = nullptr;
+  unsigned long long* stage = nullptr;
+  double *send_n = nullptr, *send_c = nullptr, *pool_n = nullptr, *pool_c = nullptr;
+  size_t send_cap = 0, pool_cap = 0;            // genomes
+
+  cudaError_t shard_init(int world, const int* bounds) {
+    cudaError_t e = cudaSuccess;
+    auto A = [&](auto** p, size_t bytes) {
+      if (e == cudaSuccess && !*p) e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    };
+    A(&need, 4 * size_t(P));
+    A(&prefix, 4 * (size_t(P) + 1));
+    A(&fitp, 4 * size_t(P));
+    A(&othp, 4 * size_t(P));
+    A(&min_u, 16);
+    A(&dfound, 8 * size_t(P));
+    A(&stage, 8 * (gn() + gc()) * kMaxSpecies);
+    if (e == cudaSuccess && world != sh_world) {
+      if (d_bounds) cudaFree(d_bounds);
+      if (counts) cudaFree(counts);
+      d_bounds = nullptr;
+      counts = nullptr;
+      A(&d_bounds, 4 * (size_t(world) + 1));
+      A(&counts, 4 * size_t(world));
+    }
+    if (e != cudaSuccess) return e;
+    sh_world = world;
+    sh_bounds.assign(bounds, bounds + world + 1);
+    return cudaMemcpyAsync(d_bounds, bounds, 4 * (size_t(world) + 1), cudaMemcpyHostToDevice, st);
+  }
+  void shard_release() {
+    void* ps[] = {need, prefix, fitp, othp, min_u, dfound, stage, d_bounds, counts, send_n, send_c, pool_n, pool_c};
+    for (void* p : ps)
+      if (p) cudaFree(p);
+  }
+  cudaError_t ensure_genomes(double** pn_, double** pc_, size_t* cap, size_t n) {
+    if (n <= *cap) return cudaSuccess;
+    if (*pn_) cudaFree(*pn_);
+    if (*pc_) cudaFree(*pc_);
+    *pn_ = *pc_ = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(pn_), 8 * gn() * n);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(pc_), 8 * gc() * n);
+    if (e == cudaSuccess) *cap = n;
+    return e;
+  }
+
+  // phase 0: speciate begins -- first match against the old representatives
+  cudaError_t shard_begin(int lo, int hi) {
+    const int T = 256, B = (hi - lo + T - 1) / T;
+    const int S_old = host_species;
+    const double* n = pn[cur];
+    const double* c = pc[cur];
+    k_spec_begin<<<1, 1, 0, st>>>(sd);
+    ++*launches;
+    if (hi <= lo) return cudaGetLastError();
+    if (S_old > 0) {
+      cudaError_t e = launch_distance_masked(n + size_t(lo) * gn(), c + size_t(lo) * gc(), hi - lo, rep_n, rep_c, S_old,
+                                             N, C, dist.compatibility_disjoint, dist.compatibility_homologous,
+                                             dmat + size_t(lo) * S_old, scratch, scratch_bytes, nullptr, nullptr, st);
+      if (e != cudaSuccess) return e;
+      *launches += kDistanceLaunches;
+    }
+    k_assign_first<<<B, T, 0, st>>>(dmat, lo, hi, S_old, cfg.threshold, species_of);
+    ++*launches;
+    return cudaGetLastError();
+  }
+  // phase 1: lowest unassigned genome of this shard -> min_u[0] (INT_MAX none)
+  cudaError_t shard_min_unassigned(int lo, int hi) {
+    k_set_int<<<1, 1, 0, st>>>(min_u, INT_MAX);
+    if (hi > lo) k_min_unassigned<<<(hi - lo + 255) / 256, 256, 0, st>>>(species_of, lo, hi, min_u);
+    *launches += 1 + (hi > lo);
+    return cudaGetLastError();
+  }
+  // phase 2 (the founder's owner): representative slot j <- genome f
+  cudaError_t shard_found(int f, int j) {
+    k_found_copy<<<1, 256, 0, st>>>(pn[cur], pc[cur], f, j, rep_n, rep_c, species_of, N, C);
+    ++*launches;
+    return cudaGetLastError();
+  }
+  // phase 3 (every rank, after the broadcast of slot j): commit species j and
+  // join the shard's unassigned genomes within the threshold of its founder
+  cudaError_t shard_join(int lo, int hi, int j) {
+    k_found_commit<<<1, 1, 0, st>>>(sd, j);
+    ++*launches;
+    if (hi > lo) {
+      cudaError_t e = launch_distance_masked(pn[cur] + size_t(lo) * gn(), pc[cur] + size_t(lo) * gc(), hi - lo,
+                                             rep_n + size_t(j) * gn(), rep_c + size_t(j) * gc(), 1, N, C,
+                                             dist.compatibility_disjoint, dist.compatibility_homologous, dfound + lo,
+                                             scratch, scratch_bytes, species_of + lo, nullptr, st);
+      if (e != cudaSuccess) return e;
+      k_join<<<(hi - lo + 255) / 256, 256, 0, st>>>(dfound, lo, hi, cfg.threshold, j, species_of);
+      *launches += kDistanceLaunches + 1;
+    }
+    return cudaGetLastError();
+  }
+  // phase 4: nearest-representative overflow, then pass 0 of the new
+  // representative search (min distance bits per old species -> sd->dmin)
+  cudaError_t shard_assign_rest(int lo, int hi) {
+    const int T = 256, B = (hi - lo + T - 1) / T;
+    const int S_old = host_species;
+    if (hi <= lo) return cudaSuccess;
+    cudaError_t e = launch_distance_masked(pn[cur] + size_t(lo) * gn(), pc[cur] + size_t(lo) * gc(), hi - lo, rep_n,
+                                           rep_c, cfg.max_species, N, C, dist.compatibility_disjoint,
+                                           dist.compatibility_homologous,
+                                           dmat + size_t(P) * S_old + size_t(lo) * cfg.max_species, scratch,
+                                           scratch_bytes, species_of + lo, nullptr, st);
+    if (e != cudaSuccess) return e;
+    k_nearest<<<B, T, 0, st>>>(dmat + size_t(P) * S_old, lo, hi, cfg.max_species, sd, species_of);
+    *launches += kDistanceLaunches + 1;
+    if (S_old > 0) {
+      k_rep_min<<<B, T, 0, st>>>(dmat, lo, hi, S_old, species_of, sd, 0);
+      ++*launches;
+    }
+    return cudaGetLastError();
+  }
+  // phase 5: pass 1 (lowest index at the minimum -> sd->argmin)
+  cudaError_t shard_rep_argmin(int lo, int hi) {
+    const int S_old = host_species;
+    if (S_old > 0 && hi > lo) {
+      k_rep_min<<<(hi - lo + 255) / 256, 256, 0, st>>>(dmat, lo, hi, S_old, species_of, sd, 1);
+      ++*launches;
+    }
+    return cudaGetLastError();
+  }
+  // phase 6: stage the new representatives this shard owns (zeros elsewhere)
+  cudaError_t shard_rep_stage(int lo, int hi) {
+    const int S_old = host_species;
+    if (S_old > 0) {
+      k_rep_stage<<<S_old, 256, 0, st>>>(sd, pn[cur], pc[cur], lo, hi, stage, N, C);
+      ++*launches;
+    }
+    return cudaGetLastError();
+  }
+  // phase 7: commit the summed stage; species sizes of the shard (-> sd->size)
+  cudaError_t shard_rep_commit(int lo, int hi) {
+    const int S_old = host_species;
+    if (S_old > 0) {
+      k_rep_commit<<<S_old, 256, 0, st>>>(sd, stage, rep_n, rep_c, N, C);
+      ++*launches;
+    }
+    if (hi > lo) {
+      k_sizes<<<(hi - lo + 255) / 256, 256, 0, st>>>(species_of, lo, hi, sd);
+      ++*launches;
+    }
+    return cudaGetLastError();
+  }
+  // phase 8: drop empty species; species max fitness of the shard (-> sd->mxbits)
+  cudaError_t shard_compact(int lo, int hi) {
+    const int T = 256, B = (hi - lo + T - 1) / T;
+    k_mark_nonempty<<<1, 1, 0, st>>>(sd);
+    k_apply_compaction<<<1, 256, 0, st>>>(sd, rep_n, rep_c, N, C);
+    k_stag_begin<<<1, 1, 0, st>>>(sd);
+    *launches += 3;
+    if (hi > lo) {
+      k_remap<<<B, T, 0, st>>>(species_of, lo, hi, sd);
+      k_species_max<<<B, T, 0, st>>>(fitness, species_of, lo, hi, sd);
+      *launches += 2;
+    }
+    return cudaGetLastError();
+  }
+  // phase 9: stagnation (replicated); fitness ranks over the whole gathered
+  // vector, mid-rank sums of the shard's genomes (-> sd->rsum, sd->cnt)
+  cudaError_t shard_stagnation(int lo, int hi) {
+    const int T = 256, B = (P + T - 1) / T;
+    k_stagnation<<<1, 1, 0, st>>>(sd, cfg.species_elitism, cfg.max_stagnation);
+    k_apply_compaction<<<1, 256, 0, st>>>(sd, rep_n, rep_c, N, C);
+    if (hi > lo) k_remap_or_drop<<<(hi - lo + T - 1) / T, T, 0, st>>>(species_of, lo, hi, sd);
+    k_fit_keys<<<B, T, 0, st>>>(fitness, P, kasc, kdesc, idx);
+    cudaError_t e = P <= kCountRankMax
+                        ? launch_count_sort<unsigned long long>(kasc, nullptr, P, skey_tmp, ktmp, idx_sorted, st)
+                        : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
+    if (e != cudaSuccess) return e;
+    k_spawn_begin<<<1, 1, 0, st>>>(sd);
+    k_rank_sums<<<B, T, 0, st>>>(ktmp, idx_sorted, P, species_of, lo, hi, sd);
+    *launches += 8 + (hi > lo);
+    return cudaGetLastError();
+  }
+  // phase 10 (after the all-gather of species_of): spawn, members, parent
+  // selection for every slot, the parents' pool positions; counts[r] = the
+  // parents rank r holds
+  cudaError_t shard_select() {
+    const int T = 256, B = (P + T - 1) / T;
+    k_spawn<<<1, 1, 0, st>>>(sd, P, cfg.spawn_rate, cfg.genome_elitism);
+    k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp);
+    k_species_keys<<<B, T, 0, st>>>(idx_tmp, P, species_of, skey);
+    cudaError_t e = P <= kCountRankMax
+                        ? launch_count_sort<int>(skey, idx_tmp, P, skey_tmp, nullptr, idx_sorted, st)
+                        : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, skey, skey_tmp, idx_tmp, idx_sorted, P,
+                                                          0, 6, st);
+    if (e != cudaSuccess) return e;
+    const Key4 root1 = key_split(key_from_seed(seed), 1);
+    k_reproduce_plan<<<B, T, 0, st>>>(sd, idx_sorted, fitness, P, root1, cfg.genome_elitism, cfg.survival, fit_idx,
+                                      oth_idx, xkeys, mkeys, active);
+    e = cudaMemsetAsync(need, 0, 4 * size_t(P), st);
+    if (e != cudaSuccess) return e;
+    k_need<<<B, T, 0, st>>>(fit_idx, oth_idx, P, need);
+    k_scan_need<<<1, 1024, 0, st>>>(need, P, prefix);
+    k_need_counts<<<1, 32 * ((sh_world + 31) / 32), 0, st>>>(prefix, d_bounds, sh_world, counts);
+    *launches += 9;
+    return cudaGetLastError();
+  }
+  // phase 11: the shard's parents into the send buffers (M genomes each)
+  cudaError_t shard_pack(int lo, int hi, int M) {
+    cudaError_t e = ensure_genomes(&send_n, &send_c, &send_cap, size_t(std::max(M, 1)));
+    if (e == cudaSuccess) e = ensure_genomes(&pool_n, &pool_c, &pool_cap, size_t(std::max(M, 1)) * sh_world);
+    if (e != cudaSuccess) return e;
+    if (hi > lo) {
+      k_pack<<<hi - lo, 128, 0, st>>>(need, prefix, lo, hi, pn[cur], pc[cur], send_n, send_c, N, C);
+      ++*launches;
+    }
+    return cudaGetLastError();
+  }
+  // phase 12 (after the all-gather of the send buffers into the pool):
+  // node-split plans and innovation keys for ALL slots from the pool
+  // (replicated), then crossover + mutation of the shard's children
+  cudaError_t shard_back(int lo, int hi, int M) {
+    const int T = 256, B = (P + T - 1) / T;
+    k_remap_parents<<<B, T, 0, st>>>(fit_idx, oth_idx, P, prefix, d_bounds, sh_world, M, fitp, othp);
+    ++*launches;
+    cudaError_t e = launch_mutate_plan(pool_n, pool_c, fitp, mkeys, P, active, &mut, sh, next_key, scratch,
+                                       scratch_bytes, nullptr, st, launches);
+    if (e != cudaSuccess || hi <= lo) return e;
+    e = launch_crossover(pool_n, pool_c, fitp + lo, othp + lo, xkeys + 4 * size_t(lo), hi - lo, N, C,
+                         pn[cur ^ 1] + size_t(lo) * gn(), pc[cur ^ 1] + size_t(lo) * gc(), st);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    e = launch_mutate_apply(pn[cur ^ 1], pc[cur ^ 1], mkeys, P, lo, hi, active, &mut, sh, status, scratch,
+                            scratch_bytes, mutate_new_keys(), st, launches);
+    if (e != cudaSuccess) return e;
+    return enqueue_first_bad(lo, hi);
   }
 };
 
@@ -1808,3 +2188,90 @@ int fnb_evolve(fnb_evolver* ev, const double* inputs, const double* targets, int
 }  // extern "C"
 
 extern "C" int fnb_evolver_run_mode(fnb_evolver* ev) { return ev ? ev->run_mode : -1; }
+
+// =================================================================================
+// the step sharded over ranks: phases and the buffers the caller's collectives
+// reduce between them (include/flatneat_b200.h, distributed.py ShardedEvolution)
+// =================================================================================
+extern "C" {
+
+int fnb_evolver_host_species(fnb_evolver* ev) { return ev ? ev->ev.host_species : -1; }
+
+int fnb_evolver_shard_init(fnb_evolver* ev, int world, const int* bounds) {
+  fnb::Evolver& v = ev->ev;
+  if (world < 1 || !bounds || bounds[0] != 0 || bounds[world] != v.P)
+    return fnb_set_error(ev->ctx, FNB_E_CONFIG_ERROR, "shard bounds must split [0, pop_size)", -1);
+  for (int r = 0; r < world; ++r)
+    if (bounds[r + 1] < bounds[r]) return fnb_set_error(ev->ctx, FNB_E_CONFIG_ERROR, "shard bounds must ascend", r);
+  cudaSetDevice(ev->ctx->device);
+  EV_CK(v.shard_init(world, bounds));
+  return 0;
+}
+
+int fnb_evolver_shard_buffers(fnb_evolver* ev, fnb_shard_buffers* b) {
+  fnb::Evolver& v = ev->ev;
+  if (!b || !v.need) return fnb_set_error(ev->ctx, FNB_E_CONFIG_ERROR, "fnb_evolver_shard_init first", -1);
+  uint8_t* sd = reinterpret_cast<uint8_t*>(v.sd);
+  *b = fnb_shard_buffers{};
+  b->min_unassigned = v.min_u;
+  b->rep_dmin = reinterpret_cast<unsigned long long*>(sd + offsetof(fnb::SpeciesDev, dmin));
+  b->rep_argmin = reinterpret_cast<int*>(sd + offsetof(fnb::SpeciesDev, argmin));
+  b->rep_stage = v.stage;
+  b->rep_stage_words = (v.gn() + v.gc()) * fnb::kMaxSpecies;
+  b->species_size = reinterpret_cast<int*>(sd + offsetof(fnb::SpeciesDev, size));
+  b->species_max = reinterpret_cast<unsigned long long*>(sd + offsetof(fnb::SpeciesDev, mxbits));
+  b->rank_sum = reinterpret_cast<long long*>(sd + offsetof(fnb::SpeciesDev, rsum));
+  b->rank_count = reinterpret_cast<int*>(sd + offsetof(fnb::SpeciesDev, cnt));
+  b->first_bad = reinterpret_cast<int*>(sd + offsetof(fnb::SpeciesDev, first_bad));
+  b->fitness = v.fitness;
+  b->species_of = v.species_of;
+  b->rep_nodes = v.rep_n;
+  b->rep_conns = v.rep_c;
+  b->send_nodes = v.send_n;
+  b->send_conns = v.send_c;
+  b->pool_nodes = v.pool_n;
+  b->pool_conns = v.pool_c;
+  return 0;
+}
+
+int fnb_evolver_shard_phase(fnb_evolver* ev, int phase, int rank, int a, int b, int* out) {
+  fnb::Evolver& v = ev->ev;
+  fnb_ctx* ctx = ev->ctx;
+  if (!v.need || rank < 0 || rank >= v.sh_world)
+    return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "fnb_evolver_shard_init first / rank out of range", -1);
+  cudaSetDevice(ctx->device);
+  const int lo = v.sh_bounds[size_t(rank)], hi = v.sh_bounds[size_t(rank) + 1];
+  switch (phase) {
+    case FNB_SHARD_BEGIN: EV_CK(v.shard_begin(lo, hi)); break;
+    case FNB_SHARD_MIN_UNASSIGNED: EV_CK(v.shard_min_unassigned(lo, hi)); break;
+    case FNB_SHARD_FOUND:
+      if (a < 0 || a >= v.P || b < 0 || b >= v.cfg.max_species)
+        return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "founder / species slot out of range", a);
+      if (a >= lo && a < hi) EV_CK(v.shard_found(a, b));
+      break;
+    case FNB_SHARD_JOIN:
+      if (b < 0 || b >= v.cfg.max_species) return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "species slot out of range", b);
+      EV_CK(v.shard_join(lo, hi, b));
+      break;
+    case FNB_SHARD_ASSIGN_REST: EV_CK(v.shard_assign_rest(lo, hi)); break;
+    case FNB_SHARD_REP_ARGMIN: EV_CK(v.shard_rep_argmin(lo, hi)); break;
+    case FNB_SHARD_REP_STAGE: EV_CK(v.shard_rep_stage(lo, hi)); break;
+    case FNB_SHARD_REP_COMMIT: EV_CK(v.shard_rep_commit(lo, hi)); break;
+    case FNB_SHARD_COMPACT: EV_CK(v.shard_compact(lo, hi)); break;
+    case FNB_SHARD_STAGNATION: EV_CK(v.shard_stagnation(lo, hi)); break;
+    case FNB_SHARD_SELECT: {
+      EV_CK(v.shard_select());
+      if (out) {
+        EV_CK(cudaMemcpyAsync(out, v.counts, sizeof(int) * size_t(v.sh_world), cudaMemcpyDeviceToHost, v.st));
+        EV_CK(cudaStreamSynchronize(v.st));
+      }
+      break;
+    }
+    case FNB_SHARD_PACK: EV_CK(v.shard_pack(lo, hi, a)); break;
+    case FNB_SHARD_BACK: EV_CK(v.shard_back(lo, hi, a)); break;
+    default: return fnb_set_error(ctx, FNB_E_CONFIG_ERROR, "unknown shard phase", phase);
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -199,3 +199,157 @@ class DeviceShardBackend:
 
     def checksum(self) -> int:
         return self.ev.checksum()
+
+
+_I64_MIN = -(2 ** 63)
+
+
+class ShardedEvolution:
+    """The whole generation sharded over ranks (north star):
+    rank r owns genomes [lo, hi) -- it evaluates them, computes their
+    speciation distances and produces children [lo, hi) -- and the ranks
+    exchange only what the step reduces:
+
+    * the fitness vector (all-gather of FP64 shards);
+    * speciation: per founding round an all-reduce MIN of the lowest
+      unassigned genome and a broadcast of the founder from its owner; the
+      new representatives as MIN of (distance bits, index) and a SUM of
+      bit-staged genomes (zeros off the owner); species sizes (SUM);
+    * stagnation: species max fitness (MAX of order-preserving bits);
+    * spawn: per-species integer sums of 2 x mid-rank (SUM; ranks come from
+      the gathered fitness on every rank);
+    * reproduce: species ids (all-gather), then the selected parents
+      themselves (all-gather of each rank's parents, padded to the largest
+      count) -- children read their parents from that pool;
+    * the lowest failing child (MIN), so every rank raises together.
+
+    Every reduction is over integers or bit patterns, so the result equals the
+    one-process step bit for bit for any world size (the test runs the device
+    backend at world sizes 1 and 2).  Collectives run on the evolver's stream
+    (torch.cuda.stream context), NCCL on GPUs, gloo in tests."""
+
+    def __init__(self, evolver, X, Y, kind: int = FIT_NEG_MSE, offset: float = 0.0,
+                 group: Optional[dist.ProcessGroup] = None):
+        self.ev = evolver
+        self.X, self.Y, self.kind, self.offset = X, Y, kind, offset
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        P = evolver.cfg.pop_size
+        self.P = P
+        self.bounds = [shard_bounds(P, self.world, r)[0] for r in range(self.world)] + [P]
+        self.lo, self.hi = self.bounds[self.rank], self.bounds[self.rank + 1]
+        self.shard = max(self.bounds[r + 1] - self.bounds[r] for r in range(self.world))
+        evolver.shard_init(self.bounds)
+        self.buf = evolver.shard_buffers()
+        self.device = self.buf["fitness"].device
+        self.stream = torch.cuda.ExternalStream(evolver.stream_handle(), device=self.device)
+        L = evolver.engine.limits
+        self.gn, self.gc = L.max_nodes * 5, L.max_conns * 4
+        if self.world > 1:
+            pad = self.shard * self.world
+            self.g_fit = torch.empty(pad, dtype=torch.float64, device=self.device)
+            self.g_sp = torch.empty(pad, dtype=torch.int32, device=self.device)
+            idx = [r * self.shard + i for r in range(self.world) for i in range(self.bounds[r + 1] - self.bounds[r])]
+            self.unpad = torch.tensor(idx, dtype=torch.long, device=self.device)
+            self.l_fit = torch.empty(self.shard, dtype=torch.float64, device=self.device)
+            self.l_sp = torch.zeros(self.shard, dtype=torch.int32, device=self.device)
+        self.collectives = 0
+        self.host_syncs = 0
+
+    # -- collectives (no-ops at world size 1) -------------------------------------------
+    def _reduce(self, t, op):
+        if self.world > 1:
+            dist.all_reduce(t, op=op, group=self.group)
+            self.collectives += 1
+
+    def _gather_shard(self, full, local, gathered):
+        """full[lo:hi] of every rank -> full (padded all-gather, back in order)."""
+        if self.world == 1:
+            return
+        n = self.hi - self.lo
+        local[:n].copy_(full[self.lo:self.hi])
+        dist.all_gather_into_tensor(gathered, local, group=self.group)
+        torch.index_select(gathered, 0, self.unpad, out=full)
+        self.collectives += 1
+
+    def _owner(self, g: int) -> int:
+        r = 0
+        while r + 1 < self.world and self.bounds[r + 1] <= g:
+            r += 1
+        return r
+
+    # -- one generation -------------------------------------------------------------------
+    def evaluate(self):
+        """Fitness of the shard, gathered into the evolver's full vector."""
+        ev, b = self.ev, self.buf
+        with torch.cuda.stream(self.stream):
+            ev.evaluate_range_d(self.lo, self.hi, self.X, self.Y, b["fitness"][self.lo:], self.kind, self.offset)
+            self._gather_shard(b["fitness"], getattr(self, "l_fit", None), getattr(self, "g_fit", None))
+
+    def step(self):
+        ev, b, r = self.ev, self.buf, self.rank
+        MIN, MAX, SUM = dist.ReduceOp.MIN, dist.ReduceOp.MAX, dist.ReduceOp.SUM
+        with torch.cuda.stream(self.stream):
+            S = ev.state_species()  # species before this step (replicated on every rank)
+            ev.shard_phase("begin", r)
+            while S < ev.cfg.max_species:  # founding rounds (oracle E2)
+                ev.shard_phase("min_unassigned", r)
+                self._reduce(b["min_unassigned"], MIN)
+                f = int(b["min_unassigned"].item())
+                self.host_syncs += 1
+                if f == 2 ** 31 - 1:
+                    break
+                ev.shard_phase("found", r, f, S)
+                if self.world > 1:
+                    o = self._owner(f)
+                    dist.broadcast(b["rep_nodes"][S * self.gn:(S + 1) * self.gn], src=o, group=self.group)
+                    dist.broadcast(b["rep_conns"][S * self.gc:(S + 1) * self.gc], src=o, group=self.group)
+                    self.collectives += 2
+                ev.shard_phase("join", r, 0, S)
+                S += 1
+            ev.shard_phase("assign_rest", r)
+            self._reduce(b["rep_dmin"], MIN)
+            ev.shard_phase("rep_argmin", r)
+            self._reduce(b["rep_argmin"], MIN)
+            ev.shard_phase("rep_stage", r)
+            self._reduce(b["rep_stage"], SUM)
+            ev.shard_phase("rep_commit", r)
+            self._reduce(b["species_size"], SUM)
+            ev.shard_phase("compact", r)
+            if self.world > 1:  # order-preserving bits compare as signed after flipping the top bit
+                m = b["species_max"]
+                m.bitwise_xor_(_I64_MIN)
+                self._reduce(m, MAX)
+                m.bitwise_xor_(_I64_MIN)
+            ev.shard_phase("stagnation", r)
+            self._reduce(b["rank_sum"], SUM)
+            self._reduce(b["rank_count"], SUM)
+            self._gather_shard(b["species_of"], getattr(self, "l_sp", None), getattr(self, "g_sp", None))
+            counts = ev.shard_phase("select", r)
+            self.host_syncs += 1
+            M = max(1, max(counts))
+            ev.shard_phase("pack", r, M)
+            b = self.buf = ev.shard_buffers(M)
+            if self.world > 1:
+                dist.all_gather_into_tensor(b["pool_nodes"], b["send_nodes"], group=self.group)
+                dist.all_gather_into_tensor(b["pool_conns"], b["send_conns"], group=self.group)
+                self.collectives += 2
+            else:  # one rank: its send buffer is the pool
+                b["pool_nodes"].copy_(b["send_nodes"])
+                b["pool_conns"].copy_(b["send_conns"])
+            ev.shard_phase("back", r, M)
+            self._reduce(b["first_bad"], MIN)
+            self.parents_exchanged = int(sum(counts))
+        ev.step_commit()
+
+    def generation(self):
+        self.evaluate()
+        self.step()
+
+    def local_population(self):
+        """This rank's genomes [lo, hi) (host numpy)."""
+        n, c = self.ev.population()
+        return n[self.lo:self.hi], c[self.lo:self.hi]

@@ -320,6 +320,53 @@ class Evolver:
                                          C.byref(gens)))
         return (bn, bc), bf.value, stats
 
+    # -- the step sharded over ranks (fnb_evolver_shard_*, distributed.ShardedEvolution) --
+    SHARD_PHASES = ("begin", "min_unassigned", "found", "join", "assign_rest", "rep_argmin", "rep_stage",
+                    "rep_commit", "compact", "stagnation", "select", "pack", "back")
+
+    def shard_init(self, bounds):
+        """Rank r of len(bounds)-1 owns genomes [bounds[r], bounds[r+1])."""
+        b = (C.c_int * len(bounds))(*[int(x) for x in bounds])
+        self._raise(self._lib.fnb_evolver_shard_init(self._h, len(bounds) - 1, b))
+        self._shard_world = len(bounds) - 1
+
+    def shard_phase(self, name: str, rank: int, a: int = 0, b: int = 0):
+        """One phase (include/flatneat_b200.h fnb_shard_phase); "select"
+        returns the parents each rank holds (a host list, synchronising)."""
+        out = (C.c_int * max(1, self._shard_world))() if name == "select" else None
+        self._raise(self._lib.fnb_evolver_shard_phase(self._h, self.SHARD_PHASES.index(name), rank, a, b, out))
+        return list(out) if out is not None else None
+
+    def shard_buffers(self, M: int = 0):
+        """Zero-copy torch views of the buffers the collectives act on."""
+        import torch
+        sb = N.fnb_shard_buffers()
+        self._raise(self._lib.fnb_evolver_shard_buffers(self._h, C.byref(sb)))
+        P, L = self.cfg.pop_size, self.engine.limits
+        dev = torch.device("cuda", self.engine.device)
+        gn, gc = L.max_nodes * 5, L.max_conns * 4
+
+        def view(ptr, n, typestr):
+            return torch.as_tensor(_DeviceArray(ptr, (n,), typestr), device=dev)
+
+        out = dict(min_unassigned=view(sb.min_unassigned, 1, "<i4"), rep_dmin=view(sb.rep_dmin, 32, "<i8"),
+                   rep_argmin=view(sb.rep_argmin, 32, "<i4"), rep_stage=view(sb.rep_stage, sb.rep_stage_words, "<i8"),
+                   species_size=view(sb.species_size, 32, "<i4"), species_max=view(sb.species_max, 32, "<i8"),
+                   rank_sum=view(sb.rank_sum, 32, "<i8"), rank_count=view(sb.rank_count, 32, "<i4"),
+                   first_bad=view(sb.first_bad, 1, "<i4"), fitness=view(sb.fitness, P, "<f8"),
+                   species_of=view(sb.species_of, P, "<i4"), rep_nodes=view(sb.rep_nodes, 32 * gn, "<f8"),
+                   rep_conns=view(sb.rep_conns, 32 * gc, "<f8"))
+        if M > 0 and sb.send_nodes:
+            W = self._shard_world
+            out.update(send_nodes=view(sb.send_nodes, M * gn, "<f8"), send_conns=view(sb.send_conns, M * gc, "<f8"),
+                       pool_nodes=view(sb.pool_nodes, W * M * gn, "<f8"),
+                       pool_conns=view(sb.pool_conns, W * M * gc, "<f8"))
+        return out
+
+    def state_species(self) -> int:
+        """Species count before the next step (the library's host mirror, no sync)."""
+        return int(self._lib.fnb_evolver_host_species(self._h))
+
     def run_mode(self) -> int:
         """2: the last run() used one CUDA graph per generation (conditional
         step node); 1: evaluate graph + host check + step graph; 0: eager."""
@@ -332,10 +379,10 @@ class Evolver:
 
 
 class _DeviceArray:
-    """__cuda_array_interface__ for a float64 device buffer owned by the library."""
+    """__cuda_array_interface__ for a device buffer owned by the library."""
 
-    def __init__(self, ptr: int, shape):
-        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (int(ptr), False),
+    def __init__(self, ptr: int, shape, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
                                          "version": 3, "strides": None}
 
 
