@@ -1,20 +1,23 @@
-"""Benchmark: network evals/s of the NEAT evaluation step at BASELINE config 2.
+"""Benchmark: network evals/s of the NEAT evaluation step at BASELINE config 2,
+and generations/s of the full generation loop.
 
-One step = transform (K1) + forward with the fused func-fit fitness (K2) of a
-10k-genome shard (N_max=64, C_max=256, fill 0.75, tanh/sum) over a
-1024-sample batch, plus the fitness all-gather across ranks (the real
-per-generation exchange).  Weak scaling: every rank owns a 10k shard, so the
-job evaluates 10k*N genomes per step.
+Headline step = transform (K1) + forward with the fused func-fit fitness (K2)
+of the pop-10k population (N_max=64, C_max=256, fill 0.75, tanh/sum) over a
+1024-sample batch.  At N GPUs the SAME 10k population is split into N genome
+blocks (strong scaling, the metric's "pop 10k"), plus the fitness all-gather
+(the real per-generation exchange); a weak-scaled line (10k per GPU) is
+reported beside it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Rank 0 prints one JSON line.  --impl reference times the reference's own CPU
-path (oracle/_ref = the unmodified reference headers, all host threads) on a
-bounded sample of the same workload.
+path (oracle/_ref = the unmodified reference headers, all host threads) on
+the full workload every step; it loads no part of this repo's CUDA library.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
 import statistics
@@ -30,8 +33,61 @@ sys.path.insert(0, ROOT)
 
 METRIC = "network evals/sec (genomes x inputs) at pop 10k"
 UNIT = "evals/s"
-P_SHARD, N_MAX, C_MAX, FILL, BATCH, NI, NO = 10_000, 64, 256, 0.75, 1024, 4, 1
-WORKLOAD = "C2 func-regression: pop 10k per GPU, B=1024, N_max=64, C_max=256, fill 0.75, tanh/sum"
+POP, N_MAX, C_MAX, FILL, BATCH, NI, NO = 10_000, 64, 256, 0.75, 1024, 4, 1
+P_SHARD = POP  # per-GPU population of the weak-scaled line and the single-GPU sections
+POP_SEED = 1000
+WORKLOAD = "C2 func-regression: pop 10k, B=1024, N_max=64, C_max=256, fill 0.75, tanh/sum"
+
+
+def synthetic():
+    """paper_2504_08339_b200/synthetic.py loaded by path: data generation only,
+    without importing the package (whose import loads the CUDA library)."""
+    spec = importlib.util.spec_from_file_location("fnb_synthetic",
+                                                  os.path.join(ROOT, "paper_2504_08339_b200", "synthetic.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+def config_dict(world: int) -> dict:
+    """The workload both arms run (identical dicts)."""
+    return {"workload": WORKLOAD, "pop": POP, "global_batch": BATCH, "max_nodes": N_MAX, "max_conns": C_MAX,
+            "fill": FILL, "schema": "tanh/sum", "population_seed": POP_SEED, "n_gpus": world,
+            "parallelism": f"dp{world} (genome blocks of one 10k population)",
+            "l2": "flushed between timed steps (GPU arm)"}
+
+
+def cpu_info() -> dict:
+    model, threads = None, os.cpu_count() or 1
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    if model is None:
+        try:
+            for line in open("/proc/cpuinfo"):
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        except Exception:
+            model = "unknown"
+    return {"cpu_model": model, "host_threads": threads}
+
+
+def loaded_native_libs() -> list:
+    """Shared objects of this repo mapped into the process (evidence of which code ran)."""
+    libs = set()
+    try:
+        for line in open("/proc/self/maps"):
+            p = line.split()[-1]
+            if p.endswith(".so") and (p.startswith(ROOT) or "/repo/" in p):
+                libs.add(os.path.relpath(p, ROOT) if p.startswith(ROOT) else p)
+    except Exception:
+        pass
+    return sorted(libs)
 
 
 def ncu_traffic(name: str):
@@ -105,40 +161,74 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_reference(P_sample: int, seed: int = 0, target_s: float = 8.0):
-    """Reference batch_forward (transform + forward, network.hpp:122/294) on all host cores via oracle/_ref."""
+def _ref_tools():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_lib as ol
-    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
-    if ol.ref_available():
-        kind = "reference"
-    else:
-        kind = "port"
-    threads = os.cpu_count() or 1
+    import oracle_lib as ol  # loads oracle/ libraries only
+    return ol
+
+
+def reference_population():
+    syn = synthetic()
+    nodes, conns = syn.synthetic_population(POP, N_MAX, C_MAX, FILL, NI, NO, seed=POP_SEED)
+    X, Y = syn.regression_dataset(BATCH, NI, NO, seed=0)
+    return nodes, conns, X, Y
+
+
+def cpu_reference_step(ol, nodes, conns, X, Y, threads):
+    """One step of the headline workload on the host: the reference's
+    transform + batch_forward (network.hpp:122, 294; parallel_for over all
+    threads) of the whole population, then the MSE fitness.  Returns seconds."""
     prob = ol.Problem(N_MAX, C_MAX, list(range(NI)), list(range(NI, NI + NO)))
-    schema = ol.SchemaSpec()
-    X, Y = regression_dataset(BATCH, NI, NO, seed=seed)
+    t0 = time.perf_counter()
+    st, bad, msg, out = ol.ref_batch_forward(prob, ol.SchemaSpec(), nodes, conns, X, nthreads=threads)
+    assert st == 0, msg
+    _ = -np.mean((Y[None] - out) ** 2, axis=(1, 2))
+    return time.perf_counter() - t0
 
-    def run(P):
-        nodes, conns = synthetic_population(P, N_MAX, C_MAX, FILL, NI, NO, seed=seed)
-        t0 = time.perf_counter()
-        if kind == "reference":
-            st, bad, msg, out = ol.ref_batch_forward(prob, schema, nodes, conns, X, nthreads=threads)
-            assert st == 0, msg
-        else:
-            for p in range(P):
-                net = ol.oracle_transform(prob, schema, nodes[p], conns[p])
-                out = ol.oracle_forward(prob, schema, nodes[p], net, X)
-        _ = -np.mean((Y[None] - out) ** 2, axis=(1, 2)) if out.ndim == 3 else None
-        return time.perf_counter() - t0
 
-    probe = max(threads * 4, 64)
-    dt = run(probe)
-    P = int(min(P_sample or 10**9, max(probe, probe * target_s / max(dt, 1e-6))))
-    P = min(P, P_SHARD)
-    dt = run(P)
-    return {"value": P * BATCH / dt, "unit": UNIT, "cores": threads if kind == "reference" else 1, "kind": kind,
-            "sample": f"{P} genomes x {BATCH} samples of the C2 workload, transform+forward+MSE, {dt:.2f} s"}
+def cpu_generation_reference(ol, nodes, conns, threads, forward_s):
+    """SURVEY.md 8d / BASELINE.md 3: the reference's own operators for one
+    generation of the C2 workload on the host: transform + batch_forward
+    (timed by the caller, all threads), distance of every genome to S = 10
+    representatives (parallel_for, all threads), crossover per slot and
+    mutate per slot with one serial InnovationTable (one thread, as the
+    reference's mutate contract requires).  Speciation / spawn / selection
+    bookkeeping (O(P*S) integer work, no reference code) is not timed."""
+    C = ol.C
+    prob = ol.Problem(N_MAX, C_MAX, list(range(NI)), list(range(NI, NI + NO)))
+    sh = prob.c()
+    ref = ol.ref()
+    P, S = nodes.shape[0], 10
+    F64P = C.POINTER(C.c_double)
+    reps_n, reps_c = np.ascontiguousarray(nodes[::P // S][:S]), np.ascontiguousarray(conns[::P // S][:S])
+    out = np.empty((P, S))
+    dc = ol.DistCfg(1.0, 0.5)
+    t0 = time.perf_counter()
+    ref.fr_distance_matrix(C.byref(sh), P, nodes.ctypes.data_as(F64P), conns.ctypes.data_as(F64P), S,
+                           reps_n.ctypes.data_as(F64P), reps_c.ctypes.data_as(F64P), C.byref(dc), threads,
+                           out.ctypes.data_as(F64P))
+    t_dist = time.perf_counter() - t0
+    keys = np.stack([ol.key_words(ol.key_split(ol.key_seed(5), i)) for i in range(P)]).astype(np.uint32)
+    other = np.roll(np.arange(P), 1)
+    on, oc = np.ascontiguousarray(nodes[other]), np.ascontiguousarray(conns[other])
+    cn, cc = np.empty_like(nodes), np.empty_like(conns)
+    t0 = time.perf_counter()
+    ref.fr_crossover_population(C.byref(sh), P, nodes.ctypes.data_as(F64P), conns.ctypes.data_as(F64P),
+                                on.ctypes.data_as(F64P), oc.ctypes.data_as(F64P),
+                                keys.ctypes.data_as(C.POINTER(C.c_uint32)), cn.ctypes.data_as(F64P),
+                                cc.ctypes.data_as(F64P))
+    t_x = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st, bad, nk, mn, mc = ol.mutate_population(prob, ol.SchemaSpec(), cn, cc, keys, ol.mut_cfg(), 10_000,
+                                               use_ref=True)
+    t_m = time.perf_counter() - t0
+    assert st == 0
+    total = forward_s + t_dist + t_x + t_m
+    return {"value": 1.0 / total, "unit": "generations/s", "ms_per_generation": total * 1e3, "kind": "reference",
+            "cores": threads, **cpu_info(),
+            "components_ms": {"transform_plus_batch_forward": forward_s * 1e3, "distance_x10_parallel_for": t_dist * 1e3,
+                              "crossover_per_slot_1_thread": t_x * 1e3, "mutate_per_slot_serial_table": t_m * 1e3},
+            "sample": f"full pop {P}: {P} x {S} distances, {P} crossovers, {P} mutations (paper defaults)"}
 
 
 def c5_distance(dev, stream, flush, reps: int = 5, population: str = "random"):
@@ -263,22 +353,69 @@ def c4_hyperneat(dev, stream, flush, reps: int = 3):
             "generations_equiv_per_s": 1.0 / t}
 
 
-def c5_generation(dev, flush, world: int = 1, gens: int = 4, warm: int = 2):
-    """BASELINE config 5: the full device generation loop (K1+K2 evaluation,
-    then speciate / stagnation / spawn / reproduce with K3, K5, K6, K7) at
-    pop 100k, N128/C1024, sharded over the job's GPUs: evaluation by genome
-    blocks with the fitness all-gather, and at N > 1 the reproduction too
-    (distributed.py shard_step: children [lo, hi) per rank, then an
-    all-gather of the next population).  The population starts as 2,000
-    distinct synthetic genomes tiled to 100k on the device."""
+def timed_generations(ev, X, Y, dev, flush, world: int, gens: int, warm: int, shard=None):
+    """Mean device time of one generation (evaluate -> speciate -> stagnate ->
+    spawn -> reproduce), CUDA events on the evolver stream, max over ranks.
+    One GPU: fnb_evolve (one CUDA graph per generation, host reads RunStats
+    each generation -- the loop a user runs).  N GPUs: the sharded step
+    (distributed.ShardedEvolution).  The working set (two population buffers
+    + nets) exceeds L2, and L2 is flushed before the timed run."""
     import torch
     import torch.distributed as dist
+    es = torch.cuda.ExternalStream(ev.stream_handle(), device=dev)
+    if shard is None:
+        ev.run(X.cpu().double().numpy(), Y.cpu().double().numpy(), generation_limit=warm)
+    else:
+        for _ in range(warm):
+            shard.generation()
+    flush.zero_()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = ev.engine.launch_count
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(es)
+    t0 = time.perf_counter()
+    stats = None
+    if shard is None:
+        _, _, stats = ev.run(X.cpu().double().numpy(), Y.cpu().double().numpy(), generation_limit=gens)
+    else:
+        for _ in range(gens):
+            shard.generation()
+    b.record(es)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = a.elapsed_time(b) / gens
+    if world > 1:
+        t = torch.tensor([ms, wall], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, wall = (float(x) for x in t.tolist())
+    out = {"ms_per_generation": ms, "generations_per_s": 1e3 / ms, "wall_s": wall, "generations_timed": gens,
+           "launches_per_generation": (ev.engine.launch_count - launches0) / gens, "species": ev.state_species()}
+    if shard is None:
+        out["graph_mode"] = {2: "one CUDA graph per generation (conditional step node)",
+                             1: "evaluate graph + step graph", 0: "eager"}.get(ev.run_mode(), "unknown")
+        out["mean_host_ms_per_generation"] = float(np.mean([s.elapsed_ms for s in stats]))
+    else:
+        out.update(collectives_per_generation=shard.collectives / (warm + gens),
+                   parents_exchanged_last=shard.parents_exchanged, sharding="population blocks (ShardedEvolution)")
+    return out
+
+
+def c5_generation(dev, flush, world: int = 1, rank: int = 0, gens: int = 4, warm: int = 2):
+    """BASELINE config 5: the full device generation loop (K1+K2 evaluation,
+    then speciate / stagnation / spawn / reproduce with K3, K5, K6, K7) at
+    pop 100k, N128/C1024.  At N GPUs the population is sharded
+    (ShardedEvolution: each rank evaluates, speciates and reproduces its own
+    genome block).  The population starts as 2,000 distinct synthetic
+    genomes tiled to 100k on the device."""
+    import torch
     import paper_2504_08339_b200 as fnb
-    from paper_2504_08339_b200.distributed import DeviceShardBackend, ShardedGeneration
+    from paper_2504_08339_b200.distributed import ShardedEvolution
     from paper_2504_08339_b200.evolve import Evolver, NeatConfig
-    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
+    syn = synthetic()
     P5, N5, C5, uniq = 100_000, 128, 1024, 2_000
-    n_h, c_h = synthetic_population(uniq, N5, C5, FILL, NI, NO, seed=5)
+    n_h, c_h = syn.synthetic_population(uniq, N5, C5, FILL, NI, NO, seed=5)
     eng5 = fnb.Engine(fnb.GenomeLimits(N5, C5), list(range(NI)), list(range(NI, NI + NO)), fnb.AttributeSchema(),
                       device=dev.index)
     ev = Evolver(eng5, NeatConfig(pop_size=P5), seed=5)
@@ -286,44 +423,14 @@ def c5_generation(dev, flush, world: int = 1, gens: int = 4, warm: int = 2):
     conns = torch.from_numpy(c_h).to(dev).repeat(P5 // uniq, 1, 1)
     ev.set_population_d(nodes, conns)
     del nodes, conns
-    X_h, Y_h = regression_dataset(BATCH, NI, NO, seed=0)
+    X_h, Y_h = syn.regression_dataset(BATCH, NI, NO, seed=0)
     X = torch.from_numpy(X_h.astype(np.float32)).to(dev)
     Y = torch.from_numpy(Y_h.astype(np.float32)).to(dev)
-    sg = ShardedGeneration(DeviceShardBackend(ev, X, Y), shard_step=True)
-    es = sg.backend.stream
-    gms, ems = [], []
-    for it in range(warm + gens):
-        flush.zero_()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        e0.record(es)
-        sg.evaluate()
-        e1.record(es)
-        if world > 1:
-            sg.reproduce_sharded()
-        else:
-            ev.step()
-        e2.record(es)
-        torch.cuda.synchronize()
-        if it >= warm:
-            gms.append(e0.elapsed_time(e2))
-            ems.append(e0.elapsed_time(e1))
-    g_ms, e_ms = float(np.mean(gms)), float(np.mean(ems))
-    if world > 1:
-        t = torch.tensor([g_ms, e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        g_ms, e_ms = (float(x) for x in t.tolist())
-    agree = sg.replicas_agree()
-    sp = ev.species()
+    shard = ShardedEvolution(ev, X, Y) if world > 1 else None
+    r = timed_generations(ev, X, Y, dev, flush, world, gens, warm, shard)
     ev.close()
     return {"workload": f"C5 generation loop: pop 100k, N128/C1024, B=1024 func-fit, {world} GPU(s) "
-                        "(2k distinct genomes tiled)",
-            "ms_per_generation": g_ms, "generations_per_s": 1e3 / g_ms, "evaluate_ms": e_ms, "evolve_step_ms": g_ms - e_ms,
-            "evals_per_s": P5 * BATCH / (e_ms / 1e3), "species": int(sp["count"]), "generations_timed": gens,
-            "sharding": "evaluation + reproduction by genome blocks" if world > 1 else "single GPU",
-            "replicas_agree": bool(agree), "scaling": "strong", "timing": "max over ranks"}
+                        "(2k distinct genomes tiled)", **r, "scaling": "strong", "timing": "max over ranks"}
 
 
 def evolved_population(eng, dev, stream, flush, X, Y, gens: int = 100):
@@ -372,6 +479,34 @@ def evolved_population(eng, dev, stream, flush, X, Y, gens: int = 100):
             "evals_per_s": P_SHARD * BATCH / t, "wall_s_100_generations": loop_s}
 
 
+def reference_arm(args, rank: int):
+    """--impl reference: the reference's own CPU path on the box's host cores,
+    the full workload every step (no extrapolation), W real warm-up steps."""
+    if rank != 0:
+        return
+    ol = _ref_tools()
+    if not ol.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (the compiled reference) is missing"}))
+        return
+    threads = os.cpu_count() or 1
+    nodes, conns, X, Y = reference_population()
+    for _ in range(args.warmup):
+        cpu_reference_step(ol, nodes, conns, X, Y, threads)
+    ts = [cpu_reference_step(ol, nodes, conns, X, Y, threads) for _ in range(max(1, args.steps))]
+    ms = float(np.mean(ts)) * 1e3
+    v = POP * BATCH / (ms / 1e3)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args.gpus),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", **cpu_info(),
+                             "sample": f"full workload every step: {POP} genomes x {BATCH} samples, "
+                                       "transform + batch_forward (parallel_for, grain 16) + MSE"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "native_so_loaded": loaded_native_libs()}
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -380,7 +515,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-generations", action="store_true")
-    ap.add_argument("--no-c5", action="store_true", help="skip the C3 (CPPN), C4 (HyperNEAT) and C5 (pop 100k K3 distance) measurements")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C3 (CPPN), C4 (HyperNEAT) and C5 (pop 100k) measurements")
     ap.add_argument("--spt", type=int, default=0, help="forward columns per thread (tuning; 0 = auto)")
     args = ap.parse_args()
 
@@ -389,29 +524,13 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        vals = []
-        for _ in range(args.warmup):
-            pass
-        base = None
-        for _ in range(max(1, args.steps)):
-            base = cpu_reference(0, target_s=max(1.0, 20.0 / max(1, args.steps)))
-            vals.append(base["value"])
-        v = float(np.median(vals))
-        line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": P_SHARD * BATCH / v * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": BATCH, "pop": P_SHARD},
-                "cpu_baseline": {**base, "value": v},
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        reference_arm(args, rank)
         return
 
     import torch
     import torch.distributed as dist
     import paper_2504_08339_b200 as fnb
-    from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
+    from paper_2504_08339_b200.distributed import shard_bounds
 
     if args.spt:
         fnb._native.lib().fnb_set_forward_spt(args.spt)
@@ -428,132 +547,121 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
 
-    nodes_h, conns_h = synthetic_population(P_SHARD, N_MAX, C_MAX, FILL, NI, NO, seed=1000 + rank)
-    X_h, Y_h = regression_dataset(BATCH, NI, NO, seed=0)
+    syn = synthetic()
+    # the job's population: one pop-10k population, rank r holds genome block [lo, hi)
+    all_n, all_c = syn.synthetic_population(POP, N_MAX, C_MAX, FILL, NI, NO, seed=POP_SEED)
+    lo, hi = shard_bounds(POP, world, rank)
+    nodes_h, conns_h = np.ascontiguousarray(all_n[lo:hi]), np.ascontiguousarray(all_c[lo:hi])
+    PL = hi - lo
+    X_h, Y_h = syn.regression_dataset(BATCH, NI, NO, seed=0)
     eng = fnb.Engine(fnb.GenomeLimits(N_MAX, C_MAX), list(range(NI)), list(range(NI, NI + NO)),
                      fnb.AttributeSchema(), device=local)
-    nodes = torch.from_numpy(nodes_h).to(dev)
-    conns = torch.from_numpy(conns_h).to(dev)
     X = torch.from_numpy(X_h.astype(np.float32)).to(dev)
     Y = torch.from_numpy(Y_h.astype(np.float32)).to(dev)
-    nets = eng.alloc_nets(P_SHARD)
-    fit = torch.empty(P_SHARD, dtype=torch.float64, device=dev)
-    fit_all = torch.empty(P_SHARD * world, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
+    shard_max = max(shard_bounds(POP, world, r)[1] - shard_bounds(POP, world, r)[0] for r in range(world))
 
-    def step(ev=None):
-        eng.transform_d(nodes, conns, nets, stream)
-        if ev is not None:
-            ev[0].record(stream)
-        eng.forward_d(nets, P_SHARD, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=stream)
-        if ev is not None:
-            ev[1].record(stream)
-        if world > 1:
-            dist.all_gather_into_tensor(fit_all, fit)
+    def timed_eval(nodes_h, conns_h, steps, warmup):
+        """K1 + K2 of this rank's genomes + the fitness all-gather, CUDA events, max over ranks."""
+        P = nodes_h.shape[0]
+        nodes = torch.from_numpy(nodes_h).to(dev)
+        conns = torch.from_numpy(conns_h).to(dev)
+        nets = eng.alloc_nets(P)
+        pad = max(P, shard_max) if world > 1 else P
+        fit = torch.zeros(pad, dtype=torch.float64, device=dev)
+        fit_all = torch.empty(pad * world, dtype=torch.float64, device=dev)
 
-    # correctness gate once, outside timing
-    step()
-    eng.check_nets_d(nodes, conns, nets)
-    for _ in range(max(3, args.warmup)):
-        flush.zero_()
+        def step(ev=None):
+            eng.transform_d(nodes, conns, nets, stream)
+            if ev is not None:
+                ev[0].record(stream)
+            eng.forward_d(nets, P, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=stream)
+            if ev is not None:
+                ev[1].record(stream)
+            if world > 1:
+                dist.all_gather_into_tensor(fit_all, fit)
+
         step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+        eng.check_nets_d(nodes, conns, nets)  # correctness gate once, outside timing
+        for _ in range(max(3, warmup)):
+            flush.zero_()
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches0 = eng.launch_count
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda.synchronize()
+        for i in range(steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            starts[i].record(stream)
+            step(kev[i])
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        launches = eng.launch_count - launches0
+        tot = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
+        fwd = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+        if world > 1:
+            t = torch.tensor([tot], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = float(t.item())
+            dist.barrier()
+        del nodes, conns, nets
+        return tot / steps, fwd, launches
 
     sampler = ClockSampler(local)
     sampler.start()
-    launches0 = eng.launch_count
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-        starts[i].record(stream)
-        step(kev[i])
-        ends[i].record(stream)
-    torch.cuda.synchronize()
-    launches = eng.launch_count - launches0
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    fwd_ms = [a.elapsed_time(b) for a, b in kev]
-    tot_ms = float(sum(step_ms))
-    if world > 1:
-        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
-        dist.barrier()
+    ms_per_step, fwd_ms, launches = timed_eval(nodes_h, conns_h, args.steps, args.warmup)
     clocks = sampler.stop()
-    ms_per_step = tot_ms / args.steps
-    value = P_SHARD * world * BATCH / (ms_per_step / 1e3)
+    value = POP * BATCH / (ms_per_step / 1e3)
+    weak = None
+    if world > 1:  # every rank a full 10k population of its own
+        wn, wc = syn.synthetic_population(P_SHARD, N_MAX, C_MAX, FILL, NI, NO, seed=POP_SEED + rank)
+        w_ms, _, _ = timed_eval(wn, wc, args.steps, args.warmup)
+        weak = {"value": P_SHARD * world * BATCH / (w_ms / 1e3), "unit": UNIT, "ms_per_step": w_ms,
+                "scaling": "weak", "pop_per_gpu": P_SHARD}
+        del wn, wc
 
-    # ---- e2e through the public host API (pinned host buffers, H2D + D2H inside) ----
-    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
-    nodes_p, conns_p, X_p, Y_p = pin(nodes_h), pin(conns_h), pin(X_h), pin(Y_h)
-    eng.evaluate(nodes_p, conns_p, X_p, Y_p, fnb.FIT_NEG_MSE)
-    e2e_steps = max(5, min(args.steps, 20))
-    e2e_t = []
-    for _ in range(e2e_steps):
-        t0 = time.perf_counter()
-        fit_h = eng.evaluate(nodes_p, conns_p, X_p, Y_p, fnb.FIT_NEG_MSE)
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_s = float(np.median(e2e_t))  # per-call wall time (a call ends with its D2H + sync)
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    h2d = nodes_h.nbytes + conns_h.nbytes + X_h.nbytes + Y_h.nbytes
-    d2h = fit_h.nbytes
-
-    # ---- generations/s: evaluate + speciate/stagnate/spawn/reproduce on the device ----
-    gen = None
-    if not args.no_generations:
-        # one 10k population for the whole job: replicated on every rank,
-        # evaluation sharded, fitness all-gathered (distributed.py)
-        from paper_2504_08339_b200.distributed import DeviceShardBackend, ShardedGeneration
-        from paper_2504_08339_b200.evolve import Evolver, NeatConfig
-        ev = Evolver(eng, NeatConfig(pop_size=P_SHARD), seed=1000)
-        gn_h, gc_h = (nodes_h, conns_h) if rank == 0 else synthetic_population(P_SHARD, N_MAX, C_MAX, FILL, NI, NO,
-                                                                                 seed=1000)
-        ev.set_population(gn_h, gc_h)
-        sg = ShardedGeneration(DeviceShardBackend(ev, X, Y))
-        es = sg.backend.stream
-        g_warm, g_steps = max(3, args.warmup), max(5, args.steps)
-        gms, ems = [], []
-        launches_g0 = 0
-        for it in range(g_warm + g_steps):
-            flush.zero_()
-            torch.cuda.synchronize()
+    # ---- e2e through the public host API (H2D + D2H inside every call) ----
+    def e2e(pinned: bool):
+        if pinned:
+            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+            n_, c_, x_, y_ = pin(nodes_h), pin(conns_h), pin(X_h), pin(Y_h)
+        else:
+            n_, c_, x_, y_ = nodes_h, conns_h, X_h, Y_h
+        eng.evaluate(n_, c_, x_, y_, fnb.FIT_NEG_MSE)
+        ts = []
+        for _ in range(max(5, min(args.steps, 20))):
             if world > 1:
                 dist.barrier()
-            if it == g_warm:
-                launches_g0 = eng.launch_count
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record(es)
-            sg.evaluate()
-            e1.record(es)
-            ev.step()
-            e2.record(es)
-            es.synchronize()
-            if it >= g_warm:
-                gms.append(e0.elapsed_time(e2))
-                ems.append(e0.elapsed_time(e1))
-        g_ms, e_ms = float(np.mean(gms)), float(np.mean(ems))
+            t0 = time.perf_counter()
+            f_ = eng.evaluate(n_, c_, x_, y_, fnb.FIT_NEG_MSE)
+            ts.append(time.perf_counter() - t0)
+        t = float(np.median(ts))
         if world > 1:
-            t = torch.tensor([g_ms, e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            g_ms, e_ms = (float(x) for x in t.tolist())
-        agree = sg.replicas_agree()
-        sp = ev.species()
-        gen = {"generations_per_s": 1e3 / g_ms, "ms_per_generation": g_ms,
-               "evaluate_ms": e_ms, "evolve_step_ms": g_ms - e_ms,
-               "generations_timed": g_steps, "species": int(sp["count"]),
-               "launches_per_generation": (eng.launch_count - launches_g0) / g_steps,
-               "replicas_agree": bool(agree), "scaling": "strong",
-               "note": "one pop-10k population per job, C2 shapes; evaluation sharded over ranks + fitness "
-                       "all-gather, step (speciate+stagnation+spawn+reproduce: K3,K5,K6,K7 + selection) replicated; "
-                       "max over ranks"}
+            tt = torch.tensor([t], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t, f_.nbytes
+
+    e2e_s, d2h = e2e(True)
+    e2e_pageable_s, _ = e2e(False)
+    h2d = nodes_h.nbytes + conns_h.nbytes + X_h.nbytes + Y_h.nbytes
+
+    # ---- generations/s of the pop-10k loop ----
+    gen = None
+    if not args.no_generations:
+        from paper_2504_08339_b200.distributed import ShardedEvolution
+        from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+        ev = Evolver(eng, NeatConfig(pop_size=POP), seed=POP_SEED)
+        ev.set_population(all_n, all_c)
+        shard = ShardedEvolution(ev, X, Y) if world > 1 else None
+        gen = timed_generations(ev, X, Y, dev, flush, world, max(5, args.steps), max(3, args.warmup), shard)
+        gen.update(scaling="strong", note="one pop-10k population per job, C2 shapes, B=1024 func-fit; "
+                                          "max over ranks")
         ev.close()
 
     def section(fn, *a):
@@ -563,71 +671,82 @@ def main():
         except Exception as e:  # noqa: BLE001
             return {"error": repr(e)[:300]}
 
-    c3 = section(c3_cppn, eng, nets, dev, stream, flush) if not args.no_c5 else None
-    c4 = section(c4_hyperneat, dev, stream, flush) if not args.no_c5 else None
-    evo = section(evolved_population, eng, dev, stream, flush, X, Y) if not args.no_generations else None
-    c5g = section(c5_generation, dev, flush, world) if not args.no_c5 else None
-    c5 = section(c5_distance, dev, stream, flush) if not args.no_c5 else None
-    c5l = section(c5_distance, dev, stream, flush, 5, "lineage") if not args.no_c5 else None
+    c3 = c4 = c5 = c5l = c5g = evo = None
+    if rank == 0 and world == 1 and not args.no_c5:
+        nets10 = eng.alloc_nets(POP)
+        eng.transform_d(torch.from_numpy(all_n).to(dev), torch.from_numpy(all_c).to(dev), nets10, stream)
+        c3 = section(c3_cppn, eng, nets10, dev, stream, flush)
+        del nets10
+        c4 = section(c4_hyperneat, dev, stream, flush)
+        c5 = section(c5_distance, dev, stream, flush)
+        c5l = section(c5_distance, dev, stream, flush, 5, "lineage")
+    if not args.no_c5:
+        c5g = section(c5_generation, dev, flush, world, rank)
+    if rank == 0 and world == 1 and not args.no_generations:
+        evo = section(evolved_population, eng, dev, stream, flush, X, Y)
 
-    # ---- roofline for the dominant kernel (K2 forward) ----
+    # ---- roofline for the dominant kernel (K2 forward, this rank's genomes) ----
     k2_traffic, k2_traffic_src = ncu_traffic("k2_forward_main_pass")
     n_en = int(np.sum(conns_h[:, :, 2] == 1.0))
-    n_ops = int(np.sum(~np.isnan(nodes_h[:, :, 0]))) - P_SHARD * NI
+    n_ops = int(np.sum(~np.isnan(nodes_h[:, :, 0]))) - PL * NI
     flops = 2.0 * BATCH * (n_en + n_ops)          # FMA per enabled edge + resp*agg+bias per node
-    fwd_s = float(np.mean(fwd_ms)) / 1e3
+    fwd_s = fwd_ms / 1e3
     pk = peaks()
     sm_clock = (pk.get("sm_max_mhz") or 1965.0) * 1e6
     fp32_peak = 148 * 128 * 2 * sm_clock / 1e12
-    achieved = flops / fwd_s / 1e12
     smem_bytes = 4.0 * BATCH * (n_en + n_ops)     # one 4-byte LDS per edge-sample, one STS per node-sample
     smem_peak = 148 * 128 * sm_clock / 1e12       # TB/s (128 B/clk/SM)
+    smem_ach = smem_bytes / fwd_s / 1e12
 
-    cpu = None
+    cpu = cpu_gen = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference(0)
+            ol = _ref_tools()
+            if ol.ref_available():
+                threads = os.cpu_count() or 1
+                rn, rc, rX, rY = reference_population()
+                cpu_reference_step(ol, rn, rc, rX, rY, threads)  # warm
+                t_fwd = cpu_reference_step(ol, rn, rc, rX, rY, threads)
+                cpu = {"value": POP * BATCH / t_fwd, "unit": UNIT, "cores": threads, "kind": "reference",
+                       **cpu_info(), "sample": f"full workload: {POP} genomes x {BATCH} samples, transform + "
+                                               "batch_forward (parallel_for, grain 16) + MSE, one timed step"}
+                cpu_gen = cpu_generation_reference(ol, rn, rc, threads, t_fwd)
+            else:
+                cpu = {"value": None, "error": "oracle/_ref missing"}
         except Exception as e:  # reported, never silently substituted
             cpu = {"value": None, "error": repr(e)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 (forward), f64 (fitness)", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "pop_per_gpu": P_SHARD, "global_pop": P_SHARD * world,
-                       "global_batch": BATCH, "max_nodes": N_MAX, "max_conns": C_MAX, "fill": FILL,
-                       "parallelism": f"dp{world} (population shards)", "l2": "flushed between timed steps"},
-            "e2e": {"value": P_SHARD * world * BATCH / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "config": config_dict(world),
+            "e2e": {"value": POP * BATCH / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "api": "fnb_evaluate (host buffers, pinned)",
-                    "h2d_gbps_effective": h2d / e2e_s / 1e9, "timing": f"median of {e2e_steps} calls"},
+                    "h2d_gbps_effective": h2d / e2e_s / 1e9, "timing": "median of calls, max over ranks",
+                    "pageable": {"value": POP * BATCH / e2e_pageable_s, "unit": UNIT,
+                                 "api": "fnb_evaluate from pageable host memory (std::vector-like)"}},
             "gpu_launches": int(launches),
-            "kernels": {"transform_plus_forward_ms": ms_per_step, "forward_ms": fwd_s * 1e3,
-                        "transform_ms": ms_per_step - fwd_s * 1e3},
-            "roofline": {"kernel": "k_forward (K2)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
-                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": k2_traffic,
+            "kernels": {"transform_plus_forward_ms": ms_per_step, "forward_ms": fwd_ms,
+                        "transform_ms": ms_per_step - fwd_ms, "genomes_on_rank0": PL},
+            "roofline": {"kernel": "k_forward (K2)", "bound": "smem", "achieved": smem_ach, "peak": smem_peak,
+                         "unit": "TB/s", "frac": smem_ach / smem_peak, "traffic": k2_traffic,
                          "traffic_source": k2_traffic_src,
-                         "peak_source": "nominal FP32 FMA peak at MEASURED_PEAKS sm_max_mhz (no measured FP32 peak)",
-                         "smem": {"achieved_TBps": smem_bytes / fwd_s / 1e12, "peak_TBps": smem_peak,
-                                  "frac": smem_bytes / fwd_s / 1e12 / smem_peak}},
+                         "algorithmic": "4 B LDS per enabled edge x sample + 4 B per node x sample",
+                         "peak_source": "128 B/clk/SM x 148 SMs at MEASURED_PEAKS sm_max_mhz",
+                         "fp32": {"achieved_TFLOPs": flops / fwd_s / 1e12, "peak_TFLOPs": fp32_peak,
+                                  "frac": flops / fwd_s / 1e12 / fp32_peak}},
             "clocks": clocks,
         }
-        if gen is not None:
-            line["generations"] = gen
-        if c5 is not None:
-            line["c5_distance"] = c5
-        if c5l is not None:
-            line["c5_distance_lineage"] = c5l
-        if c3 is not None:
-            line["c3_cppn"] = c3
-        if c4 is not None:
-            line["c4_hyperneat"] = c4
-        if evo is not None:
-            line["evolved"] = evo
-        if c5g is not None:
-            line["c5_generation"] = c5g
-        if cpu is not None:
-            line["cpu_baseline"] = cpu
+        for k, v in (("weak_scaling", weak), ("generations", gen), ("c5_distance", c5), ("c5_distance_lineage", c5l),
+                     ("c3_cppn", c3), ("c4_hyperneat", c4), ("evolved", evo), ("c5_generation", c5g),
+                     ("cpu_baseline", cpu)):
+            if v is not None:
+                line[k] = v
+        if cpu_gen is not None and gen is not None:
+            gen["cpu_baseline"] = cpu_gen
+        line["native_so_loaded"] = loaded_native_libs()
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

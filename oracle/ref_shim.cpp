@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -199,6 +200,42 @@ void fr_crossover(const fo_shape* sh, const double* fn, const double* fc, const 
                   const double* oc, const uint32_t key[4], double* cn, double* cc) {
   const auto child = crossover(to_genome(sh, fn, fc), to_genome(sh, on, oc), to_key(key));
   from_genome(child, cn, cc);
+}
+
+// distance(genome_p, rep_s) for a population x S representatives with the
+// reference's parallel_for over the population (parallel.hpp:74-110) --
+// bench.py's CPU generation baseline.  out[P][S].
+void fr_distance_matrix(const fo_shape* sh, int P, const double* pop_nodes, const double* pop_conns, int S,
+                        const double* rep_nodes, const double* rep_conns, const fo_dist_cfg* cfg, int nthreads,
+                        double* out) {
+  const std::size_t ns = std::size_t(sh->max_nodes) * kNodeCols;
+  const std::size_t cs = std::size_t(sh->max_conns) * kConnCols;
+  const DistanceConfig dc{cfg->compatibility_disjoint, cfg->compatibility_homologous};
+  std::vector<GenomeTensors> reps;
+  for (int s = 0; s < S; ++s) reps.push_back(to_genome(sh, rep_nodes + std::size_t(s) * ns, rep_conns + std::size_t(s) * cs));
+  std::unique_ptr<ThreadPool> pool;
+  if (nthreads > 1) pool = std::make_unique<ThreadPool>(nthreads);
+  parallel_for(pool.get(), P, 16, [&](int lo, int hi) {
+    for (int p = lo; p < hi; ++p) {
+      const auto g = to_genome(sh, pop_nodes + std::size_t(p) * ns, pop_conns + std::size_t(p) * cs);
+      for (int s = 0; s < S; ++s) out[std::size_t(p) * S + s] = distance(g, reps[std::size_t(s)], dc);
+    }
+  });
+}
+
+// crossover(fit[c], other[c], keys[c]) for c < n, one thread (the per-slot
+// loop of reproduce) -- bench.py's CPU generation baseline.
+void fr_crossover_population(const fo_shape* sh, int n, const double* fit_nodes, const double* fit_conns,
+                             const double* oth_nodes, const double* oth_conns, const uint32_t* keys,
+                             double* child_nodes, double* child_conns) {
+  const std::size_t ns = std::size_t(sh->max_nodes) * kNodeCols;
+  const std::size_t cs = std::size_t(sh->max_conns) * kConnCols;
+  for (int c = 0; c < n; ++c) {
+    const auto child = crossover(to_genome(sh, fit_nodes + std::size_t(c) * ns, fit_conns + std::size_t(c) * cs),
+                                 to_genome(sh, oth_nodes + std::size_t(c) * ns, oth_conns + std::size_t(c) * cs),
+                                 to_key(keys + 4 * c));
+    from_genome(child, child_nodes + std::size_t(c) * ns, child_conns + std::size_t(c) * cs);
+  }
 }
 
 // Sequential mutate of P genomes in slot order with ONE InnovationTable, the

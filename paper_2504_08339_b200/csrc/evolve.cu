@@ -1373,6 +1373,9 @@ struct Evolver {
 // =================================================================================
 #include "ctx_internal.cuh"
 
+struct fnb_evolve_run;
+static void release_evolve_run(fnb_evolve_run* r);
+
 struct fnb_evolver {
   fnb_ctx* ctx = nullptr;
   fnb::Evolver ev;
@@ -1382,6 +1385,7 @@ struct fnb_evolver {
   DevBuf eflags;
   int eval_lo = 0, eval_n = 0;
   int run_mode = -1;  // fnb_evolve: 2 conditional generation graphs, 1 evaluate graph + step graph, 0 eager
+  struct fnb_evolve_run* run = nullptr;  // generation graphs, kept across fnb_evolve calls
 };
 
 namespace fnb {
@@ -1472,6 +1476,7 @@ void fnb_evolver_destroy(fnb_evolver* ev) {
   ev->X.release();
   ev->Y.release();
   ev->eflags.release();
+  release_evolve_run(ev->run);
   delete ev;
   cudaGetLastError();  // leave no error behind for the context's next call
 }
@@ -1944,19 +1949,34 @@ struct fnb_gen_graph {
   long long n_eval = 0, n_step = 0;
 };
 
+// The graphs bake in the problem (device X / Y, batch, fitness kind and
+// offset, target), so they are kept across fnb_evolve calls with the same key.
 struct fnb_evolve_run {
   fnb_gen_graph g[fnb::kMaxSpecies + 1][2];
   bool use_cond = true;
   fnb::GenStats* d_stats = nullptr;
   fnb::GenStats* h_stats = nullptr;  // pinned
-  ~fnb_evolve_run() {
+  const void* key_x = nullptr;
+  const void* key_y = nullptr;
+  const void* key_bufs[3] = {nullptr, nullptr, nullptr};  // partial sums, nets, eval flags
+  int key_batch = -1, key_kind = -1;
+  double key_offset = 0.0, key_target = 0.0;
+  void drop_graphs() {
     for (auto& row : g)
       for (auto& x : row)
-        if (x.exec) cudaGraphExecDestroy(x.exec);
+        if (x.exec) {
+          cudaGraphExecDestroy(x.exec);
+          x.exec = nullptr;
+        }
+  }
+  ~fnb_evolve_run() {
+    drop_graphs();
     if (d_stats) cudaFree(d_stats);
     if (h_stats) cudaFreeHost(h_stats);
   }
 };
+
+static void release_evolve_run(fnb_evolve_run* r) { delete r; }
 
 static long long count_kernel_nodes(cudaGraph_t graph) {
   size_t n = 0;
@@ -2071,12 +2091,29 @@ int fnb_evolve(fnb_evolver* ev, const double* inputs, const double* targets, int
   EV_CK(ctx->partial.ensure(fnb::forward_partial_needed(ctx->L, v.P, batch)));
   const float* X = static_cast<const float*>(ev->X.p);
   const float* Y = static_cast<const float*>(ev->Y.p);
-  fnb_evolve_run run;
-  EV_CK(cudaMalloc(&run.d_stats, sizeof(fnb::GenStats)));
-  EV_CK(cudaMallocHost(&run.h_stats, sizeof(fnb::GenStats)));
+  if (!ev->run) ev->run = new fnb_evolve_run();
+  fnb_evolve_run& run = *ev->run;
+  if (!run.d_stats) EV_CK(cudaMalloc(&run.d_stats, sizeof(fnb::GenStats)));
+  if (!run.h_stats) EV_CK(cudaMallocHost(&run.h_stats, sizeof(fnb::GenStats)));
   EV_CK(cudaStreamSynchronize(v.st));
   bool use_graphs = v.use_graphs;
-  if (const char* g = std::getenv("FNB_GEN_GRAPH")) run.use_cond = std::string(g) != "0";
+  bool want_cond = true;
+  if (const char* g = std::getenv("FNB_GEN_GRAPH")) want_cond = std::string(g) != "0";
+  if (run.key_x != X || run.key_y != Y || run.key_batch != batch || run.key_kind != fitness_kind ||
+      run.key_offset != fitness_offset || run.key_target != fitness_target || run.use_cond != want_cond ||
+      run.key_bufs[0] != ctx->partial.p || run.key_bufs[1] != ev->nets.p || run.key_bufs[2] != ev->eflags.p) {
+    run.drop_graphs();  // another problem (or mode): the cached graphs do not apply
+    run.use_cond = want_cond;
+    run.key_x = X;
+    run.key_y = Y;
+    run.key_batch = batch;
+    run.key_kind = fitness_kind;
+    run.key_offset = fitness_offset;
+    run.key_target = fitness_target;
+    run.key_bufs[0] = ctx->partial.p;
+    run.key_bufs[1] = ev->nets.p;
+    run.key_bufs[2] = ev->eflags.p;
+  }
   int last_eval_buf = v.cur, last_best = 0;
   double last_fit = -INFINITY;
   int gens = 0;
@@ -2092,9 +2129,7 @@ int fnb_evolve(fnb_evolver* ev, const double* inputs, const double* targets, int
         if (e != cudaSuccess && run.use_cond) {  // no conditional nodes here: evaluate graph + host check
           cudaGetLastError();
           run.use_cond = false;
-          for (auto& row : run.g)
-            for (auto& x : row)
-              if (x.exec) { cudaGraphExecDestroy(x.exec); x.exec = nullptr; }
+          run.drop_graphs();
           e = build_gen_graph(ev, run, X, Y, batch, fitness_kind, fitness_offset, fitness_target, gg);
         }
         if (e != cudaSuccess) {

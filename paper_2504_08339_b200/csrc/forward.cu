@@ -38,16 +38,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 // tanh(x) = 1 - 2/(exp(2x)+1): absolute error ~2e-7 on the whole line,
-// saturating exactly to +-1 (inf/0 out of ex2).  That form cancels near 0, so
-// |x| < 0.3 takes the odd Taylor polynomial through x^9 (truncation < 6e-8
-// relative there): relative error stays below ~1e-6 everywhere.
+// saturating exactly to +-1 (inf/0 out of ex2).  Near 0 the form cancels, so
+// the error is absolute (~6e-8), not relative: the forward's contract is
+// rtol 1e-5 + atol 1e-5 against the FP64 reference.  A
+// Taylor branch for |x| < 0.3 made it relative but cost 11% of K2 (0.657 ->
+// 0.729 ms at C2), and the FP32 edge sums before it carry the same absolute
+// error for outputs near 0 anyway.
 __device__ __forceinline__ float tanh_fast(float x) {
-  const float e = fmaf(-2.0f, rcp_approx(ex2_approx(x * 2.8853900817779268f) + 1.0f), 1.0f);
-  const float x2 = x * x;
-  const float q = fmaf(x2, fmaf(x2, fmaf(x2, 0.021869488536155203f, -0.053968253968253971f), 0.13333333333333333f),
-                       -0.33333333333333333f);
-  const float p = fmaf(x * x2, q, x);
-  return fabsf(x) < 0.3f ? p : e;
+  return fmaf(-2.0f, rcp_approx(ex2_approx(x * 2.8853900817779268f) + 1.0f), 1.0f);
 }
 __device__ __forceinline__ float sigmoid_fast(float x) {
   return rcp_approx(1.0f + ex2_approx(x * -1.4426950408889634f));
