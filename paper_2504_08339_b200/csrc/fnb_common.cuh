@@ -86,6 +86,34 @@ constexpr int kDistanceLaunches = 7;
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// L2 residency hints (createpolicy + ld.global.L2::cache_hint).  A kernel
+// that reads a genome row early, runs a long per-genome phase, and reads the
+// row again (K1's weights, K6's weights) loads it evict_last the first time,
+// so it is still in L2 at the second access, and evict_first the last time,
+// which releases it: the genome crosses HBM once.
+#ifdef __CUDACC__
+__device__ __forceinline__ uint64_t l2_keep() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_drop() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_l2(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld2_l2(const double* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+#endif
+
 struct NetLayout {
   int N, C, I, O;
   size_t ops_off, edges_off, order_off, in_off, out_off, bytes;

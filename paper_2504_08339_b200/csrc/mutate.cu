@@ -827,11 +827,17 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
 
   // rows of the structurally final child: mutable nodes, live connections
   int nn = 0, nc = 0;
+  // rows read here are read-modify-written by apply_normals after the long
+  // decision walk: evict_last (fnb_common.cuh).  Measured at C5: reads 5.64 ->
+  // 5.55 GB, 5.89 -> 5.73 ms; an evict_first re-read made it worse, and an L2
+  // persisting set-aside (75 MB) cut reads to 4.90 GB at the same time -- the
+  // kernel is latency-bound, not HBM-bound (24% occupancy, 50% issue).
+  const uint64_t keep = l2_keep();
   for (int r0 = 0; r0 < N; r0 += 32) {
     const int r = r0 + lane;
     bool h = false;
     if (r < N) {
-      const double k = n[r * kNodeCols + kKey];
+      const double k = ld_l2(n + r * kNodeCols + kKey, keep);
       h = !isnan(k) && !is_key_in(int(k), sh.input_keys, sh.I);
       hid[r] = h;
     }
@@ -839,7 +845,7 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   }
   for (int r0 = 0; r0 < C; r0 += 32) {
     const int r = r0 + lane;
-    const bool live = r < C && !isnan(cc[r * kConnCols + kIn]);
+    const bool live = r < C && !isnan(ld_l2(cc + r * kConnCols + kIn, keep));
     const unsigned bl = __ballot_sync(kFullMask, live);
     if (live) live_row[nc + __popc(bl & ((1u << lane) - 1u))] = int16_t(r);
     nc += __popc(bl);

@@ -278,12 +278,13 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
 
   // ---- 4. connection rows: dangling check, in-degree, predecessor bits in
   //         row and rank space (network.hpp:167-183)
+  const uint64_t keep = l2_keep();  // the weights are read again in step 7
   for (int r0 = 0; r0 < C; r0 += 32) {
     const int r = r0 + lane;
     double cin = __longlong_as_double(0x7ff8000000000000ll), cout = 0, en = 0, w = 0;
     if (r < C) {
-      const double2 a = *reinterpret_cast<const double2*>(crow + r * kConnCols);
-      const double2 b = *reinterpret_cast<const double2*>(crow + r * kConnCols + 2);
+      const double2 a = ld2_l2(crow + r * kConnCols, keep);
+      const double2 b = ld2_l2(crow + r * kConnCols + 2, keep);
       cin = a.x; cout = a.y; en = b.x; w = b.y;
     }
     const bool ne = !isnan(cin);
@@ -539,10 +540,11 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
 
   // ---- 7. edges: the i-th predecessor (ascending source row) of an op goes
   //         to slot i%4 of its record i/4, reading the source's value slot
+  const uint64_t drop = l2_drop();  // the last read of the connection rows
   for (int r = lane; r < C; r += 32) {
-    const double w = crow[r * kConnCols + kW];
     const int dst = s.cdst[r];
     if (dst == kNoRow || (s.flags[dst] & 2)) continue;
+    const double w = ld_l2(crow + r * kConnCols + kW, drop);
     const int src = s.csrc[r];
     int below = 0;
     const int sw = src >> 5;
