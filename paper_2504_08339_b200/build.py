@@ -33,6 +33,12 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    # the glibc log / cos tables of the device normal() (gen_libm_tables.py)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_fnb_libm", os.path.join(PKG, "gen_libm_tables.py"))
+    libm = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(libm)
+    libm.check()
     if not force and not _stale():
         return LIB
     objdir = os.path.join(PKG, "build")
