@@ -119,6 +119,7 @@ void fnb_ctx_destroy(fnb_ctx* ctx) {
     b->release();
   ctx->flags.release();
   ctx->hyper.release();
+  ctx->stage.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) {
     cudaStreamDestroy(ctx->copy_stream);
@@ -338,29 +339,55 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
   const int chunks = int(std::max<size_t>(
       1, std::min<size_t>(std::min<size_t>(fnb_ctx::kMaxChunks, size_t(P)), total / (size_t(chunk_mb) << 20))));
   auto lo_of = [&](int k) { return int((long long)P * k / chunks); };
+  // pageable host arrays (what a std::vector caller passes) go through pinned
+  // bounce buffers: the host threads copy chunk k+1 while chunk k is on the
+  // wire and chunk k-1 in K1/K2 (a plain cudaMemcpyAsync from pageable memory
+  // is staged synchronously by the driver)
+  auto pageable = [](const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+  };
+  const bool staged = pageable(pop_nodes) || pageable(pop_conns);
+  if (staged) {
+    size_t most = 0;
+    for (int k = 0; k < chunks; ++k) most = std::max(most, size_t(lo_of(k + 1) - lo_of(k)) * (nrow + crow));
+    CK(ctx->stage.ensure(most));
+  }
   // the copies must not overwrite buffers still read by earlier work on the compute stream
   CK(cudaEventRecord(ctx->chunk_ev[fnb_ctx::kMaxChunks], ctx->stream));
   CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[fnb_ctx::kMaxChunks], 0));
   uint8_t* dn = static_cast<uint8_t*>(ctx->nodes.p);
   uint8_t* dc = static_cast<uint8_t*>(ctx->conns.p);
-  for (int k = 0; k < chunks; ++k) {
-    const size_t lo = size_t(lo_of(k)), n = size_t(lo_of(k + 1)) - lo;
-    cudaStream_t cs = ctx->copy_stream;
-    CK(cudaMemcpyAsync(dn + lo * nrow, reinterpret_cast<const uint8_t*>(pop_nodes) + lo * nrow, n * nrow,
-                       cudaMemcpyHostToDevice, cs));
-    CK(cudaMemcpyAsync(dc + lo * crow, reinterpret_cast<const uint8_t*>(pop_conns) + lo * crow, n * crow,
-                       cudaMemcpyHostToDevice, cs));
-    CK(cudaEventRecord(ctx->chunk_ev[k], cs));
-  }
   uint8_t* nets = static_cast<uint8_t*>(ctx->nets.p);
   for (int k = 0; k < chunks; ++k) {
     const int lo = lo_of(k), n = lo_of(k + 1) - lo;
+    cudaStream_t cs = ctx->copy_stream;
+    const uint8_t* hn = reinterpret_cast<const uint8_t*>(pop_nodes) + size_t(lo) * nrow;
+    const uint8_t* hc = reinterpret_cast<const uint8_t*>(pop_conns) + size_t(lo) * crow;
+    if (staged) {
+      const int slot = k % HostStage::kSlots;
+      CK(cudaEventSynchronize(ctx->stage.free_ev[slot]));  // that slot's previous chunk has left
+      uint8_t* b = static_cast<uint8_t*>(ctx->stage.buf[slot]);
+      ctx->stage.pool->copy(b, hn, size_t(n) * nrow);
+      ctx->stage.pool->copy(b + size_t(n) * nrow, hc, size_t(n) * crow);
+      hn = b;
+      hc = b + size_t(n) * nrow;
+    }
+    CK(cudaMemcpyAsync(dn + size_t(lo) * nrow, hn, size_t(n) * nrow, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(dc + size_t(lo) * crow, hc, size_t(n) * crow, cudaMemcpyHostToDevice, cs));
+    if (staged) CK(cudaEventRecord(ctx->stage.free_ev[k % HostStage::kSlots], cs));
+    CK(cudaEventRecord(ctx->chunk_ev[k], cs));
+    // chunk k's K1 + K2 on the compute stream as soon as its copy lands
     CK(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[k], 0));
     int st = fnb_transform_d(ctx, reinterpret_cast<const double*>(dn + size_t(lo) * nrow),
                              reinterpret_cast<const double*>(dc + size_t(lo) * crow), n,
                              nets + size_t(lo) * ctx->L.bytes, ctx->stream);
     if (st) return st;
-    // genomes that failed K1 carry no records: K2 runs them as empty programs
+    // genomes that failed K1 carry no records: K2 skips them
     st = fnb_forward_d(ctx, nets + size_t(lo) * ctx->L.bytes, n, static_cast<float*>(ctx->X.p),
                        kind != FNB_FIT_NONE ? static_cast<float*>(ctx->Y.p) : nullptr, batch, kind, offset,
                        d_fit ? d_fit + lo : nullptr, d_out ? d_out + size_t(lo) * batch * O : nullptr, ctx->stream);
