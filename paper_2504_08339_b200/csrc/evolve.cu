@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(128) k_found_rounds(SpeciesDev* sd, int S_old,
 // to [P - hi, P - lo), keeping its (index-ascending) order -- replaces a
 // second 64-bit radix sort with two binary searches per element.
 __global__ void k_desc_from_asc(const unsigned long long* __restrict__ keys, const int* __restrict__ idx, int P,
-                                int* __restrict__ out) {
+                                int* __restrict__ out, int* __restrict__ rank2) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const unsigned long long k = keys[i];
@@ -246,6 +246,7 @@ __global__ void k_desc_from_asc(const unsigned long long* __restrict__ keys, con
     else b = m;
   }
   out[(P - a) + (i - lo)] = idx[i];
+  rank2[i] = lo + a - 1;  // 2 x the mid-rank of position i (oracle E4): the tie group is [lo, a)
 }
 
 __global__ void k_nearest(const double* __restrict__ d, int lo, int hi, int stride, const SpeciesDev* sd,
@@ -397,9 +398,10 @@ __global__ void k_fit_keys(const double* fitness, int P, unsigned long long* asc
   idx[i] = i;
 }
 // mid-ranks (oracle E4): position r of the ascending sort lies in the tie
-// group [lo, hi) of its key; 2 * rank = lo + hi - 1, an exact integer
-__global__ void k_rank_sums(const unsigned long long* __restrict__ sorted_keys, const int* sorted_idx, int P,
-                            const int* species_of, int lo, int hi, SpeciesDev* sd) {
+// group [lo, hi) of its key; 2 * rank = lo + hi - 1 (k_desc_from_asc), an
+// exact integer
+__global__ void k_rank_sums(const int* __restrict__ rank2, const int* sorted_idx, int P, const int* species_of,
+                            int lo, int hi, SpeciesDev* sd) {
   __shared__ unsigned long long s_sum[kMaxSpecies];
   __shared__ int s_cnt[kMaxSpecies];
   for (int t = threadIdx.x; t < kMaxSpecies; t += blockDim.x) {
@@ -412,22 +414,7 @@ __global__ void k_rank_sums(const unsigned long long* __restrict__ sorted_keys, 
   if (r < P && gi >= lo && gi < hi) {  // this process's genomes; ranks are over the whole population
     const int j = species_of[gi];
     if (j >= 0) {
-      const unsigned long long k = sorted_keys[r];
-      int a = 0, b = r;  // lo = first position with key >= k
-      while (a < b) {
-        const int m = (a + b) >> 1;
-        if (sorted_keys[m] < k) a = m + 1;
-        else b = m;
-      }
-      const int lo = a;
-      a = r + 1;
-      b = P;  // hi = first position with key > k
-      while (a < b) {
-        const int m = (a + b) >> 1;
-        if (sorted_keys[m] <= k) a = m + 1;
-        else b = m;
-      }
-      atomicAdd(&s_sum[j], (unsigned long long)(lo + a - 1));
+      atomicAdd(&s_sum[j], (unsigned long long)rank2[r]);
       atomicAdd(&s_cnt[j], 1);
     }
   }
@@ -804,7 +791,7 @@ struct Evolver {
   SpeciesDev* sd = nullptr;
   unsigned long long *kasc = nullptr, *kdesc = nullptr, *ktmp = nullptr;
   int *idx = nullptr, *idx_sorted = nullptr, *idx_tmp = nullptr, *skey = nullptr, *skey_tmp = nullptr;
-  int *fit_idx = nullptr, *oth_idx = nullptr, *status = nullptr, *next_key = nullptr;
+  int *fit_idx = nullptr, *oth_idx = nullptr, *status = nullptr, *next_key = nullptr, *rank2 = nullptr;
   uint32_t *xkeys = nullptr, *mkeys = nullptr;
   uint8_t* active = nullptr;
   void* cub_tmp = nullptr;
@@ -841,6 +828,7 @@ struct Evolver {
     A(&fit_idx, 4 * size_t(P));
     A(&oth_idx, 4 * size_t(P));
     A(&status, 4 * size_t(P));
+    A(&rank2, 4 * size_t(P));
     A(&next_key, 8);
     A(&xkeys, 16 * size_t(P));
     A(&mkeys, 16 * size_t(P));
@@ -868,7 +856,7 @@ struct Evolver {
     release_graphs();
     shard_release();
     void* ps[] = {pn[0], pn[1], pc[0], pc[1], fitness, rep_n, rep_c, dmat, species_of, sd,
-                  kasc, kdesc, ktmp, idx, idx_sorted, idx_tmp, skey, skey_tmp, fit_idx, oth_idx, status, next_key,
+                  kasc, kdesc, ktmp, idx, idx_sorted, idx_tmp, skey, skey_tmp, fit_idx, oth_idx, status, next_key, rank2,
                   xkeys, mkeys, active, cub_tmp, scratch};
     for (void* p : ps)
       if (p) cudaFree(p);
@@ -1046,10 +1034,11 @@ struct Evolver {
             : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
     if (e != cudaSuccess) return e;
     k_spawn_begin<<<1, 1, 0, st>>>(sd);
-    k_rank_sums<<<B, T, 0, st>>>(ktmp, idx_sorted, P, species_of, 0, P, sd);
+    // members by (fitness desc, index asc) for reproduce, and the mid-ranks
+    k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp, rank2);
+    k_rank_sums<<<B, T, 0, st>>>(rank2, idx_sorted, P, species_of, 0, P, sd);
     k_spawn<<<1, 1, 0, st>>>(sd, P, cfg.spawn_rate, cfg.genome_elitism);
-    // ---- reproduce: members by (fitness desc, index asc), then by species
-    k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp);
+    // ---- reproduce: members by species
     k_species_keys<<<B, T, 0, st>>>(idx_tmp, P, species_of, skey);
     e = P <= kCountRankMax
             ? launch_count_sort<int>(skey, idx_tmp, P, skey_tmp, nullptr, idx_sorted, st)
@@ -1306,8 +1295,9 @@ struct Evolver {
                         : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
     if (e != cudaSuccess) return e;
     k_spawn_begin<<<1, 1, 0, st>>>(sd);
-    k_rank_sums<<<B, T, 0, st>>>(ktmp, idx_sorted, P, species_of, lo, hi, sd);
-    *launches += 8 + (hi > lo);
+    k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp, rank2);
+    k_rank_sums<<<B, T, 0, st>>>(rank2, idx_sorted, P, species_of, lo, hi, sd);
+    *launches += 9 + (hi > lo);
     return cudaGetLastError();
   }
   // phase 10 (after the all-gather of species_of): spawn, members, parent
@@ -1316,7 +1306,6 @@ struct Evolver {
   cudaError_t shard_select() {
     const int T = 256, B = (P + T - 1) / T;
     k_spawn<<<1, 1, 0, st>>>(sd, P, cfg.spawn_rate, cfg.genome_elitism);
-    k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp);
     k_species_keys<<<B, T, 0, st>>>(idx_tmp, P, species_of, skey);
     cudaError_t e = P <= kCountRankMax
                         ? launch_count_sort<int>(skey, idx_tmp, P, skey_tmp, nullptr, idx_sorted, st)
@@ -1331,7 +1320,7 @@ struct Evolver {
     k_need<<<B, T, 0, st>>>(fit_idx, oth_idx, P, need);
     k_scan_need<<<1, 1024, 0, st>>>(need, P, prefix);
     k_need_counts<<<1, 32 * ((sh_world + 31) / 32), 0, st>>>(prefix, d_bounds, sh_world, counts);
-    *launches += 9;
+    *launches += 8;
     return cudaGetLastError();
   }
   // phase 11: the shard's parents into the send buffers (M genomes each)
