@@ -433,6 +433,47 @@ def c5_generation(dev, flush, world: int = 1, rank: int = 0, gens: int = 4, warm
                         "(2k distinct genomes tiled)", **r, "scaling": "strong", "timing": "max over ranks"}
 
 
+def rich_schema(dev, stream, flush, reps: int = 5):
+    """The generic forward (k_forward<SPT, -1, -1>: per-node activation and
+    aggregation) on the C2 workload with the rich schema {identity, tanh,
+    sigmoid, relu, sin} x {sum, product, max, mean}, seeds 0..2 of the
+    population generator."""
+    import torch
+    import paper_2504_08339_b200 as fnb
+    syn = synthetic()
+    schema = fnb.AttributeSchema(["identity", "tanh", "sigmoid", "relu", "sin"], ["sum", "product", "max", "mean"])
+    eng = fnb.Engine(fnb.GenomeLimits(N_MAX, C_MAX), list(range(NI)), list(range(NI, NI + NO)), schema,
+                     device=dev.index)
+    X_h, Y_h = syn.regression_dataset(BATCH, NI, NO, seed=0)
+    X = torch.from_numpy(X_h.astype(np.float32)).to(dev)
+    Y = torch.from_numpy(Y_h.astype(np.float32)).to(dev)
+    out = {}
+    for seed in range(3):
+        n_h, c_h = syn.synthetic_population(POP, N_MAX, C_MAX, FILL, NI, NO, n_act=5, n_agg=4, seed=seed)
+        nodes, conns = torch.from_numpy(n_h).to(dev), torch.from_numpy(c_h).to(dev)
+        nets = eng.alloc_nets(POP)
+        fit = torch.empty(POP, dtype=torch.float64, device=dev)
+
+        def run():
+            eng.transform_d(nodes, conns, nets, stream)
+            eng.forward_d(nets, POP, X, Y, fnb.FIT_NEG_MSE, 0.0, fitness=fit, stream=stream)
+
+        run()
+        ms = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        t = float(np.median(ms)) / 1e3
+        out[f"seed{seed}"] = {"transform_plus_forward_ms": t * 1e3, "evals_per_s": POP * BATCH / t}
+    return {"workload": "C2 shapes, rich schema (5 activations x 4 aggregations per node), pop 10k, B=1024",
+            **out}
+
+
 def evolved_population(eng, dev, stream, flush, X, Y, gens: int = 100):
     """K1+K2 on an EVOLVED pop-10k population (100 generations
     of the device loop from minimal genomes on the C2 func-fit data) -- the
@@ -671,7 +712,7 @@ def main():
         except Exception as e:  # noqa: BLE001
             return {"error": repr(e)[:300]}
 
-    c3 = c4 = c5 = c5l = c5g = evo = None
+    c3 = c4 = c5 = c5l = c5g = evo = rich = None
     if rank == 0 and world == 1 and not args.no_c5:
         nets10 = eng.alloc_nets(POP)
         eng.transform_d(torch.from_numpy(all_n).to(dev), torch.from_numpy(all_c).to(dev), nets10, stream)
@@ -680,6 +721,7 @@ def main():
         c4 = section(c4_hyperneat, dev, stream, flush)
         c5 = section(c5_distance, dev, stream, flush)
         c5l = section(c5_distance, dev, stream, flush, 5, "lineage")
+        rich = section(rich_schema, dev, stream, flush)
     if not args.no_c5:
         c5g = section(c5_generation, dev, flush, world, rank)
     if rank == 0 and world == 1 and not args.no_generations:
@@ -741,6 +783,7 @@ def main():
         }
         for k, v in (("weak_scaling", weak), ("generations", gen), ("c5_distance", c5), ("c5_distance_lineage", c5l),
                      ("c3_cppn", c3), ("c4_hyperneat", c4), ("evolved", evo), ("c5_generation", c5g),
+                     ("rich_schema", rich),
                      ("cpu_baseline", cpu)):
             if v is not None:
                 line[k] = v
