@@ -693,24 +693,25 @@ def main():
     h2d = nodes_h.nbytes + conns_h.nbytes + X_h.nbytes + Y_h.nbytes
 
     # ---- generations/s of the pop-10k loop ----
-    gen = None
-    if not args.no_generations:
-        from paper_2504_08339_b200.distributed import ShardedEvolution
-        from paper_2504_08339_b200.evolve import Evolver, NeatConfig
-        ev = Evolver(eng, NeatConfig(pop_size=POP), seed=POP_SEED)
-        ev.set_population(all_n, all_c)
-        shard = ShardedEvolution(ev, X, Y) if world > 1 else None
-        gen = timed_generations(ev, X, Y, dev, flush, world, max(5, args.steps), max(3, args.warmup), shard)
-        gen.update(scaling="strong", note="one pop-10k population per job, C2 shapes, B=1024 func-fit; "
-                                          "max over ranks")
-        ev.close()
-
     def section(fn, *a):
         """A secondary measurement; its failure is reported, never fatal to the headline line."""
         try:
             return fn(*a)
         except Exception as e:  # noqa: BLE001
             return {"error": repr(e)[:300]}
+
+    def generations_c2():
+        from paper_2504_08339_b200.distributed import ShardedEvolution
+        from paper_2504_08339_b200.evolve import Evolver, NeatConfig
+        ev = Evolver(eng, NeatConfig(pop_size=POP), seed=POP_SEED)
+        ev.set_population(all_n, all_c)
+        shard = ShardedEvolution(ev, X, Y) if world > 1 else None
+        g = timed_generations(ev, X, Y, dev, flush, world, max(5, args.steps), max(3, args.warmup), shard)
+        g.update(scaling="strong", note="one pop-10k population per job, C2 shapes, B=1024 func-fit; max over ranks")
+        ev.close()
+        return g
+
+    gen = None if args.no_generations else section(generations_c2)
 
     c3 = c4 = c5 = c5l = c5g = evo = rich = None
     if rank == 0 and world == 1 and not args.no_c5:
@@ -787,7 +788,7 @@ def main():
                      ("cpu_baseline", cpu)):
             if v is not None:
                 line[k] = v
-        if cpu_gen is not None and gen is not None:
+        if cpu_gen is not None and gen is not None and "error" not in gen:
             gen["cpu_baseline"] = cpu_gen
         line["native_so_loaded"] = loaded_native_libs()
         print(json.dumps(line))

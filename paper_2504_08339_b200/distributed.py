@@ -138,6 +138,11 @@ class ShardedGeneration:
         self.backend.before_collective()
         self._gather_rows(nodes)
         self._gather_rows(conns)
+        # every rank must see the lowest failing child, or a failure on one
+        # rank leaves the others waiting in the next collective
+        bad = self.backend.first_bad()
+        if bad is not None and self.world > 1:
+            dist.all_reduce(bad, op=dist.ReduceOp.MIN, group=self.group)
         self.backend.after_collective()
         self.backend.step_commit()
 
@@ -196,6 +201,13 @@ class DeviceShardBackend:
 
     def step_commit(self):
         self.ev.step_commit()
+
+    def first_bad(self):
+        """The evolver's lowest-failing-child word (device int32 view)."""
+        if not hasattr(self, "_first_bad"):
+            self.ev.shard_init([0, self.pop_size])
+            self._first_bad = self.ev.shard_buffers()["first_bad"]
+        return self._first_bad
 
     def checksum(self) -> int:
         return self.ev.checksum()

@@ -61,3 +61,15 @@ def test_synthetic_population_is_valid():
         t = ol.oracle_transform(prob, ol.RICH, n, c)
         assert t["status"] == 0 and t["order_count"] == 48
         assert int(np.sum(~np.isnan(c[:, 0]))) == 192
+
+
+def test_python_innovation_table_mirrors_reference():
+    """api.InnovationTable == ops.hpp:145-167: memo per generation, counter never runs back."""
+    from paper_2504_08339_b200.api import InnovationTable
+    t = InnovationTable(10)
+    assert t.get_or_assign(1, 2) == 10 and t.get_or_assign(3, 4) == 11 and t.get_or_assign(1, 2) == 10
+    t.reserve_up_to(5)
+    assert t.next_key() == 12
+    t.reserve_up_to(20)
+    t.next_generation()
+    assert t.get_or_assign(1, 2) == 20 and t.next_key() == 21

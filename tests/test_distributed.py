@@ -93,6 +93,11 @@ class OracleShardBackend:
         self.orc.nodes = self.next[0].numpy().copy()
         self.orc.conns = self.next[1].numpy().copy()
 
+    def first_bad(self):
+        # the oracle's children never fail: each rank reports "none"
+        self.bad = torch.tensor([2 ** 31 - 1], dtype=torch.int32)
+        return self.bad
+
     def checksum(self):
         return host_checksum(self.orc.nodes, self.orc.conns)
 

@@ -19,6 +19,8 @@ CASES = {
     "founding": (301, (24, 80), 0.7, 8, 15, 8),
     "stagnation": (240, (20, 60), 0.9, 6, 1, 8),
     "overflow": (150, (20, 60), 0.05, 4, 3, 6),
+    # BASELINE config 2 genome shape, 2,000 genomes: many founding rounds across both shards
+    "c2-shape": (2000, (64, 256), 1.2, 10, 15, 4),
 }
 
 
@@ -26,7 +28,8 @@ def _make(case, seed=31):
     import paper_2504_08339_b200 as fnb
     from paper_2504_08339_b200.evolve import Evolver, NeatConfig
     P, limits, th, ms, stag, G = CASES[case]
-    eng = fnb.Engine(fnb.GenomeLimits(*limits), [0, 1, 2], [3], fnb.AttributeSchema(ACTS, AGGS))
+    ni = 4 if limits[0] >= 64 else 3
+    eng = fnb.Engine(fnb.GenomeLimits(*limits), list(range(ni)), [ni], fnb.AttributeSchema(ACTS, AGGS))
     m = fnb.MutationConfig()
     m.node_add, m.conn_add, m.node_delete, m.conn_delete = 0.4, 0.6, 0.05, 0.05
     cfg = NeatConfig(pop_size=P, compatibility_threshold=th, max_species=ms, max_stagnation=stag, mutation=m)
@@ -35,10 +38,10 @@ def _make(case, seed=31):
     return eng, ev, G
 
 
-def _data():
+def _data(ni=3):
     import torch
     from paper_2504_08339_b200.synthetic import regression_dataset
-    X, Y = regression_dataset(64, 3, 1, seed=9)
+    X, Y = regression_dataset(64, ni, 1, seed=9)
     return (torch.as_tensor(X, dtype=torch.float32, device="cuda"),
             torch.as_tensor(Y, dtype=torch.float32, device="cuda"))
 
@@ -46,7 +49,7 @@ def _data():
 def _reference_run(case):
     """The one-process device loop: evaluate + fnb_evolver_step per generation."""
     eng, ev, G = _make(case)
-    X, Y = _data()
+    X, Y = _data(eng.num_inputs)
     out = []
     for _ in range(G):
         ev.evaluate_d(X, Y)
@@ -60,7 +63,7 @@ def _reference_run(case):
 def _sharded_run(case, world=1, rank=0):
     from paper_2504_08339_b200.distributed import ShardedEvolution
     eng, ev, G = _make(case)
-    X, Y = _data()
+    X, Y = _data(eng.num_inputs)
     se = ShardedEvolution(ev, X, Y)
     out = []
     for _ in range(G):
