@@ -57,6 +57,43 @@ def config_dict(world: int) -> dict:
             "l2": "flushed between timed steps (GPU arm)"}
 
 
+def streaming_rooflines(net_bytes_c2=None, net_bytes_c5=None):
+    """HBM rooflines of the streaming step kernels from the committed ncu
+    summary (profiles/*_ncu_summary.json; cold-cache, serialised durations):
+    DRAM bytes, the algorithmic bytes (genomes read + written), achieved
+    GB/s and the fraction of the measured HBM peak.  C5 = pop 100k N128/C1024
+    (37,888 B per genome), C2 = pop 10k N64/C256 (10,752 B)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")))
+    if not files:
+        return None
+    d = json.load(open(files[-1]))
+    peak, peak_src = hbm_peak()
+    g5, g2 = 37_888, 10_752
+    # kernel: (genome reads, genome writes, genome bytes, population, extra bytes written per genome)
+    alg = {"step_c5_k_transform": (1, 0, g5, 100_000), "step_c5_k_crossover": (2, 1, g5, 100_000),
+           "step_c5_k_mutate_apply": (1, 0, g5, 100_000), "step_c5_k_mutate_attrs": (1, 1, g5, 100_000),
+           "k3_distance_c5": (1, 0, g5, 100_000), "k1_transform_c2": (1, 0, g2, 10_000),
+           "step_c2_k_crossover": (2, 1, g2, 10_000), "step_c2_k_mutate_apply": (1, 0, g2, 10_000),
+           "step_c2_k_mutate_attrs": (1, 1, g2, 10_000)}
+    out = {}
+    extra = {"step_c5_k_transform": net_bytes_c5 or 0, "k1_transform_c2": net_bytes_c2 or 0}  # K1 writes a NetLayout block
+    for k, (r, w, gb, pop) in alg.items():
+        v = d.get(k)
+        if not v or "duration_us" not in v:
+            continue
+        t = v["duration_us"] * 1e-6
+        a = (r + w) * gb * pop + extra.get(k, 0) * pop
+        dram = v.get("dram_read", 0.0) + v.get("dram_write", 0.0)
+        out[k] = {"ms": t * 1e3, "algorithmic_bytes": a, "dram_bytes": dram, "achieved_GBps": a / t / 1e9,
+                  "frac_of_hbm": a / t / 1e9 / peak, "dram_over_algorithmic": dram / a if a else None}
+    return {"source": os.path.relpath(files[-1], ROOT), "peak_GBps": peak, "peak_source": peak_src,
+            "note": "algorithmic bytes = genomes read + written in the canonical FP64 layout (+ the NetLayout block "
+                    "K1 writes); crossover reads two parents (elites read one), mutate_apply reads and rewrites only "
+                    "structural edits; at C2 the population fits L2, so DRAM bytes can be below the algorithmic bytes",
+            "kernels": out}
+
+
 def cpu_info() -> dict:
     model, threads = None, os.cpu_count() or 1
     try:
@@ -790,6 +827,11 @@ def main():
                 line[k] = v
         if cpu_gen is not None and gen is not None and "error" not in gen:
             gen["cpu_baseline"] = cpu_gen
+        nb5 = fnb.Engine(fnb.GenomeLimits(128, 1024), list(range(NI)), list(range(NI, NI + NO)), fnb.AttributeSchema(),
+                         device=local).net_bytes
+        sr = streaming_rooflines(eng.net_bytes, nb5)
+        if sr is not None:
+            line["streaming_rooflines"] = sr
         line["native_so_loaded"] = loaded_native_libs()
         print(json.dumps(line))
     if world > 1:
