@@ -463,7 +463,39 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   //          find-first-zero and one queue update.  The used mask is a W-word
   //          register array indexed only by unrolled loops.
   int n_slots = 0;
-  if (lane == 0) {
+  if (W == 2 && lane == 0) {
+    // N <= 64: the used mask is one 64-bit register and free_at one 64-bit
+    // word per op (the same lowest-free-slot allocation, fewer instructions
+    // on this single-lane chain)
+    unsigned long long used = 0ull;
+    unsigned long long* fa = reinterpret_cast<unsigned long long*>(free_at);
+    auto alloc = [&]() {
+      const int sl = __ffsll(static_cast<long long>(~used)) - 1;
+      used |= 1ull << sl;
+      n_slots = max(n_slots, sl + 1);
+      return sl;
+    };
+    auto retire = [&](int sl, int lu) {
+      if (lu < 0) used &= ~(1ull << sl);
+      else if (lu != kLastForever) fa[lu] |= 1ull << sl;
+    };
+    for (int i = 0; i < sh.I; ++i) {
+      const int r = in_rows[i];
+      if (slot_of[r] == 0xffff) {
+        const int sl = alloc();
+        slot_of[r] = uint16_t(sl);
+        const int lu = last_use[r];
+        if (lu >= 0) retire(sl, lu);
+      }
+    }
+    for (int k = 0; k < op_base; ++k) {
+      used &= ~fa[k];
+      const int row = s.op_row[k];
+      const int sl = alloc();
+      slot_of[row] = uint16_t(sl);
+      retire(sl, last_use[row]);
+    }
+  } else if (lane == 0) {
     uint32_t used[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) used[w] = 0u;
