@@ -149,3 +149,43 @@ def test_evolve_error_context(fnb):
         ev.run(X, Y, generation_limit=3)
     assert ei.value.code == "cycle_detected" and ei.value.index == 17
     assert "generation 0, genome 17: cycle " in str(ei.value)
+
+
+def test_run_graph_cache_follows_the_problem(fnb):
+    """The generation graphs cached across fnb_evolve calls bake in the
+    problem's device buffers: a run on another dataset (another batch size,
+    so the input buffer moves) must equal the step loop on that dataset."""
+    from paper_2504_08339_b200.synthetic import regression_dataset
+    eng, cfg, a, X, Y = _setup(fnb, P=200)
+    _, _, b, _, _ = _setup(fnb, P=200)
+    a.init_population()
+    b.init_population()
+    a.run(X, Y, generation_limit=3)
+    for _ in range(3):
+        b.evaluate(X, Y)
+        b.step()
+    X2, Y2 = regression_dataset(300, 3, 1, seed=11)
+    _, _, stats = a.run(X2, Y2, generation_limit=3)
+    for g in range(3):
+        b.evaluate(X2, Y2)
+        f = b.fitness()
+        assert stats[g].best == f.max()
+        b.step()
+    an, ac = a.population()
+    bn, bc = b.population()
+    assert np.array_equal(_bits(an), _bits(bn)) and np.array_equal(_bits(ac), _bits(bc))
+
+
+def test_checkpoint_before_any_step(fnb):
+    """A checkpoint of a fresh population (no species yet) restores and runs like the original."""
+    eng, cfg, a, X, Y = _setup(fnb, P=150)
+    a.init_population()
+    text = a.save_checkpoint()
+    _, _, b, _, _ = _setup(fnb, P=150, seed=7)
+    b.load_checkpoint(text)
+    _, _, sa = a.run(X, Y, generation_limit=4)
+    _, _, sb = b.run(X, Y, generation_limit=4)
+    assert _stats_key(sa) == _stats_key(sb)
+    an, ac = a.population()
+    bn, bc = b.population()
+    assert np.array_equal(_bits(an), _bits(bn)) and np.array_equal(_bits(ac), _bits(bc))
