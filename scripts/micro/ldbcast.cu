@@ -1,6 +1,6 @@
 // Microbenchmark (round-2 K2 investigation): cost of warp-uniform record
-// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/micro/ldbcast scripts/micro/ldbcast.cu
 // fetches -- LDS.128 / LDS.64 broadcast vs LDG.128 (L1 hit) broadcast.
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/micro/ldbcast scripts/micro/ldbcast.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 
