@@ -1528,9 +1528,12 @@ static int evolver_eval_enqueue(fnb_evolver* ev, int lo, int n, const float* d_X
   ev->eval_lo = lo;
   ev->eval_n = n;
   fnb::k_eval_flags_init<<<1, 1, 0, v.st>>>(fl);
+  ++ctx->launches;
   const size_t nx = size_t(batch) * ctx->sh.I;
-  fnb::k_nonfinite_f32<<<int(std::min<size_t>((nx + 255) / 256, 148)), 256, 0, v.st>>>(d_X, nx, fl + 1);
-  ctx->launches += 2;
+  if (nx > 0) {
+    fnb::k_nonfinite_f32<<<int(std::min<size_t>((nx + 255) / 256, 148)), 256, 0, v.st>>>(d_X, nx, fl + 1);
+    ++ctx->launches;
+  }
   if (n == 0) return 0;
   EV_CK(fnb::launch_transform(v.pn[v.cur] + size_t(lo) * v.gn(), v.pc[v.cur] + size_t(lo) * v.gc(), n,
                               static_cast<uint8_t*>(ev->nets.p), ctx->L, ctx->sh, v.st));
