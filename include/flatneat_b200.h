@@ -127,6 +127,10 @@ void fnb_set_forward_spt(int spt);
  * max_nodes + 1 (default 62), group_kb shared-memory budget per genome group
  * (default 72).  Fitness bits do not depend on any of them. */
 void fnb_set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb);
+/* main-pass record capacity in % of the most records a genome can have
+ * (default set in forward.cu); genomes with more records run in the overflow
+ * pass.  Process-wide; fitness bits do not depend on it. */
+void fnb_set_forward_recs_pct(int pct);
 
 /* ---- host layer (synchronous) ------------------------------------------ */
 

@@ -27,6 +27,7 @@ int launch_forward(const void* nets, NetLayout L, int P, const float* X, const f
 size_t forward_partial_needed(NetLayout L, int P, int B);
 void set_forward_spt(int spt);
 void set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb);
+void set_forward_recs_pct(int pct);
 cudaError_t launch_to_float(const double* src, float* dst, size_t n, int* bad, cudaStream_t st);
 }  // namespace fnb
 
@@ -136,6 +137,8 @@ void fnb_set_forward_spt(int spt) { set_forward_spt(spt); }
 void fnb_set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb) {
   set_forward_tuning(spt, max_cols, rows_pct, group_kb);
 }
+
+void fnb_set_forward_recs_pct(int pct) { set_forward_recs_pct(pct); }
 
 // ---- device layer ------------------------------------------------------
 

@@ -158,11 +158,15 @@ struct FwdParams {
   double* partial;      // [P][units]: squared error of each 32-sample unit
   int units;            // ceil(B / 32)
   size_t group_smem;    // bytes per group
-  int rows_lo, rows_hi; // this pass evaluates genomes needing rows_lo < n_slots+1 <= rows_hi value rows
+  // this pass evaluates genomes that fit (n_slots + 1 <= rows_hi value rows and
+  // n_rec + 1 <= recs_hi records) and, for the overflow pass, do not fit the
+  // main pass's (prev_rows, prev_recs); prev_rows = 0 in the main pass
+  int rows_hi, recs_hi, prev_rows, prev_recs;
+  uint32_t rec_bytes;   // record area of a group (recs_hi records, 16-byte aligned)
 };
 
-__host__ __device__ inline size_t fwd_group_smem(int N, int C, int I, int O, int T, int spt, int rows) {
-  size_t b = align16(size_t(max_records(N, C) + 1) * sizeof(SRec));  // + zero sentinel
+__host__ __device__ inline size_t fwd_group_smem(int N, int C, int I, int O, int T, int spt, int rows, int recs) {
+  size_t b = align16(size_t(recs) * sizeof(SRec));  // records + the zero sentinel
   b += align16(size_t(I + O) * sizeof(uint32_t));
   b += size_t(rows) * size_t(T) * spt * sizeof(float);      // value slots + zero slot
   return align16(b);
@@ -179,7 +183,7 @@ k_forward(FwdParams p) {
   const NetLayout& L = p.L;
   uint8_t* base = smem_raw + size_t(grp < p.groups ? grp : 0) * p.group_smem;
   SRec* s_rec = reinterpret_cast<SRec*>(base);
-  uint32_t* s_io = reinterpret_cast<uint32_t*>(base + align16(size_t(max_records(L.N, L.C) + 1) * sizeof(SRec)));
+  uint32_t* s_io = reinterpret_cast<uint32_t*>(base + p.rec_bytes);
   uint8_t* v = reinterpret_cast<uint8_t*>(s_io) + align16(size_t(L.I + L.O) * sizeof(uint32_t));
   const int TC = T * SPT;                                 // columns per tile
   const uint32_t row_shift = uint32_t(__ffs(TC * 4) - 1);  // v row stride = TC*4 bytes (a power of two)
@@ -188,10 +192,13 @@ k_forward(FwdParams p) {
 
   bool live = grp < p.groups && g < p.P;
   int n_rec = 0, n_slots = 0;
-  if (live) {  // genomes whose live values need more slots go to the overflow pass
+  if (live) {  // genomes needing more value rows or records than the main pass holds go to the overflow pass
     const NetHeader* hd = reinterpret_cast<const NetHeader*>(p.nets + size_t(g) * L.bytes);
     n_slots = hd->n_slots;
-    live = hd->status == 0 && n_slots + 1 > p.rows_lo && n_slots + 1 <= p.rows_hi;
+    const int nr = hd->n_rec;
+    const bool fits = n_slots + 1 <= p.rows_hi && nr + 1 <= p.recs_hi;
+    const bool fits_main = n_slots + 1 <= p.prev_rows && nr + 1 <= p.prev_recs;
+    live = hd->status == 0 && fits && (p.prev_rows == 0 || !fits_main);
   }
   if (live) {
     const uint8_t* net = p.nets + size_t(g) * L.bytes;
@@ -374,34 +381,43 @@ __global__ void k_to_float(const double* __restrict__ src, float* __restrict__ d
 // ---- host launchers --------------------------------------------------------
 
 struct FwdConfig {
-  int T, spt, block, groups, chunks, grid_x, rows;
+  int T, spt, block, groups, chunks, grid_x, rows, recs;
   size_t group_smem, cta_smem;
 };
 
 static int g_force_spt = 0;       // tuning override (fnb_set_forward_spt)
-static int g_rows_pct = 62;       // main-pass slot capacity, % of max_nodes + 1
-static int g_max_cols = 128;      // sample columns per genome group (tile width; swept, scripts/sweep_forward.py)
+static int g_rows_pct = 0;        // main-pass slot capacity, % of max_nodes + 1 (0: by shape, main_rows)
+static int g_max_cols = 256;      // sample columns per genome group (tile width; swept, scripts/sweep_forward.py)
 static int g_group_kb = 72;       // shared-memory budget of one genome group
+static int g_recs_pct = 60;       // main-pass record capacity, % of max_records + 1
 
 // Launch geometry for `rows` value rows per column (slots + the zero slot).
-static FwdConfig fwd_config(const NetLayout& L, int P, int B, int rows, bool single_chunk) {
+static FwdConfig fwd_config(const NetLayout& L, int P, int B, int rows, int recs, bool single_chunk) {
   FwdConfig c{};
   c.rows = rows;
+  c.recs = recs;
   // columns per group: cover the batch, at most 256, shrinking until a
   // group fits ~72 KB (>= 3 resident CTAs per SM)
   int cols = 1;
   while (cols < B && cols < g_max_cols) cols <<= 1;
   int spt = g_force_spt ? g_force_spt : (cols >= 128 ? 2 : 1);
-  while (cols > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, std::max(1, cols / spt), spt, rows) > size_t(g_group_kb) * 1024)
+  while (cols > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, std::max(1, cols / spt), spt, rows, recs) > size_t(g_group_kb) * 1024)
     cols >>= 1;
   spt = std::min(spt, cols);
   const int T = std::max(1, cols / spt);
   c.spt = spt;
   c.T = T;
-  c.group_smem = fwd_group_smem(L.N, L.C, L.I, L.O, T, spt, rows);
-  // groups per CTA: up to 256 threads and ~96 KB of shared memory
-  int groups = std::max(1, 256 / T);
-  while (groups > 1 && c.group_smem * groups > 96 * 1024) groups >>= 1;
+  c.group_smem = fwd_group_smem(L.N, L.C, L.I, L.O, T, spt, rows, recs);
+  // groups per CTA: up to 256 threads, chosen to fit the most groups into an
+  // SM's 228 KB (each CTA also reserves 1 KB): at C2 (24.6 KB groups) 1 or 3
+  // groups per CTA make 9 resident groups where 2 or 4 make 8
+  int groups = 1, best = 0;
+  for (int g = 1; g <= std::max(1, 256 / T); ++g) {
+    const size_t cta = c.group_smem * size_t(g) + 1024;
+    if (cta > 227 * 1024 + 1024) break;
+    const int resident = int((228 * 1024) / cta) * g;
+    if (resident > best) { best = resident; groups = g; }
+  }
   c.groups = groups;
   c.block = std::max(32, groups * T);
   c.cta_smem = c.group_smem * groups;
@@ -413,16 +429,27 @@ static FwdConfig fwd_config(const NetLayout& L, int P, int B, int rows, bool sin
   return c;
 }
 
+// Main-pass capacities (round-2 sweep, scripts/sweep_forward.py and
+// scripts/exp_forward_cfg.py, fill-0.75 populations): 62% of the value rows
+// at N_max <= 64 (C2: 0.643 -> 0.608 ms together with 256-column tiles and
+// 60% of the records) and 72% above (C5: 5.43 -> 5.20 ms per 20k genomes);
+// genomes beyond either capacity run in the overflow pass
 static int main_rows(const NetLayout& L) {
-  return std::min(L.N + 1, std::max(16, ((L.N + 1) * g_rows_pct + 99) / 100));
+  const int pct = g_rows_pct ? g_rows_pct : (L.N <= 64 ? 62 : 72);
+  return std::min(L.N + 1, std::max(16, ((L.N + 1) * pct + 99) / 100));
 }
+static int all_recs(const NetLayout& L) { return max_records(L.N, L.C) + 1; }
+static int main_recs(const NetLayout& L) {
+  return std::min(all_recs(L), std::max(16, (all_recs(L) * g_recs_pct + 99) / 100));
+}
+void set_forward_recs_pct(int pct) { g_recs_pct = (pct >= 10 && pct <= 100) ? pct : 60; }
 
 void set_forward_spt(int spt) { g_force_spt = (spt == 1 || spt == 2 || spt == 4) ? spt : 0; }
-void set_forward_rows_pct(int pct) { g_rows_pct = (pct >= 10 && pct <= 100) ? pct : 62; }
+void set_forward_rows_pct(int pct) { g_rows_pct = (pct >= 10 && pct <= 100) ? pct : 0; }
 void set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb) {
   set_forward_spt(spt);
   set_forward_rows_pct(rows_pct);
-  g_max_cols = (max_cols >= 32 && max_cols <= 1024 && (max_cols & (max_cols - 1)) == 0) ? max_cols : 128;
+  g_max_cols = (max_cols >= 32 && max_cols <= 1024 && (max_cols & (max_cols - 1)) == 0) ? max_cols : 256;
   g_group_kb = (group_kb >= 8 && group_kb <= 220) ? group_kb : 72;
 }
 
@@ -465,13 +492,17 @@ static cudaError_t launch_spt(const FwdConfig& c, const FwdParams& p, int agg, i
   return launch_k<SPT, -1, -1>(c, p, st);
 }
 
-static cudaError_t launch_pass(const FwdConfig& c, FwdParams p, int rows_lo, int agg, int act, cudaStream_t st) {
+static cudaError_t launch_pass(const FwdConfig& c, FwdParams p, int prev_rows, int prev_recs, int agg, int act,
+                               cudaStream_t st) {
   if (c.cta_smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   p.T = c.T;
   p.groups = c.groups;
   p.group_smem = c.group_smem;
-  p.rows_lo = rows_lo;
   p.rows_hi = c.rows;
+  p.recs_hi = c.recs;
+  p.prev_rows = prev_rows;
+  p.prev_recs = prev_recs;
+  p.rec_bytes = uint32_t(align16(size_t(c.recs) * sizeof(SRec)));
   switch (c.spt) {
     case 4: return launch_spt<4>(c, p, agg, act, st);
     case 2: return launch_spt<2>(c, p, agg, act, st);
@@ -507,8 +538,8 @@ static FwdAux& fwd_aux() {
 int launch_forward(const void* nets, NetLayout L, int P, const float* X, const float* Y, int B, int fit_kind,
                    double offset, double* fitness, double* out, double* partial_buf, size_t partial_cap,
                    int uniform_agg, int uniform_act, cudaStream_t st, long long* launches) {
-  const int rows_main = main_rows(L);
-  const FwdConfig c = fwd_config(L, P, B, rows_main, false);
+  const int rows_main = main_rows(L), recs_main = main_recs(L);
+  const FwdConfig c = fwd_config(L, P, B, rows_main, recs_main, false);
   FwdParams p;
   p.nets = static_cast<const uint8_t*>(nets);
   p.L = L;
@@ -524,21 +555,21 @@ int launch_forward(const void* nets, NetLayout L, int P, const float* X, const f
   p.units = fitness_units(B);
   const bool fit = fit_kind != FNB_FIT_NONE;
   if (fit && sizeof(double) * size_t(P) * p.units > partial_cap) return 1;
-  if (rows_main < L.N + 1) {
+  if (rows_main < L.N + 1 || recs_main < all_recs(L)) {
     // The overflow pass (a few genomes, long per-CTA latency) runs on a side
     // stream next to the main pass instead of as a tail after it; both write
     // disjoint genomes' units, so no bit depends on the overlap.
     FwdAux& x = fwd_aux();
     if (!x.side) return 1;
-    const FwdConfig co = fwd_config(L, P, B, L.N + 1, true);
+    const FwdConfig co = fwd_config(L, P, B, L.N + 1, all_recs(L), true);
     if (cudaEventRecord(x.fork, st) != cudaSuccess || cudaStreamWaitEvent(x.side, x.fork, 0) != cudaSuccess) return 1;
-    if (launch_pass(co, p, rows_main, uniform_agg, uniform_act, x.side) != cudaSuccess) return 1;
+    if (launch_pass(co, p, rows_main, recs_main, uniform_agg, uniform_act, x.side) != cudaSuccess) return 1;
     if (cudaEventRecord(x.join, x.side) != cudaSuccess) return 1;
-    if (launch_pass(c, p, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
+    if (launch_pass(c, p, 0, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
     if (cudaStreamWaitEvent(st, x.join, 0) != cudaSuccess) return 1;
     *launches += 2;
   } else {
-    if (launch_pass(c, p, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
+    if (launch_pass(c, p, 0, 0, uniform_agg, uniform_act, st) != cudaSuccess) return 1;
     ++*launches;
   }
   if (fit) {

@@ -131,7 +131,7 @@ __device__ inline void tf_fail(uint8_t* net, int status, int kind, int a, int b,
   h->n_ops = 0;
   h->n_edges = 0;
   h->n_rec = 0;
-  h->n_slots = -2;  // never inside any forward pass's (rows_lo, rows_hi] window
+  h->n_slots = -2;  // no value-slot count (K2 also skips the genome by its status)
 }
 
 template <int W>

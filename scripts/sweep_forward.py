@@ -56,24 +56,30 @@ def main():
     base_ms = run()
     base_fit = fit.clone()
     res = []
-    grid = ((1, 2, 4), (64, 128, 256, 512), (45, 55, 62, 75, 100), (48, 72, 96))
+    grid = ((2, 4), (128, 256, 512), (45, 50, 55, 62, 75), (72,))
+    recs_grid = (40, 50, 60, 75, 100)
+    if os.environ.get("FNB_SWEEP_GRID"):  # JSON [[spt...], [cols...], [pct...], [kb...], [recs_pct...]]
+        g = json.loads(os.environ["FNB_SWEEP_GRID"])
+        grid, recs_grid = tuple(tuple(x) for x in g[:4]), tuple(g[4])
     if os.environ.get("FNB_SWEEP_SHAPE") == "c5":
-        grid = ((2, 4), (64, 128, 256), (30, 40, 50, 62, 75), (48, 72, 96, 144, 200))
-    for spt, cols, pct, kb in itertools.product(*grid):
+        grid = ((2, 4), (64, 128, 256), (30, 40, 50, 62, 75), (72, 144))
+    for spt, cols, pct, kb, rp in itertools.product(*grid, recs_grid):
         lib.fnb_set_forward_tuning(spt, cols, pct, kb)
+        lib.fnb_set_forward_recs_pct(rp)
         try:
             ms = run()
         except Exception as e:  # geometry that does not fit is reported, not fatal
-            res.append({"spt": spt, "cols": cols, "pct": pct, "kb": kb, "error": str(e)[:80]})
+            res.append({"spt": spt, "cols": cols, "pct": pct, "kb": kb, "recs_pct": rp, "error": str(e)[:80]})
             continue
         same = bool(torch.equal(fit, base_fit))
-        res.append({"spt": spt, "cols": cols, "pct": pct, "kb": kb, "ms": ms, "bit_equal": same})
-        assert same, ("fitness bits changed with the launch geometry", spt, cols, pct, kb)
+        res.append({"spt": spt, "cols": cols, "pct": pct, "kb": kb, "recs_pct": rp, "ms": ms, "bit_equal": same})
+        assert same, ("fitness bits changed with the launch geometry", spt, cols, pct, kb, rp)
     lib.fnb_set_forward_tuning(0, 0, 0, 0)
+    lib.fnb_set_forward_recs_pct(0)
     ok = sorted([r for r in res if "ms" in r], key=lambda r: r["ms"])
     best_by_spt = {spt: min((r for r in ok if r["spt"] == spt), key=lambda r: r["ms"], default=None)
-                   for spt in (1, 2, 4)}
-    print(json.dumps({"default_ms": base_ms, "best": ok[:12], "best_by_spt": best_by_spt,
+                   for spt in (2, 4)}
+    print(json.dumps({"default_ms": base_ms, "best": ok[:12], "all": ok, "best_by_spt": best_by_spt,
                       "errors": [r for r in res if "error" in r][:5], "n": len(res)}, indent=1))
 
 
