@@ -151,7 +151,7 @@ inline int warps_per_cta_for_smem(size_t per_warp, int max_warps) {
   }();
   int best_w = 1;
   long best = -1;
-  for (int w = max_warps; w >= 1; w >>= 1) {
+  for (int w = max_warps; w >= 1; --w) {
     long ctas = long(smem_sm) / long(size_t(w) * per_warp + 1024);
     if (ctas > 32) ctas = 32;
     if (ctas * w > best) {
