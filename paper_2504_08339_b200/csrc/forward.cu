@@ -21,6 +21,7 @@
 // Arithmetic is FP32 (north star: 1e-5 relative to the FP64 reference); the
 // squared-error fitness accumulates in FP64.
 #include <algorithm>
+#include <cstdlib>
 
 #include "fnb_common.cuh"
 
@@ -400,7 +401,12 @@ static FwdConfig fwd_config(const NetLayout& L, int P, int B, int rows, int recs
   // group fits ~72 KB (>= 3 resident CTAs per SM)
   int cols = 1;
   while (cols < B && cols < g_max_cols) cols <<= 1;
-  int spt = g_force_spt ? g_force_spt : (cols >= 128 ? 2 : 1);
+  static const int env_spt = [] {  // experiment knob (fnb_set_forward_spt overrides)
+    const char* e = std::getenv("FNB_FWD_SPT");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int force = g_force_spt ? g_force_spt : (env_spt == 1 || env_spt == 2 || env_spt == 4 ? env_spt : 0);
+  int spt = force ? force : (cols >= 128 ? 2 : 1);
   while (cols > 32 && fwd_group_smem(L.N, L.C, L.I, L.O, std::max(1, cols / spt), spt, rows, recs) > size_t(g_group_kb) * 1024)
     cols >>= 1;
   spt = std::min(spt, cols);
@@ -426,6 +432,11 @@ static FwdConfig fwd_config(const NetLayout& L, int P, int B, int rows, int recs
   const int target = 4 * 148;  // >= 4 CTAs per SM before splitting samples
   c.chunks = 1;
   if (!single_chunk && c.grid_x < target) c.chunks = std::min(tiles, (target + c.grid_x - 1) / c.grid_x);
+  static const int force_chunks = [] {  // experiment knob: sample tiles split over blockIdx.y
+    const char* e = std::getenv("FNB_FWD_CHUNKS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (!single_chunk && force_chunks > 0) c.chunks = std::min(tiles, force_chunks);
   return c;
 }
 
