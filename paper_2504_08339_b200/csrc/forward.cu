@@ -68,8 +68,11 @@ __device__ __forceinline__ float act_apply(int code, float x) {
 }
 
 // ---- staged record (32 B, two float4) ---------------------------------------
-//   a = {bias, resp, meta, srcs}   meta = dst | cnt << 8 | first << 11 | last << 12
-//                                         | act << 13 | agg << 16 | fanin << 18
+//   a = {bias, resp, meta, srcs}   meta = dst | valid << 8 | first << 12 | last << 13
+//                                         | act << 16 | agg << 19 | fanin << 21
+//                                  valid = one bit per real edge slot; the slot
+//                                  bits and first / last share byte 1, so one
+//                                  R2P sets all six predicates
 //                                  srcs = four u8 source rows (row N = zero row)
 //   w = {w0, w1, w2, w3}
 struct SRec {
@@ -112,6 +115,21 @@ __device__ __forceinline__ void lds_pred(bool p, uint32_t addr, float (&x)[SPT])
   } else {
     asm volatile("{ .reg .pred q; setp.ne.b32 q, %4, 0; @q ld.shared.v4.f32 {%0, %1, %2, %3}, [%5]; }"
                  : "+f"(x[0]), "+f"(x[1]), "+f"(x[2]), "+f"(x[3]) : "r"(int(p)), "r"(addr));
+  }
+}
+// the same with the predicate bit B of `word` (a single LOP3 into a predicate)
+template <int SPT, uint32_t B>
+__device__ __forceinline__ void lds_bit(uint32_t word, uint32_t addr, float (&x)[SPT]) {
+  if constexpr (SPT == 1) {
+    asm volatile("{ .reg .pred q; .reg .b32 t; and.b32 t, %1, %2; setp.ne.b32 q, t, 0; @q ld.shared.f32 %0, [%3]; }"
+                 : "+f"(x[0]) : "r"(word), "n"(B), "r"(addr));
+  } else if constexpr (SPT == 2) {
+    asm volatile("{ .reg .pred q; .reg .b32 t; and.b32 t, %2, %3; setp.ne.b32 q, t, 0; @q ld.shared.v2.f32 {%0, %1}, [%4]; }"
+                 : "+f"(x[0]), "+f"(x[1]) : "r"(word), "n"(B), "r"(addr));
+  } else {
+    asm volatile("{ .reg .pred q; .reg .b32 t; and.b32 t, %4, %5; setp.ne.b32 q, t, 0; "
+                 "@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%6]; }"
+                 : "+f"(x[0]), "+f"(x[1]), "+f"(x[2]), "+f"(x[3]) : "r"(word), "n"(B), "r"(addr));
   }
 }
 template <int SPT>
@@ -176,6 +194,7 @@ __host__ __device__ inline size_t fwd_group_smem(int N, int C, int I, int O, int
 template <int SPT, int AGG, int ACT>
 __global__ void __launch_bounds__(256)
 k_forward(FwdParams p) {
+  constexpr bool kBounded = ACT == FNB_ACT_TANH || ACT == FNB_ACT_SIGMOID;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int T = p.T;
   const int grp = threadIdx.x / T;
@@ -207,8 +226,8 @@ k_forward(FwdParams p) {
     const Rec* gr = reinterpret_cast<const Rec*>(net + L.ops_off);
     for (int i = j; i < n_rec; i += T) {
       const Rec r = gr[i];
-      const uint32_t meta = uint32_t(r.h.dst) | (uint32_t(r.h.cnt) << 8) | (uint32_t(r.h.flags) << 11) |
-                            (uint32_t(r.h.act) << 13) | (uint32_t(r.h.agg) << 16) | (uint32_t(r.h.fanin) << 18);
+      const uint32_t meta = uint32_t(r.h.dst) | (((1u << r.h.cnt) - 1u) << 8) | (uint32_t(r.h.flags) << 12) |
+                            (uint32_t(r.h.act) << 16) | (uint32_t(r.h.agg) << 19) | (uint32_t(r.h.fanin) << 21);
       const uint32_t srcs = uint32_t(r.slot[0].src) | (uint32_t(r.slot[1].src) << 8) |
                             (uint32_t(r.slot[2].src) << 16) | (uint32_t(r.slot[3].src) << 24);
       s_rec[i] = SRec{make_float4(r.h.bias, r.h.resp, __uint_as_float(meta), __uint_as_float(srcs)),
@@ -254,23 +273,30 @@ k_forward(FwdParams p) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k) acc[k] = 0.0f;
     SRec cur = s_rec[0];
+    float x0[SPT], x1[SPT], x2[SPT], x3[SPT];
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) x0[k] = x1[k] = x2[k] = x3[k] = 0.0f;
 #pragma unroll 1
     for (int r = 0; r < n_rec; ++r) {
       const uint32_t meta = __float_as_uint(cur.a.z);
       const uint32_t srcs = __float_as_uint(cur.a.w);
-      const int cnt = int((meta >> 8) & 7u);
-      const bool first = (meta >> 11) & 1u;
-      const bool last = (meta >> 12) & 1u;
-      const int agg = AGG >= 0 ? AGG : int((meta >> 16) & 3u);
-      float x0[SPT], x1[SPT], x2[SPT], x3[SPT];
+      const bool first = (meta >> 12) & 1u;
+      const bool last = (meta >> 13) & 1u;
+      const int agg = AGG >= 0 ? AGG : int((meta >> 19) & 3u);
+      // pad slots are predicated off (no shared-memory traffic; their weight
+      // is 0).  With a bounded activation every value a slot register can
+      // hold (an input, a node value, 0) is finite, so a pad slot's stale
+      // operand contributes 0 * x = +-0 and the registers need no zeroing;
+      // otherwise (identity / relu could overflow to inf) they are zeroed.
+      if (!kBounded) {
 #pragma unroll
-      for (int k = 0; k < SPT; ++k) x0[k] = x1[k] = x2[k] = x3[k] = 0.0f;
-      // pad slots are predicated off (no shared-memory traffic), reading 0
+        for (int k = 0; k < SPT; ++k) x0[k] = x1[k] = x2[k] = x3[k] = 0.0f;
+      }
       // one PRMT (byte extract) + one IMAD (row address) per slot
-      lds_pred<SPT>(cnt > 0, vb + __byte_perm(srcs, 0u, 0x4440) * row_bytes, x0);
-      lds_pred<SPT>(cnt > 1, vb + __byte_perm(srcs, 0u, 0x4441) * row_bytes, x1);
-      lds_pred<SPT>(cnt > 2, vb + __byte_perm(srcs, 0u, 0x4442) * row_bytes, x2);
-      lds_pred<SPT>(cnt > 3, vb + __byte_perm(srcs, 0u, 0x4443) * row_bytes, x3);
+      lds_bit<SPT, 1u << 8>(meta, vb + __byte_perm(srcs, 0u, 0x4440) * row_bytes, x0);
+      lds_bit<SPT, 1u << 9>(meta, vb + __byte_perm(srcs, 0u, 0x4441) * row_bytes, x1);
+      lds_bit<SPT, 1u << 10>(meta, vb + __byte_perm(srcs, 0u, 0x4442) * row_bytes, x2);
+      lds_bit<SPT, 1u << 11>(meta, vb + __byte_perm(srcs, 0u, 0x4443) * row_bytes, x3);
       if (agg == FNB_AGG_SUM || agg == FNB_AGG_MEAN) {
         // pad slots contribute 0 * 0: branch-free, ascending source row
 if constexpr (SPT == 1) {
@@ -292,6 +318,7 @@ if constexpr (SPT == 1) {
           }
         }
       } else {
+        const int cnt = __popc((meta >> 8) & 15u);  // real slots are a prefix
         const float w[4] = {cur.w.x, cur.w.y, cur.w.z, cur.w.w};
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
@@ -316,7 +343,7 @@ if constexpr (SPT == 1) {
       cur.w = s_rec[r + 1].w;
       if (last) {
         if (agg == FNB_AGG_MEAN) {
-          const uint32_t fanin = meta >> 18;
+          const uint32_t fanin = meta >> 21;
           if (fanin > 0) {
             const float rn = rcp_approx(float(fanin));  // fanin <= 255: rcp.approx is within 1 ulp
 #pragma unroll
@@ -326,7 +353,7 @@ if constexpr (SPT == 1) {
         float y[SPT];
 #pragma unroll
         for (int k = 0; k < SPT; ++k)
-          y[k] = act_apply<ACT>(int((meta >> 13) & 7u), fmaf(cur.a.y, acc[k], cur.a.x));
+          y[k] = act_apply<ACT>(int((meta >> 16) & 7u), fmaf(cur.a.y, acc[k], cur.a.x));
         sts<SPT>(vb + ((meta & 0xffu) << row_shift), y);
       }
       cur.a = s_rec[r + 1].a;
