@@ -195,6 +195,9 @@ template <int SPT, int AGG, int ACT>
 __global__ void __launch_bounds__(256)
 k_forward(FwdParams p) {
   constexpr bool kBounded = ACT == FNB_ACT_TANH || ACT == FNB_ACT_SIGMOID;
+  // {sum} schemas: the accumulators are reset at each finalize instead of on
+  // each op's first record
+  constexpr bool kSumOnly = AGG == FNB_AGG_SUM;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int T = p.T;
   const int grp = threadIdx.x / T;
@@ -276,7 +279,7 @@ k_forward(FwdParams p) {
     float x0[SPT], x1[SPT], x2[SPT], x3[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) x0[k] = x1[k] = x2[k] = x3[k] = 0.0f;
-#pragma unroll 1
+#pragma unroll 2
     for (int r = 0; r < n_rec; ++r) {
       const uint32_t meta = __float_as_uint(cur.a.z);
       const uint32_t srcs = __float_as_uint(cur.a.w);
@@ -300,7 +303,7 @@ k_forward(FwdParams p) {
       if (agg == FNB_AGG_SUM || agg == FNB_AGG_MEAN) {
         // pad slots contribute 0 * 0: branch-free, ascending source row
 if constexpr (SPT == 1) {
-          float a = first ? 0.0f : acc[0];
+          float a = (kSumOnly || !first) ? acc[0] : 0.0f;
           a = fmaf(cur.w.x, x0[0], a);
           a = fmaf(cur.w.y, x1[0], a);
           a = fmaf(cur.w.z, x2[0], a);
@@ -309,7 +312,7 @@ if constexpr (SPT == 1) {
         } else {
 #pragma unroll
           for (int k = 0; k < SPT; k += 2) {
-            unsigned long long a = first ? 0ull : pk2(acc[k], acc[k + 1]);
+            unsigned long long a = (kSumOnly || !first) ? pk2(acc[k], acc[k + 1]) : 0ull;
             a = ffma2(cur.w.x, pk2(x0[k], x0[k + 1]), a);
             a = ffma2(cur.w.y, pk2(x1[k], x1[k + 1]), a);
             a = ffma2(cur.w.z, pk2(x2[k], x2[k + 1]), a);
@@ -354,7 +357,11 @@ if constexpr (SPT == 1) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k)
           y[k] = act_apply<ACT>(int((meta >> 16) & 7u), fmaf(cur.a.y, acc[k], cur.a.x));
-        sts<SPT>(vb + ((meta & 0xffu) << row_shift), y);
+        sts<SPT>(vb + (meta & 0xffu) * row_bytes, y);
+        if constexpr (kSumOnly) {
+#pragma unroll
+          for (int k = 0; k < SPT; ++k) acc[k] = 0.0f;  // the next op starts from 0
+        }
       }
       cur.a = s_rec[r + 1].a;
     }
