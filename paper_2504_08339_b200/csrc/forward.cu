@@ -247,6 +247,7 @@ k_forward(FwdParams p) {
   __syncthreads();
 
   const int I = L.I, O = L.O;
+  const bool vec_x = (reinterpret_cast<uintptr_t>(p.X) & 15) == 0;
   // fitness units: 32 consecutive samples, reduced by an adjacent-pair tree
   // (in-thread over SPT, then shfl_xor over the unit's lanes); samples >= B
   // add exact zeros, so a unit's sum depends on neither T, SPT, the chunking
@@ -262,12 +263,34 @@ k_forward(FwdParams p) {
   const int t_hi = live ? min(tiles, t_lo + per) : t_lo;
   for (int tile = t_lo; tile < t_hi; ++tile) {
     const int s0 = tile * TC + j * SPT;  // first sample of this thread
-    // seed input rows (network.hpp:249-250)
-    for (int i = 0; i < I; ++i) {
+    // seed input rows (network.hpp:249-250).  A thread's SPT samples are
+    // SPT*I consecutive floats of X; with I = 4 they are read as SPT float4
+    // (two lines per warp-instruction instead of eight scalar loads' worth)
+    if (I == 4 && s0 + SPT <= p.B && vec_x) {
+      const float4* xs = reinterpret_cast<const float4*>(p.X + size_t(s0) * 4);
+      float4 v[SPT];
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) v[k] = __ldg(xs + k);
       float x[SPT];
 #pragma unroll
-      for (int k = 0; k < SPT; ++k) x[k] = (s0 + k < p.B) ? __ldg(p.X + size_t(s0 + k) * I + i) : 0.0f;
-      sts<SPT>(vb + s_io[i], x);
+      for (int k = 0; k < SPT; ++k) x[k] = v[k].x;
+      sts<SPT>(vb + s_io[0], x);
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) x[k] = v[k].y;
+      sts<SPT>(vb + s_io[1], x);
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) x[k] = v[k].z;
+      sts<SPT>(vb + s_io[2], x);
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) x[k] = v[k].w;
+      sts<SPT>(vb + s_io[3], x);
+    } else {
+      for (int i = 0; i < I; ++i) {
+        float x[SPT];
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) x[k] = (s0 + k < p.B) ? __ldg(p.X + size_t(s0 + k) * I + i) : 0.0f;
+        sts<SPT>(vb + s_io[i], x);
+      }
     }
     // ops in topological order (network.hpp:252-264), one record per step.
     // cur.w is reloaded once this record's FMAs are done and cur.a after its
