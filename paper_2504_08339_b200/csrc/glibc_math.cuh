@@ -29,11 +29,14 @@ namespace glibc {
 #define GM_SUB(a, b) __dsub_rn((a), (b))
 #define GM_MUL(a, b) __dmul_rn((a), (b))
 #define GM_SQRT(a) __dsqrt_rn(a)
-__device__ static const double kLogA[5] = FNB_LIBM_LOG_A;
-__device__ static const double kLogB[11] = FNB_LIBM_LOG_B;
+// polynomial coefficients (constant indices): constant-bank operands of the DFMAs
+__constant__ static const double kLogA[5] = FNB_LIBM_LOG_A;
+__constant__ static const double kLogB[11] = FNB_LIBM_LOG_B;
+// lookup tables (data-dependent indices): read-only global loads
 __device__ static const double kLogTab[256] = FNB_LIBM_LOG_TAB;
 __device__ static const double kSinCos[FNB_LIBM_SINCOSTAB_N] = FNB_LIBM_SINCOSTAB;
 #define GM_TAB(t, i) __ldg(&(t)[i])
+#define GM_CT(t, i) ((t)[i])
 #else
 #define GM_FMA(a, b, c) std::fma((a), (b), (c))
 #define GM_ADD(a, b) ((a) + (b))
@@ -45,6 +48,7 @@ static const double kLogB[11] = FNB_LIBM_LOG_B;
 static const double kLogTab[256] = FNB_LIBM_LOG_TAB;
 static const double kSinCos[FNB_LIBM_SINCOSTAB_N] = FNB_LIBM_SINCOSTAB;
 #define GM_TAB(t, i) ((t)[i])
+#define GM_CT(t, i) ((t)[i])
 #endif
 
 __host__ __device__ __forceinline__ uint64_t bits(double x) {
@@ -72,20 +76,20 @@ __host__ __device__ inline double log(double x) {
   if (ix - 0x3fee000000000000ull < 0x3090000000000ull) {  // |x - 1| small: polynomial path
     if (ix == 0x3ff0000000000000ull) return 0.0;
     const double r = GM_SUB(x, FNB_LIBM_ONE);
-    double p = GM_FMA(r, GM_TAB(kLogB, 2), GM_TAB(kLogB, 1));
-    double q = GM_FMA(r, GM_TAB(kLogB, 5), GM_TAB(kLogB, 4));
-    double s = GM_FMA(r, GM_TAB(kLogB, 8), GM_TAB(kLogB, 7));
+    double p = GM_FMA(r, GM_CT(kLogB, 2), GM_CT(kLogB, 1));
+    double q = GM_FMA(r, GM_CT(kLogB, 5), GM_CT(kLogB, 4));
+    double s = GM_FMA(r, GM_CT(kLogB, 8), GM_CT(kLogB, 7));
     const double r2 = GM_MUL(r, r);
-    p = GM_FMA(r2, GM_TAB(kLogB, 3), p);
-    q = GM_FMA(r2, GM_TAB(kLogB, 6), q);
+    p = GM_FMA(r2, GM_CT(kLogB, 3), p);
+    q = GM_FMA(r2, GM_CT(kLogB, 6), q);
     const double r3 = GM_MUL(r, r2);
-    s = GM_FMA(r2, GM_TAB(kLogB, 9), s);
-    s = GM_FMA(r3, GM_TAB(kLogB, 10), s);
+    s = GM_FMA(r2, GM_CT(kLogB, 9), s);
+    s = GM_FMA(r3, GM_CT(kLogB, 10), s);
     q = GM_FMA(s, r3, q);
     p = GM_FMA(q, r3, p);
     const double t = GM_FMA(r, FNB_LIBM_TWO27, r);     // r + r*2^27
     const double rhi = GM_FMA(-FNB_LIBM_TWO27, r, t);  // (r + w) - w
-    const double b0 = GM_TAB(kLogB, 0);
+    const double b0 = GM_CT(kLogB, 0);
     const double rhi2 = GM_MUL(rhi, rhi);
     const double rlo = GM_SUB(r, rhi);
     const double hi = GM_FMA(rhi2, b0, r);
@@ -105,15 +109,15 @@ __host__ __device__ inline double log(double x) {
   const double kd = double(k);
   const double w = GM_FMA(kd, FNB_LIBM_LN2HI, logc);
   const double r = GM_FMA(z, invc, FNB_LIBM_MINUS_ONE);
-  const double p1 = GM_FMA(r, GM_TAB(kLogA, 2), GM_TAB(kLogA, 1));
+  const double p1 = GM_FMA(r, GM_CT(kLogA, 2), GM_CT(kLogA, 1));
   const double hi = GM_ADD(r, w);
   const double r2 = GM_MUL(r, r);
   double t = GM_SUB(w, hi);
   t = GM_ADD(t, r);
   double lo = GM_FMA(kd, FNB_LIBM_LN2LO, t);
   const double r3 = GM_MUL(r, r2);
-  const double p2 = GM_FMA(r, GM_TAB(kLogA, 4), GM_TAB(kLogA, 3));
-  lo = GM_FMA(r2, GM_TAB(kLogA, 0), lo);
+  const double p2 = GM_FMA(r, GM_CT(kLogA, 4), GM_CT(kLogA, 3));
+  lo = GM_FMA(r2, GM_CT(kLogA, 0), lo);
   const double q = GM_FMA(p2, r2, p1);
   const double y = GM_FMA(r3, q, lo);
   return GM_ADD(y, hi);

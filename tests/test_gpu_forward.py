@@ -131,6 +131,36 @@ def test_batch_forward_matches_reference(fnb, seed, limits, schema_name):
         np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("act", ["tanh", "sigmoid", "identity", "relu"])
+def test_single_activation_sum_kernels(fnb, act):
+    """The {act},{sum} K2 instantiations (forward.cu) against the reference,
+    and bit for bit against the generic kernel (a two-function schema whose
+    first entries are the same functions, so the genomes mean the same).
+    Bounded activations (tanh, sigmoid) leave pad-slot operand registers
+    stale, unbounded ones zero them: with weights scaled by 1e20 the FP32
+    identity / relu values overflow to +-inf (and inf - inf to NaN), where a
+    stale inf under a pad slot's zero weight would turn an inf into NaN."""
+    schema = ol.SchemaSpec([act], ["sum"])
+    other = "identity" if act != "identity" else "tanh"
+    generic = ol.SchemaSpec([act, other], ["sum", "product"])
+    prob = ol.Problem(24, 96, [0, 1, 2], [3])
+    nodes, conns = ol.random_genomes(515, schema, 160, 24, 96)
+    rng = np.random.default_rng(515)
+    X = rng.uniform(-2, 2, size=(300, 3))
+    eng, eng_g = _engine(fnb, prob, schema), _engine(fnb, prob, generic)
+    want = _ref_forward(prob, schema, nodes, conns, X)
+    got = eng.batch_forward(nodes, conns, X).values
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    assert np.array_equal(got, eng_g.batch_forward(nodes, conns, X).values)
+    big = conns.copy()
+    big[:, :, 3] *= 1e20
+    got = eng.batch_forward(nodes, big, X).values
+    ref = eng_g.batch_forward(nodes, big, X).values
+    if act in ("identity", "relu"):
+        assert not np.isfinite(ref).all()  # the case is exercised
+    assert np.array_equal(got, ref, equal_nan=True), act
+
+
 def test_forward_c2_shape_and_fitness(fnb):
     """Config-2 shape (N_max=64, C_max=256, fill 0.75) on a 512-genome slice."""
     from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population
