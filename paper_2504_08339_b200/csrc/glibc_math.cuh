@@ -35,7 +35,14 @@ __constant__ static const double kLogB[11] = FNB_LIBM_LOG_B;
 // lookup tables (data-dependent indices): read-only global loads
 __device__ static const double kLogTab[256] = FNB_LIBM_LOG_TAB;
 __device__ static const double kSinCos[FNB_LIBM_SINCOSTAB_N] = FNB_LIBM_SINCOSTAB;
-#define GM_TAB(t, i) __ldg(&(t)[i])
+// the tables (6 KB) stay L1-resident next to the genome rows the mutation
+// kernels stream through L1 (evict_last: evicted after normal-priority lines)
+__device__ __forceinline__ double ld_table(const double* a) {
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(a));
+  return v;
+}
+#define GM_TAB(t, i) ld_table(&(t)[i])
 #define GM_CT(t, i) ((t)[i])
 #else
 #define GM_FMA(a, b, c) std::fma((a), (b), (c))
