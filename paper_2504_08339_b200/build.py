@@ -18,6 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+# experiment builds (A/B variants in a package copy): extra nvcc flags, e.g. -DFNB_GLIBC_BF=0
+FLAGS += os.environ.get("FNB_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -112,6 +112,12 @@ __device__ __forceinline__ double2 ld2_l2(const double* a, uint64_t pol) {
   asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
   return v;
 }
+// One TMA bulk prefetch of [a, a + bytes) into L2 (bytes a multiple of 16, a
+// 16-byte aligned): a warp that will stream a genome's rows after a long
+// shared-memory phase issues it first, so the rows come from L2, not HBM.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* a, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+}
 #endif
 
 struct NetLayout {

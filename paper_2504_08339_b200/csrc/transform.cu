@@ -13,6 +13,8 @@
 // weights block their target exactly like the reference), the
 // initial-ready `key >= 0` filter (network.hpp:195), and incoming edges in
 // ascending source row (network.hpp:184-190).
+#include <cstdlib>
+
 #include "fnb_common.cuh"
 
 namespace fnb {
@@ -137,7 +139,7 @@ __device__ inline void tf_fail(uint8_t* net, int status, int kind, int a, int b,
 template <int W>
 __global__ void __launch_bounds__(128)
 k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, int P,
-            uint8_t* __restrict__ nets, NetLayout L, DevShape sh, size_t smem_per_warp) {
+            uint8_t* __restrict__ nets, NetLayout L, DevShape sh, size_t smem_per_warp, int l2_prefetch) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -146,6 +148,9 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   TfSmem s = tf_carve(smem_raw + size_t(warp) * smem_per_warp, N, C, W);
   const double* nrow = nodes + size_t(g) * N * kNodeCols;
   const double* crow = conns + size_t(g) * C * kConnCols;
+  // the connection rows are first read in step 4, after the node, rank and
+  // hash phases: one bulk prefetch brings them to L2 meanwhile
+  if (l2_prefetch && lane == 0) prefetch_l2_bulk(crow, uint32_t(C) * kConnCols * 8u);
   uint8_t* net = nets + size_t(g) * L.bytes;
 
   // ---- 1. node rows: keys, activation/aggregation ids (network.hpp:139-152);
@@ -279,13 +284,27 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   // ---- 4. connection rows: dangling check, in-degree, predecessor bits in
   //         row and rank space (network.hpp:167-183)
   const uint64_t keep = l2_keep();  // the weights are read again in step 7
+  // rows of the next two 32-row chunks are in flight while a chunk is processed
+  const double2 kNoConn = make_double2(__longlong_as_double(0x7ff8000000000000ll), 0.0);
+  double2 qa0 = kNoConn, qb0 = kNoConn, qa1 = kNoConn, qb1 = kNoConn;
+  if (lane < C) {
+    qa0 = ld2_l2(crow + lane * kConnCols, keep);
+    qb0 = ld2_l2(crow + lane * kConnCols + 2, keep);
+  }
+  if (32 + lane < C) {
+    qa1 = ld2_l2(crow + (32 + lane) * kConnCols, keep);
+    qb1 = ld2_l2(crow + (32 + lane) * kConnCols + 2, keep);
+  }
   for (int r0 = 0; r0 < C; r0 += 32) {
     const int r = r0 + lane;
-    double cin = __longlong_as_double(0x7ff8000000000000ll), cout = 0, en = 0, w = 0;
-    if (r < C) {
-      const double2 a = ld2_l2(crow + r * kConnCols, keep);
-      const double2 b = ld2_l2(crow + r * kConnCols + 2, keep);
-      cin = a.x; cout = a.y; en = b.x; w = b.y;
+    const double cin = qa0.x, cout = qa0.y, en = qb0.x, w = qb0.y;
+    qa0 = qa1;
+    qb0 = qb1;
+    qa1 = kNoConn;
+    qb1 = kNoConn;
+    if (r + 64 < C) {
+      qa1 = ld2_l2(crow + (r + 64) * kConnCols, keep);
+      qb1 = ld2_l2(crow + (r + 64) * kConnCols + 2, keep);
     }
     const bool ne = !isnan(cin);
     int src = -1, dst = -1;
@@ -688,7 +707,11 @@ static cudaError_t launch_transform_w(const double* n, const double* c, int P, u
   cudaError_t e = cudaFuncSetAttribute(k_transform<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   const int blocks = (P + warps - 1) / warps;
-  k_transform<W><<<blocks, 32 * warps, smem, st>>>(n, c, P, nets, L, sh, per_warp);
+  static const int l2pf = [] {  // experiment knob: measured neutral at C5, 4% slower at C2 (default off)
+    const char* e = std::getenv("FNB_K1_L2PF");
+    return e ? std::atoi(e) : 0;
+  }();
+  k_transform<W><<<blocks, 32 * warps, smem, st>>>(n, c, P, nets, L, sh, per_warp, l2pf);
   return cudaGetLastError();
 }
 
