@@ -118,6 +118,12 @@ __device__ __forceinline__ double2 ld2_l2(const double* a, uint64_t pol) {
 __device__ __forceinline__ void prefetch_l2_bulk(const void* a, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
 }
+// the same for any byte range (widened to 16-byte boundaries)
+__device__ __forceinline__ void prefetch_l2_range(const void* a, size_t bytes) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15);
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(a) + bytes + 15) & ~uintptr_t(15);
+  if (hi > lo) prefetch_l2_bulk(reinterpret_cast<const void*>(lo), uint32_t(hi - lo));
+}
 #endif
 
 struct NetLayout {

@@ -23,6 +23,8 @@
 // (glibc_math.cuh) and apply them.
 #include <climits>
 
+#include <cstdlib>
+
 #include "fnb_common.cuh"
 #include "glibc_math.cuh"
 #include "keytable.cuh"
@@ -496,7 +498,7 @@ __global__ void __launch_bounds__(128, 8)
 k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
                int n_children, const uint8_t* __restrict__ active, int N, int C, MutCfgDev cfg, DevShape sh,
                const int* __restrict__ plan_flag, const unsigned long long* __restrict__ plan_pair,
-               const int* __restrict__ new_key, int* __restrict__ status, size_t smem_per_warp) {
+               const int* __restrict__ new_key, int* __restrict__ status, size_t smem_per_warp, int l2_prefetch) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -508,6 +510,11 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
   MutSmem sm = mut_carve(smem_raw + size_t(warp) * smem_per_warp, N, C);
   double* n = nodes + size_t(c) * N * kNodeCols;
   double* cc = conns + size_t(c) * C * kConnCols;
+  // the staging loops walk the child chunk by chunk: its rows go to L2 first
+  if (l2_prefetch && lane == 0) {
+    prefetch_l2_range(cc, size_t(C) * kConnCols * 8);
+    prefetch_l2_range(n, size_t(N) * kNodeCols * 8);
+  }
   const Key4 key = load_key(keys, c);
   const int Hn = table_capacity(N), W = (N + 31) / 32;
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
@@ -801,7 +808,7 @@ template <typename DW>
 __global__ void __launch_bounds__(256)
 k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
                int n_children, const uint8_t* __restrict__ active, const int* __restrict__ status, int N, int C,
-               MutCfgDev cfg, DevShape sh, int win, size_t smem_per_warp) {
+               MutCfgDev cfg, DevShape sh, int win, size_t smem_per_warp, int l2_prefetch) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -824,6 +831,10 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   double* n = nodes + size_t(c) * N * kNodeCols;
   double* cc = conns + size_t(c) * C * kConnCols;
   const Key4 k5 = key_split(load_key(keys, c), 5);
+  if (l2_prefetch && lane == 0) {  // the row scans below walk the child chunk by chunk
+    prefetch_l2_range(cc, size_t(C) * kConnCols * 8);
+    prefetch_l2_range(n, size_t(N) * kNodeCols * 8);
+  }
 
   // rows of the structurally final child: mutable nodes, live connections
   int nn = 0, nc = 0;
@@ -1013,8 +1024,12 @@ cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* ke
   cudaError_t e = cudaFuncSetAttribute(k_mutate_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(per_warp * warps));
   if (e != cudaSuccess) return e;
+  static const int l2pf = [] {  // experiment knob
+    const char* e = std::getenv("FNB_K6_L2PF");
+    return e ? std::atoi(e) : 1;
+  }();
   k_mutate_apply<<<(k + warps - 1) / warps, 32 * warps, per_warp * warps, st>>>(
-      nd, cd, ky, k, ac, N, C, cfg, sh, ms.flag + lo, ms.pair + lo, ms.newk + lo, d_status + lo, per_warp);
+      nd, cd, ky, k, ac, N, C, cfg, sh, ms.flag + lo, ms.pair + lo, ms.newk + lo, d_status + lo, per_warp, l2pf);
   const int win = attr_window(N, C, attr_per_node(cfg));
   const bool narrow = attr_words_narrow(cfg);
   const size_t aw = attr_smem_bytes(N, C, win, narrow);
@@ -1023,7 +1038,7 @@ cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* ke
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(aw * awarps));
   if (e != cudaSuccess) return e;
   kern<<<(k + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nd, cd, ky, k, ac, d_status + lo, N, C, cfg, sh,
-                                                                    win, aw);
+                                                                    win, aw, l2pf);
   *launches += 2;
   return cudaGetLastError();
 }
