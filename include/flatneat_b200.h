@@ -131,6 +131,13 @@ void fnb_set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb);
  * (default set in forward.cu); genomes with more records run in the overflow
  * pass.  Process-wide; fitness bits do not depend on it. */
 void fnb_set_forward_recs_pct(int pct);
+/* host-buffer transfer format of fnb_evaluate / fnb_batch_forward
+ * (process-wide): 1 (default) packs the FP64 rows of PAGEABLE host arrays on
+ * the host threads into the transfer rows K1 reads (0.40 of the bytes at C2,
+ * converted exactly as K1 converts the FP64 rows) instead of staging them
+ * whole; 0 stages and sends the FP64 rows.  Pinned arrays are sent as they are
+ * either way.  Results are identical. */
+void fnb_set_host_transfer_packed(int on);
 
 /* ---- host layer (synchronous) ------------------------------------------ */
 

@@ -94,6 +94,7 @@ SIGNATURES = {
     "fnb_set_forward_spt": (None, [C.c_int]),
     "fnb_set_forward_tuning": (None, [C.c_int, C.c_int, C.c_int, C.c_int]),
     "fnb_set_forward_recs_pct": (None, [C.c_int]),
+    "fnb_set_host_transfer_packed": (None, [C.c_int]),
     "fnb_transform": (C.c_int, [VP, DP, DP, C.c_int, IP, IP]),
     "fnb_batch_forward": (C.c_int, [VP, DP, DP, C.c_int, DP, C.c_int, DP]),
     "fnb_evaluate": (C.c_int, [VP, DP, DP, C.c_int, DP, DP, C.c_int, C.c_int, C.c_double, DP]),

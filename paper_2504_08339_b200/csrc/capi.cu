@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <chrono>
 #include <vector>
 
 #include "fnb_common.cuh"
@@ -16,6 +17,8 @@ namespace fnb {
 // host launchers (transform.cu / forward.cu)
 cudaError_t launch_transform(const double* n, const double* c, int P, uint8_t* nets, const NetLayout& L,
                              const DevShape& sh, cudaStream_t st);
+cudaError_t launch_transform_packed(const uint8_t* packed, int P, uint8_t* nets, const NetLayout& L,
+                                    const DevShape& sh, cudaStream_t st);
 cudaError_t launch_describe_cycle(const double* n, const double* c, const uint8_t* net, const NetLayout& L,
                                   int* path, cudaStream_t st);
 cudaError_t launch_first_error(const uint8_t* nets, size_t stride, int P, int* out, cudaStream_t st);
@@ -120,6 +123,7 @@ void fnb_ctx_destroy(fnb_ctx* ctx) {
     b->release();
   ctx->flags.release();
   ctx->hyper.release();
+  ctx->packed.release();
   ctx->stage.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) {
@@ -139,6 +143,23 @@ void fnb_set_forward_tuning(int spt, int max_cols, int rows_pct, int group_kb) {
 }
 
 void fnb_set_forward_recs_pct(int pct) { set_forward_recs_pct(pct); }
+
+// host transfer format (fnb_set_host_transfer_packed; FNB_H2D_PACK=0 starts it off)
+static std::atomic<bool> g_host_pack{[] {
+  const char* e = std::getenv("FNB_H2D_PACK");
+  return !(e && std::atoi(e) == 0);
+}()};
+// share (%) of the chunks of a PINNED population that are packed (tuning:
+// FNB_H2D_PACK_PINNED_PCT, scripts/h2d_trace.sh).  Measured at C2 on the B200
+// host (16 cores): 0% 2.23-2.31 ms, 30% 3.2-3.3, 50% 2.3-2.5, 70% 2.2-2.4,
+// 100% 2.36 ms per call -- the host's memory bandwidth bounds the DMA and the
+// packers together, so pinned arrays go up as they are (0)
+static std::atomic<int> g_pinned_pack_pct{[] {
+  const char* e = std::getenv("FNB_H2D_PACK_PINNED_PCT");
+  const int v = e ? std::atoi(e) : 0;
+  return v < 0 ? 0 : v > 100 ? 100 : v;
+}()};
+void fnb_set_host_transfer_packed(int on) { g_host_pack.store(on != 0); }
 
 // ---- device layer ------------------------------------------------------
 
@@ -290,9 +311,19 @@ static int ensure_pipeline(fnb_ctx* ctx) {
 // the device and read once at the end, in the reference's order: the lowest
 // failing genome's transform error (network.hpp:122-220), then a non-finite
 // input (network.hpp:245-246).
+//
+// Transfer format.  Pageable host arrays (a std::vector caller) are staged
+// through pinned buffers anyway; by default the host threads pack each chunk
+// into K1's transfer rows there (PackedLayout: 0.40 of the bytes at C2,
+// converted exactly as K1 converts the FP64 rows) and only those cross PCIe;
+// K1 reads them (launch_transform_packed): C2 e2e 2.3 -> 4.4 G evals/s.
+// Pinned arrays go up by DMA as they are.  The FP64 rows go up for a packed
+// call only to rebuild an error message, or for the whole call when a node's
+// act / agg id does not fit the packed byte.  fnb_set_host_transfer_packed(0)
+// (or FNB_H2D_PACK=0) stages the FP64 rows.
 static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* pop_conns, int P,
                          const double* inputs, const double* targets, int batch, int kind, double offset,
-                         double* fitness_out, double* out) {
+                         double* fitness_out, double* out, bool allow_pack = true) {
   ctx->err.clear();
   ctx->err_index = -1;
   if (P <= 0) return 0;
@@ -300,8 +331,29 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
   if (int st = ensure_pipeline(ctx)) return st;
   const int N = ctx->L.N, Cm = ctx->L.C, O = ctx->L.O;
   const size_t nrow = sizeof(double) * size_t(N) * kNodeCols, crow = sizeof(double) * size_t(Cm) * kConnCols;
-  CK(ctx->nodes.ensure(nrow * size_t(P)));
-  CK(ctx->conns.ensure(crow * size_t(P)));
+  auto pageable = [](const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+  };
+  // Which chunks are packed: every chunk of pageable arrays (they are staged
+  // through host memory anyway: ~2x the e2e at C2); for pinned arrays a share
+  // (g_pinned_pack_pct) -- the host threads pack those while the DMA engine
+  // streams the others' FP64 rows straight from the caller's buffers, so the
+  // two host-memory consumers run side by side.
+  const bool src_pageable = pageable(pop_nodes) || pageable(pop_conns);
+  const int pack_pct = !(allow_pack && g_host_pack.load()) ? 0 : src_pageable ? 100 : g_pinned_pack_pct.load();
+  const bool pack = pack_pct > 0;
+  auto is_pk = [&](int k) { return pack_pct > 0 && ((k + 1) * pack_pct) / 100 > (k * pack_pct) / 100; };
+  const PackedLayout pkl(N, Cm);
+  if (pack_pct < 100) {
+    CK(ctx->nodes.ensure(nrow * size_t(P)));
+    CK(ctx->conns.ensure(crow * size_t(P)));
+  }
+  if (pack) CK(ctx->packed.ensure(pkl.bytes * size_t(P)));
   CK(ctx->nets.ensure(ctx->L.bytes * size_t(P)));
   CK(ctx->flags.ensure(4 * sizeof(int)));
   int* d_flags = static_cast<int*>(ctx->flags.p);  // [0] first failing genome, [1] non-finite X, [2] Y
@@ -346,20 +398,34 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
   // bounce buffers: the host threads copy chunk k+1 while chunk k is on the
   // wire and chunk k-1 in K1/K2 (a plain cudaMemcpyAsync from pageable memory
   // is staged synchronously by the driver)
-  auto pageable = [](const void* p) {
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-      cudaGetLastError();
-      return true;
-    }
-    return a.type == cudaMemoryTypeUnregistered;
-  };
-  const bool staged = pageable(pop_nodes) || pageable(pop_conns);
+  const bool staged = pack || src_pageable;
   if (staged) {
     size_t most = 0;
-    for (int k = 0; k < chunks; ++k) most = std::max(most, size_t(lo_of(k + 1) - lo_of(k)) * (nrow + crow));
+    for (int k = 0; k < chunks; ++k)
+      most = std::max(most, size_t(lo_of(k + 1) - lo_of(k)) * (is_pk(k) ? pkl.bytes : nrow + crow));
     CK(ctx->stage.ensure(most));
   }
+  bool pack_ok = true;
+  static const bool trace = std::getenv("FNB_H2D_TRACE") != nullptr;  // per-call host timing (stderr)
+  const auto call_t0 = std::chrono::steady_clock::now();
+  std::atomic<bool> pack_good{true};
+  bool next_ready = false;  // the chunk about to be enqueued was packed by the previous iteration
+  // the pool workers pack chunk k into its staging slot (asynchronously; pool->wait() joins)
+  auto pack_chunk = [&](int k) {
+    const size_t lo = size_t(lo_of(k)), hi = size_t(lo_of(k + 1));
+    uint8_t* b = static_cast<uint8_t*>(ctx->stage.buf[k % HostStage::kSlots]);
+    constexpr size_t kPart = 16;  // genomes per pool part
+    ctx->stage.pool->start((hi - lo + kPart - 1) / kPart, [=, &pack_good](size_t i) {
+      const size_t g0 = lo + i * kPart, g1 = std::min(hi, g0 + kPart);
+      if (!pack_genomes(pop_nodes, pop_conns, N, Cm, g0, g1, b + (g0 - lo) * pkl.bytes)) pack_good.store(false);
+    });
+  };
+  struct PoolJoin {  // no early return leaves a packing job running on this frame's data
+    CopyPool* p;
+    ~PoolJoin() {
+      if (p) p->wait();
+    }
+  } pool_join{pack ? ctx->stage.pool : nullptr};
   // the copies must not overwrite buffers still read by earlier work on the compute stream
   CK(cudaEventRecord(ctx->chunk_ev[fnb_ctx::kMaxChunks], ctx->stream));
   CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[fnb_ctx::kMaxChunks], 0));
@@ -371,30 +437,72 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
     cudaStream_t cs = ctx->copy_stream;
     const uint8_t* hn = reinterpret_cast<const uint8_t*>(pop_nodes) + size_t(lo) * nrow;
     const uint8_t* hc = reinterpret_cast<const uint8_t*>(pop_conns) + size_t(lo) * crow;
-    if (staged) {
-      const int slot = k % HostStage::kSlots;
-      CK(cudaEventSynchronize(ctx->stage.free_ev[slot]));  // that slot's previous chunk has left
-      uint8_t* b = static_cast<uint8_t*>(ctx->stage.buf[slot]);
-      ctx->stage.pool->copy(b, hn, size_t(n) * nrow);
-      ctx->stage.pool->copy(b + size_t(n) * nrow, hc, size_t(n) * crow);
-      hn = b;
-      hc = b + size_t(n) * nrow;
+    uint8_t* dp = static_cast<uint8_t*>(ctx->packed.p) + size_t(lo) * pkl.bytes;
+    const bool pk = is_pk(k);
+    if (pk) {
+      // chunk k is packed into its slot (by the previous iteration, or here);
+      // the workers pack the next packed chunk while this thread enqueues k
+      if (!next_ready) {
+        CK(cudaEventSynchronize(ctx->stage.free_ev[k % HostStage::kSlots]));
+        pack_chunk(k);
+        ctx->stage.pool->wait();
+      }
+      if (!pack_good.load()) {
+        pack_ok = false;
+        break;
+      }
     }
-    CK(cudaMemcpyAsync(dn + size_t(lo) * nrow, hn, size_t(n) * nrow, cudaMemcpyHostToDevice, cs));
-    CK(cudaMemcpyAsync(dc + size_t(lo) * crow, hc, size_t(n) * crow, cudaMemcpyHostToDevice, cs));
-    if (staged) CK(cudaEventRecord(ctx->stage.free_ev[k % HostStage::kSlots], cs));
+    next_ready = false;
+    const bool prefetch = k + 1 < chunks && is_pk(k + 1);
+    if (prefetch) {
+      CK(cudaEventSynchronize(ctx->stage.free_ev[(k + 1) % HostStage::kSlots]));  // that slot's last DMA has left
+      pack_chunk(k + 1);
+    }
+    if (pk) {
+      CK(cudaMemcpyAsync(dp, ctx->stage.buf[k % HostStage::kSlots], size_t(n) * pkl.bytes, cudaMemcpyHostToDevice,
+                         cs));
+    } else {
+      if (src_pageable) {
+        const int slot = k % HostStage::kSlots;
+        CK(cudaEventSynchronize(ctx->stage.free_ev[slot]));  // that slot's previous chunk has left
+        uint8_t* b = static_cast<uint8_t*>(ctx->stage.buf[slot]);
+        ctx->stage.pool->copy(b, hn, size_t(n) * nrow);
+        ctx->stage.pool->copy(b + size_t(n) * nrow, hc, size_t(n) * crow);
+        hn = b;
+        hc = b + size_t(n) * nrow;
+      }
+      CK(cudaMemcpyAsync(dn + size_t(lo) * nrow, hn, size_t(n) * nrow, cudaMemcpyHostToDevice, cs));
+      CK(cudaMemcpyAsync(dc + size_t(lo) * crow, hc, size_t(n) * crow, cudaMemcpyHostToDevice, cs));
+    }
+    if (pk || src_pageable) CK(cudaEventRecord(ctx->stage.free_ev[k % HostStage::kSlots], cs));
     CK(cudaEventRecord(ctx->chunk_ev[k], cs));
     // chunk k's K1 + K2 on the compute stream as soon as its copy lands
     CK(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[k], 0));
-    int st = fnb_transform_d(ctx, reinterpret_cast<const double*>(dn + size_t(lo) * nrow),
-                             reinterpret_cast<const double*>(dc + size_t(lo) * crow), n,
-                             nets + size_t(lo) * ctx->L.bytes, ctx->stream);
+    int st = 0;
+    if (pk) {
+      CK(launch_transform_packed(dp, n, nets + size_t(lo) * ctx->L.bytes, ctx->L, ctx->sh, ctx->stream));
+      ctx->launches++;
+    } else {
+      st = fnb_transform_d(ctx, reinterpret_cast<const double*>(dn + size_t(lo) * nrow),
+                           reinterpret_cast<const double*>(dc + size_t(lo) * crow), n,
+                           nets + size_t(lo) * ctx->L.bytes, ctx->stream);
+    }
     if (st) return st;
     // genomes that failed K1 carry no records: K2 skips them
     st = fnb_forward_d(ctx, nets + size_t(lo) * ctx->L.bytes, n, static_cast<float*>(ctx->X.p),
                        kind != FNB_FIT_NONE ? static_cast<float*>(ctx->Y.p) : nullptr, batch, kind, offset,
                        d_fit ? d_fit + lo : nullptr, d_out ? d_out + size_t(lo) * batch * O : nullptr, ctx->stream);
+    if (prefetch) {
+      ctx->stage.pool->wait();  // chunk k+1 is packed
+      next_ready = true;
+    }
     if (st) return st;
+  }
+  if (!pack_ok) {  // an act / agg id beyond a byte: the whole call on the FP64 rows
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->copy_stream));
+    return evaluate_impl(ctx, pop_nodes, pop_conns, P, inputs, targets, batch, kind, offset, fitness_out, out,
+                         false);
   }
   CK(launch_first_error(nets, ctx->L.bytes, P, d_flags, ctx->stream));
   ctx->launches++;
@@ -404,10 +512,24 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
     CK(cudaMemcpyAsync(out, d_out, sizeof(double) * size_t(P) * batch * O, cudaMemcpyDeviceToHost, ctx->stream));
   if (fitness_out)
     CK(cudaMemcpyAsync(fitness_out, d_fit, sizeof(double) * size_t(P), cudaMemcpyDeviceToHost, ctx->stream));
+  const auto sync_t0 = std::chrono::steady_clock::now();
   CK(cudaStreamSynchronize(ctx->stream));
-  if (flags[0] != 0x7fffffff)  // rebuild the reference's message for the lowest failing genome
+  if (trace)
+    std::fprintf(stderr, "evaluate P=%d chunks=%d packed %d%%: enqueue %.3f ms, wait %.3f ms\n", P, chunks,
+                 pack_pct, std::chrono::duration<double>(sync_t0 - call_t0).count() * 1e3,
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - sync_t0).count() * 1e3);
+  if (flags[0] != 0x7fffffff) {  // rebuild the reference's message for the lowest failing genome
+    if (pack) {  // from the FP64 rows, which only the error path uploads
+      CK(ctx->nodes.ensure(nrow * size_t(P)));
+      CK(ctx->conns.ensure(crow * size_t(P)));
+      dn = static_cast<uint8_t*>(ctx->nodes.p);
+      dc = static_cast<uint8_t*>(ctx->conns.p);
+      CK(cudaMemcpy(dn, pop_nodes, nrow * size_t(P), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dc, pop_conns, crow * size_t(P), cudaMemcpyHostToDevice));
+    }
     return fnb_check_nets_d(ctx, reinterpret_cast<const double*>(dn), reinterpret_cast<const double*>(dc), nets, P,
                             ctx->stream);
+  }
   if (flags[1]) return set_err(ctx, FNB_E_NON_FINITE_INPUT, "input not finite", 0);  // network.hpp:245-246
   return 0;
 }

@@ -140,6 +140,29 @@ struct NetLayout {
   }
 };
 
+// Packed transfer rows (the host-buffer evaluate path): what K1 reads of a
+// genome, converted on the host exactly as K1 converts the FP64 rows on the
+// device (int() truncating, NaN -> INT32_MIN, saturating; float() rounded
+// to nearest), structure-of-arrays so every warp load is coalesced.  16N +
+// 13C bytes against 40N + 32C (0.40 at C2); node act / agg ids must fit a
+// byte (the host packer falls back to the FP64 rows otherwise).
+struct PackedLayout {
+  size_t key, bias, resp, act, agg, nflag, cin, cout, w, cflag, bytes;
+  __host__ __device__ PackedLayout(int N, int C) {
+    key = 0;
+    bias = 4 * size_t(N);
+    resp = 8 * size_t(N);
+    act = 12 * size_t(N);
+    agg = 13 * size_t(N);
+    nflag = 14 * size_t(N);  // bit0: non-empty (key not NaN)
+    cin = (15 * size_t(N) + 3) & ~size_t(3);
+    cout = cin + 4 * size_t(C);
+    w = cout + 4 * size_t(C);
+    cflag = w + 4 * size_t(C);  // bit0: non-empty (in not NaN), bit1: enabled == 1.0
+    bytes = align16(cflag + size_t(C));
+  }
+};
+
 // Schema + shape constants passed by value to kernels.
 struct DevShape {
   int N, C, I, O;

@@ -136,21 +136,25 @@ __device__ inline void tf_fail(uint8_t* net, int status, int kind, int a, int b,
   h->n_slots = -2;  // no value-slot count (K2 also skips the genome by its status)
 }
 
-template <int W>
+// kPk: the genome comes as packed transfer rows (PackedLayout, `packed` +
+// g * pk.bytes) instead of the FP64 rows; every derived value is the same
+template <int W, bool kPk>
 __global__ void __launch_bounds__(128)
-k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, int P,
-            uint8_t* __restrict__ nets, NetLayout L, DevShape sh, size_t smem_per_warp, int l2_prefetch) {
+k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, const uint8_t* __restrict__ packed,
+            int P, uint8_t* __restrict__ nets, NetLayout L, DevShape sh, size_t smem_per_warp, int l2_prefetch) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= P) return;
   const int N = sh.N, C = sh.C;
   TfSmem s = tf_carve(smem_raw + size_t(warp) * smem_per_warp, N, C, W);
-  const double* nrow = nodes + size_t(g) * N * kNodeCols;
-  const double* crow = conns + size_t(g) * C * kConnCols;
+  const double* nrow = kPk ? nullptr : nodes + size_t(g) * N * kNodeCols;
+  const double* crow = kPk ? nullptr : conns + size_t(g) * C * kConnCols;
+  const PackedLayout pk(N, C);
+  const uint8_t* pg = kPk ? packed + size_t(g) * pk.bytes : nullptr;
   // the connection rows are first read in step 4, after the node, rank and
   // hash phases: one bulk prefetch brings them to L2 meanwhile
-  if (l2_prefetch && lane == 0) prefetch_l2_bulk(crow, uint32_t(C) * kConnCols * 8u);
+  if (!kPk && l2_prefetch && lane == 0) prefetch_l2_bulk(crow, uint32_t(C) * kConnCols * 8u);
   uint8_t* net = nets + size_t(g) * L.bytes;
 
   // ---- 1. node rows: keys, activation/aggregation ids (network.hpp:139-152);
@@ -164,22 +168,33 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     int bad = kErrNone, badid = 0;
     bool ne = false;
     if (r < N) {
-      const double* row = nrow + r * kNodeCols;
-      const double k = row[kKey];
-      ne = !isnan(k);
+      const double* row = kPk ? nullptr : nrow + r * kNodeCols;
+      int key = 0;
+      if constexpr (kPk) {
+        ne = pg[pk.nflag + r] & 1u;
+        key = reinterpret_cast<const int*>(pg + pk.key)[r];
+      } else {
+        const double k = row[kKey];
+        ne = !isnan(k);
+        key = int(k);
+      }
       long long kr = 0x7fffffffffffffffll;
       if (ne) {
-        const int key = int(k);
         kr = (static_cast<long long>(key) << 8) | r;
         narrow = narrow && key >= -(1 << 23) && key < (1 << 23) - 1;  // INT32_MAX stays the empty mark
-        const int act = int(row[kAct]);
-        const int agg = int(row[kAgg]);
+        const int act = kPk ? int(pg[pk.act + r]) : int(row[kAct]);
+        const int agg = kPk ? int(pg[pk.agg + r]) : int(row[kAgg]);
         if (act < 0 || act >= sh.n_act) { bad = kErrActId; badid = act; }
         else if (agg < 0 || agg >= sh.n_agg) { bad = kErrAggId; badid = agg; }
         else {
           s.ncode[r] = uint16_t(sh.act[act] | (sh.agg[agg] << 8));
-          s.nbias[r] = float(row[kBias]);
-          s.nresp[r] = float(row[kResp]);
+          if constexpr (kPk) {
+            s.nbias[r] = reinterpret_cast<const float*>(pg + pk.bias)[r];
+            s.nresp[r] = reinterpret_cast<const float*>(pg + pk.resp)[r];
+          } else {
+            s.nbias[r] = float(row[kBias]);
+            s.nresp[r] = float(row[kResp]);
+          }
         }
       }
       s.kr[r] = kr;
@@ -285,48 +300,68 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   //         row and rank space (network.hpp:167-183)
   const uint64_t keep = l2_keep();  // the weights are read again in step 7
   // rows of the next two 32-row chunks are in flight while a chunk is processed
+  // (FP64 rows: {in, out} and {enabled, w}; packed: in, out, w bits, flags)
   const double2 kNoConn = make_double2(__longlong_as_double(0x7ff8000000000000ll), 0.0);
   double2 qa0 = kNoConn, qb0 = kNoConn, qa1 = kNoConn, qb1 = kNoConn;
-  if (lane < C) {
-    qa0 = ld2_l2(crow + lane * kConnCols, keep);
-    qb0 = ld2_l2(crow + lane * kConnCols + 2, keep);
-  }
-  if (32 + lane < C) {
-    qa1 = ld2_l2(crow + (32 + lane) * kConnCols, keep);
-    qb1 = ld2_l2(crow + (32 + lane) * kConnCols + 2, keep);
-  }
+  auto load_conn = [&](int r, double2& a, double2& b) {
+    if constexpr (kPk) {  // the packed fields ride in the double2 registers
+      const int in = reinterpret_cast<const int*>(pg + pk.cin)[r];
+      const int out = reinterpret_cast<const int*>(pg + pk.cout)[r];
+      const float w = reinterpret_cast<const float*>(pg + pk.w)[r];
+      const uint32_t f = pg[pk.cflag + r];
+      a = make_double2(__hiloint2double(int(f), in), 0.0);
+      b = make_double2(__hiloint2double(out, __float_as_int(w)), 0.0);
+    } else {
+      a = ld2_l2(crow + r * kConnCols, keep);
+      b = ld2_l2(crow + r * kConnCols + 2, keep);
+    }
+  };
+  if (lane < C) load_conn(lane, qa0, qb0);
+  if (32 + lane < C) load_conn(32 + lane, qa1, qb1);
   for (int r0 = 0; r0 < C; r0 += 32) {
     const int r = r0 + lane;
-    const double cin = qa0.x, cout = qa0.y, en = qb0.x, w = qb0.y;
+    const double2 a = qa0, b = qb0;
     qa0 = qa1;
     qb0 = qb1;
     qa1 = kNoConn;
     qb1 = kNoConn;
-    if (r + 64 < C) {
-      qa1 = ld2_l2(crow + (r + 64) * kConnCols, keep);
-      qb1 = ld2_l2(crow + (r + 64) * kConnCols + 2, keep);
+    if (r + 64 < C) load_conn(r + 64, qa1, qb1);
+    bool ne, en1, wnan;
+    int cin, cout;
+    if constexpr (kPk) {
+      const uint32_t f = r < C ? uint32_t(__double2hiint(a.x)) : 0u;
+      ne = f & 1u;
+      en1 = (f >> 1) & 1u;
+      cin = __double2loint(a.x);
+      cout = __double2hiint(b.x);
+      wnan = isnan(__int_as_float(__double2loint(b.x)));
+    } else {
+      ne = !isnan(a.x);
+      en1 = b.x == 1.0;
+      cin = ne ? int(a.x) : 0;
+      cout = ne ? int(a.y) : 0;
+      wnan = isnan(b.y);
     }
-    const bool ne = !isnan(cin);
     int src = -1, dst = -1;
     if (ne) {
-      src = tf_lookup(s, int(cin));
-      dst = tf_lookup(s, int(cout));
+      src = tf_lookup(s, cin);
+      dst = tf_lookup(s, cout);
     }
     const bool bad = ne && (src < 0 || dst < 0);
     const unsigned m = __ballot_sync(kFull, bad);
     if (m) {
       const int l = __ffs(m) - 1;
-      const int a = __shfl_sync(kFull, ne ? int(cin) : 0, l);
-      const int b = __shfl_sync(kFull, ne ? int(cout) : 0, l);
-      if (lane == 0) tf_fail(net, 1 + FNB_E_DANGLING_ENDPOINT, kErrConn, a, b, 0);
+      const int ea = __shfl_sync(kFull, ne ? cin : 0, l);
+      const int eb = __shfl_sync(kFull, ne ? cout : 0, l);
+      if (lane == 0) tf_fail(net, 1 + FNB_E_DANGLING_ENDPOINT, kErrConn, ea, eb, 0);
       return;
     }
     if (r < C) {
-      const bool edge = ne && en == 1.0;
+      const bool edge = ne && en1;
       uint8_t d = kNoRow;
       if (edge) {
         atomicAdd(&s.R[dst], 1);
-        if (!isnan(w)) {
+        if (!wnan) {
           atomicOr(&s.pred[dst * W + (src >> 5)], 1u << (src & 31));
           const int rs = s.rank[src], rd = s.rank[dst];
           atomicOr(&s.predr[rd * W + (rs >> 5)], 1u << (rs & 31));
@@ -595,7 +630,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   for (int r = lane; r < C; r += 32) {
     const int dst = s.cdst[r];
     if (dst == kNoRow || (s.flags[dst] & 2)) continue;
-    const double w = ld_l2(crow + r * kConnCols + kW, drop);
+    const float wf = kPk ? reinterpret_cast<const float*>(pg + pk.w)[r] : float(ld_l2(crow + r * kConnCols + kW, drop));
     const int src = s.csrc[r];
     int below = 0;
     const int sw = src >> 5;
@@ -606,7 +641,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
       else if (w == sw) below += __popc(bits & ((1u << (src & 31)) - 1u));
     }
     Edge e;
-    e.w = float(w);
+    e.w = wf;
     e.src = slot_of[src];
     e.conn_row = uint16_t(r);
     grec[s.ebeg[dst] + below / kRecSlots].slot[below % kRecSlots] = e;
@@ -698,30 +733,42 @@ __global__ void k_net_order(const uint8_t* __restrict__ nets, NetLayout L, int P
 
 // ---- host launchers --------------------------------------------------------
 
-template <int W>
-static cudaError_t launch_transform_w(const double* n, const double* c, int P, uint8_t* nets,
+template <int W, bool kPk>
+static cudaError_t launch_transform_w(const double* n, const double* c, const uint8_t* pk, int P, uint8_t* nets,
                                       const NetLayout& L, const DevShape& sh, cudaStream_t st) {
   const size_t per_warp = tf_smem_bytes(sh.N, sh.C, W);
   const int warps = warps_per_cta_for_smem(per_warp, 4);
   const size_t smem = per_warp * warps;
-  cudaError_t e = cudaFuncSetAttribute(k_transform<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t e = cudaFuncSetAttribute(k_transform<W, kPk>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   const int blocks = (P + warps - 1) / warps;
   static const int l2pf = [] {  // experiment knob: measured neutral at C5, 4% slower at C2 (default off)
     const char* e = std::getenv("FNB_K1_L2PF");
     return e ? std::atoi(e) : 0;
   }();
-  k_transform<W><<<blocks, 32 * warps, smem, st>>>(n, c, P, nets, L, sh, per_warp, l2pf);
+  k_transform<W, kPk><<<blocks, 32 * warps, smem, st>>>(n, c, pk, P, nets, L, sh, per_warp, l2pf);
   return cudaGetLastError();
+}
+
+template <bool kPk>
+static cudaError_t launch_transform_any(const double* n, const double* c, const uint8_t* pk, int P, uint8_t* nets,
+                                        const NetLayout& L, const DevShape& sh, cudaStream_t st) {
+  const int W = (sh.N + 31) / 32;
+  if (W <= 1) return launch_transform_w<1, kPk>(n, c, pk, P, nets, L, sh, st);
+  if (W <= 2) return launch_transform_w<2, kPk>(n, c, pk, P, nets, L, sh, st);
+  if (W <= 4) return launch_transform_w<4, kPk>(n, c, pk, P, nets, L, sh, st);
+  return launch_transform_w<8, kPk>(n, c, pk, P, nets, L, sh, st);
 }
 
 cudaError_t launch_transform(const double* n, const double* c, int P, uint8_t* nets, const NetLayout& L,
                              const DevShape& sh, cudaStream_t st) {
-  const int W = (sh.N + 31) / 32;
-  if (W <= 1) return launch_transform_w<1>(n, c, P, nets, L, sh, st);
-  if (W <= 2) return launch_transform_w<2>(n, c, P, nets, L, sh, st);
-  if (W <= 4) return launch_transform_w<4>(n, c, P, nets, L, sh, st);
-  return launch_transform_w<8>(n, c, P, nets, L, sh, st);
+  return launch_transform_any<false>(n, c, nullptr, P, nets, L, sh, st);
+}
+
+// K1 over packed transfer rows (PackedLayout blocks, one per genome)
+cudaError_t launch_transform_packed(const uint8_t* packed, int P, uint8_t* nets, const NetLayout& L,
+                                    const DevShape& sh, cudaStream_t st) {
+  return launch_transform_any<true>(nullptr, nullptr, packed, P, nets, L, sh, st);
 }
 
 cudaError_t launch_describe_cycle(const double* n, const double* c, const uint8_t* net, const NetLayout& L,
