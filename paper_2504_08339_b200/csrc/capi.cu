@@ -681,7 +681,7 @@ int fnb_crossover(fnb_ctx* ctx, const double* fit_nodes, const double* fit_conns
 
 // ---- mutation -----------------------------------------------------------------
 namespace fnb {
-size_t mutate_scratch_bytes(int n);
+size_t mutate_scratch_bytes(int n, int N, int C);
 cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, int n, const uint8_t* active,
                           const fnb_mutation_config* m, const DevShape& sh, int* d_next_key, int* d_status,
                           void* scratch, size_t scratch_bytes, int* d_new_key_out, cudaStream_t st,
@@ -704,7 +704,7 @@ int fnb_mutate_d(fnb_ctx* ctx, double* d_nodes, double* d_conns, int P, const ui
                  int* d_new_key, void* stream) {
   if (P <= 0) return 0;
   CK(cudaSetDevice(ctx->device));
-  CK(ctx->scratch.ensure(mutate_scratch_bytes(P)));
+  CK(ctx->scratch.ensure(mutate_scratch_bytes(P, ctx->L.N, ctx->L.C)));
   CK(launch_mutate(d_nodes, d_conns, d_keys, P, d_active, cfg, ctx->sh, d_next_key, d_status, ctx->scratch.p,
                    ctx->scratch.cap, d_new_key, static_cast<cudaStream_t>(stream), &ctx->launches));
   return 0;
@@ -782,7 +782,7 @@ int fnb_mutate_table(fnb_ctx* ctx, double* pop_nodes, double* pop_conns, int P, 
   const size_t nb = sizeof(double) * nrow * size_t(P), cb = sizeof(double) * crow * size_t(P);
   CK(ctx->nodes.ensure(nb));
   CK(ctx->conns.ensure(cb));
-  CK(ctx->scratch.ensure(mutate_scratch_bytes(P)));
+  CK(ctx->scratch.ensure(mutate_scratch_bytes(P, ctx->L.N, ctx->L.C)));
   CK(ctx->misc.ensure(sizeof(uint32_t) * 4 * size_t(P) + sizeof(int) * (size_t(P) + 2) + 64));
   uint32_t* d_keys = static_cast<uint32_t*>(ctx->misc.p);
   int* d_status = reinterpret_cast<int*>(d_keys + 4 * size_t(P));

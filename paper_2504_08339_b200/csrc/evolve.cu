@@ -623,7 +623,7 @@ cudaError_t launch_distance_masked(const double* nodes, const double* conns, int
 size_t distance_scratch_bytes(int S, int N, int C);
 cudaError_t launch_crossover(const double* nodes, const double* conns, const int32_t* fit, const int32_t* oth,
                              const uint32_t* keys, int n, int N, int C, double* cn, double* cc, cudaStream_t st);
-size_t mutate_scratch_bytes(int n);
+size_t mutate_scratch_bytes(int n, int N, int C);
 cudaError_t launch_mutate_plan(const double* nodes, const double* conns, const int32_t* src, const uint32_t* keys,
                                int n, const uint8_t* active, const fnb_mutation_config* m, const DevShape& sh,
                                int* d_next_key, void* scratch, size_t scratch_bytes, int* d_new_key_out,
@@ -839,7 +839,7 @@ struct Evolver {
     cub::DeviceRadixSort::SortPairs(nullptr, b2, skey, skey_tmp, idx, idx_tmp, P, 0, 6);
     cub_bytes = std::max(b1, b2);
     A(&cub_tmp, cub_bytes);
-    scratch_bytes = std::max(distance_scratch_bytes(kMaxSpecies, N, C), mutate_scratch_bytes(P));
+    scratch_bytes = std::max(distance_scratch_bytes(kMaxSpecies, N, C), mutate_scratch_bytes(P, N, C));
     A(&scratch, scratch_bytes);
     if (e != cudaSuccess) return e;
     // representatives start as empty genomes (never read before founded)

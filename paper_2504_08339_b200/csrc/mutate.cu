@@ -211,6 +211,12 @@ struct MutSmem {
   uint32_t* bfs;              // [3W] visited / frontier / next row bitsets
 };
 
+// words of one slot's live-row masks, written by k_mutate_apply from its
+// staged flags after the structural edits and read by k_mutate_attrs instead
+// of scanning the child's rows again: mutable node rows (non-empty, not an
+// input), then live connection rows (non-empty)
+__host__ __device__ inline int live_mask_words(int N, int C) { return (N + 31) / 32 + (C + 31) / 32; }
+
 __host__ __device__ inline size_t mut_smem_bytes(int N, int C) {
   const int W = (N + 31) / 32;
   size_t b = size_t(table_capacity(N)) * 12;
@@ -492,13 +498,17 @@ __device__ bool conn_walk(const DW* dw, uint32_t need, uint32_t p0, int m, const
   return true;
 }
 
-// 8 CTAs (32 warps) per SM: the kernel is latency-bound (lane-0 streams, warp
-// scans), so occupancy is worth a few spilled registers
-__global__ void __launch_bounds__(128, 8)
+// MINB = 8: 8 CTAs (32 warps) per SM where shared memory allows it (C2): the
+// kernel is latency-bound (lane-0 streams, warp scans), so occupancy is worth
+// a few spilled registers.  MINB = 4 where shared memory holds residency to
+// <= 16 warps anyway (C5: 19 KB per warp): registers without spills.
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB)
 k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
                int n_children, const uint8_t* __restrict__ active, int N, int C, MutCfgDev cfg, DevShape sh,
                const int* __restrict__ plan_flag, const unsigned long long* __restrict__ plan_pair,
-               const int* __restrict__ new_key, int* __restrict__ status, size_t smem_per_warp, int l2_prefetch) {
+               const int* __restrict__ new_key, int* __restrict__ status, size_t smem_per_warp, int l2_prefetch,
+               uint32_t* __restrict__ live_mask) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -775,6 +785,23 @@ k_mutate_apply(double* __restrict__ nodes, double* __restrict__ conns, const uin
     }
   }
 
+  // the live-row masks of the structurally final child (k_mutate_attrs):
+  // lane l builds word l from 32 staged flags
+  {
+    const int WN = (N + 31) >> 5, WT = live_mask_words(N, C);
+    uint32_t* lm = live_mask + size_t(c) * WT;
+    for (int w = lane; w < WT; w += 32) {
+      const bool node = w < WN;
+      const uint8_t* f = node ? sm.nflag + 32 * w : sm.cflag + 32 * (w - WN);
+      const int lim = node ? N - 32 * w : C - 32 * (w - WN);
+      uint32_t bits = 0;
+      for (int i = 0; i < 32 && i < lim; ++i) {
+        const uint32_t x = f[i];
+        bits |= uint32_t(node ? (x & 3u) == 1u : (x & 1u) != 0u) << i;
+      }
+      lm[w] = bits;
+    }
+  }
   if (lane == 0) status[c] = st;
 }
 
@@ -808,7 +835,8 @@ template <typename DW>
 __global__ void __launch_bounds__(256)
 k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uint32_t* __restrict__ keys,
                int n_children, const uint8_t* __restrict__ active, const int* __restrict__ status, int N, int C,
-               MutCfgDev cfg, DevShape sh, int win, size_t smem_per_warp, int l2_prefetch) {
+               MutCfgDev cfg, DevShape sh, int win, size_t smem_per_warp, int l2_prefetch,
+               const uint32_t* __restrict__ live_mask) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -831,34 +859,25 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
   double* n = nodes + size_t(c) * N * kNodeCols;
   double* cc = conns + size_t(c) * C * kConnCols;
   const Key4 k5 = key_split(load_key(keys, c), 5);
-  if (l2_prefetch && lane == 0) {  // the row scans below walk the child chunk by chunk
+  if (l2_prefetch && lane == 0) {  // the rows are read-modify-written after the decision walk
     prefetch_l2_range(cc, size_t(C) * kConnCols * 8);
     prefetch_l2_range(n, size_t(N) * kNodeCols * 8);
   }
 
-  // rows of the structurally final child: mutable nodes, live connections
+  // rows of the structurally final child: mutable nodes, live connections,
+  // from the masks k_mutate_apply left (no pass over the rows themselves)
   int nn = 0, nc = 0;
-  // rows read here are read-modify-written by apply_normals after the long
-  // decision walk: evict_last (fnb_common.cuh).  Measured at C5: reads 5.64 ->
-  // 5.55 GB, 5.89 -> 5.73 ms; an evict_first re-read made it worse, and an L2
-  // persisting set-aside (75 MB) cut reads to 4.90 GB at the same time -- the
-  // kernel is latency-bound, not HBM-bound (24% occupancy, 50% issue).
-  const uint64_t keep = l2_keep();
+  const uint32_t* lm = live_mask + size_t(c) * live_mask_words(N, C);
   for (int r0 = 0; r0 < N; r0 += 32) {
+    const uint32_t b = lm[r0 >> 5];
     const int r = r0 + lane;
-    bool h = false;
-    if (r < N) {
-      const double k = ld_l2(n + r * kNodeCols + kKey, keep);
-      h = !isnan(k) && !is_key_in(int(k), sh.input_keys, sh.I);
-      hid[r] = h;
-    }
-    nn += __popc(__ballot_sync(kFullMask, h));
+    if (r < N) hid[r] = (b >> lane) & 1u;
+    nn += __popc(b);
   }
   for (int r0 = 0; r0 < C; r0 += 32) {
+    const uint32_t bl = lm[((N + 31) >> 5) + (r0 >> 5)];
     const int r = r0 + lane;
-    const bool live = r < C && !isnan(ld_l2(cc + r * kConnCols + kIn, keep));
-    const unsigned bl = __ballot_sync(kFullMask, live);
-    if (live) live_row[nc + __popc(bl & ((1u << lane) - 1u))] = int16_t(r);
+    if ((bl >> lane) & 1u) live_row[nc + __popc(bl & ((1u << lane) - 1u))] = int16_t(r);
     nc += __popc(bl);
   }
   const int need = min(win, (nn * attr_per_node(cfg) + nc * 3 + 1) & ~1);
@@ -935,9 +954,9 @@ k_mutate_attrs(double* __restrict__ nodes, double* __restrict__ conns, const uin
 // ---------------------------------------------------------------------------
 // host launcher: plan -> K7 -> apply, all on `st`
 // ---------------------------------------------------------------------------
-size_t mutate_scratch_bytes(int n) {
+size_t mutate_scratch_bytes(int n, int N, int C) {
   const size_t H = size_t(table_capacity(n));
-  return size_t(n) * (8 + 4 + 4 + 4) + H * 12 + 64;
+  return size_t(n) * (8 + 4 + 4 + 4) + H * 12 + 64 + size_t(n) * live_mask_words(N, C) * 4 + 16;
 }
 
 static MutCfgDev mut_cfg_dev(const fnb_mutation_config* m, const DevShape& sh) {
@@ -954,9 +973,11 @@ static MutCfgDev mut_cfg_dev(const fnb_mutation_config* m, const DevShape& sh) {
 struct MutScratch {
   unsigned long long *pair, *tkeys;
   int *flag, *rank, *newk, *tmin;
+  uint32_t* mask;  // [n][live_mask_words] live-row masks
   int H;
 };
-static bool mut_scratch(void* scratch, size_t scratch_bytes, int n, int* d_new_key_out, MutScratch* ms) {
+static bool mut_scratch(void* scratch, size_t scratch_bytes, int n, int N, int C, int* d_new_key_out,
+                        MutScratch* ms) {
   ms->H = table_capacity(n);
   uint8_t* p = static_cast<uint8_t*>(scratch);
   ms->pair = reinterpret_cast<unsigned long long*>(p); p += size_t(n) * 8;
@@ -966,13 +987,15 @@ static bool mut_scratch(void* scratch, size_t scratch_bytes, int n, int* d_new_k
   ms->newk = d_new_key_out ? d_new_key_out : reinterpret_cast<int*>(p);
   p += size_t(n) * 4;
   ms->tmin = reinterpret_cast<int*>(p); p += size_t(ms->H) * 4;
+  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  ms->mask = reinterpret_cast<uint32_t*>(p); p += size_t(n) * live_mask_words(N, C) * 4;
   return size_t(p - static_cast<uint8_t*>(scratch)) <= scratch_bytes;
 }
 
 // the plan arrays inside the scratch (host-layer replay of a caller's InnovationTable)
 void mutate_scratch_views(void* scratch, int n, unsigned long long** pair, int** flag, int** newk) {
   MutScratch ms;
-  mut_scratch(scratch, size_t(-1), n, nullptr, &ms);
+  mut_scratch(scratch, size_t(-1), n, 1, 1, nullptr, &ms);
   *pair = ms.pair;
   *flag = ms.flag;
   *newk = ms.newk;
@@ -988,7 +1011,7 @@ cudaError_t launch_mutate_plan(const double* nodes, const double* conns, const i
   if (n <= 0) return cudaSuccess;
   const MutCfgDev cfg = mut_cfg_dev(m, sh);
   MutScratch ms;
-  if (!mut_scratch(scratch, scratch_bytes, n, d_new_key_out, &ms)) return cudaErrorInvalidValue;
+  if (!mut_scratch(scratch, scratch_bytes, n, sh.N, sh.C, d_new_key_out, &ms)) return cudaErrorInvalidValue;
   const int wpb = 4, H = ms.H;
   k_mutate_plan<<<(n + wpb - 1) / wpb, 32 * wpb, 0, st>>>(nodes, conns, src, keys, n, active, sh.N, sh.C, cfg, ms.pair,
                                                           ms.flag);
@@ -1014,31 +1037,45 @@ cudaError_t launch_mutate_apply(double* nodes, double* conns, const uint32_t* ke
   const int N = sh.N, C = sh.C, k = hi - lo;
   const MutCfgDev cfg = mut_cfg_dev(m, sh);
   MutScratch ms;
-  if (!mut_scratch(scratch, scratch_bytes, n, const_cast<int*>(d_new_key), &ms)) return cudaErrorInvalidValue;
+  if (!mut_scratch(scratch, scratch_bytes, n, sh.N, sh.C, const_cast<int*>(d_new_key), &ms)) return cudaErrorInvalidValue;
   double* nd = nodes + size_t(lo) * N * kNodeCols;
   double* cd = conns + size_t(lo) * C * kConnCols;
   const uint32_t* ky = keys + 4 * size_t(lo);
   const uint8_t* ac = active ? active + lo : nullptr;
   const size_t per_warp = align16(mut_smem_bytes(N, C));
   const int warps = warps_per_cta_for_smem(per_warp, 4);
-  cudaError_t e = cudaFuncSetAttribute(k_mutate_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static int smem_sm = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    return v > 0 ? v : 233472;
+  }();
+  const int resident = int(smem_sm / (per_warp * warps + 1024)) * warps;
+  auto apply_kern = resident <= 16 ? k_mutate_apply<4> : k_mutate_apply<8>;
+  cudaError_t e = cudaFuncSetAttribute(apply_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(per_warp * warps));
   if (e != cudaSuccess) return e;
   static const int l2pf = [] {  // experiment knob
     const char* e = std::getenv("FNB_K6_L2PF");
     return e ? std::atoi(e) : 1;
   }();
-  k_mutate_apply<<<(k + warps - 1) / warps, 32 * warps, per_warp * warps, st>>>(
-      nd, cd, ky, k, ac, N, C, cfg, sh, ms.flag + lo, ms.pair + lo, ms.newk + lo, d_status + lo, per_warp, l2pf);
+  apply_kern<<<(k + warps - 1) / warps, 32 * warps, per_warp * warps, st>>>(
+      nd, cd, ky, k, ac, N, C, cfg, sh, ms.flag + lo, ms.pair + lo, ms.newk + lo, d_status + lo, per_warp, l2pf,
+      ms.mask + size_t(lo) * live_mask_words(N, C));
   const int win = attr_window(N, C, attr_per_node(cfg));
   const bool narrow = attr_words_narrow(cfg);
   const size_t aw = attr_smem_bytes(N, C, win, narrow);
   const int awarps = warps_per_cta_for_smem(aw, 8);
   auto kern = narrow ? k_mutate_attrs<uint8_t> : k_mutate_attrs<uint16_t>;
+  static const int l2pf_attrs = [] {  // experiment knob
+    const char* e = std::getenv("FNB_K6A_L2PF");
+    return e ? std::atoi(e) : 1;
+  }();
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(aw * awarps));
   if (e != cudaSuccess) return e;
   kern<<<(k + awarps - 1) / awarps, 32 * awarps, aw * awarps, st>>>(nd, cd, ky, k, ac, d_status + lo, N, C, cfg, sh,
-                                                                    win, aw, l2pf);
+                                                                    win, aw, l2pf_attrs,
+                                                                    ms.mask + size_t(lo) * live_mask_words(N, C));
   *launches += 2;
   return cudaGetLastError();
 }
@@ -1052,7 +1089,7 @@ cudaError_t launch_mutate(double* nodes, double* conns, const uint32_t* keys, in
                                      scratch_bytes, d_new_key_out, st, launches);
   if (e != cudaSuccess) return e;
   MutScratch ms;
-  if (!mut_scratch(scratch, scratch_bytes, n, d_new_key_out, &ms)) return cudaErrorInvalidValue;
+  if (!mut_scratch(scratch, scratch_bytes, n, sh.N, sh.C, d_new_key_out, &ms)) return cudaErrorInvalidValue;
   return launch_mutate_apply(nodes, conns, keys, n, 0, n, active, m, sh, d_status, scratch, scratch_bytes, ms.newk,
                              st, launches);
 }
