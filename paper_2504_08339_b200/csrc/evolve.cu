@@ -770,6 +770,15 @@ __global__ void k_remap_parents(const int* fit_idx, const int* oth_idx, int P, c
   othp[c] = pos(oth_idx[c]);
 }
 
+// FNB_STEP_OVERLAP=0: the one-process step on one stream (A/B, debugging)
+static bool step_overlap_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FNB_STEP_OVERLAP");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 struct Evolver {
   NeatCfg cfg;
   fnb_mutation_config mut;
@@ -852,9 +861,31 @@ struct Evolver {
     return e;
   }
 
+  // one-process step (enqueue_step): two independent branches run on a side
+  // stream -- the fitness sort next to speciation + stagnation, and the
+  // mutation plans + K7 next to crossover -- joined by events (graph capture
+  // turns them into parallel graph branches)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork[2] = {}, ev_join[2] = {};
+  bool overlap = false;
+  cudaError_t ensure_side() {
+    if (side) return cudaSuccess;
+    cudaError_t e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&ev_fork[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_join[i], cudaEventDisableTiming);
+    }
+    return e;
+  }
+
   void release() {
     release_graphs();
     shard_release();
+    for (int i = 0; i < 2; ++i) {
+      if (ev_fork[i]) cudaEventDestroy(ev_fork[i]);
+      if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    }
+    if (side) cudaStreamDestroy(side);
     void* ps[] = {pn[0], pn[1], pc[0], pc[1], fitness, rep_n, rep_c, dmat, species_of, sd,
                   kasc, kdesc, ktmp, idx, idx_sorted, idx_tmp, skey, skey_tmp, fit_idx, oth_idx, status, next_key, rank2,
                   xkeys, mkeys, active, cub_tmp, scratch};
@@ -994,6 +1025,26 @@ struct Evolver {
     const double* c = pc[cur];
     cudaError_t e;
     const int S_old = host_species;
+    const bool ov = overlap;
+    // the fitness order (ranks by a stable ascending sort, members by fitness
+    // desc / index asc) needs only the fitness: on the side stream, next to
+    // speciation and stagnation
+    auto fitness_sort = [&](cudaStream_t s) -> cudaError_t {
+      k_fit_keys<<<B, T, 0, s>>>(fitness, P, kasc, kdesc, idx);
+      cudaError_t r = P <= kCountRankMax
+                          ? launch_count_sort<unsigned long long>(kasc, nullptr, P, skey_tmp, ktmp, idx_sorted, s)
+                          : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, s);
+      if (r != cudaSuccess) return r;
+      k_desc_from_asc<<<B, T, 0, s>>>(ktmp, idx_sorted, P, idx_tmp, rank2);
+      return cudaGetLastError();
+    };
+    if (ov) {
+      e = cudaEventRecord(ev_fork[0], st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_fork[0], 0);
+      if (e == cudaSuccess) e = fitness_sort(side);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_join[0], side);
+      if (e != cudaSuccess) return e;
+    }
     // ---- speciate
     k_spec_begin<<<1, 1, 0, st>>>(sd);
     if (S_old > 0) {
@@ -1027,15 +1078,17 @@ struct Evolver {
     k_stagnation<<<1, 1, 0, st>>>(sd, cfg.species_elitism, cfg.max_stagnation);
     k_apply_compaction<<<1, 256, 0, st>>>(sd, rep_n, rep_c, N, C);
     k_remap_or_drop<<<B, T, 0, st>>>(species_of, 0, P, sd);
-    // ---- compute_spawn_counts: ranks by a stable ascending radix sort
-    k_fit_keys<<<B, T, 0, st>>>(fitness, P, kasc, kdesc, idx);
-    e = P <= kCountRankMax
-            ? launch_count_sort<unsigned long long>(kasc, nullptr, P, skey_tmp, ktmp, idx_sorted, st)
-            : cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kasc, ktmp, idx, idx_sorted, P, 0, 64, st);
-    if (e != cudaSuccess) return e;
+    // ---- compute_spawn_counts: ranks by a stable ascending sort; members by
+    //      (fitness desc, index asc) for reproduce, and the mid-ranks
+    if (!ov) {
+      e = fitness_sort(st);
+      if (e != cudaSuccess) return e;
+    }
     k_spawn_begin<<<1, 1, 0, st>>>(sd);
-    // members by (fitness desc, index asc) for reproduce, and the mid-ranks
-    k_desc_from_asc<<<B, T, 0, st>>>(ktmp, idx_sorted, P, idx_tmp, rank2);
+    if (ov) {
+      e = cudaStreamWaitEvent(st, ev_join[0], 0);
+      if (e != cudaSuccess) return e;
+    }
     k_rank_sums<<<B, T, 0, st>>>(rank2, idx_sorted, P, species_of, 0, P, sd);
     k_spawn<<<1, 1, 0, st>>>(sd, P, cfg.spawn_rate, cfg.genome_elitism);
     // ---- reproduce: members by species
@@ -1049,7 +1102,17 @@ struct Evolver {
                                       oth_idx, xkeys, mkeys, active);
     *launches += 22 + kDistanceLaunches;
     // mutate phase 1 over all slots (replicated on every rank of a sharded
-    // run): node-split plans read from the fit parents, K7 innovation keys
+    // run): node-split plans read from the fit parents, K7 innovation keys;
+    // in the one-process step on the side stream, next to crossover
+    if (ov) {
+      e = cudaEventRecord(ev_fork[1], st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_fork[1], 0);
+      if (e == cudaSuccess)
+        e = launch_mutate_plan(n, c, fit_idx, mkeys, P, active, &mut, sh, next_key, scratch, scratch_bytes, nullptr,
+                               side, launches);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_join[1], side);
+      return e;
+    }
     e = launch_mutate_plan(n, c, fit_idx, mkeys, P, active, &mut, sh, next_key, scratch, scratch_bytes, nullptr, st,
                            launches);
     return e;
@@ -1065,6 +1128,10 @@ struct Evolver {
                                      pn[cur ^ 1] + size_t(lo) * gn(), pc[cur ^ 1] + size_t(lo) * gc(), st);
     if (e != cudaSuccess) return e;
     ++*launches;
+    if (overlap) {  // the mutation plans (side stream) before the structural pass
+      e = cudaStreamWaitEvent(st, ev_join[1], 0);
+      if (e != cudaSuccess) return e;
+    }
     int* newk = mutate_new_keys();
     return launch_mutate_apply(pn[cur ^ 1], pc[cur ^ 1], mkeys, P, lo, hi, active, &mut, sh, status, scratch,
                                scratch_bytes, newk, st, launches);
@@ -1094,8 +1161,11 @@ struct Evolver {
 
   // speciate -> update_stagnation -> compute_spawn_counts -> reproduce
   cudaError_t enqueue_step() {
-    cudaError_t e = enqueue_front();
+    cudaError_t e = step_overlap_enabled() ? ensure_side() : cudaSuccess;
+    overlap = e == cudaSuccess && step_overlap_enabled();
+    if (e == cudaSuccess) e = enqueue_front();
     if (e == cudaSuccess) e = enqueue_back(0, P);
+    overlap = false;
     if (e == cudaSuccess) e = enqueue_first_bad(0, P);
     if (e == cudaSuccess) e = enqueue_advance();
     return e;
