@@ -25,6 +25,10 @@
 
 #include "fnb_common.cuh"
 
+#ifndef FNB_K2_UNROLL
+#define FNB_K2_UNROLL 8
+#endif
+
 namespace fnb {
 
 // ---- activations (functions.hpp:17-21) in FP32 -----------------------------
@@ -198,6 +202,10 @@ k_forward(FwdParams p) {
   // {sum} schemas: the accumulators are reset at each finalize instead of on
   // each op's first record
   constexpr bool kSumOnly = AGG == FNB_AGG_SUM;
+  // record loop unrolling: the single-function instantiations gain from a
+  // deeper unroll (more independent record bodies in flight), the generic
+  // one (activation / aggregation dispatch per op) does not
+  constexpr int kRecUnroll = (AGG >= 0 && ACT >= 0) ? FNB_K2_UNROLL : 2;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int T = p.T;
   const int grp = threadIdx.x / T;
@@ -307,7 +315,7 @@ k_forward(FwdParams p) {
     float x0[SPT], x1[SPT], x2[SPT], x3[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) x0[k] = x1[k] = x2[k] = x3[k] = 0.0f;
-#pragma unroll 2
+#pragma unroll kRecUnroll
     for (int r = 0; r < n_rec; ++r) {
       const uint32_t meta = __float_as_uint(cur.a.z);
       const uint32_t srcs = __float_as_uint(cur.a.w);
