@@ -7,6 +7,7 @@ for side in ${SIDES:-old new}; do
   case $side in
     old) export FNB_AB_ROOT=$GRAFT_REPO_ROOT/ab_old ;;
     newB) export FNB_AB_ROOT=$GRAFT_REPO_ROOT/ab_b ;;
+    ab_*) export FNB_AB_ROOT=$GRAFT_REPO_ROOT/$side ;;
     off) export FNB_XOVER_L2PF=0 FNB_K6_L2PF=0 ;;
   esac
   timeout 600 ncu --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg --clock-control none -k regex:"k_mutate|k_crossover|k_transform" --csv \
