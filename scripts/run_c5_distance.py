@@ -7,6 +7,8 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("FNB_AB_ROOT"):  # A/B: a package copy with another library build
+    sys.path.insert(0, os.environ["FNB_AB_ROOT"])
 import bench  # noqa: E402
 
 dev = torch.device("cuda", 0)
