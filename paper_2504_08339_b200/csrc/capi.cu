@@ -407,6 +407,7 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
   }
   bool pack_ok = true;
   static const bool trace = std::getenv("FNB_H2D_TRACE") != nullptr;  // per-call host timing (stderr)
+  double t_copy = 0.0, t_launch = 0.0;
   const auto call_t0 = std::chrono::steady_clock::now();
   std::atomic<bool> pack_good{true};
   bool next_ready = false;  // the chunk about to be enqueued was packed by the previous iteration
@@ -471,14 +472,17 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
         hn = b;
         hc = b + size_t(n) * nrow;
       }
+      const auto tm0 = std::chrono::steady_clock::now();
       CK(cudaMemcpyAsync(dn + size_t(lo) * nrow, hn, size_t(n) * nrow, cudaMemcpyHostToDevice, cs));
       CK(cudaMemcpyAsync(dc + size_t(lo) * crow, hc, size_t(n) * crow, cudaMemcpyHostToDevice, cs));
+      if (trace) t_copy += std::chrono::duration<double>(std::chrono::steady_clock::now() - tm0).count();
     }
     if (pk || src_pageable) CK(cudaEventRecord(ctx->stage.free_ev[k % HostStage::kSlots], cs));
     CK(cudaEventRecord(ctx->chunk_ev[k], cs));
     // chunk k's K1 + K2 on the compute stream as soon as its copy lands
     CK(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[k], 0));
     int st = 0;
+    const auto tk0 = std::chrono::steady_clock::now();
     if (pk) {
       CK(launch_transform_packed(dp, n, nets + size_t(lo) * ctx->L.bytes, ctx->L, ctx->sh, ctx->stream));
       ctx->launches++;
@@ -492,6 +496,7 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
     st = fnb_forward_d(ctx, nets + size_t(lo) * ctx->L.bytes, n, static_cast<float*>(ctx->X.p),
                        kind != FNB_FIT_NONE ? static_cast<float*>(ctx->Y.p) : nullptr, batch, kind, offset,
                        d_fit ? d_fit + lo : nullptr, d_out ? d_out + size_t(lo) * batch * O : nullptr, ctx->stream);
+    if (trace) t_launch += std::chrono::duration<double>(std::chrono::steady_clock::now() - tk0).count();
     if (prefetch) {
       ctx->stage.pool->wait();  // chunk k+1 is packed
       next_ready = true;
@@ -515,8 +520,8 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
   const auto sync_t0 = std::chrono::steady_clock::now();
   CK(cudaStreamSynchronize(ctx->stream));
   if (trace)
-    std::fprintf(stderr, "evaluate P=%d chunks=%d packed %d%%: enqueue %.3f ms, wait %.3f ms\n", P, chunks,
-                 pack_pct, std::chrono::duration<double>(sync_t0 - call_t0).count() * 1e3,
+    std::fprintf(stderr, "evaluate P=%d chunks=%d packed %d%%: copies %.3f ms, K1/K2 launches %.3f ms, enqueue %.3f ms, wait %.3f ms\n", P, chunks,
+                 pack_pct, t_copy * 1e3, t_launch * 1e3, std::chrono::duration<double>(sync_t0 - call_t0).count() * 1e3,
                  std::chrono::duration<double>(std::chrono::steady_clock::now() - sync_t0).count() * 1e3);
   if (flags[0] != 0x7fffffff) {  // rebuild the reference's message for the lowest failing genome
     if (pack) {  // from the FP64 rows, which only the error path uploads
