@@ -13,6 +13,8 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("FNB_AB_ROOT"):  # A/B: a package copy with another library build
+    sys.path.insert(0, os.environ["FNB_AB_ROOT"])
 import paper_2504_08339_b200 as fnb  # noqa: E402
 from paper_2504_08339_b200.synthetic import regression_dataset, synthetic_population  # noqa: E402
 
