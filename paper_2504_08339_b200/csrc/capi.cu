@@ -149,16 +149,7 @@ static std::atomic<bool> g_host_pack{[] {
   const char* e = std::getenv("FNB_H2D_PACK");
   return !(e && std::atoi(e) == 0);
 }()};
-// share (%) of the chunks of a PINNED population that are packed (tuning:
-// FNB_H2D_PACK_PINNED_PCT, scripts/h2d_trace.sh).  Measured at C2 on the B200
-// host (16 cores): 0% 2.23-2.31 ms, 30% 3.2-3.3, 50% 2.3-2.5, 70% 2.2-2.4,
-// 100% 2.36 ms per call -- the host's memory bandwidth bounds the DMA and the
-// packers together, so pinned arrays go up as they are (0)
-static std::atomic<int> g_pinned_pack_pct{[] {
-  const char* e = std::getenv("FNB_H2D_PACK_PINNED_PCT");
-  const int v = e ? std::atoi(e) : 0;
-  return v < 0 ? 0 : v > 100 ? 100 : v;
-}()};
+
 void fnb_set_host_transfer_packed(int on) { g_host_pack.store(on != 0); }
 
 // ---- device layer ------------------------------------------------------
@@ -339,21 +330,21 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
     }
     return a.type == cudaMemoryTypeUnregistered;
   };
-  // Which chunks are packed: every chunk of pageable arrays (they are staged
-  // through host memory anyway: ~2x the e2e at C2); for pinned arrays a share
-  // (g_pinned_pack_pct) -- the host threads pack those while the DMA engine
-  // streams the others' FP64 rows straight from the caller's buffers, so the
-  // two host-memory consumers run side by side.
+  // Pageable arrays are packed (they are staged through host memory anyway:
+  // ~2x the e2e at C2).  Pinned arrays go up by DMA as they are: packing all
+  // or a share of their chunks on the host threads measured 2.2-3.3 ms per C2
+  // call against 2.23 ms (scripts/h2d_trace.sh, round 2) -- the host's memory
+  // bandwidth bounds the DMA and the packers together.
   const bool src_pageable = pageable(pop_nodes) || pageable(pop_conns);
-  const int pack_pct = !(allow_pack && g_host_pack.load()) ? 0 : src_pageable ? 100 : g_pinned_pack_pct.load();
-  const bool pack = pack_pct > 0;
-  auto is_pk = [&](int k) { return pack_pct > 0 && ((k + 1) * pack_pct) / 100 > (k * pack_pct) / 100; };
+  const bool pack = allow_pack && g_host_pack.load() && src_pageable;
+  auto is_pk = [&](int) { return pack; };
   const PackedLayout pkl(N, Cm);
-  if (pack_pct < 100) {
+  if (!pack) {
     CK(ctx->nodes.ensure(nrow * size_t(P)));
     CK(ctx->conns.ensure(crow * size_t(P)));
+  } else {
+    CK(ctx->packed.ensure(pkl.bytes * size_t(P)));
   }
-  if (pack) CK(ctx->packed.ensure(pkl.bytes * size_t(P)));
   CK(ctx->nets.ensure(ctx->L.bytes * size_t(P)));
   CK(ctx->flags.ensure(4 * sizeof(int)));
   int* d_flags = static_cast<int*>(ctx->flags.p);  // [0] first failing genome, [1] non-finite X, [2] Y
@@ -539,8 +530,8 @@ static int evaluate_impl(fnb_ctx* ctx, const double* pop_nodes, const double* po
     for (auto& e : tev) cudaEventDestroy(e);
   }
   if (trace)
-    std::fprintf(stderr, "evaluate P=%d chunks=%d packed %d%%: copies %.3f ms, K1/K2 launches %.3f ms, enqueue %.3f ms, wait %.3f ms\n", P, chunks,
-                 pack_pct, t_copy * 1e3, t_launch * 1e3, std::chrono::duration<double>(sync_t0 - call_t0).count() * 1e3,
+    std::fprintf(stderr, "evaluate P=%d chunks=%d packed %d: copies %.3f ms, K1/K2 launches %.3f ms, enqueue %.3f ms, wait %.3f ms\n", P, chunks,
+                 int(pack), t_copy * 1e3, t_launch * 1e3, std::chrono::duration<double>(sync_t0 - call_t0).count() * 1e3,
                  std::chrono::duration<double>(std::chrono::steady_clock::now() - sync_t0).count() * 1e3);
   if (flags[0] != 0x7fffffff) {  // rebuild the reference's message for the lowest failing genome
     if (pack) {  // from the FP64 rows, which only the error path uploads

@@ -11,8 +11,6 @@
 // gene k consumes draws 4k..4k+3 (attributes 1..4), connection gene k draw
 // 4*M_nodes + k -- so the whole child is produced in one parallel pass.
 // coin(0.5) is uniform() < 0.5, i.e. the top bit of the u64 draw is 0.
-#include <cstdlib>
-
 #include "fnb_common.cuh"
 #include "keytable.cuh"
 #include "philox.cuh"
@@ -45,7 +43,7 @@ __device__ __forceinline__ int block_prefix(bool flag, int* s_cnt, int& total) {
 __global__ void __launch_bounds__(kXWarps * 32)
 k_crossover(const double* __restrict__ nodes, const double* __restrict__ conns, const int32_t* __restrict__ fit_idx,
             const int32_t* __restrict__ oth_idx, const uint32_t* __restrict__ keys, int n_children, int N, int C,
-            double* __restrict__ child_nodes, double* __restrict__ child_conns, int l2_prefetch) {
+            double* __restrict__ child_nodes, double* __restrict__ child_conns) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ int s_cnt[kXWarps];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -65,12 +63,6 @@ k_crossover(const double* __restrict__ nodes, const double* __restrict__ conns, 
   double* cn = child_nodes + size_t(c) * N * kNodeCols;
   double* cc = child_conns + size_t(c) * C * kConnCols;
   const Key4 key{{keys[4 * c], keys[4 * c + 1], keys[4 * c + 2], keys[4 * c + 3]}};
-  // the fit parent is first read after the table build: one bulk L2 prefetch
-  // of its rows now, so the chunk loop below reads L2 instead of HBM
-  if (l2_prefetch && tid == 0) {
-    prefetch_l2_range(fc, size_t(C) * kConnCols * 8);
-    prefetch_l2_range(fn, size_t(N) * kNodeCols * 8);
-  }
 
   // the fit parent's first node chunk is loaded before the table build
   double row0[kNodeCols];
@@ -169,11 +161,7 @@ cudaError_t launch_crossover(const double* nodes, const double* conns, const int
   const size_t smem = crossover_smem(N, C);
   cudaError_t e = cudaFuncSetAttribute(k_crossover, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  static const int l2pf = [] {  // experiment knob
-    const char* e = std::getenv("FNB_XOVER_L2PF");
-    return e ? std::atoi(e) : 0;  // measured: +2% at C5 (2.63 -> 2.69 ms); off
-  }();
-  k_crossover<<<n, kXWarps * 32, smem, st>>>(nodes, conns, fit, oth, keys, n, N, C, cn, cc, l2pf);
+  k_crossover<<<n, kXWarps * 32, smem, st>>>(nodes, conns, fit, oth, keys, n, N, C, cn, cc);
   return cudaGetLastError();
 }
 

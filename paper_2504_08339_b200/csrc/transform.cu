@@ -13,8 +13,6 @@
 // weights block their target exactly like the reference), the
 // initial-ready `key >= 0` filter (network.hpp:195), and incoming edges in
 // ascending source row (network.hpp:184-190).
-#include <cstdlib>
-
 #include "fnb_common.cuh"
 
 namespace fnb {
@@ -141,7 +139,7 @@ __device__ inline void tf_fail(uint8_t* net, int status, int kind, int a, int b,
 template <int W, bool kPk>
 __global__ void __launch_bounds__(128)
 k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, const uint8_t* __restrict__ packed,
-            int P, uint8_t* __restrict__ nets, NetLayout L, DevShape sh, size_t smem_per_warp, int l2_prefetch) {
+            int P, uint8_t* __restrict__ nets, NetLayout L, DevShape sh, size_t smem_per_warp) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -152,9 +150,6 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   const double* crow = kPk ? nullptr : conns + size_t(g) * C * kConnCols;
   const PackedLayout pk(N, C);
   const uint8_t* pg = kPk ? packed + size_t(g) * pk.bytes : nullptr;
-  // the connection rows are first read in step 4, after the node, rank and
-  // hash phases: one bulk prefetch brings them to L2 meanwhile
-  if (!kPk && l2_prefetch && lane == 0) prefetch_l2_bulk(crow, uint32_t(C) * kConnCols * 8u);
   uint8_t* net = nets + size_t(g) * L.bytes;
 
   // ---- 1. node rows: keys, activation/aggregation ids (network.hpp:139-152);
@@ -742,11 +737,7 @@ static cudaError_t launch_transform_w(const double* n, const double* c, const ui
   cudaError_t e = cudaFuncSetAttribute(k_transform<W, kPk>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   const int blocks = (P + warps - 1) / warps;
-  static const int l2pf = [] {  // experiment knob: measured neutral at C5, 4% slower at C2 (default off)
-    const char* e = std::getenv("FNB_K1_L2PF");
-    return e ? std::atoi(e) : 0;
-  }();
-  k_transform<W, kPk><<<blocks, 32 * warps, smem, st>>>(n, c, pk, P, nets, L, sh, per_warp, l2pf);
+  k_transform<W, kPk><<<blocks, 32 * warps, smem, st>>>(n, c, pk, P, nets, L, sh, per_warp);
   return cudaGetLastError();
 }
 

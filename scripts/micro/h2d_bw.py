@@ -24,3 +24,23 @@ for mode in ("one", "two", "one", "two"):
         ts.append(a.elapsed_time(b))
     ts.sort()
     print(mode, "median ms", round(ts[5], 3), "GB/s", round(n / ts[5] / 1e6, 1))
+# the evaluate pipeline's copy pattern: 12 chunks x (nodes 2.1 MB + conns 6.7 MB)
+nb, cb = 10_000 * 64 * 40, 10_000 * 256 * 32
+hn, hc = h[:nb], h[nb:nb + cb]
+dn_, dc_ = d[:nb], d[nb:nb + cb]
+for chunks in (1, 6, 12, 24):
+    ts = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        for k in range(chunks):
+            n0, n1 = nb * k // chunks, nb * (k + 1) // chunks
+            c0, c1 = cb * k // chunks, cb * (k + 1) // chunks
+            dn_[n0:n1].copy_(hn[n0:n1], non_blocking=True)
+            dc_[c0:c1].copy_(hc[c0:c1], non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    print("chunks", chunks, "median ms", round(ts[5], 3), "GB/s", round(n / ts[5] / 1e6, 1))
