@@ -28,6 +28,9 @@
 #ifndef FNB_K2_UNROLL
 #define FNB_K2_UNROLL 8
 #endif
+#ifndef FNB_K2_UNROLL_GENERIC
+#define FNB_K2_UNROLL_GENERIC 2
+#endif
 
 namespace fnb {
 
@@ -205,7 +208,7 @@ k_forward(FwdParams p) {
   // record loop unrolling: the single-function instantiations gain from a
   // deeper unroll (more independent record bodies in flight), the generic
   // one (activation / aggregation dispatch per op) does not
-  constexpr int kRecUnroll = (AGG >= 0 && ACT >= 0) ? FNB_K2_UNROLL : 2;
+  constexpr int kRecUnroll = (AGG >= 0 && ACT >= 0) ? FNB_K2_UNROLL : FNB_K2_UNROLL_GENERIC;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int T = p.T;
   const int grp = threadIdx.x / T;
@@ -359,16 +362,20 @@ if constexpr (SPT == 1) {
       } else {
         const int cnt = __popc((meta >> 8) & 15u);  // real slots are a prefix
         const float w[4] = {cur.w.x, cur.w.y, cur.w.z, cur.w.w};
+        if (agg == FNB_AGG_PRODUCT) {  // one (warp-uniform) branch per record, not per sample
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-          const float xs[4] = {x0[k], x1[k], x2[k], x3[k]};
-          if (agg == FNB_AGG_PRODUCT) {
+          for (int k = 0; k < SPT; ++k) {
+            const float xs[4] = {x0[k], x1[k], x2[k], x3[k]};
             float a = first ? 1.0f : acc[k];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               if (q < cnt) a *= w[q] * xs[q];
             acc[k] = a;
-          } else {  // max; empty fan-in falls back to 0 (network.hpp:258-261)
+          }
+        } else {  // max; empty fan-in falls back to 0 (network.hpp:258-261)
+#pragma unroll
+          for (int k = 0; k < SPT; ++k) {
+            const float xs[4] = {x0[k], x1[k], x2[k], x3[k]};
             float a = first ? 0.0f : acc[k];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -390,9 +397,32 @@ if constexpr (SPT == 1) {
           }
         }
         float y[SPT];
+        if constexpr (ACT >= 0) {
 #pragma unroll
-        for (int k = 0; k < SPT; ++k)
-          y[k] = act_apply<ACT>(int((meta >> 16) & 7u), fmaf(cur.a.y, acc[k], cur.a.x));
+          for (int k = 0; k < SPT; ++k) y[k] = act_apply<ACT>(ACT, fmaf(cur.a.y, acc[k], cur.a.x));
+        } else {  // one dispatch per op (warp-uniform), not per sample
+#pragma unroll
+          for (int k = 0; k < SPT; ++k) y[k] = fmaf(cur.a.y, acc[k], cur.a.x);
+          switch (int((meta >> 16) & 7u)) {
+            case FNB_ACT_TANH:
+#pragma unroll
+              for (int k = 0; k < SPT; ++k) y[k] = tanh_fast(y[k]);
+              break;
+            case FNB_ACT_SIGMOID:
+#pragma unroll
+              for (int k = 0; k < SPT; ++k) y[k] = sigmoid_fast(y[k]);
+              break;
+            case FNB_ACT_RELU:
+#pragma unroll
+              for (int k = 0; k < SPT; ++k) y[k] = y[k] > 0.0f ? y[k] : 0.0f;
+              break;
+            case FNB_ACT_SIN:
+#pragma unroll
+              for (int k = 0; k < SPT; ++k) y[k] = act_apply<FNB_ACT_SIN>(FNB_ACT_SIN, y[k]);
+              break;
+            default: break;  // identity
+          }
+        }
         sts<SPT>(vb + (meta & 0xffu) * row_bytes, y);
         if constexpr (kSumOnly) {
 #pragma unroll
