@@ -732,7 +732,9 @@ template <int W, bool kPk>
 static cudaError_t launch_transform_w(const double* n, const double* c, const uint8_t* pk, int P, uint8_t* nets,
                                       const NetLayout& L, const DevShape& sh, cudaStream_t st) {
   const size_t per_warp = tf_smem_bytes(sh.N, sh.C, W);
-  const int warps = warps_per_cta_for_smem(per_warp, 4);
+  // CTA width (measured, round 2): 2 warps at N <= 64 (C2 0.104 -> 0.102 ms),
+  // 4 above (C5: 0.72 ms per 20k genomes against 0.76 / 0.73 for 2 / 1)
+  const int warps = warps_per_cta_for_smem(per_warp, W <= 2 ? 2 : 4);
   const size_t smem = per_warp * warps;
   cudaError_t e = cudaFuncSetAttribute(k_transform<W, kPk>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
