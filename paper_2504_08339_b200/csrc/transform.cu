@@ -30,7 +30,7 @@ struct TfSmem {
   int* sorted_key;      // [N] key of rank k
   int* R;               // [N] enabled rows per destination row
   uint32_t* pred;       // [N * W] predecessor rows of each row (row bits)
-  uint32_t* predr;      // [N * W] predecessor ranks of each rank (rank bits); free_at after Kahn
+  uint32_t* predr;      // [N * W] predecessor ranks of each rank (rank bits); slot-chain scratch after Kahn
   uint16_t* row_of_rank;// [N]
   uint16_t* rank;       // [N]
   uint16_t* order;      // [N]
@@ -451,12 +451,11 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   // ---- 6a. ops in topological order, skipping input rows (network.hpp:252-254):
   //          op index and record base per row; each op = max(1, ceil(fanin/4))
   //          records.  (rank / row_of_rank / R / sorted_key / predr are free
-  //          after Kahn and reused as opos / slot_of / last_use / fanin / free_at.)
+  //          after Kahn and reused as opos / slot_of / last_use / fanin / slot scratch.)
   uint16_t* opos = s.rank;
   uint16_t* slot_of = s.row_of_rank;
   int* last_use = s.R;
   int* fanin = s.sorted_key;
-  uint32_t* free_at = s.predr;  // [op][W]: slots whose value's last reader is the op
   int op_base = 0, rec_base = 0, edge_total = 0;
   for (int p0 = 0; p0 < count; p0 += 32) {
     const int p = p0 + lane;
@@ -494,8 +493,6 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   for (int r = lane; r < N; r += 32) {
     last_use[r] = -1;
     slot_of[r] = 0xffff;
-#pragma unroll
-    for (int w = 0; w < W; ++w) free_at[r * W + w] = 0u;
   }
   __syncwarp();
   for (int i = lane; i < sh.O; i += 32) last_use[out_rows[i]] = kLastForever;
@@ -506,89 +503,101 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     atomicMax(&last_use[s.csrc[r]], int(opos[dst]));
   }
   __syncwarp();
-  // ---- 6c. value slots: linear scan over the op order, lowest free slot
-  //          (slots = max live values).  A value's slot is queued on the op
-  //          that reads it last (free_at), so each op costs W mask words, one
-  //          find-first-zero and one queue update.  The used mask is a W-word
-  //          register array indexed only by unrolled loops.
+  // ---- 6c. value slots (slots = max live values), warp-parallel: an interval
+  //          colouring with a FIFO of free slots (below).  Round 1-2 ran the
+  //          lowest-free-slot scan on lane 0, one op after another (27% of K1's
+  //          instructions and 23% of its stall samples at C2); this form took K1
+  //          from 0.102 to 0.090 ms at C2 and 0.73 to 0.62 ms per 20k genomes at C5.
   int n_slots = 0;
-  if (W == 2 && lane == 0) {
-    // N <= 64: the used mask is one 64-bit register and free_at one 64-bit
-    // word per op (the same lowest-free-slot allocation, fewer instructions
-    // on this single-lane chain)
-    unsigned long long used = 0ull;
-    unsigned long long* fa = reinterpret_cast<unsigned long long*>(free_at);
-    auto alloc = [&]() {
-      const int sl = __ffsll(static_cast<long long>(~used)) - 1;
-      used |= 1ull << sl;
-      n_slots = max(n_slots, sl + 1);
-      return sl;
-    };
-    auto retire = [&](int sl, int lu) {
-      if (lu < 0) used &= ~(1ull << sl);
-      else if (lu != kLastForever) fa[lu] |= 1ull << sl;
-    };
-    for (int i = 0; i < sh.I; ++i) {
-      const int r = in_rows[i];
-      if (slot_of[r] == 0xffff) {
-        const int sl = alloc();
-        slot_of[r] = uint16_t(sl);
-        const int lu = last_use[r];
-        if (lu >= 0) retire(sl, lu);
-      }
+  {
+    // Warp-parallel form of the same allocation problem.  Values: the distinct
+    // input rows (first appearance), then the ops in order; value v starts at
+    // time v and ends at Ip + (its last reader's op index) -- freed before that
+    // op's own output is placed, as in the scan -- or right after it starts
+    // (an op value nobody reads), or never (outputs, inputs nobody reads).
+    // The slot count is the maximum overlap M (what the lowest-free-slot scan
+    // reaches: both are optimal for intervals), and the slots come from a FIFO
+    // of free slots: start s < M takes slot s, start s >= M the slot of the
+    // value whose end is the (s - M)-th end event (time order, ties by value
+    // index; __match_any_sync ranks each 32-value chunk).  Slot chains are
+    // resolved by pointer jumping.  Any valid assignment gives K2 the same
+    // arithmetic, so fitness bits do not depend on it.
+    constexpr int kInf = 0x7fff;
+    int16_t* endt = reinterpret_cast<int16_t*>(s.kr);  // [N] end time (s.kr is dead after step 2)
+    int16_t* vrow = endt + N;                            // [N] row of value v
+    int* cnt = reinterpret_cast<int*>(vrow + N);         // [N + 2] end-time histogram, then cursors
+    int16_t* srcv = reinterpret_cast<int16_t*>(s.predr);  // [N] value of end event e (predr is dead)
+    int16_t* par = endt;                                 // [N] slot chains (endt is dead by then)
+    const unsigned lt = (1u << lane) - 1u;
+    // distinct inputs in order of first appearance (I <= 32)
+    const int irow = lane < sh.I ? in_rows[lane] : -1;
+    bool first = lane < sh.I;
+    for (int j = 0; j < sh.I; ++j)
+      if (j < lane && in_rows[j] == irow) first = false;
+    const unsigned fm = __ballot_sync(kFull, first);
+    const int Ip = __popc(fm);
+    if (first) vrow[__popc(fm & lt)] = int16_t(irow);
+    for (int k = lane; k < op_base; k += 32) vrow[Ip + k] = int16_t(s.op_row[k]);
+    const int V = Ip + op_base;
+    for (int t = lane; t <= V + 1; t += 32) cnt[t] = 0;
+    __syncwarp();
+    for (int v = lane; v < V; v += 32) {
+      const int lu = last_use[vrow[v]];
+      int e;
+      if (lu == kLastForever) e = kInf;
+      else if (lu < 0) e = v < Ip ? kInf : v + 1;
+      else e = Ip + lu;
+      endt[v] = int16_t(e);
+      if (e != kInf) atomicAdd(&cnt[e], 1);
     }
-    for (int k = 0; k < op_base; ++k) {
-      used &= ~fa[k];
-      const int row = s.op_row[k];
-      const int sl = alloc();
-      slot_of[row] = uint16_t(sl);
-      retire(sl, last_use[row]);
-    }
-  } else if (lane == 0) {
-    uint32_t used[W];
+    __syncwarp();
+    // cnt[t] -> #ends before t; live(t) = (t + 1) - #ends at or before t
+    int carry = 0, mx = 0;
+    for (int t0 = 0; t0 <= V; t0 += 32) {
+      const int t = t0 + lane;
+      const int c = t <= V ? cnt[t] : 0;
+      int incl = c;
 #pragma unroll
-    for (int w = 0; w < W; ++w) used[w] = 0u;
-    auto alloc = [&]() {  // lowest free slot (select chain, no branches)
-      int sl = 0;
-#pragma unroll
-      for (int w = W - 1; w >= 0; --w) {
-        const uint32_t f = ~used[w];
-        sl = f ? w * 32 + __ffs(f) - 1 : sl;
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += y;
       }
-      const int sw = sl >> 5;
-      const uint32_t bit = 1u << (sl & 31);
-#pragma unroll
-      for (int w = 0; w < W; ++w) used[w] |= (w == sw) ? bit : 0u;
-      n_slots = max(n_slots, sl + 1);
-      return sl;
-    };
-    auto retire = [&](int sl, int lu) {  // queue the slot on its last reader, or free it now
-      const int sw = sl >> 5;
-      const uint32_t bit = 1u << (sl & 31);
-      if (lu < 0) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) used[w] &= (w == sw) ? ~bit : 0xffffffffu;
-      } else if (lu != kLastForever) {
-        free_at[lu * W + sw] |= bit;
-      }
-    };
-    for (int i = 0; i < sh.I; ++i) {
-      const int r = in_rows[i];
-      if (slot_of[r] == 0xffff) {
-        const int sl = alloc();
-        slot_of[r] = uint16_t(sl);
-        const int lu = last_use[r];
-        if (lu >= 0) retire(sl, lu);  // an unread input keeps its slot (as before)
-      }
+      if (t <= V) cnt[t] = carry + incl - c;
+      if (t < V) mx = max(mx, t + 1 - (carry + incl));
+      carry += __shfl_sync(kFull, incl, 31);
     }
-    for (int k = 0; k < op_base; ++k) {
-#pragma unroll
-      for (int w = 0; w < W; ++w) used[w] &= ~free_at[k * W + w];
-      const int row = s.op_row[k];
-      const int sl = alloc();
-      slot_of[row] = uint16_t(sl);
-      retire(sl, last_use[row]);
+    const int M = int(__reduce_max_sync(kFull, unsigned(mx)));
+    __syncwarp();
+    // end events in (time, value) order: srcv[e-th end] = value
+    for (int v0 = 0; v0 < V; v0 += 32) {
+      const int v = v0 + lane;
+      const int e = v < V ? int(endt[v]) : kInf;
+      const unsigned grp = __match_any_sync(kFull, e);
+      const int pos = e != kInf ? cnt[e] + __popc(grp & lt) : 0;
+      __syncwarp();
+      if (e != kInf) {
+        srcv[pos] = int16_t(v);
+        if ((grp >> lane) == 1u) cnt[e] += __popc(grp);  // the group's highest lane advances the cursor
+      }
+      __syncwarp();
     }
+    // start s < M takes slot s; start s >= M the slot of the (s - M)-th end
+    for (int v = lane; v < V; v += 32) par[v] = int16_t(v < M ? v : srcv[v - M]);
+    __syncwarp();
+    for (;;) {  // pointer jumping to the chain roots (the slots)
+      bool changed = false;
+      for (int v = lane; v < V; v += 32) {
+        const int q = par[v], qq = par[q];
+        if (qq != q) {
+          par[v] = int16_t(qq);
+          changed = true;
+        }
+      }
+      __syncwarp();
+      if (!__any_sync(kFull, changed)) break;
+    }
+    for (int v = lane; v < V; v += 32) slot_of[vrow[v]] = uint16_t(par[v]);
+    n_slots = M;
   }
   n_slots = __shfl_sync(kFull, n_slots, 0);
   __syncwarp();

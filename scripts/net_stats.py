@@ -8,6 +8,8 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("FNB_AB_ROOT"):  # A/B: a package copy with another library build
+    sys.path.insert(0, os.environ["FNB_AB_ROOT"])
 import paper_2504_08339_b200 as fnb  # noqa: E402
 from paper_2504_08339_b200.synthetic import synthetic_population  # noqa: E402
 
@@ -23,6 +25,8 @@ for name, (P, N, C) in {"c2": (10_000, 64, 256), "c5": (20_000, 128, 1024)}.item
     h = hb.view(np.int32).reshape(P, 8)
     h16 = hb.view(np.int16).reshape(P, 16)
     n_slots = h[:, 6]
+    if os.environ.get("FNB_DUMP_SLOTS"):
+        np.save(os.environ["FNB_DUMP_SLOTS"] + f"_{name}.npy", n_slots)
     n_rec = h16[:, 11]
     n_ops = h16[:, 9]
     n_edges = h16[:, 10]
