@@ -264,8 +264,11 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   __syncwarp();
 
   // ---- 3. inputs then outputs (network.hpp:155-165)
+  // lane i keeps input / output i's row in a register (I, O <= 32); the net
+  // block receives their value slots in step 8
   uint16_t* in_rows = reinterpret_cast<uint16_t*>(net + L.in_off);
   uint16_t* out_rows = reinterpret_cast<uint16_t*>(net + L.out_off);
+  int my_in = -1, my_out = -1;
   for (int pass = 0; pass < 2; ++pass) {
     const int n = pass == 0 ? sh.I : sh.O;
     for (int i0 = 0; i0 < n; i0 += 32) {
@@ -284,8 +287,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
         return;
       }
       if (i < n) {
-        if (pass == 0) { in_rows[i] = uint16_t(row); s.flags[row] |= 2; }
-        else out_rows[i] = uint16_t(row);
+        if (pass == 0) { my_in = row; s.flags[row] |= 2; }
+        else my_out = row;
       }
     }
   }
@@ -495,7 +498,7 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     slot_of[r] = 0xffff;
   }
   __syncwarp();
-  for (int i = lane; i < sh.O; i += 32) last_use[out_rows[i]] = kLastForever;
+  if (my_out >= 0) last_use[my_out] = kLastForever;
   __syncwarp();
   for (int r = lane; r < C; r += 32) {
     const int dst = s.cdst[r];
@@ -530,10 +533,12 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     int16_t* par = endt;                                 // [N] slot chains (endt is dead by then)
     const unsigned lt = (1u << lane) - 1u;
     // distinct inputs in order of first appearance (I <= 32)
-    const int irow = lane < sh.I ? in_rows[lane] : -1;
+    const int irow = my_in;
     bool first = lane < sh.I;
-    for (int j = 0; j < sh.I; ++j)
-      if (j < lane && in_rows[j] == irow) first = false;
+    for (int j = 0; j < sh.I; ++j) {
+      const int rj = __shfl_sync(kFull, my_in, j);
+      if (j < lane && rj == irow) first = false;
+    }
     const unsigned fm = __ballot_sync(kFull, first);
     const int Ip = __popc(fm);
     if (first) vrow[__popc(fm & lt)] = int16_t(irow);
@@ -652,8 +657,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   }
   __syncwarp();
   // ---- 8. input / output rows become value slots for the forward
-  for (int i = lane; i < sh.I; i += 32) in_rows[i] = slot_of[in_rows[i]];
-  for (int i = lane; i < sh.O; i += 32) out_rows[i] = slot_of[out_rows[i]];
+  if (lane < sh.I) in_rows[lane] = slot_of[my_in];
+  if (lane < sh.O) out_rows[lane] = slot_of[my_out];
   if (lane == 0) {
     NetHeader* h = reinterpret_cast<NetHeader*>(net);
     h->n_slots = n_slots;
