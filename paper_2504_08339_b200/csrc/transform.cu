@@ -42,6 +42,7 @@ struct TfSmem {
   uint8_t* flags;       // [N] bit0 non-empty, bit1 input
   uint8_t* csrc;        // [C] source row (rows fit a byte: N_max <= 255)
   uint8_t* cdst;        // [C] destination row of an enabled finite edge, else kNoRow
+  float* cw;            // [C] FP32 weight of an edge row (W <= 2 only)
   uint32_t ht_mask, ht_shift;
 };
 
@@ -61,6 +62,7 @@ __host__ __device__ inline size_t tf_smem_bytes(int N, int C, int W) {
   b += align16(size_t(N) * 4) * 2;       // nbias, nresp
   b += align16(size_t(N));               // flags
   b += align16(size_t(C)) * 2;           // csrc, cdst
+  if (W <= 2) b += align16(size_t(C) * 4);  // cw: FP32 weights staged in step 4 (kStageW)
   return b;
 }
 
@@ -86,6 +88,8 @@ __device__ inline TfSmem tf_carve(uint8_t* p, int N, int C, int W) {
   s.flags = p; p += align16(size_t(N));
   s.csrc = p; p += align16(size_t(C));
   s.cdst = p;
+  p += align16(size_t(C));
+  s.cw = W <= 2 ? reinterpret_cast<float*>(p) : nullptr;
   return s;
 }
 
@@ -359,6 +363,10 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
       uint8_t d = kNoRow;
       if (edge) {
         atomicAdd(&s.R[dst], 1);
+        if constexpr (W <= 2) {  // the weight, for step 7 (no re-read of the row)
+          if constexpr (kPk) s.cw[r] = __int_as_float(__double2loint(b.x));
+          else s.cw[r] = float(b.y);
+        }
         if (!wnan) {
           atomicOr(&s.pred[dst * W + (src >> 5)], 1u << (src & 31));
           const int rs = s.rank[src], rd = s.rank[dst];
@@ -639,7 +647,9 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
   for (int r = lane; r < C; r += 32) {
     const int dst = s.cdst[r];
     if (dst == kNoRow || (s.flags[dst] & 2)) continue;
-    const float wf = kPk ? reinterpret_cast<const float*>(pg + pk.w)[r] : float(ld_l2(crow + r * kConnCols + kW, drop));
+    float wf;
+    if constexpr (W <= 2) wf = s.cw[r];
+    else wf = kPk ? reinterpret_cast<const float*>(pg + pk.w)[r] : float(ld_l2(crow + r * kConnCols + kW, drop));
     const int src = s.csrc[r];
     int below = 0;
     const int sw = src >> 5;
