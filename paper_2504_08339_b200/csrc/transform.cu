@@ -169,11 +169,16 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
     if (r < N) {
       const double* row = kPk ? nullptr : nrow + r * kNodeCols;
       int key = 0;
+      double rb = 0.0, rr = 0.0, rg = 0.0, ra = 0.0;
       if constexpr (kPk) {
         ne = pg[pk.nflag + r] & 1u;
         key = reinterpret_cast<const int*>(pg + pk.key)[r];
-      } else {
+      } else {  // the whole row in one round trip (its columns share two sectors)
         const double k = row[kKey];
+        rb = row[kBias];
+        rr = row[kResp];
+        rg = row[kAgg];
+        ra = row[kAct];
         ne = !isnan(k);
         key = int(k);
       }
@@ -181,8 +186,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
       if (ne) {
         kr = (static_cast<long long>(key) << 8) | r;
         narrow = narrow && key >= -(1 << 23) && key < (1 << 23) - 1;  // INT32_MAX stays the empty mark
-        const int act = kPk ? int(pg[pk.act + r]) : int(row[kAct]);
-        const int agg = kPk ? int(pg[pk.agg + r]) : int(row[kAgg]);
+        const int act = kPk ? int(pg[pk.act + r]) : int(ra);
+        const int agg = kPk ? int(pg[pk.agg + r]) : int(rg);
         if (act < 0 || act >= sh.n_act) { bad = kErrActId; badid = act; }
         else if (agg < 0 || agg >= sh.n_agg) { bad = kErrAggId; badid = agg; }
         else {
@@ -191,8 +196,8 @@ k_transform(const double* __restrict__ nodes, const double* __restrict__ conns, 
             s.nbias[r] = reinterpret_cast<const float*>(pg + pk.bias)[r];
             s.nresp[r] = reinterpret_cast<const float*>(pg + pk.resp)[r];
           } else {
-            s.nbias[r] = float(row[kBias]);
-            s.nresp[r] = float(row[kResp]);
+            s.nbias[r] = float(rb);
+            s.nresp[r] = float(rr);
           }
         }
       }
