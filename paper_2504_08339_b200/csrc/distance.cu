@@ -552,10 +552,13 @@ __device__ __forceinline__ void step_terms(uint32_t msk, uint32_t e, int lane, i
   const uint32_t wm = __reduce_or_sync(kFull, msk);
   if (!wm) return;
   const uint32_t my = warp_transpose32(msk, lane);
-  const bool dense = __reduce_max_sync(kFull, lane < S ? __popc(my) : 0u) > kDenseRows;
+  // representatives matching many rows of the step take their whole tile row
+  // (every entry written, +0.0 where unmatched); the others only their matches
+  const uint32_t dm = __ballot_sync(kFull, lane < S && uint32_t(__popc(my)) > kDenseRows);
+  const bool dense = (dm >> lane) & 1u;
   double* col = tile + lane;
-  if (dense) {
-    for (uint32_t m = wm; m; m &= m - 1u) {
+  if (dm) {
+    for (uint32_t m = msk | dm; m; m &= m - 1u) {
       const int s = __ffs(m) - 1;
       double t = 0.0;
       if ((msk >> s) & 1u) t = term(s, e++);
